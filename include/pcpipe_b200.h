@@ -1,0 +1,204 @@
+/* pcpipe_b200.h — C ABI of the B200-native PcRecord → training-batch stage.
+ *
+ * Drop-in for the hot path of the reference library "pcpipe"
+ * (arXiv 2603.16945; reference sources under proj/core/ of the reference
+ * tree).  Each entry point names the reference interface it replaces.
+ *
+ *   - plain pointers and sizes only; no CUDA/torch types in signatures
+ *     (`stream` is a cudaStream_t passed as void*, NULL = the legacy stream);
+ *   - every call returns an int status: 0 = OK, otherwise (int)Errc + 1 with
+ *     Errc exactly as errors.hpp:8-53 (PCP_E_* below); pcp_last_error() holds
+ *     the message (thread-local).  No C++ exception crosses this ABI;
+ *   - device-side failures (CRC mismatch, corrupt LZ4, blob overrun, empty
+ *     cloud …) surface at the batch boundary as PCP_E_WORKER_PANIC naming the
+ *     op, exactly like Pipeline::next_batch (pipeline.cpp:677-689).
+ *
+ * There is no CPU fallback: on a host without a usable sm_100 device every
+ * compute entry point returns PCP_E_IO_FAILURE with a message saying so.
+ */
+#ifndef PCPIPE_B200_H
+#define PCPIPE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes = (int)pcpipe::Errc + 1 (errors.hpp:8-53) ---------- */
+enum {
+  PCP_OK = 0,
+  PCP_E_DUPLICATE_FIELD = 1,
+  PCP_E_EMPTY_SCHEMA,
+  PCP_E_BAD_SHAPE,
+  PCP_E_BAD_ALIGNMENT,
+  PCP_E_COLUMN_OUT_OF_RANGE,
+  PCP_E_CHECKSUM_MISMATCH,
+  PCP_E_CORRUPT_PAGE,
+  PCP_E_SCHEMA_MISMATCH,
+  PCP_E_IO_FAILURE,
+  PCP_E_EMPTY_DATASET,
+  PCP_E_BAD_MAGIC,
+  PCP_E_UNSUPPORTED_VERSION,
+  PCP_E_CORRUPT_HEADER,
+  PCP_E_RANGE_OUT_OF_BOUNDS,
+  PCP_E_SCHEMA_CONFLICT,
+  PCP_E_OUT_OF_RANGE,
+  PCP_E_NOT_PADDED,
+  PCP_E_MALFORMED_HEADER,
+  PCP_E_TRUNCATED_PAYLOAD,
+  PCP_E_UNSUPPORTED_PROPERTY,
+  PCP_E_NO_INPUT_FILES,
+  PCP_E_PARSE_FAILURE,
+  PCP_E_SHUTDOWN,
+  PCP_E_MISSING_FIELD,
+  PCP_E_EMPTY_CLOUD,
+  PCP_E_UNKNOWN_OP,
+  PCP_E_OUT_OF_BOUNDS,
+  PCP_E_WORKER_PANIC,
+  PCP_E_SHAPE_MISMATCH,
+};
+
+/* Thread-local message of the last failing call on this thread. */
+const char* pcp_last_error(void);
+/* Errc name for a status ("kChecksumMismatch" …), errors.cpp:5-50. */
+const char* pcp_errc_name(int status);
+/* Library/device info; returns PCP_OK when an sm_100 device is usable. */
+int pcp_device_info(int device, int* sm_count, int* cc_major, int* cc_minor);
+
+/* ---- seeding: mix_seed (transforms.hpp:27-28, transforms.cpp:82-96) --- */
+uint64_t pcp_mix_seed(uint64_t base_seed, uint64_t epoch, uint64_t sample_index,
+                      uint64_t op_id);
+
+/* ---- codec (format.hpp:88-105, lz4_block.hpp:22-26) -------------------
+ * Batched page decode on the device.  d_bytes holds serialized EncodedPage
+ * records ([u8 flags][u64 raw_len][u64 payload_len][u32 crc][payload],
+ * format.cpp:276-299) at d_page_off[i]; each decodes to d_out + d_out_off[i]
+ * (capacity raw_len).  Inner-delta columns (offset,length pairs in raw-page
+ * coordinates, width 4) are d_col_off/d_col_len[d_col_first[i] ..
+ * d_col_first[i+1]).  Per-page status (0 or Errc+1: kChecksumMismatch,
+ * kCorruptPage, kColumnOutOfRange, kBadAlignment) lands in d_status[i].
+ * Replaces decode_block_page / decode_scalar_page (format.cpp:243-274). */
+int pcp_decode_pages(const uint8_t* d_bytes, const uint64_t* d_page_off, uint32_t n_pages,
+                     uint8_t* d_out, const uint64_t* d_out_off,
+                     const uint32_t* d_col_first, const uint64_t* d_col_off,
+                     const uint64_t* d_col_len, int32_t* d_status, void* stream);
+
+/* zlib-compatible CRC-32 of n_ranges byte ranges of device memory
+ * (crc32_of, format.cpp:163-166).  Results to d_crc[i]. */
+int pcp_crc32_ranges(const uint8_t* d_bytes, const uint64_t* d_off, const uint64_t* d_len,
+                     uint32_t n_ranges, uint32_t* d_crc, void* stream);
+
+/* ---- operators: apply_map (transforms.hpp:33-34) over a cloud set -----
+ * A cloud set is CSR over n_clouds clouds in device memory.  Per-point
+ * fields are optional (NULL = absent): data/normal/color float32 [N][3],
+ * intensity float32 [N], plus up to 4 extra per-point byte fields gathered
+ * by index ops when listed in params "gather".  apply_map semantics per cloud
+ * c with seed d_seeds[c]; outputs go to `out` (capacity out->cap_points per
+ * cloud, dense slots of that stride; out->d_count receives sizes).
+ * kind: PCP_MAP_* (map_kind_from_name names, transforms.cpp:54-80, plus the
+ * App. C extensions).  Per-cloud status → d_status[c]. */
+enum {
+  PCP_MAP_NORMALIZE = 0,
+  PCP_MAP_TRANSLATE,
+  PCP_MAP_JITTER,
+  PCP_MAP_ROTATE,
+  PCP_MAP_RANDOM_SCALE,
+  PCP_MAP_FLIP_YZ,
+  PCP_MAP_COLOR_AUGMENT,
+  PCP_MAP_RANDOM_CROP,
+  PCP_MAP_DOWNSAMPLE,
+  PCP_MAP_FPS = 16,
+  PCP_MAP_VOXEL,
+  PCP_MAP_RANGE_CROP,
+};
+int pcp_map_kind_from_name(const char* name, int* kind);
+
+typedef struct {
+  uint32_t n_clouds;
+  const uint64_t* d_offset; /* input: [n_clouds+1] point offsets (CSR) */
+  float* d_data;            /* [total][3] (required) */
+  float* d_normal;          /* [total][3] or NULL */
+  float* d_color;           /* [total][3] or NULL */
+  float* d_intensity;       /* [total] or NULL */
+  uint8_t* d_extra[4];      /* [total][extra_elem[e]] or NULL */
+  uint32_t extra_elem[4];
+} pcp_cloud_set;
+
+typedef struct {
+  uint32_t cap_points; /* per-cloud slot capacity */
+  float* d_data;       /* [n_clouds][cap][3] */
+  float* d_normal;
+  float* d_color;
+  float* d_intensity;
+  uint8_t* d_extra[4];
+  int32_t* d_voxel_count; /* [n_clouds][cap] (voxel only) or NULL */
+  uint32_t* d_count;      /* [n_clouds] points out */
+} pcp_cloud_out;
+
+int pcp_apply_map(int kind, const char* params_json, const pcp_cloud_set* in,
+                  const pcp_cloud_out* out, const uint64_t* d_seeds, int32_t* d_status,
+                  void* stream);
+
+/* ---- dataset writer (format.cpp:499-610), host side -------------------
+ * Writes <out_dir>/<stem>.pcrecord[N] byte-identical to write_dataset.
+ * schema_json = Schema::to_json ({"fields": {...}}).  samples = TLV stream
+ * (u32 n_fields {u16 name_len, name, u8 kind, u64 nbytes, bytes}) * n. */
+int pcp_write_dataset(const char* out_dir, const char* stem, const char* schema_json,
+                      const uint8_t* samples_tlv, size_t tlv_len, uint32_t n_samples,
+                      uint32_t slice_count, uint32_t group_size, uint32_t n_threads);
+
+/* ---- pipeline (pipeline.hpp:157-186) -----------------------------------
+ * Opens <primary>.pcrecord (+ continuation slices), parses the reference
+ * graph JSON (PipelineGraph::from_json, pipeline.cpp:122-146) and runs
+ * source → maps → batch on `device`.  entry_ids (optional) is the list of
+ * index entries this pipeline walks — e.g. one GPU's shard; index i of the
+ * walk is the seed index, like Item.index (pipeline.cpp:447-448).
+ * Options: JSON {"epochs": n, "resident": true|false, "wave_batches": k}. */
+typedef struct pcp_pipeline pcp_pipeline;
+
+int pcp_pipeline_open(const char* primary_path, const char* graph_json,
+                      const uint64_t* entry_ids, uint64_t n_entries, int device,
+                      const char* options_json, pcp_pipeline** out);
+
+#define PCP_MAX_BATCH_FIELDS 16
+typedef struct {
+  char name[48];
+  int32_t kind;              /* 0 bytes 1 int32 2 int64 3 float32 4 float64 */
+  uint8_t* d_ptr;            /* device, samples concatenated in order */
+  uint64_t nbytes;           /* total bytes */
+  const uint64_t* h_offsets; /* host [n_samples+1] byte offsets per sample */
+  int32_t uniform;           /* 1 when every sample has the same length */
+} pcp_field;
+
+typedef struct {
+  uint64_t epoch;
+  uint64_t batch_index;
+  uint32_t n_samples;
+  uint32_t n_fields;
+  pcp_field fields[PCP_MAX_BATCH_FIELDS]; /* std::map (name) order */
+} pcp_batch;
+
+/* Next batch in dataset order (Pipeline::next_batch); *end_of_stream = 1
+ * and PCP_OK once the final epoch drained.  The views stay valid until the
+ * pipeline has moved two waves further. */
+int pcp_pipeline_next_batch(pcp_pipeline* p, pcp_batch* out, int* end_of_stream);
+/* Stream on which the returned batch views are ready (use it for D2H of the
+ * batch; waves are computed on an internal stream). cudaStream_t as void*. */
+void* pcp_pipeline_stream(pcp_pipeline* p);
+/* Stats JSON (clouds, points, bytes, kernel ms …); caller must not free. */
+const char* pcp_pipeline_stats(pcp_pipeline* p);
+void pcp_pipeline_close(pcp_pipeline* p);
+
+/* ---- small device-memory helpers for hosts without a CUDA runtime ----- */
+int pcp_malloc(void** d_ptr, size_t n);
+int pcp_free(void* d_ptr);
+int pcp_memcpy_h2d(void* d_dst, const void* h_src, size_t n, void* stream);
+int pcp_memcpy_d2h(void* h_dst, const void* d_src, size_t n, void* stream);
+int pcp_stream_sync(void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PCPIPE_B200_H */

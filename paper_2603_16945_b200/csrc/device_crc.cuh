@@ -1,0 +1,151 @@
+// device_crc.cuh — zlib-compatible CRC-32 (crc32_of, format.cpp:163-166) for
+// sm_100a, split into independent chunks and recombined with GF(2) algebra:
+//
+//   crc(M) = XOR_i  x^(8 * bytes_after_i) (x) crc(chunk_i)     (mod P)
+//
+// (the closed form of zlib's crc32_combine applied left to right), so every
+// lane / CTA can CRC its own bytes and fold the result into one 32-bit XOR
+// accumulator per page with atomicXor — no ordering between chunks.
+#pragma once
+
+#include <cstdint>
+
+namespace pcp {
+namespace crc {
+
+constexpr uint32_t kPoly = 0xEDB88320u;
+
+__host__ __device__ inline uint32_t table_entry(uint32_t i) {
+  uint32_t c = i;
+  for (int k = 0; k < 8; ++k) c = (c & 1) ? kPoly ^ (c >> 1) : c >> 1;
+  return c;
+}
+
+// a (x) b mod P, reflected (zlib multmodp).
+__host__ __device__ inline uint32_t multmodp(uint32_t a, uint32_t b) {
+  uint32_t m = 1u << 31, p = 0;
+  for (;;) {
+    if (a & m) {
+      p ^= b;
+      if ((a & (m - 1)) == 0) break;
+    }
+    m >>= 1;
+    b = (b & 1) ? (b >> 1) ^ kPoly : b >> 1;
+  }
+  return p;
+}
+
+// x^(2^k) mod P for k = 0..31 (zlib x2n_table), in constant memory.
+struct X2N {
+  uint32_t v[32];
+};
+
+__host__ inline X2N make_x2n() {
+  X2N t;
+  uint32_t p = 1u << 30;  // x^1
+  t.v[0] = p;
+  for (int n = 1; n < 32; ++n) t.v[n] = p = multmodp(p, p);
+  return t;
+}
+
+// x^(8n) mod P (zlib x2nmodp(n, 3)).
+__device__ inline uint32_t x8n(const uint32_t* x2n, uint64_t n) {
+  uint32_t p = 1u << 31;
+  unsigned k = 3;
+  while (n) {
+    if (n & 1) p = multmodp(x2n[k & 31], p);
+    n >>= 1;
+    ++k;
+  }
+  return p;
+}
+
+// Standard CRC of bytes p[0..n) (init/xorout 0xFFFFFFFF), table in smem.
+__device__ inline uint32_t bytes(const uint32_t* tab, const uint8_t* p, uint64_t n) {
+  uint32_t c = 0xFFFFFFFFu;
+  for (uint64_t i = 0; i < n; ++i) c = tab[(c ^ p[i]) & 0xFF] ^ (c >> 8);
+  return c ^ 0xFFFFFFFFu;
+}
+
+// Same over 4-byte words read from an aligned smem copy starting at byte
+// `mis` (0..3) — used for staged blobs.  Falls back to bytes for the edges.
+__device__ inline uint32_t bytes_words(const uint32_t* tab, const uint8_t* p, uint64_t n) {
+  uint32_t c = 0xFFFFFFFFu;
+  uint64_t i = 0;
+  const uint64_t head = (4 - ((uintptr_t)p & 3)) & 3;
+  for (; i < head && i < n; ++i) c = tab[(c ^ p[i]) & 0xFF] ^ (c >> 8);
+  for (; i + 4 <= n; i += 4) {
+    uint32_t w = *reinterpret_cast<const uint32_t*>(p + i);
+    c ^= w;
+    c = tab[c & 0xFF] ^ (c >> 8);
+    c = tab[c & 0xFF] ^ (c >> 8);
+    c = tab[c & 0xFF] ^ (c >> 8);
+    c = tab[c & 0xFF] ^ (c >> 8);
+  }
+  for (; i < n; ++i) c = tab[(c ^ p[i]) & 0xFF] ^ (c >> 8);
+  return c ^ 0xFFFFFFFFu;
+}
+
+__device__ inline uint32_t warp_xor(uint32_t v) {
+  for (int o = 16; o > 0; o >>= 1) v ^= __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Chunk size of the parallel CRC.  Chunks are aligned to the END of a
+// range, so chunk k sits 256*k bytes before it and its shift is the constant
+// x^(8*256*k), read from a host-built table (kShiftEntries entries).
+constexpr uint32_t kChunk = 256;
+constexpr uint32_t kShiftEntries = 8192;  // ranges up to 2 MiB use the table
+
+__device__ inline uint32_t chunk_shift(const uint32_t* shift_tab, const uint32_t* x2n,
+                                       uint64_t k) {
+  return k < kShiftEntries ? shift_tab[k] : x8n(x2n, k * kChunk);
+}
+
+// CTA-cooperative CRC contribution of bytes p[0..n), which sit `after`
+// bytes before the end of the page:  x^(8*after) (x) crc(p[0..n)).
+// Returns the value on thread 0 (others: 0).  `red` is >= 32 words of smem.
+__device__ inline uint32_t cta_range(const uint32_t* tab, const uint32_t* x2n,
+                                     const uint32_t* shift_tab, const uint8_t* p,
+                                     uint64_t n, uint64_t after, uint32_t* red) {
+  const int t = threadIdx.x, nt = blockDim.x;
+  const uint64_t nchunks = (n + kChunk - 1) / kChunk;
+  uint32_t c = 0;
+  for (uint64_t k = t; k < nchunks; k += nt) {
+    const uint64_t e = n - k * kChunk;
+    const uint64_t s = e > kChunk ? e - kChunk : 0;
+    c ^= multmodp(chunk_shift(shift_tab, x2n, k), bytes_words(tab, p + s, e - s));
+  }
+  c = warp_xor(c);
+  if ((t & 31) == 0) red[t >> 5] = c;
+  __syncthreads();
+  uint32_t r = 0;
+  if (t < 32) {
+    r = (t < (nt + 31) / 32) ? red[t] : 0;
+    r = warp_xor(r);
+    if (t == 0 && after) r = multmodp(x8n(x2n, after), r);
+  }
+  __syncthreads();
+  return t == 0 ? r : 0;
+}
+
+// Warp-cooperative version (no block barriers): used by the standalone page
+// CRC kernel, where one warp owns one window of a page.
+__device__ inline uint32_t warp_range(const uint32_t* tab, const uint32_t* x2n,
+                                      const uint32_t* shift_tab, const uint8_t* p,
+                                      uint64_t n, uint64_t after) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t nchunks = (n + kChunk - 1) / kChunk;
+  uint32_t c = 0;
+  for (uint64_t k = lane; k < nchunks; k += 32) {
+    const uint64_t e = n - k * kChunk;
+    const uint64_t s = e > kChunk ? e - kChunk : 0;
+    c ^= multmodp(chunk_shift(shift_tab, x2n, k), bytes_words(tab, p + s, e - s));
+  }
+  c = warp_xor(c);
+  if (after) c = multmodp(x8n(x2n, after), c);
+  return c;
+}
+
+}  // namespace crc
+}  // namespace pcp

@@ -1,0 +1,1222 @@
+// host_pipeline.cpp — the B200 replacement for the reference Pipeline on the
+// PcRecord → batch path, and the extern "C" boundary (include/pcpipe_b200.h).
+//
+// Reference behaviour kept (proj/core/src/pipeline.cpp):
+//   * graph JSON + validation (PipelineGraph::from_json / validate, :40-146),
+//     fused map nodes expanded with their original op ids for seeding;
+//   * Item (epoch, index = position within the epoch) drives mix_seed
+//     (:442-462,474-476); output order = walk order; batch_index resets per
+//     epoch; drop_remainder (:567-613);
+//   * failures surface from next_batch as WorkerPanic "op <id>: ..." (:677-689).
+// Replaced: the thread/Connector/BoundedQueue machinery.  Work is cut into
+// waves of whole batches; each wave is one set of kernel launches on one
+// CUDA stream (copy → CRC → page decode → record parse → per-sample
+// interpreter), and the next wave is launched before the current one is
+// served, so host staging, H2D copies and compute overlap.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <filesystem>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/pcpipe_b200.h"
+#include "host_format.h"
+#include "json.hpp"
+#include "kernels.h"
+
+namespace pcp {
+
+using json = nlohmann::ordered_json;
+namespace fs = std::filesystem;
+
+namespace {
+
+thread_local std::string g_err;
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(kIoFailure, std::string("CUDA ") + what + ": " + cudaGetErrorString(e));
+}
+#define CK(x) cuda_check((x), #x)
+
+template <typename Fn>
+int guarded(Fn&& fn) {
+  try {
+    fn();
+    return kOk;
+  } catch (const Fail& f) {
+    g_err = std::string(errc_name(f.code)) + ": " + f.what();
+    return f.code;
+  } catch (const std::exception& e) {
+    g_err = std::string("WorkerPanic: ") + e.what();
+    return kWorkerPanic;
+  }
+}
+
+int require_device(int device) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+    fail(kIoFailure, "no CUDA device: the B200 path has no CPU fallback");
+  if (device < 0 || device >= n) fail(kOutOfBounds, "device index out of range");
+  cudaDeviceProp p;
+  CK(cudaGetDeviceProperties(&p, device));
+  if (p.major != 10) fail(kIoFailure, "device is not sm_100 (B200); this build targets sm_100a only");
+  CK(cudaSetDevice(device));
+  return p.multiProcessorCount;
+}
+
+// ---------------------------------------------------------------- device memory
+struct DevBuf {
+  void* p = nullptr;
+  size_t n = 0;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  void ensure(size_t want) {
+    if (want <= n) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    want = std::max<size_t>(want, 256);
+    CK(cudaMalloc(&p, want));
+    n = want;
+  }
+  template <typename T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+struct HostBuf {  // pinned
+  void* p = nullptr;
+  size_t n = 0;
+  ~HostBuf() {
+    if (p) cudaFreeHost(p);
+  }
+  void ensure(size_t want) {
+    if (want <= n) return;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    n = 0;
+    want = std::max<size_t>(want, 256);
+    CK(cudaMallocHost(&p, want));
+    n = want;
+  }
+  template <typename T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+inline uint64_t align16(uint64_t v) { return (v + 15) & ~uint64_t(15); }
+
+// ---------------------------------------------------------------- graph
+struct MapStep {
+  int32_t kind;
+  uint32_t node_id;     // the (possibly fused) map node, for error messages
+  uint32_t seed_op_id;  // original op id (fuse_maps, pipeline.cpp:148-168)
+  json params;
+};
+
+struct Graph {
+  uint64_t base_seed = 0;
+  bool drop_remainder = true;
+  uint32_t source_id = 0, batch_id = 0;
+  uint32_t batch_size = 1;
+  std::vector<MapStep> maps;
+};
+
+int32_t map_kind_from_name(const std::string& n) {  // transforms.cpp:54-66 + App. C
+  static const std::map<std::string, int32_t> m = {
+      {"normalize", kNormalize}, {"translate", kTranslate}, {"jitter", kJitter},
+      {"rotate", kRotate}, {"random_scale", kRandomScale}, {"flip_yz", kFlipYz},
+      {"color_augment", kColorAugment}, {"random_crop", kRandomCrop},
+      {"downsample", kDownsample}, {"fps", kFps}, {"voxel", kVoxel},
+      {"grid_subsample", kVoxel}, {"range_crop", kRangeCrop}};
+  auto it = m.find(n);
+  if (it == m.end()) fail(kUnknownOp, "unknown map '" + n + "'");
+  return it->second;
+}
+
+Graph parse_graph(const std::string& text) {
+  json j = json::parse(text, nullptr, false);
+  if (j.is_discarded()) fail(kUnknownOp, "graph is not valid JSON");
+  Graph g;
+  struct Node {
+    uint32_t id;
+    std::string kind;
+    uint32_t workers, queue, batch;
+    std::vector<MapStep> steps;
+  };
+  std::vector<Node> nodes;
+  try {
+    g.base_seed = j.value("base_seed", uint64_t{0});
+    g.drop_remainder = j.value("drop_remainder", true);
+    for (const auto& o : j.at("ops")) {
+      Node n;
+      n.id = o.at("id").get<uint32_t>();
+      n.kind = o.at("kind").get<std::string>();
+      if (n.kind != "source" && n.kind != "map" && n.kind != "batch" && n.kind != "sink")
+        fail(kUnknownOp, "op kind '" + n.kind + "'");
+      n.workers = o.value("num_workers", 1u);
+      n.queue = o.value("queue_capacity", 8u);
+      n.batch = o.value("batch_size", 1u);
+      if (n.kind == "map") {
+        if (o.contains("fused")) {
+          for (const auto& f : o["fused"])
+            n.steps.push_back({map_kind_from_name(f.at("map").get<std::string>()), n.id,
+                               f.at("op_id").get<uint32_t>(), f.value("params", json::object())});
+        } else {
+          n.steps.push_back({map_kind_from_name(o.at("map").get<std::string>()), n.id, n.id,
+                             o.value("params", json::object())});
+        }
+      }
+      nodes.push_back(std::move(n));
+    }
+  } catch (const json::exception& e) {
+    fail(kUnknownOp, std::string("malformed graph: ") + e.what());
+  }
+  // PipelineGraph::validate (:40-80)
+  if (nodes.size() < 3) fail(kUnknownOp, "graph needs source, batch, sink");
+  if (nodes.front().kind != "source") fail(kUnknownOp, "first node must be a source");
+  if (nodes.back().kind != "sink") fail(kUnknownOp, "last node must be a sink");
+  bool batch_seen = false;
+  for (size_t i = 0; i < nodes.size(); ++i) {
+    const auto& n = nodes[i];
+    for (size_t k = 0; k < i; ++k)
+      if (nodes[k].id == n.id) fail(kUnknownOp, "duplicate op id");
+    if (n.workers < 1 || n.queue < 1) fail(kOutOfBounds, "workers and queue capacity must be >= 1");
+    if (n.kind == "source" && i != 0) fail(kUnknownOp, "source must come first");
+    if (n.kind == "map") {
+      if (batch_seen) fail(kUnknownOp, "map after batch");
+      if (n.steps.empty()) fail(kUnknownOp, "map without transform");
+      for (const auto& s : n.steps) g.maps.push_back(s);
+    }
+    if (n.kind == "batch") {
+      if (batch_seen) fail(kUnknownOp, "more than one batch node");
+      if (n.batch < 1) fail(kOutOfBounds, "batch_size must be >= 1");
+      batch_seen = true;
+      g.batch_size = n.batch;
+      g.batch_id = n.id;
+    }
+    if (n.kind == "sink" && i + 1 != nodes.size()) fail(kUnknownOp, "sink must come last");
+  }
+  if (!batch_seen) fail(kUnknownOp, "graph needs a batch node");
+  g.source_id = nodes.front().id;
+  if (g.maps.size() > (size_t)kMaxOps) fail(kOutOfBounds, "too many map transforms for one stage");
+  return g;
+}
+
+// Map params JSON → OpDesc (transforms.cpp:103-113,171-172,273 + App. C).
+// busy_us / sleep_us are CPU cost-injection knobs of the reference
+// (transforms.cpp:103-113); they have no meaning on the device and are ignored.
+template <typename IndexOf>
+void parse_op_params(OpDesc& op, const json& p, IndexOf bytes_index_of) {
+  if (!p.is_object() && !p.is_null()) fail(kUnknownOp, "map params must be an object");
+  try {
+    if (p.is_object()) {
+      if (p.contains("theta")) {
+        op.has_theta = 1;
+        op.theta = p["theta"].get<float>();
+      }
+      if (p.contains("num_points")) op.num_points = p["num_points"].get<int64_t>();
+      if (p.contains("gather")) {
+        for (const auto& nm : p["gather"]) {
+          const int bi = bytes_index_of(nm.get<std::string>());
+          if (bi < 0) fail(kMissingField, "gather field '" + nm.get<std::string>() + "' is not a bytes field");
+          op.gather_mask |= 1u << bi;
+        }
+      }
+      if (p.contains("voxel_size")) op.voxel = p["voxel_size"].get<float>();
+      if (p.contains("origin")) {
+        op.has_origin = 1;
+        for (int i = 0; i < 3; ++i) op.origin[i] = p["origin"][i].get<float>();
+      }
+      op.counts = p.value("counts", op.kind == kVoxel ? 1 : 0);
+      if (p.contains("lo"))
+        for (int i = 0; i < 3; ++i) op.lo[i] = p["lo"][i].get<float>();
+      if (p.contains("hi"))
+        for (int i = 0; i < 3; ++i) op.hi[i] = p["hi"][i].get<float>();
+    }
+  } catch (const json::exception& e) {
+    fail(kOutOfBounds, std::string("bad map params: ") + e.what());
+  }
+  if ((op.kind == kDownsample || op.kind == kFps) && op.num_points <= 0)
+    fail(kOutOfBounds, "num_points must be positive");
+  if (op.kind == kVoxel) fail(kUnknownOp, "voxel/grid_subsample is not in this build yet");
+}
+
+// Per-device state for the stateless entry points (codec + operator API).
+struct DeviceCtx {
+  int sms = 0;
+  DevBuf shift, scratch;
+};
+DeviceCtx& device_ctx(cudaStream_t st) {
+  static std::mutex mu;
+  static std::map<int, std::unique_ptr<DeviceCtx>> ctxs;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  auto& c = ctxs[dev];
+  if (!c) {
+    c = std::make_unique<DeviceCtx>();
+    c->sms = require_device(dev);
+    upload_x2n(st);
+    std::vector<uint32_t> shift(kShiftEntries);
+    build_shift_table(shift.data());
+    c->shift.ensure(shift.size() * 4);
+    CK(cudaMemcpy(c->shift.p, shift.data(), shift.size() * 4, cudaMemcpyHostToDevice));
+  }
+  return *c;
+}
+
+// ---------------------------------------------------------------- pipeline
+struct OutField {
+  std::string name;
+  int32_t kind;        // value kind of the batch field
+  int32_t schema_idx;  // schema field, or -1 for synthesized fields
+  uint64_t stride;     // slot bytes per sample
+};
+
+struct Wave {
+  uint64_t epoch = 0;
+  uint64_t pos0 = 0, n = 0;  // positions [pos0, pos0+n) of the epoch
+  uint64_t first_batch = 0;  // batch index of the wave's first batch
+  uint32_t n_batches = 0;
+  bool launched = false;
+  cudaEvent_t done = nullptr, k0 = nullptr, k1 = nullptr;
+  // device
+  DevBuf bytes_stage, raw, tables, outs, compact, compact_meta;
+  HostBuf h_tables, h_res, h_compact_meta;
+  std::vector<uint64_t> out_base;  // per output field: offset in outs
+  // results (pinned, filled by D2H)
+  int32_t* h_status = nullptr;
+  int32_t* h_op = nullptr;
+  int32_t* h_where = nullptr;
+  uint64_t* h_len = nullptr;
+  uint64_t in_payload_bytes = 0, in_points = 0;
+  std::vector<std::vector<uint64_t>> offsets;  // per field, for the served batch
+};
+
+}  // namespace
+
+struct Pipeline {
+  int device = 0, sms = 0;
+  Graph g;
+  Header h;
+  std::string dir;
+  std::vector<Entry> index, walk;
+  bool resident = true;
+  uint32_t wave_batches = 0;
+  uint64_t epochs = 1;
+  bool force_serial_fy = false;
+  cudaStream_t stream = nullptr;        // wave compute (copies + kernels)
+  cudaStream_t serve_stream = nullptr;  // batch views: compaction, user D2H
+  // byte store: all slice data areas, 16-B aligned, 64 B slack each side
+  std::vector<uint64_t> slice_base;
+  uint64_t store_bytes = 0;
+  DevBuf d_store;
+  HostBuf h_store;
+  DevBuf d_shift, d_gscratch;
+  // page heads: [group] -> scalar, block
+  std::vector<PageHead> scalar_head, block_head;
+  bool block_tiles_payload_ok = true;
+  // schema / outputs
+  std::vector<int32_t> bytes_fields;  // schema index per bytes field
+  std::vector<OutField> outs;
+  WaveArgs proto{};
+  int threads = 512, grid = 0;
+  size_t smem = 0;
+  // iteration
+  std::vector<Wave> slots;
+  std::vector<std::pair<uint64_t, uint64_t>> plan;  // (epoch, pos0) of waves
+  std::vector<uint64_t> plan_n;
+  size_t next_plan = 0;  // next wave to launch
+  int cur = -1;          // slot being served
+  uint32_t served = 0;   // batches served from cur
+  bool failed = false;
+  int32_t fail_code = 0;
+  std::string fail_msg;
+  std::string stats_json;
+  // stats
+  uint64_t clouds = 0, points_in = 0, payload_bytes = 0, batches = 0;
+  uint64_t h2d_bytes = 0, launches = 0, alg_bytes = 0;
+  double kernel_ms = 0, cloud_kernel_ms = 0;
+  uint32_t waves_done = 0;
+
+  ~Pipeline() {
+    for (auto& w : slots) {
+      if (w.done) cudaEventDestroy(w.done);
+      if (w.k0) cudaEventDestroy(w.k0);
+      if (w.k1) cudaEventDestroy(w.k1);
+    }
+    if (stream) cudaStreamDestroy(stream);
+    if (serve_stream) cudaStreamDestroy(serve_stream);
+  }
+
+  void open(const std::string& primary, const std::string& graph_json, const uint64_t* ids,
+            uint64_t n_ids, int dev, const std::string& options) {
+    sms = require_device(dev);
+    device = dev;
+    g = parse_graph(graph_json);
+    if (!options.empty()) {
+      json o = json::parse(options, nullptr, false);
+      if (o.is_discarded()) fail(kOutOfBounds, "options are not valid JSON");
+      epochs = o.value("epochs", uint64_t{1});
+      resident = o.value("resident", true);
+      wave_batches = o.value("wave_batches", 0u);
+      force_serial_fy = o.value("force_serial_fy", false);
+    }
+    h = read_header(primary);
+    dir = fs::path(primary).parent_path().string();
+    index = build_index(h);
+    if (ids) {
+      for (uint64_t i = 0; i < n_ids; ++i) {
+        if (ids[i] >= index.size()) fail(kOutOfRange, "sample id " + std::to_string(ids[i]));
+        walk.push_back(index[ids[i]]);
+      }
+    } else {
+      walk = index;
+    }
+    if (walk.empty()) fail(kEmptyDataset, "no samples");
+    CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&serve_stream, cudaStreamNonBlocking));
+    load_store();
+    plan_schema();
+    plan_waves();
+    upload_x2n(stream);
+    std::vector<uint32_t> shift(kShiftEntries);
+    build_shift_table(shift.data());
+    d_shift.ensure(shift.size() * 4);
+    CK(cudaMemcpyAsync(d_shift.p, shift.data(), shift.size() * 4, cudaMemcpyHostToDevice, stream));
+    CK(cudaStreamSynchronize(stream));
+    slots.resize(2);
+    for (auto& w : slots) {
+      CK(cudaEventCreate(&w.done));
+      CK(cudaEventCreate(&w.k0));
+      CK(cudaEventCreate(&w.k1));
+    }
+  }
+
+  // Slice data areas → one byte store (HBM when resident, pinned host else).
+  void load_store() {
+    slice_base.resize(h.slice_paths.size());
+    std::vector<std::vector<uint8_t>> data(h.slice_paths.size());
+    uint64_t at = 64;
+    for (uint32_t s = 0; s < h.slice_paths.size(); ++s) {
+      data[s] = read_slice_data(h, dir, s);
+      slice_base[s] = at;
+      at = align16(at + data[s].size()) + 64;
+    }
+    store_bytes = at;
+    h_store.ensure(store_bytes);
+    std::memset(h_store.p, 0, 64);
+    for (uint32_t s = 0; s < data.size(); ++s) {
+      std::memcpy(h_store.as<uint8_t>() + slice_base[s], data[s].data(), data[s].size());
+    }
+    // page heads (EncodedPage::deserialize of both pages per group)
+    scalar_head.resize(h.groups.size());
+    block_head.resize(h.groups.size());
+    for (size_t gi = 0; gi < h.groups.size(); ++gi) {
+      const Group& gr = h.groups[gi];
+      const uint8_t* base = h_store.as<uint8_t>() + slice_base[gr.slice];
+      const uint64_t avail_s = data[gr.slice].size() - std::min<uint64_t>(gr.scalar_off, data[gr.slice].size());
+      const uint64_t avail_b = data[gr.slice].size() - std::min<uint64_t>(gr.block_off, data[gr.slice].size());
+      scalar_head[gi] = parse_page_head(base + gr.scalar_off, std::min(avail_s, gr.scalar_len));
+      block_head[gi] = parse_page_head(base + gr.block_off, std::min(avail_b, gr.block_len));
+    }
+    if (resident) {
+      d_store.ensure(store_bytes);
+      CK(cudaMemcpyAsync(d_store.p, h_store.p, store_bytes, cudaMemcpyHostToDevice, stream));
+      CK(cudaStreamSynchronize(stream));
+    }
+  }
+
+  int bytes_index_of(const std::string& name) const {
+    for (size_t k = 0; k < bytes_fields.size(); ++k)
+      if (h.schema[bytes_fields[k]].name == name) return (int)k;
+    return -1;
+  }
+
+  void plan_schema() {
+    WaveArgs& a = proto;
+    std::memset(&a, 0, sizeof(a));
+    if (h.schema.size() > (size_t)kMaxFields) fail(kOutOfBounds, "too many schema fields");
+    a.n_fields = (int32_t)h.schema.size();
+    for (size_t f = 0; f < h.schema.size(); ++f) {
+      a.fields[f].kind = h.schema[f].kind;
+      a.fields[f].elems = h.schema[f].elems();
+      a.fields[f].bytes_index = -1;
+      if (h.schema[f].kind == kBytes) {
+        a.fields[f].bytes_index = (int32_t)bytes_fields.size();
+        bytes_fields.push_back((int32_t)f);
+      }
+    }
+    if (bytes_fields.size() > (size_t)kMaxBytesFields) fail(kOutOfBounds, "too many bytes fields");
+    a.n_bytes_fields = (int32_t)bytes_fields.size();
+    a.role_data = bytes_index_of("data");
+    a.role_normal = bytes_index_of("normal");
+    a.role_color = bytes_index_of("color");
+    a.role_intensity = bytes_index_of("intensity");
+    // ops
+    a.n_ops = (int32_t)g.maps.size();
+    a.base_seed = g.base_seed;
+    uint32_t gather_all = 0;
+    uint64_t max_target = 0;
+    for (size_t k = 0; k < g.maps.size(); ++k) {
+      OpDesc& op = a.ops[k];
+      const MapStep& m = g.maps[k];
+      op.kind = m.kind;
+      op.seed_op_id = m.seed_op_id;
+      parse_op_params(op, m.params, [&](const std::string& nm) { return bytes_index_of(nm); });
+      gather_all |= op.gather_mask;
+      max_target = std::max<uint64_t>(max_target, op.num_points > 0 ? (uint64_t)op.num_points : 0);
+    }
+    // tracked fields: point-cloud roles + gathered extras (only with ops)
+    uint32_t tracked = 0;
+    if (a.n_ops) {
+      for (int r : {a.role_data, a.role_normal, a.role_color, a.role_intensity})
+        if (r >= 0) tracked |= 1u << r;
+      tracked |= gather_all;
+    }
+    a.tracked_mask = tracked;
+    // capacities from the header's blob lengths
+    std::vector<uint64_t> max_len(bytes_fields.size(), 0);
+    uint64_t max_blob = 0, max_pts = 0;
+    std::vector<uint32_t> ext_elem(bytes_fields.size(), 1);
+    for (const auto& gr : h.groups)
+      for (uint32_t r = 0; r < gr.sample_count; ++r) {
+        const auto& L = gr.blob_lens[r];
+        max_blob = std::max<uint64_t>(max_blob, gr.blob_ranges[r][1] - gr.blob_ranges[r][0]);
+        const uint64_t nd = (a.role_data >= 0 && a.role_data < (int)L.size()) ? L[a.role_data] / 12 : 0;
+        max_pts = std::max(max_pts, nd);
+        for (size_t f = 0; f < L.size() && f < max_len.size(); ++f) {
+          max_len[f] = std::max(max_len[f], L[f]);
+          const uint64_t e = nd ? (L[f] + nd - 1) / nd : L[f];
+          ext_elem[f] = std::max<uint32_t>(ext_elem[f], (uint32_t)std::max<uint64_t>(1, e));
+        }
+      }
+    uint64_t cap = std::max<uint64_t>(max_pts, max_target);
+    for (size_t f = 0; f < bytes_fields.size(); ++f) {
+      if (!((tracked >> f) & 1u)) continue;
+      uint32_t e = 1;
+      if ((int)f == a.role_data || (int)f == a.role_normal || (int)f == a.role_color) e = 12;
+      else if ((int)f == a.role_intensity) e = 4;
+      else e = ext_elem[f];
+      a.field_cap[f] = e;
+      cap = std::max<uint64_t>(cap, (max_len[f] + e - 1) / e);
+    }
+    cap = std::max<uint64_t>(cap, 1);
+    if (cap > (1u << 30)) fail(kOutOfBounds, "cloud too large");
+    a.cap_points = (uint32_t)cap;
+    a.max_blob = (uint32_t)max_blob;
+    // static size analysis per tracked field: 0 = input size, 1 = fixed T,
+    // 2 = data dependent (crop / voxel)
+    std::vector<int> state(bytes_fields.size(), 0);
+    std::vector<uint64_t> fixed_pts(bytes_fields.size(), 0);
+    for (size_t k = 0; k < g.maps.size(); ++k) {
+      const OpDesc& op = a.ops[k];
+      uint32_t moved = 0;
+      for (int r : {a.role_data, a.role_normal, a.role_color})
+        if (r >= 0) moved |= 1u << r;
+      if (op.kind == kFps || op.kind == kRangeCrop || op.kind == kVoxel || op.kind == kRandomCrop)
+        if (a.role_intensity >= 0) moved |= 1u << a.role_intensity;
+      moved |= op.gather_mask;
+      if (op.kind == kVoxel) moved = tracked;
+      for (size_t f = 0; f < bytes_fields.size(); ++f) {
+        if (!((moved >> f) & 1u)) continue;
+        if (op.kind == kDownsample || op.kind == kFps) {
+          state[f] = 1;
+          fixed_pts[f] = (uint64_t)op.num_points;
+        } else if (op.kind == kRandomCrop || op.kind == kRangeCrop || op.kind == kVoxel) {
+          state[f] = 2;
+        }
+      }
+    }
+    // outputs in std::map (name) order
+    std::vector<int32_t> order(h.schema.size());
+    for (size_t f = 0; f < order.size(); ++f) order[f] = (int32_t)f;
+    std::sort(order.begin(), order.end(),
+              [&](int32_t x, int32_t y) { return h.schema[x].name < h.schema[y].name; });
+    for (int k = 0; k < kMaxBytesFields; ++k) a.bytes_out[k] = -1;
+    for (int32_t f : order) {
+      OutField o;
+      o.name = h.schema[f].name;
+      o.kind = h.schema[f].kind;
+      o.schema_idx = f;
+      const int bi = a.fields[f].bytes_index;
+      if (bi >= 0) {
+        if ((tracked >> bi) & 1u) {
+          const uint64_t e = a.field_cap[bi];
+          if (state[bi] == 1) o.stride = align16(fixed_pts[bi] * e);
+          else if (state[bi] == 2) o.stride = align16(cap * e);
+          else o.stride = align16(std::max<uint64_t>(max_len[bi], 1));
+        } else {
+          o.stride = align16(max_len[bi]);
+        }
+        a.bytes_out[bi] = (int32_t)outs.size();
+      } else if (h.schema[f].kind == kString) {
+        o.stride = 4096;
+      } else {
+        const uint64_t es = (h.schema[f].kind == kInt64 || h.schema[f].kind == kFloat64) ? 8 : 4;
+        o.stride = align16(es * h.schema[f].elems());
+      }
+      o.stride = std::max<uint64_t>(o.stride, 16);
+      a.fields[f].out_index = (int32_t)outs.size();
+      outs.push_back(o);
+    }
+    if (outs.size() > (size_t)PCP_MAX_BATCH_FIELDS) fail(kOutOfBounds, "too many batch fields");
+    a.n_out = (int32_t)outs.size();
+    // shared-memory plan for k_cloud
+    auto rnd = [](uint64_t v) { return (v + 127) & ~uint64_t(127); };
+    uint64_t need = rnd(a.max_blob + 64) + 4 * rnd((uint64_t)cap * 4 + 16);
+    for (size_t f = 0; f < bytes_fields.size(); ++f)
+      if ((tracked >> f) & 1u) need += 2 * rnd((uint64_t)cap * a.field_cap[f] + 16);
+    const size_t fixed = cloud_smem_fixed();
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    const size_t limit = prop.sharedMemPerBlockOptin;
+    a.smem_mode = (fixed + need <= limit) ? 1 : 0;
+    smem = a.smem_mode ? fixed + need : fixed;
+    CK(set_cloud_smem(smem));
+    int per_sm = 0;
+    CK(occupancy_cloud(&per_sm, threads, smem));
+    grid = std::max(1, per_sm) * sms;
+    if (!a.smem_mode) {
+      uint64_t per = 4 * rnd((uint64_t)cap * 4 + 16);
+      for (size_t f = 0; f < bytes_fields.size(); ++f)
+        if ((tracked >> f) & 1u) per += 2 * rnd((uint64_t)cap * a.field_cap[f] + 16);
+      a.gscratch_per_cta = per;
+      d_gscratch.ensure(per * grid);
+      a.gscratch = d_gscratch.as<uint8_t>();
+    }
+    a.force_serial_fy = force_serial_fy ? 1 : 0;
+  }
+
+
+  void plan_waves() {
+    const uint64_t n = walk.size();
+    const uint32_t B = g.batch_size;
+    uint32_t wb = wave_batches;
+    if (!wb) wb = (uint32_t)std::max<uint64_t>(1, 8192 / B);
+    const uint64_t W = (uint64_t)wb * B;
+    const uint64_t usable = g.drop_remainder ? (n / B) * B : n;
+    for (uint64_t e = 0; e < epochs; ++e)
+      for (uint64_t p = 0; p < usable; p += W) {
+        plan.push_back({e, p});
+        plan_n.push_back(std::min<uint64_t>(W, usable - p));
+      }
+  }
+
+  // ---- wave construction ---------------------------------------------------
+  void launch(Wave& w, size_t pi) {
+    w.epoch = plan[pi].first;
+    w.pos0 = plan[pi].second;
+    w.n = plan_n[pi];
+    const uint32_t B = g.batch_size;
+    w.first_batch = w.pos0 / B;
+    w.n_batches = (uint32_t)((w.n + B - 1) / B);
+    WaveArgs a = proto;
+    // groups touched, in first-use order
+    std::map<uint32_t, uint32_t> gmap;  // header group index -> wave group
+    std::vector<uint32_t> groups;
+    std::vector<uint32_t> rows_seen;  // per wave group: bitmap count check
+    std::vector<std::vector<uint32_t>> hits;
+    for (uint64_t k = 0; k < w.n; ++k) {
+      const Entry& e = walk[w.pos0 + k];
+      auto it = gmap.find(e.group_index);
+      if (it == gmap.end()) {
+        gmap.emplace(e.group_index, (uint32_t)groups.size());
+        groups.push_back(e.group_index);
+        hits.emplace_back(h.groups[e.group_index].sample_count, 0);
+      }
+      hits[gmap[e.group_index]][e.row]++;
+    }
+    const uint32_t ng = (uint32_t)groups.size();
+    // pages: [0, ng) scalar, [ng, 2ng) block
+    std::vector<PageRef> pages(2 * ng);
+    std::vector<GroupWork> gw(ng);
+    std::vector<uint32_t> todo;
+    std::vector<CrcWindow> wins;
+    uint64_t raw_at = 0, vals_at = 0;
+    uint32_t rec_at = 0;
+    // staged mode: copy the wave's pages into a device staging buffer
+    std::vector<std::pair<uint64_t, uint64_t>> runs;  // (store off, len)
+    auto page_src = [&](uint32_t slice, uint64_t off) { return slice_base[slice] + off; };
+    uint64_t stage_at = 64;
+    std::vector<uint64_t> stage_off(2 * ng);
+    for (uint32_t i = 0; i < ng; ++i) {
+      const Group& gr = h.groups[groups[i]];
+      for (int kind = 0; kind < 2; ++kind) {
+        const uint64_t so = page_src(gr.slice, kind ? gr.block_off : gr.scalar_off);
+        const uint64_t len = kind ? gr.block_len : gr.scalar_len;
+        if (!resident) {
+          stage_off[kind * ng + i] = stage_at + (so & 15);
+          runs.push_back({so & ~uint64_t(15), align16((so & 15) + len)});
+          stage_at += align16((so & 15) + len) + 64;
+        } else {
+          stage_off[kind * ng + i] = so;
+        }
+      }
+    }
+    for (uint32_t i = 0; i < ng; ++i) {
+      const uint32_t gi = groups[i];
+      const Group& gr = h.groups[gi];
+      const PageHead& sh = scalar_head[gi];
+      const PageHead& bh = block_head[gi];
+      PageRef& sp = pages[i];
+      sp.off = stage_off[i];
+      sp.raw_len = sh.raw_len;
+      sp.pay_len = sh.pay_len;
+      sp.crc = sh.crc;
+      sp.flags = sh.flags;
+      sp.raw_dst = raw_at;
+      raw_at = align16(raw_at + sh.raw_len) + 16;
+      sp.crc_mode = 0;
+      todo.push_back(i);
+      PageRef& bp = pages[ng + i];
+      bp.off = stage_off[ng + i];
+      bp.raw_len = bh.raw_len;
+      bp.pay_len = bh.pay_len;
+      bp.crc = bh.crc;
+      bp.flags = bh.flags;
+      bp.raw_dst = ~uint64_t(0);
+      if (bh.flags & kFlagOuterLz4) {
+        bp.raw_dst = raw_at;
+        raw_at = align16(raw_at + bh.raw_len) + 16;
+        todo.push_back(ng + i);
+      }
+      // fused CRC only when this wave's samples tile the stored-raw payload
+      // exactly once
+      bool fused = !(bh.flags & kFlagOuterLz4) && bh.pay_len == bh.raw_len;
+      uint64_t at = 0;
+      for (uint32_t r = 0; fused && r < gr.sample_count; ++r) {
+        if (hits[i][r] != 1 || gr.blob_ranges[r][0] != at) fused = false;
+        at = gr.blob_ranges[r][1];
+      }
+      if (at != bh.raw_len) fused = false;
+      bp.crc_mode = fused ? 1 : 0;
+      for (uint32_t kind = 0; kind < 2; ++kind) {
+        const PageRef& p = pages[kind * ng + i];
+        if (kind == 1 && p.crc_mode == 1) continue;
+        const uint64_t pay0 = p.off + kPageHeaderBytes;
+        const uint64_t win = 65536;
+        for (uint64_t end = p.pay_len; end > 0;) {
+          const uint64_t st = end > win ? end - win : 0;
+          wins.push_back({pay0 + st, end - st, p.pay_len - end, kind * ng + i, 0});
+          end = st;
+        }
+      }
+      gw[i].scalar_page = i;
+      gw[i].first_rec = rec_at;
+      gw[i].n_rows = gr.sample_count;
+      gw[i].vals_base = (uint32_t)vals_at;
+      rec_at += gr.sample_count;
+      // value bytes per row: fixed fields + strings (bounded by the page)
+      uint64_t fixed = 0;
+      bool has_string = false;
+      for (const auto& f : h.schema) {
+        if (f.kind == kBytes) continue;
+        if (f.kind == kString) { has_string = true; fixed += 4; continue; }
+        fixed += ((f.kind == kInt64 || f.kind == kFloat64) ? 8 : 4) * (uint64_t)f.elems();
+      }
+      vals_at += fixed * gr.sample_count + (has_string ? sh.raw_len : 0);
+      vals_at = align16(vals_at);
+    }
+    std::vector<SampleWork> sw(w.n);
+    w.in_payload_bytes = 0;
+    w.in_points = 0;
+    for (uint64_t k = 0; k < w.n; ++k) {
+      const Entry& e = walk[w.pos0 + k];
+      SampleWork& s = sw[k];
+      s.epoch = w.epoch;
+      s.index = w.pos0 + k;
+      s.blob_start = e.blob_start;
+      s.blob_end = e.blob_end;
+      s.group = gmap[e.group_index];
+      s.scalar_page = s.group;
+      s.block_page = ng + s.group;
+      s.row = e.row;
+      w.in_payload_bytes += e.blob_end - e.blob_start;
+      const auto& L = h.groups[e.group_index].blob_lens[e.row];
+      if (a.role_data >= 0 && a.role_data < (int)L.size()) w.in_points += L[a.role_data] / 12;
+    }
+    // ---- pack tables into one pinned blob, one H2D copy ---------------------
+    auto sz = [](uint64_t v) { return align16(v); };
+    const uint64_t o_pages = 0;
+    const uint64_t o_groups = o_pages + sz(pages.size() * sizeof(PageRef));
+    const uint64_t o_samples = o_groups + sz(gw.size() * sizeof(GroupWork));
+    const uint64_t o_todo = o_samples + sz(sw.size() * sizeof(SampleWork));
+    const uint64_t o_wins = o_todo + sz(todo.size() * 4);
+    const uint64_t up_bytes = o_wins + sz(wins.size() * sizeof(CrcWindow));
+    // device-only regions after the uploaded part
+    const uint64_t o_recs = up_bytes;
+    const uint64_t o_vals = o_recs + sz((uint64_t)rec_at * sizeof(ScalarRec));
+    const uint64_t o_acc = o_vals + sz(vals_at + 16);
+    const uint64_t o_pst = o_acc + sz(pages.size() * 4);
+    const uint64_t o_sst = o_pst + sz(pages.size() * 4);
+    const uint64_t o_sop = o_sst + sz(w.n * 4);
+    const uint64_t o_swh = o_sop + sz(w.n * 4);
+    const uint64_t o_len = o_swh + sz(w.n * 4);
+    const uint64_t total = o_len + sz(outs.size() * w.n * 8);
+    w.h_tables.ensure(up_bytes);
+    uint8_t* ht = w.h_tables.as<uint8_t>();
+    std::memcpy(ht + o_pages, pages.data(), pages.size() * sizeof(PageRef));
+    std::memcpy(ht + o_groups, gw.data(), gw.size() * sizeof(GroupWork));
+    std::memcpy(ht + o_samples, sw.data(), sw.size() * sizeof(SampleWork));
+    std::memcpy(ht + o_todo, todo.data(), todo.size() * 4);
+    std::memcpy(ht + o_wins, wins.data(), wins.size() * sizeof(CrcWindow));
+    w.tables.ensure(total);
+    uint8_t* dt = w.tables.as<uint8_t>();
+    // staged input bytes
+    const uint8_t* bytes = d_store.as<uint8_t>();
+    if (!resident) {
+      w.bytes_stage.ensure(stage_at + 64);
+      uint64_t d_at = 64;
+      for (const auto& r : runs) {
+        CK(cudaMemcpyAsync(w.bytes_stage.as<uint8_t>() + d_at, h_store.as<uint8_t>() + r.first,
+                           r.second, cudaMemcpyHostToDevice, stream));
+        d_at += r.second + 64;
+      }
+      bytes = w.bytes_stage.as<uint8_t>();
+      for (const auto& r : runs) h2d_bytes += r.second;
+    }
+    CK(cudaMemcpyAsync(dt, ht, up_bytes, cudaMemcpyHostToDevice, stream));
+    CK(cudaMemsetAsync(dt + o_acc, 0, o_len - o_acc, stream));
+    w.raw.ensure(raw_at + 64);
+    // outputs
+    w.out_base.resize(outs.size());
+    uint64_t out_total = 0;
+    for (size_t f = 0; f < outs.size(); ++f) {
+      w.out_base[f] = out_total;
+      out_total += align16(outs[f].stride * w.n) + 64;
+    }
+    w.outs.ensure(out_total);
+    // ---- args ----------------------------------------------------------------
+    a.bytes = bytes;
+    a.raw = w.raw.as<uint8_t>();
+    a.pages = reinterpret_cast<const PageRef*>(dt + o_pages);
+    a.n_pages = (uint32_t)pages.size();
+    a.groups = reinterpret_cast<const GroupWork*>(dt + o_groups);
+    a.n_groups = ng;
+    a.samples = reinterpret_cast<const SampleWork*>(dt + o_samples);
+    a.n_samples = (uint32_t)w.n;
+    a.recs = reinterpret_cast<ScalarRec*>(dt + o_recs);
+    a.vals = dt + o_vals;
+    a.page_crc_acc = reinterpret_cast<uint32_t*>(dt + o_acc);
+    a.page_status = reinterpret_cast<int32_t*>(dt + o_pst);
+    a.sample_status = reinterpret_cast<int32_t*>(dt + o_sst);
+    a.sample_op = reinterpret_cast<int32_t*>(dt + o_sop);
+    a.sample_where = reinterpret_cast<int32_t*>(dt + o_swh);
+    a.out_len = reinterpret_cast<uint64_t*>(dt + o_len);
+    a.shift_tab = d_shift.as<uint32_t>();
+    for (size_t f = 0; f < outs.size(); ++f) {
+      a.out[f] = w.outs.as<uint8_t>() + w.out_base[f];
+      a.out_stride[f] = outs[f].stride;
+    }
+    // ---- kernels ---------------------------------------------------------------
+    CK(launch_crc_windows(bytes, reinterpret_cast<const CrcWindow*>(dt + o_wins),
+                          (uint32_t)wins.size(), d_shift.as<uint32_t>(), a.page_crc_acc, sms, stream));
+    CK(launch_page_decode(bytes, a.raw, a.pages, reinterpret_cast<const uint32_t*>(dt + o_todo),
+                          (uint32_t)todo.size(), a.page_status, stream));
+    CK(launch_wave(a, grid, threads, smem, stream, w.k0, w.k1));
+    launches += (wins.empty() ? 0 : 1) + (todo.empty() ? 0 : 1) + (ng ? 1 : 0) + 1 + 1 + 1;
+    h2d_bytes += up_bytes;
+    // ---- results back to pinned host -------------------------------------------
+    const uint64_t res = 3 * align16(w.n * 4) + outs.size() * w.n * 8;
+    w.h_res.ensure(res);
+    uint8_t* hr = w.h_res.as<uint8_t>();
+    w.h_status = reinterpret_cast<int32_t*>(hr);
+    w.h_op = reinterpret_cast<int32_t*>(hr + align16(w.n * 4));
+    w.h_where = reinterpret_cast<int32_t*>(hr + 2 * align16(w.n * 4));
+    w.h_len = reinterpret_cast<uint64_t*>(hr + 3 * align16(w.n * 4));
+    CK(cudaMemcpyAsync(w.h_status, dt + o_sst, w.n * 4, cudaMemcpyDeviceToHost, stream));
+    CK(cudaMemcpyAsync(w.h_op, dt + o_sop, w.n * 4, cudaMemcpyDeviceToHost, stream));
+    CK(cudaMemcpyAsync(w.h_where, dt + o_swh, w.n * 4, cudaMemcpyDeviceToHost, stream));
+    CK(cudaMemcpyAsync(w.h_len, dt + o_len, outs.size() * w.n * 8, cudaMemcpyDeviceToHost, stream));
+    CK(cudaEventRecord(w.done, stream));
+    w.launched = true;
+  }
+
+  std::string op_message(int32_t st, int32_t op, int32_t where) const {
+    uint32_t node = g.source_id;
+    if (op >= 1 && op <= (int32_t)g.maps.size()) node = g.maps[op - 1].node_id;
+    std::string what;
+    switch (st) {
+      case kChecksumMismatch: what = "block page checksum"; break;
+      case kCorruptPage: what = where ? "corrupt page (lz4 stream / stored length)" : "record truncated"; break;
+      case kRangeOutOfBounds: what = "blob range outside block page"; break;
+      case kMissingField: what = "sample has no usable coordinates / missing field"; break;
+      case kEmptyCloud: what = "zero points"; break;
+      case kOutOfBounds: what = "index or size out of bounds"; break;
+      case kUnknownOp: what = "unknown map"; break;
+      default: what = "device failure"; break;
+    }
+    return "op " + std::to_string(node) + ": " + errc_name(st) + ": " + what;
+  }
+
+  // ---- iteration -------------------------------------------------------------
+  int next_batch(pcp_batch* out, int* eos) {
+    *eos = 0;
+    if (failed) fail(fail_code, fail_msg);
+    if (cur < 0 || served >= slots[cur].n_batches) {
+      if (cur >= 0) ++waves_done;
+      if (next_plan >= plan.size() && !(next_plan < plan.size())) {
+        // nothing prefetched beyond?  check whether the other slot is in flight
+      }
+      const int nxt = cur < 0 ? 0 : 1 - cur;
+      Wave& wn = slots[nxt];
+      if (!wn.launched) {
+        if (next_plan >= plan.size()) {
+          *eos = 1;
+          return kOk;
+        }
+        launch(wn, next_plan++);
+      }
+      CK(cudaEventSynchronize(wn.done));
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, wn.k0, wn.k1));
+      cloud_kernel_ms += ms;
+      if (cur >= 0) slots[cur].launched = false;
+      cur = nxt;
+      served = 0;
+      clouds += wn.n;
+      for (size_t f = 0; f < outs.size(); ++f)
+        for (uint64_t k = 0; k < wn.n; ++k) alg_bytes += wn.h_len[f * wn.n + k];
+      alg_bytes += wn.in_payload_bytes;
+      points_in += wn.in_points;
+      payload_bytes += wn.in_payload_bytes;
+      // prefetch the following wave into the slot we just left
+      if (next_plan < plan.size()) launch(slots[1 - cur], next_plan++);
+    }
+    Wave& w = slots[cur];
+    const uint32_t B = g.batch_size;
+    const uint64_t s0 = (uint64_t)served * B;
+    const uint64_t s1 = std::min<uint64_t>(s0 + B, w.n);
+    const uint32_t nb = (uint32_t)(s1 - s0);
+    for (uint64_t s = s0; s < s1; ++s)
+      if (w.h_status[s] != kOk) {
+        failed = true;
+        fail_code = kWorkerPanic;
+        fail_msg = op_message(w.h_status[s], w.h_op[s], w.h_where[s]);
+        fail(fail_code, fail_msg);
+      }
+    std::memset(out, 0, sizeof(*out));
+    out->epoch = w.epoch;
+    out->batch_index = w.first_batch + served;
+    out->n_samples = nb;
+    out->n_fields = (uint32_t)outs.size();
+    w.offsets.assign(outs.size(), std::vector<uint64_t>(nb + 1, 0));
+    {  // per-field CSR buffers for ragged batches live back to back in w.compact
+      uint64_t need = 0;
+      for (size_t q = 0; q < outs.size(); ++q) need += align16(outs[q].stride * B) + 64;
+      w.compact.ensure(need);
+      w.compact_meta.ensure(2 * (uint64_t)(B + 1) * 8 * outs.size());
+      w.h_compact_meta.ensure(2 * (uint64_t)(B + 1) * 8 * outs.size());
+    }
+    for (size_t f = 0; f < outs.size(); ++f) {
+      pcp_field& pf = out->fields[f];
+      std::snprintf(pf.name, sizeof(pf.name), "%s", outs[f].name.c_str());
+      pf.kind = outs[f].kind;
+      auto& off = w.offsets[f];
+      bool dense = true;
+      for (uint32_t k = 0; k < nb; ++k) {
+        const uint64_t L = w.h_len[f * w.n + s0 + k];
+        off[k + 1] = off[k] + L;
+        if (L != outs[f].stride) dense = false;
+      }
+      bool uniform = true;
+      for (uint32_t k = 1; k < nb; ++k)
+        if (w.h_len[f * w.n + s0 + k] != w.h_len[f * w.n + s0]) uniform = false;
+      pf.uniform = uniform ? 1 : 0;
+      pf.nbytes = off[nb];
+      pf.h_offsets = off.data();
+      uint8_t* slot0 = w.outs.as<uint8_t>() + w.out_base[f] + s0 * outs[f].stride;
+      if (dense) {
+        pf.d_ptr = slot0;
+      } else {
+        // pack the batch's slots into CSR (one small kernel, synchronous)
+        const uint64_t meta = 2 * (nb + 1) * 8;
+        uint64_t* hm = w.h_compact_meta.as<uint64_t>() + 2 * (uint64_t)(B + 1) * f;
+        uint64_t* dm = w.compact_meta.as<uint64_t>() + 2 * (uint64_t)(B + 1) * f;
+        for (uint32_t k = 0; k < nb; ++k) {
+          hm[k] = off[k];
+          hm[nb + 1 + k] = off[k + 1] - off[k];
+        }
+        CK(cudaMemcpyAsync(dm, hm, meta, cudaMemcpyHostToDevice, serve_stream));
+        uint64_t base = 0;
+        for (size_t q = 0; q < f; ++q) base += align16(outs[q].stride * B) + 64;
+        uint8_t* dst = w.compact.as<uint8_t>() + base;
+        CK(launch_compact(slot0, outs[f].stride, dm, dm + nb + 1, nb, dst, serve_stream));
+        ++launches;
+        CK(cudaStreamSynchronize(serve_stream));
+        pf.d_ptr = dst;
+      }
+    }
+    ++served;
+    ++batches;
+    return kOk;
+  }
+
+  const char* stats() {
+    json j{{"clouds", clouds},
+           {"points_in", points_in},
+           {"payload_bytes", payload_bytes},
+           {"batches", batches},
+           {"waves", waves_done},
+           {"cloud_kernel_ms", cloud_kernel_ms},
+           {"cloud_kernel_alg_bytes", alg_bytes},
+           {"h2d_bytes", h2d_bytes},
+           {"launches", launches},
+           {"grid", grid},
+           {"threads", threads},
+           {"smem_bytes", smem},
+           {"smem_mode", proto.smem_mode},
+           {"cap_points", proto.cap_points},
+           {"resident", resident}};
+    stats_json = j.dump();
+    return stats_json.c_str();
+  }
+};
+
+
+}  // namespace pcp
+
+// =========================================================================
+// C ABI
+// =========================================================================
+using namespace pcp;
+
+extern "C" {
+
+struct pcp_pipeline {
+  pcp::Pipeline impl;
+};
+
+const char* pcp_last_error(void) { return g_err.c_str(); }
+
+const char* pcp_errc_name(int status) { return errc_name(status); }
+
+int pcp_device_info(int device, int* sm_count, int* cc_major, int* cc_minor) {
+  return guarded([&] {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) fail(kIoFailure, "no CUDA device");
+    cudaDeviceProp p;
+    CK(cudaGetDeviceProperties(&p, device));
+    *sm_count = p.multiProcessorCount;
+    *cc_major = p.major;
+    *cc_minor = p.minor;
+  });
+}
+
+uint64_t pcp_mix_seed(uint64_t base, uint64_t epoch, uint64_t index, uint64_t op) {
+  auto mix = [](uint64_t h, uint64_t v) {
+    h += 0x9e3779b97f4a7c15ull + v;
+    h = (h ^ (h >> 30)) * 0xbf58476d1ce4e5b9ull;
+    h = (h ^ (h >> 27)) * 0x94d049bb133111ebull;
+    return h ^ (h >> 31);
+  };
+  uint64_t h = mix(base, 0x706370ull);
+  h = mix(h, epoch);
+  h = mix(h, index);
+  return mix(h, op);
+}
+
+int pcp_map_kind_from_name(const char* name, int* kind) {
+  return guarded([&] { *kind = map_kind_from_name(name ? name : ""); });
+}
+
+int pcp_crc32_ranges(const uint8_t* d_bytes, const uint64_t* d_off, const uint64_t* d_len,
+                     uint32_t n, uint32_t* d_crc, void* stream) {
+  return guarded([&] {
+    auto st = (cudaStream_t)stream;
+    DeviceCtx& c = device_ctx(st);
+    CK(launch_crc_ranges(d_bytes, d_off, d_len, n, c.shift.as<uint32_t>(), d_crc, st));
+  });
+}
+
+int pcp_decode_pages(const uint8_t* d_bytes, const uint64_t* d_page_off, uint32_t n_pages,
+                     uint8_t* d_out, const uint64_t* d_out_off, const uint32_t* d_col_first,
+                     const uint64_t* d_col_off, const uint64_t* d_col_len, int32_t* d_status,
+                     void* stream) {
+  return guarded([&] {
+    auto st = (cudaStream_t)stream;
+    DeviceCtx& c = device_ctx(st);
+    CK(launch_decode_pages(d_bytes, d_page_off, n_pages, d_out, d_out_off, d_col_first, d_col_off,
+                           d_col_len, c.shift.as<uint32_t>(), d_status, st));
+  });
+}
+
+int pcp_apply_map(int kind, const char* params_json, const pcp_cloud_set* in,
+                  const pcp_cloud_out* out, const uint64_t* d_seeds, int32_t* d_status,
+                  void* stream) {
+  return guarded([&] {
+    auto st = (cudaStream_t)stream;
+    DeviceCtx& ctx = device_ctx(st);
+    if (!in || !out || !in->d_data) fail(kMissingField, "cloud set needs data");
+    const uint32_t n = in->n_clouds;
+    if (!n) return;
+    std::vector<uint64_t> off(n + 1);
+    CK(cudaMemcpyAsync(off.data(), in->d_offset, (n + 1) * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    uint64_t max_n = 0;
+    for (uint32_t i = 0; i < n; ++i) max_n = std::max<uint64_t>(max_n, off[i + 1] - off[i]);
+    WaveArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.set_mode = 1;
+    a.n_bytes_fields = kMaxBytesFields;
+    a.role_data = 0;
+    a.role_normal = in->d_normal ? 1 : -1;
+    a.role_color = in->d_color ? 2 : -1;
+    a.role_intensity = in->d_intensity ? 3 : -1;
+    const uint8_t* srcs[8] = {(const uint8_t*)in->d_data, (const uint8_t*)in->d_normal,
+                              (const uint8_t*)in->d_color, (const uint8_t*)in->d_intensity,
+                              in->d_extra[0], in->d_extra[1], in->d_extra[2], in->d_extra[3]};
+    uint8_t* dsts[8] = {(uint8_t*)out->d_data, (uint8_t*)out->d_normal, (uint8_t*)out->d_color,
+                        (uint8_t*)out->d_intensity, out->d_extra[0], out->d_extra[1],
+                        out->d_extra[2], out->d_extra[3]};
+    const uint32_t elems[8] = {12, 12, 12, 4, in->extra_elem[0], in->extra_elem[1],
+                               in->extra_elem[2], in->extra_elem[3]};
+    for (int f = 0; f < 8; ++f) {
+      if (!srcs[f]) continue;
+      if (elems[f] == 0) fail(kOutOfBounds, "extra field with zero element size");
+      a.tracked_mask |= 1u << f;
+      a.set_src[f] = srcs[f];
+      a.set_out[f] = dsts[f];
+      a.set_elem[f] = elems[f];
+      a.field_cap[f] = elems[f];
+    }
+    OpDesc& op = a.ops[0];
+    op.kind = kind;
+    json params = (params_json && *params_json) ? json::parse(params_json, nullptr, false) : json::object();
+    if (params.is_discarded()) fail(kOutOfBounds, "params are not valid JSON");
+    parse_op_params(op, params, [&](const std::string& nm) -> int {
+      static const char* names[8] = {"data", "normal", "color", "intensity",
+                                     "extra0", "extra1", "extra2", "extra3"};
+      for (int f = 0; f < 8; ++f)
+        if (nm == names[f] && srcs[f]) return f;
+      return -1;
+    });
+    if (kind != kNormalize && kind != kTranslate && kind != kJitter && kind != kRotate &&
+        kind != kRandomScale && kind != kFlipYz && kind != kColorAugment && kind != kRandomCrop &&
+        kind != kDownsample && kind != kFps && kind != kRangeCrop)
+      fail(kUnknownOp, "unknown map kind " + std::to_string(kind));
+    a.n_ops = 1;
+    a.cap_points = (uint32_t)std::max<uint64_t>({max_n, (uint64_t)std::max<int64_t>(op.num_points, 0), 1});
+    a.set_out_cap = out->cap_points;
+    a.n_samples = n;
+    a.set_offset = in->d_offset;
+    a.set_seeds = d_seeds;
+    a.set_count = out->d_count;
+    a.sample_status = d_status;
+    auto rnd = [](uint64_t v) { return (v + 127) & ~uint64_t(127); };
+    uint64_t need = rnd(64) + 4 * rnd((uint64_t)a.cap_points * 4 + 16);
+    for (int f = 0; f < 8; ++f)
+      if ((a.tracked_mask >> f) & 1u) need += 2 * rnd((uint64_t)a.cap_points * a.field_cap[f] + 16);
+    cudaDeviceProp prop;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaGetDeviceProperties(&prop, dev));
+    const size_t fixed = cloud_smem_fixed();
+    a.smem_mode = (fixed + need <= prop.sharedMemPerBlockOptin) ? 1 : 0;
+    const size_t smem = a.smem_mode ? fixed + need : fixed;
+    int grid = ctx.sms * 2;
+    if (!a.smem_mode) {
+      a.gscratch_per_cta = need;
+      grid = std::min<int>(grid, (int)n);
+      ctx.scratch.ensure(need * grid);
+      a.gscratch = ctx.scratch.as<uint8_t>();
+    }
+    CK(launch_apply_set(a, grid, 512, smem, st));
+  });
+}
+
+int pcp_write_dataset(const char* out_dir, const char* stem, const char* schema_json,
+                      const uint8_t* tlv, size_t tlv_len, uint32_t n_samples,
+                      uint32_t slice_count, uint32_t group_size, uint32_t n_threads) {
+  return guarded([&] {
+    const auto schema = schema_from_json(schema_json);
+    std::vector<SampleIn> samples(n_samples);
+    size_t pos = 0;
+    auto need = [&](size_t k) {
+      if (pos + k > tlv_len) fail(kSchemaMismatch, "sample stream truncated");
+    };
+    for (uint32_t i = 0; i < n_samples; ++i) {
+      need(4);
+      uint32_t nf;
+      std::memcpy(&nf, tlv + pos, 4);
+      pos += 4;
+      samples[i].values.assign(schema.size(), {});
+      std::vector<bool> seen(schema.size(), false);
+      for (uint32_t f = 0; f < nf; ++f) {
+        need(2);
+        uint16_t nl;
+        std::memcpy(&nl, tlv + pos, 2);
+        pos += 2;
+        need(nl + 9);
+        std::string name(reinterpret_cast<const char*>(tlv + pos), nl);
+        pos += nl;
+        const uint8_t kind = tlv[pos++];
+        uint64_t nb;
+        std::memcpy(&nb, tlv + pos, 8);
+        pos += 8;
+        need(nb);
+        size_t fi = 0;
+        while (fi < schema.size() && schema[fi].name != name) ++fi;
+        if (fi == schema.size() || schema[fi].kind != (int32_t)kind)
+          fail(kSchemaMismatch, "field '" + name + "' not in schema or mistyped");
+        samples[i].values[fi].assign(tlv + pos, tlv + pos + nb);
+        seen[fi] = true;
+        pos += nb;
+      }
+      for (size_t f = 0; f < schema.size(); ++f)
+        if (!seen[f]) fail(kSchemaMismatch, "missing field '" + schema[f].name + "'");
+    }
+    write_dataset(schema, samples, slice_count, group_size, out_dir, stem, n_threads ? n_threads : 8);
+  });
+}
+
+int pcp_pipeline_open(const char* primary, const char* graph_json, const uint64_t* ids,
+                      uint64_t n_ids, int device, const char* options, pcp_pipeline** out) {
+  *out = nullptr;
+  return guarded([&] {
+    auto p = std::make_unique<pcp_pipeline>();
+    p->impl.open(primary, graph_json, ids, n_ids, device, options ? options : "");
+    *out = p.release();
+  });
+}
+
+int pcp_pipeline_next_batch(pcp_pipeline* p, pcp_batch* out, int* eos) {
+  return guarded([&] { p->impl.next_batch(out, eos); });
+}
+
+void* pcp_pipeline_stream(pcp_pipeline* p) { return p->impl.serve_stream; }
+
+const char* pcp_pipeline_stats(pcp_pipeline* p) { return p->impl.stats(); }
+
+void pcp_pipeline_close(pcp_pipeline* p) { delete p; }
+
+int pcp_malloc(void** d, size_t n) {
+  return guarded([&] { CK(cudaMalloc(d, n)); });
+}
+int pcp_free(void* d) {
+  return guarded([&] { CK(cudaFree(d)); });
+}
+int pcp_memcpy_h2d(void* d, const void* h, size_t n, void* st) {
+  return guarded([&] {
+    CK(cudaMemcpyAsync(d, h, n, cudaMemcpyHostToDevice, (cudaStream_t)st));
+    CK(cudaStreamSynchronize((cudaStream_t)st));
+  });
+}
+int pcp_memcpy_d2h(void* h, const void* d, size_t n, void* st) {
+  return guarded([&] {
+    CK(cudaMemcpyAsync(h, d, n, cudaMemcpyDeviceToHost, (cudaStream_t)st));
+    CK(cudaStreamSynchronize((cudaStream_t)st));
+  });
+}
+int pcp_stream_sync(void* st) {
+  return guarded([&] { CK(cudaStreamSynchronize((cudaStream_t)st)); });
+}
+
+}  // extern "C"

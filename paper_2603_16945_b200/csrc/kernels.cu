@@ -1,0 +1,1431 @@
+// kernels.cu — the sm_100a kernels of the PcRecord → batch stage.
+//
+//   k_crc_windows   zlib CRC-32 of page payloads, one warp per 64 KiB window,
+//                   XOR-folded per page (device_crc.cuh)           [HBM]
+//   k_page_decode   LZ4 block decode (lz4_block.cpp:113-156) / stored-raw
+//                   copy of pages into the wave raw arena, one warp per page
+//   k_scalar_parse  scalar-record walk (format.cpp:426-474) per group
+//   k_cloud         persistent per-sample interpreter: stage blob (TMA bulk),
+//                   fused payload CRC, XOR-delta decode + field split
+//                   (format.cpp:183-195,483-493), the op chain
+//                   (transforms.cpp:98-306 + App. C ops) and the write into
+//                   the batch slot (Batch::stacked, pipeline.cpp:170-200)
+//   k_finalize      page CRC verdicts + per-sample status precedence
+//
+// Every float op on a path whose result feeds a decision or an integer
+// output uses explicit _rn intrinsics (no FMA), like the reference build.
+#include <cuda_runtime.h>
+
+#include <cfloat>
+#include <cstdint>
+
+#include "device_crc.cuh"
+#include "device_rng.cuh"
+#include "device_util.cuh"
+#include "kernels.h"
+#include "pcp_internal.h"
+
+namespace pcp {
+
+__constant__ crc::X2N c_x2n;
+
+// =========================================================================
+// CRC over page payload windows
+// =========================================================================
+__global__ void k_crc_windows(const uint8_t* bytes, const CrcWindow* win, uint32_t n_win,
+                              const uint32_t* shift_tab, uint32_t* page_acc) {
+  __shared__ uint32_t tab[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) tab[i] = crc::table_entry(i);
+  __syncthreads();
+  const uint32_t warps = blockDim.x >> 5;
+  for (uint32_t w = blockIdx.x * warps + (threadIdx.x >> 5); w < n_win; w += gridDim.x * warps) {
+    const CrcWindow cw = win[w];
+    const uint32_t c = crc::warp_range(tab, c_x2n.v, shift_tab, bytes + cw.start, cw.len, cw.after);
+    if ((threadIdx.x & 31) == 0) atomicXor(page_acc + cw.page, c);
+  }
+}
+
+// =========================================================================
+// Page decode: LZ4 (warp per page) or stored-raw copy into the raw arena.
+// Checks mirror decode_block_page (format.cpp:243-266) and lz4::decompress.
+// The CRC verdict is folded in by k_finalize.
+// =========================================================================
+namespace {
+
+struct Lz4Seq {
+  uint64_t lit_src;  // payload offset of the literals
+  uint64_t out;      // output offset of the literals
+  uint32_t lit_len;
+  uint32_t match_len;  // 0 = last sequence
+  uint32_t offset;
+};
+
+// Parse one sequence starting at *ip (lane-0 work).  Returns status.
+__device__ int32_t lz4_parse(const uint8_t* src, uint64_t n, uint64_t raw_len, uint64_t& ip,
+                             uint64_t& op, Lz4Seq& s, bool& last) {
+  if (ip >= n) return kCorruptPage;
+  const uint8_t token = src[ip++];
+  uint64_t lit = token >> 4;
+  if (lit == 15) {
+    uint8_t b;
+    do {
+      if (ip >= n) return kCorruptPage;
+      b = src[ip++];
+      lit += b;
+    } while (b == 255);
+  }
+  if (ip + lit > n || op + lit > raw_len) return kCorruptPage;
+  s.lit_src = ip;
+  s.out = op;
+  s.lit_len = (uint32_t)lit;
+  ip += lit;
+  op += lit;
+  if (ip == n) {
+    if (op != raw_len) return kCorruptPage;
+    s.match_len = 0;
+    s.offset = 0;
+    last = true;
+    return kOk;
+  }
+  if (ip + 2 > n) return kCorruptPage;
+  const uint32_t offset = (uint32_t)src[ip] | ((uint32_t)src[ip + 1] << 8);
+  ip += 2;
+  if (offset == 0 || offset > op) return kCorruptPage;
+  uint64_t ml = token & 0x0f;
+  if (ml == 15) {
+    uint8_t b;
+    do {
+      if (ip >= n) return kCorruptPage;
+      b = src[ip++];
+      ml += b;
+    } while (b == 255);
+  }
+  ml += 4;
+  if (op + ml > raw_len) return kCorruptPage;
+  s.match_len = (uint32_t)ml;
+  s.offset = offset;
+  op += ml;
+  last = false;
+  return kOk;
+}
+
+}  // namespace
+
+// Warp-cooperative LZ4 block decode (all 32 lanes call it).  Lane 0 parses
+// up to 32 sequences ahead into shared memory; the warp then copies literal
+// and match bytes cooperatively (a match with offset < length is copied in
+// offset-sized strides, reproducing the byte-wise overlapping copy of
+// lz4_block.cpp:151-153).  Returns the status on every lane.
+__device__ int32_t warp_lz4_decode(const uint8_t* src, uint64_t n, uint8_t* dst, uint64_t raw_len,
+                                   Lz4Seq* seqs, int32_t* sst, uint32_t* scount) {
+  const int lane = threadIdx.x & 31;
+  uint64_t ip = 0, op = 0;
+  bool last = false;
+  int32_t status = kOk;
+  while (!last && status == kOk) {
+    if (lane == 0) {
+      uint32_t k = 0;
+      int32_t st = kOk;
+      while (k < 32 && !last) {
+        st = lz4_parse(src, n, raw_len, ip, op, seqs[k], last);
+        if (st != kOk) break;
+        ++k;
+      }
+      *sst = st;
+      *scount = k;
+    }
+    __syncwarp();
+    const uint32_t k = *scount;
+    status = *sst;
+    last = __shfl_sync(0xffffffffu, last ? 1 : 0, 0) != 0;
+    for (uint32_t q = 0; q < k; ++q) {
+      const Lz4Seq s = seqs[q];
+      for (uint32_t i = lane; i < s.lit_len; i += 32) dst[s.out + i] = src[s.lit_src + i];
+      __syncwarp();
+      if (s.match_len) {
+        const uint64_t mo = s.out + s.lit_len;
+        const uint32_t stride = s.offset < 32 ? s.offset : 32;
+        for (uint32_t base = 0; base < s.match_len; base += stride) {
+          const uint32_t i = base + lane;
+          uint8_t b = 0;
+          if (lane < stride && i < s.match_len) b = dst[mo - s.offset + i];
+          __syncwarp();
+          if (lane < stride && i < s.match_len) dst[mo + i] = b;
+          __syncwarp();
+        }
+      }
+    }
+    __syncwarp();
+  }
+  return status;
+}
+
+// One warp per page: LZ4 decode or stored-raw copy into the raw arena.
+__global__ void k_page_decode(const uint8_t* bytes, uint8_t* raw, const PageRef* pages,
+                              const uint32_t* todo, uint32_t n_todo, int32_t* page_status) {
+  constexpr int kWarps = 4;
+  __shared__ Lz4Seq seqs[kWarps][32];
+  __shared__ int32_t sst[kWarps];
+  __shared__ uint32_t scount[kWarps];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  for (uint32_t w = blockIdx.x * kWarps + wl; w < n_todo; w += gridDim.x * kWarps) {
+    const uint32_t pi = todo[w];
+    const PageRef pg = pages[pi];
+    const uint8_t* src = bytes + pg.off + kPageHeaderBytes;
+    uint8_t* dst = raw + pg.raw_dst;
+    int32_t status = kOk;
+    if (pg.flags & kFlagOuterLz4) {
+      status = warp_lz4_decode(src, pg.pay_len, dst, pg.raw_len, seqs[wl], &sst[wl], &scount[wl]);
+    } else if (pg.flags & kFlagStoredRaw) {
+      if (pg.pay_len != pg.raw_len) {
+        status = kCorruptPage;
+      } else {
+        for (uint64_t i = lane; i < pg.raw_len; i += 32) dst[i] = src[i];
+      }
+    } else {
+      status = kCorruptPage;
+    }
+    if (lane == 0 && status != kOk) page_status[pi] = status;
+    __syncwarp();
+  }
+}
+
+// =========================================================================
+// Scalar-record parse: one thread walks one group's decoded scalar page
+// (parse_scalar_record, format.cpp:426-474).  Values of non-bytes fields are
+// copied, in schema order, into the value arena for the batch.
+// =========================================================================
+__global__ void k_scalar_parse(WaveArgs a) {
+  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= a.n_groups) return;
+  const GroupWork gw = a.groups[g];
+  const PageRef pg = a.pages[gw.scalar_page];
+  const uint8_t* p = a.raw + pg.raw_dst;
+  const uint64_t n = pg.raw_len;
+  uint64_t pos = 0;
+  uint32_t vo = gw.vals_base;
+  int32_t fatal = kOk;
+  for (uint32_t r = 0; r < gw.n_rows; ++r) {
+    ScalarRec rec{};
+    rec.status = fatal;
+    if (fatal == kOk) {
+      auto rd = [&](void* dstp, uint32_t k) -> bool {
+        if (pos + k > n) return false;
+        uint8_t* d = static_cast<uint8_t*>(dstp);
+        for (uint32_t i = 0; i < k; ++i) d[i] = p[pos + i];
+        pos += k;
+        return true;
+      };
+      uint32_t nl = 0;
+      bool ok = rd(&rec.blob_start, 8) && rd(&rec.blob_end, 8) && rd(&nl, 4);
+      if (ok && nl > kMaxBytesFields) ok = false;
+      rec.n_lens = nl;
+      for (uint32_t i = 0; ok && i < nl; ++i) ok = rd(&rec.lens[i], 8);
+      rec.vals_off = vo;
+      for (int f = 0; ok && f < a.n_fields; ++f) {
+        const FieldDesc fd = a.fields[f];
+        uint32_t es = 0;
+        switch (fd.kind) {
+          case kBytes: continue;
+          case kInt32: case kFloat32: es = 4; break;
+          case kInt64: case kFloat64: es = 8; break;
+          case kString: {
+            uint32_t len = 0;
+            ok = rd(&len, 4);
+            if (ok && pos + len > n) ok = false;
+            if (ok) {
+              // strings keep their u32 length prefix in the value arena
+              uint8_t* d = a.vals + vo;
+              *reinterpret_cast<uint32_t*>(d) = len;
+              for (uint32_t i = 0; i < len; ++i) d[4 + i] = p[pos + i];
+              pos += len;
+              vo += 4 + len;
+            }
+            continue;
+          }
+        }
+        const uint32_t nb = es * fd.elems;
+        if (pos + nb > n) {
+          ok = false;
+          break;
+        }
+        for (uint32_t i = 0; i < nb; ++i) a.vals[vo + i] = p[pos + i];
+        pos += nb;
+        vo += nb;
+      }
+      rec.vals_len = vo - rec.vals_off;
+      if (!ok) {
+        fatal = kCorruptPage;  // "record truncated" (format.cpp:25-27)
+        rec.status = fatal;
+      }
+    }
+    a.recs[gw.first_rec + r] = rec;
+  }
+}
+
+// =========================================================================
+// The per-sample interpreter
+// =========================================================================
+namespace {
+
+constexpr int kRed = 64;  // reduction scratch words (8 B)
+
+struct Smem {
+  uint32_t crc_tab[256];
+  unsigned long long red[kRed];
+  uint64_t mt[rng::kN];
+  uint64_t bar;
+  int32_t status;
+  int32_t flag;
+  uint32_t u32s[8];
+  float f32s[8];
+  double f64s[8];
+};
+
+struct Cloud {
+  uint8_t* cur[kMaxBytesFields];
+  uint8_t* alt[kMaxBytesFields];
+  uint32_t n[kMaxBytesFields];     // points (tracked fields)
+  uint32_t elem[kMaxBytesFields];  // bytes per point
+  uint32_t present;                // tracked + present bits
+  int32_t* ix[4];                  // index scratch, cap entries each
+  uint32_t cap;
+};
+
+__device__ __forceinline__ float* F(Cloud& c, int f) { return reinterpret_cast<float*>(c.cur[f]); }
+
+__device__ __forceinline__ bool has(const Cloud& c, int f) {
+  return f >= 0 && ((c.present >> f) & 1u);
+}
+
+// Lowest-set-bit exponent of a finite nonzero float: x = odd * 2^e.
+__device__ __forceinline__ int lowbit_exp(float x) {
+  const uint32_t b = __float_as_uint(x) & 0x7fffffffu;
+  const uint32_t e = b >> 23, m = b & 0x7fffffu;
+  if (e == 0) return -149 + __ffs(m) - 1;
+  return (int)e - 150 + __ffs(m | 0x800000u) - 1;
+}
+
+// ---- gather helpers -------------------------------------------------------
+__device__ void gather_field(Cloud& c, int f, const int32_t* idx, uint32_t m) {
+  const uint32_t es = c.elem[f];
+  const uint8_t* src = c.cur[f];
+  uint8_t* dst = c.alt[f];
+  if (es == 12) {
+    const float* s = reinterpret_cast<const float*>(src);
+    float* d = reinterpret_cast<float*>(dst);
+    for (uint32_t k = threadIdx.x; k < m; k += blockDim.x) {
+      const uint32_t i = (uint32_t)idx[k];
+      d[3 * k] = s[3 * i];
+      d[3 * k + 1] = s[3 * i + 1];
+      d[3 * k + 2] = s[3 * i + 2];
+    }
+  } else if (es == 4) {
+    const uint32_t* s = reinterpret_cast<const uint32_t*>(src);
+    uint32_t* d = reinterpret_cast<uint32_t*>(dst);
+    for (uint32_t k = threadIdx.x; k < m; k += blockDim.x) d[k] = s[idx[k]];
+  } else {
+    for (uint32_t k = threadIdx.x; k < m * es; k += blockDim.x) {
+      const uint32_t p = k / es, b = k - p * es;
+      dst[k] = src[(uint64_t)idx[p] * es + b];
+    }
+  }
+  __syncthreads();
+  uint8_t* t = c.cur[f];
+  c.cur[f] = c.alt[f];
+  c.alt[f] = t;
+  c.n[f] = m;
+}
+
+// Mask of tracked fields an index op moves.
+__device__ __forceinline__ uint32_t move_mask(const WaveArgs& a, const Cloud& c, bool all_fields,
+                                              uint32_t gather_mask) {
+  uint32_t m = 0;
+  if (a.role_data >= 0) m |= 1u << a.role_data;
+  if (a.role_normal >= 0) m |= 1u << a.role_normal;
+  if (a.role_color >= 0) m |= 1u << a.role_color;
+  if (all_fields && a.role_intensity >= 0) m |= 1u << a.role_intensity;
+  m |= gather_mask;
+  return m & c.present;
+}
+
+__device__ int32_t check_move(const WaveArgs& a, const Cloud& c, uint32_t mm) {
+  const uint32_t n = c.n[a.role_data];
+  for (int f = 0; f < a.n_bytes_fields; ++f)
+    if (((mm >> f) & 1u) && c.n[f] < n) return kOutOfBounds;
+  return kOk;
+}
+
+__device__ void gather_mask_fields(const WaveArgs& a, Cloud& c, uint32_t mm, const int32_t* idx,
+                                   uint32_t m) {
+  for (int f = 0; f < a.n_bytes_fields; ++f)
+    if ((mm >> f) & 1u) gather_field(c, f, idx, m);
+}
+
+// ---- Fisher-Yates (transforms.cpp:278-287), parallel resolution ----------
+// J[i] = draw i's swap partner.  idx[i] = value at position J[i] just before
+// swap i = W[prev(i)] if an earlier swap wrote that position, else J[i];
+// W[k] (value at position k before swap k) follows the chain of last
+// writers back to an untouched original.
+__device__ void fy_resolve(Cloud& c, Smem& S, uint32_t N, uint32_t T) {
+  int32_t* J = c.ix[0];
+  int32_t* last = c.ix[1];
+  int32_t* prev = c.ix[2];
+  int32_t* ptr = c.ix[3];
+  for (uint32_t p = threadIdx.x; p < N; p += blockDim.x) last[p] = -1;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const uint32_t lane = threadIdx.x;
+    const uint32_t lt = (1u << lane) - 1u, gt = ~((2u << lane) - 1u);
+    for (uint32_t base = 0; base < T; base += 32) {
+      const uint32_t i = base + lane;
+      const bool v = i < T;
+      const uint32_t j = v ? (uint32_t)J[i] : (0x80000000u | lane);
+      const uint32_t m = __match_any_sync(0xffffffffu, j);
+      const int32_t cand = v ? last[j] : -1;
+      __syncwarp();
+      if (v) {
+        const uint32_t lower = m & lt;
+        prev[i] = lower ? (int32_t)(base + 31 - __clz(lower)) : cand;
+        if ((m & gt) == 0) last[j] = (int32_t)i;
+      }
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  for (uint32_t k = threadIdx.x; k < T; k += blockDim.x) {
+    const int32_t l = last[k];
+    ptr[k] = (l == (int32_t)k) ? prev[k] : l;
+  }
+  __syncthreads();
+  for (;;) {
+    if (threadIdx.x == 0) S.flag = 0;
+    __syncthreads();
+    bool ch = false;
+    for (uint32_t k = threadIdx.x; k < T; k += blockDim.x) {
+      const int32_t p = ptr[k];
+      if (p >= 0) {
+        const int32_t q = ptr[p];
+        if (q >= 0) {
+          ptr[k] = q;
+          ch = true;
+        }
+      }
+    }
+    if (ch) S.flag = 1;
+    __syncthreads();
+    if (!S.flag) break;
+    __syncthreads();
+  }
+  for (uint32_t i = threadIdx.x; i < T; i += blockDim.x) {
+    const int32_t pv = prev[i];
+    int32_t v;
+    if (pv >= 0) {
+      const int32_t r = ptr[pv];
+      v = r >= 0 ? r : pv;
+    } else {
+      v = J[i];
+    }
+    J[i] = v;  // J becomes idx (each i is read and written by one thread)
+  }
+  __syncthreads();
+}
+
+// Draw index vector for downsample; returns false if a Lemire rejection
+// (probability ~range/2^64) needs the serial path.
+__device__ bool downsample_draws(Cloud& c, Smem& S, uint64_t seed, uint32_t N, uint32_t T) {
+  if (threadIdx.x == 0) {
+    rng::seed_state(S.mt, seed);
+    S.flag = 0;
+  }
+  __syncthreads();
+  int32_t* J = c.ix[0];
+  const bool fy = N >= T;
+  for (uint32_t blk = 0; blk * rng::kN < T; ++blk) {
+    rng::twist_block(S.mt);
+    for (uint32_t t = threadIdx.x; t < rng::kN; t += blockDim.x) {
+      const uint32_t i = blk * rng::kN + t;
+      if (i < T) {
+        const uint64_t u = rng::temper(S.mt[t]);
+        const uint64_t range = fy ? (uint64_t)(N - i) : (uint64_t)N;
+        uint64_t r;
+        if (!rng::lemire_fast(u, range, r)) S.flag = 1;
+        J[i] = (int32_t)(fy ? i + r : r);
+      }
+    }
+    __syncthreads();
+  }
+  return S.flag == 0;
+}
+
+__device__ void downsample_serial(Cloud& c, Smem& S, uint64_t seed, uint32_t N, uint32_t T) {
+  int32_t* idx = c.ix[0];
+  int32_t* all = c.ix[1];
+  if (threadIdx.x == 0) {
+    rng::Serial g{S.mt, 0};
+    g.seed(seed);
+    if (N >= T) {
+      for (uint32_t i = 0; i < N; ++i) all[i] = (int32_t)i;
+      for (uint32_t i = 0; i < T; ++i) {
+        const uint32_t j = (uint32_t)g.uniform_int(i, N - 1);
+        const int32_t t = all[i];
+        all[i] = all[j];
+        all[j] = t;
+        idx[i] = all[i];
+      }
+    } else {
+      for (uint32_t i = 0; i < T; ++i) idx[i] = (int32_t)g.uniform_int(0, N - 1);
+    }
+  }
+  __syncthreads();
+}
+
+// ---- ops -------------------------------------------------------------------
+__device__ int32_t op_normalize(const WaveArgs& a, Cloud& c, Smem& S) {
+  float* d = F(c, a.role_data);
+  const uint32_t n = c.n[a.role_data];
+  double s[3] = {0, 0, 0}, ab[3] = {0, 0, 0};
+  int e[3] = {INT_MAX, INT_MAX, INT_MAX};
+  uint32_t bad = 0;
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const float x = d[3 * i + k];
+      s[k] = __dadd_rn(s[k], (double)x);
+      ab[k] = __dadd_rn(ab[k], fabs((double)x));
+      if (!isfinite(x)) bad |= 1u << k;
+      else if (x != 0.0f) e[k] = min(e[k], lowbit_exp(x));
+    }
+  }
+  double sum[3], A[3];
+  int em[3];
+  for (int k = 0; k < 3; ++k) {
+    sum[k] = dev::block_reduce(s[k], dev::OpDAdd{}, 0.0, S.red);
+    A[k] = dev::block_reduce(ab[k], dev::OpDAdd{}, 0.0, S.red);
+    em[k] = dev::block_reduce(e[k], dev::OpMin{}, INT_MAX, S.red);
+  }
+  bad = dev::block_reduce(bad, dev::OpOr{}, 0u, S.red);
+  // Exactness certificate: all coordinates are multiples of 2^em and every
+  // partial sum is bounded by A <= 2^(52+em), so every partial sum of every
+  // order is exact and equals the sequential double sum of the reference
+  // (transforms.cpp:124-129).  Otherwise replay the sequential sum.
+  if (threadIdx.x < 3) {
+    const int k = threadIdx.x;
+    const bool ok = !((bad >> k) & 1u) &&
+                    (em[k] == INT_MAX || A[k] <= ldexp(1.0, min(52 + em[k], 1023)));
+    double r = sum[k];
+    if (!ok) {
+      r = 0.0;
+      for (uint32_t i = 0; i < n; ++i) r = __dadd_rn(r, (double)d[3 * i + k]);
+    }
+    S.f64s[k] = __ddiv_rn(r, (double)n);
+  }
+  __syncthreads();
+  const double cx = S.f64s[0], cy = S.f64s[1], cz = S.f64s[2];
+  double mx = 0.0;
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const double dx = __dsub_rn((double)d[3 * i], cx);
+    const double dy = __dsub_rn((double)d[3 * i + 1], cy);
+    const double dz = __dsub_rn((double)d[3 * i + 2], cz);
+    const double r = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)),
+                                          __dmul_rn(dz, dz)));
+    mx = fmax(mx, r);  // std::max(s, r): NaN never replaces
+  }
+  const double sc = dev::block_reduce(mx, dev::OpFMax{}, 0.0, S.red);
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+    if (sc == 0.0) {
+      d[3 * i] = d[3 * i + 1] = d[3 * i + 2] = 0.0f;
+    } else {
+      d[3 * i] = __double2float_rn(__ddiv_rn(__dsub_rn((double)d[3 * i], cx), sc));
+      d[3 * i + 1] = __double2float_rn(__ddiv_rn(__dsub_rn((double)d[3 * i + 1], cy), sc));
+      d[3 * i + 2] = __double2float_rn(__ddiv_rn(__dsub_rn((double)d[3 * i + 2], cz), sc));
+    }
+  }
+  __syncthreads();
+  return kOk;
+}
+
+// Broadcast the first k (<= 8) engine outputs to S.u32s/f32s via thread 0.
+__device__ void first_draws(Smem& S, uint64_t seed, int k, uint64_t* out) {
+  __shared__ uint64_t o[8];
+  if (threadIdx.x == 0) rng::first_outputs(seed, k, o);
+  __syncthreads();
+  for (int i = 0; i < k; ++i) out[i] = o[i];
+  __syncthreads();
+}
+
+__device__ int32_t op_translate(const WaveArgs& a, Cloud& c, Smem& S, uint64_t seed) {
+  uint64_t u[3];
+  first_draws(S, seed, 3, u);
+  const float t[3] = {rng::uniform_real(u[0], -0.2f, 0.2f), rng::uniform_real(u[1], -0.2f, 0.2f),
+                      rng::uniform_real(u[2], -0.2f, 0.2f)};
+  float* d = F(c, a.role_data);
+  const uint32_t n3 = 3 * c.n[a.role_data];
+  for (uint32_t i = threadIdx.x; i < n3; i += blockDim.x) d[i] = __fadd_rn(d[i], t[i % 3]);
+  __syncthreads();
+  return kOk;
+}
+
+__device__ int32_t op_scale(const WaveArgs& a, Cloud& c, Smem& S, uint64_t seed) {
+  uint64_t u[1];
+  first_draws(S, seed, 1, u);
+  const float s = rng::uniform_real(u[0], 0.8f, 1.25f);
+  float* d = F(c, a.role_data);
+  const uint32_t n3 = 3 * c.n[a.role_data];
+  for (uint32_t i = threadIdx.x; i < n3; i += blockDim.x) d[i] = __fmul_rn(d[i], s);
+  __syncthreads();
+  return kOk;
+}
+
+__device__ int32_t op_flip(const WaveArgs& a, Cloud& c, Smem& S, uint64_t seed) {
+  uint64_t u[1];
+  first_draws(S, seed, 1, u);
+  if (rng::uniform_real(u[0], 0.0f, 1.0f) < 0.5f) {
+    float* d = F(c, a.role_data);
+    for (uint32_t i = threadIdx.x; i < c.n[a.role_data]; i += blockDim.x) d[3 * i] = -d[3 * i];
+    if (has(c, a.role_normal)) {
+      float* nm = F(c, a.role_normal);
+      for (uint32_t i = threadIdx.x; i < c.n[a.role_normal]; i += blockDim.x) nm[3 * i] = -nm[3 * i];
+    }
+  }
+  __syncthreads();
+  return kOk;
+}
+
+__device__ void rotate_field(float* v, uint32_t n, float cs, float sn) {
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const float px = v[3 * i], py = v[3 * i + 1];
+    v[3 * i] = __fsub_rn(__fmul_rn(px, cs), __fmul_rn(py, sn));
+    v[3 * i + 1] = __fadd_rn(__fmul_rn(px, sn), __fmul_rn(py, cs));
+  }
+}
+
+__device__ int32_t op_rotate(const WaveArgs& a, Cloud& c, Smem& S, const OpDesc& op,
+                             uint64_t seed) {
+  float theta = op.theta;
+  if (!op.has_theta) {
+    uint64_t u[1];
+    first_draws(S, seed, 1, u);
+    theta = rng::uniform_real(u[0], 0.0f, 6.28318548202514648f);  // (float)(2*M_PI)
+  }
+  float sn, cs;
+  sincosf(theta, &sn, &cs);
+  rotate_field(F(c, a.role_data), c.n[a.role_data], cs, sn);
+  if (has(c, a.role_normal)) rotate_field(F(c, a.role_normal), c.n[a.role_normal], cs, sn);
+  __syncthreads();
+  return kOk;
+}
+
+__device__ __forceinline__ float clampf(float v, float lo, float hi) {
+  return v < lo ? lo : (hi < v ? hi : v);  // std::clamp
+}
+
+// jitter (transforms.cpp:159-168): normals n_0, n_1, ... from the polar
+// method; accepted attempt j yields n_2j = y*mult (returned) and
+// n_2j+1 = x*mult (saved).  Attempts are scanned 156 per twist.
+__device__ int32_t op_jitter(const WaveArgs& a, Cloud& c, Smem& S, uint64_t seed) {
+  float* d = F(c, a.role_data);
+  const uint32_t need = 3 * c.n[a.role_data];
+  if (threadIdx.x == 0) rng::seed_state(S.mt, seed);
+  __syncthreads();
+  uint32_t done = 0;  // normals produced
+  while (done < need) {
+    rng::twist_block(S.mt);
+    for (uint32_t base = 0; base < rng::kM; base += blockDim.x) {
+      const uint32_t t = base + threadIdx.x;
+      float x = 0, y = 0, r2 = 0;
+      bool acc = false;
+      if (t < rng::kM)
+        acc = rng::polar_attempt(rng::temper(S.mt[2 * t]), rng::temper(S.mt[2 * t + 1]), x, y, r2);
+      uint32_t tot;
+      const uint32_t rank = dev::block_scan_excl(acc ? 1u : 0u, &tot, S.red);
+      if (acc) {
+        const uint32_t k0 = done + 2 * rank;
+        const float mult = rng::polar_mult(r2);
+        if (k0 < need) {
+          const float v = clampf(__fadd_rn(__fmul_rn(__fmul_rn(y, mult), 0.01f), 0.0f), -0.05f, 0.05f);
+          d[k0] = __fadd_rn(d[k0], v);
+        }
+        if (k0 + 1 < need) {
+          const float v = clampf(__fadd_rn(__fmul_rn(__fmul_rn(x, mult), 0.01f), 0.0f), -0.05f, 0.05f);
+          d[k0 + 1] = __fadd_rn(d[k0 + 1], v);
+        }
+      }
+      done += 2 * tot;
+      __syncthreads();
+    }
+  }
+  return kOk;
+}
+
+__device__ int32_t op_color(const WaveArgs& a, Cloud& c, Smem& S, uint64_t seed) {
+  if (!has(c, a.role_color) || c.n[a.role_color] == 0) return kMissingField;
+  float* col = F(c, a.role_color);
+  const uint32_t need = 3 * c.n[a.role_color];
+  if (threadIdx.x == 0) rng::seed_state(S.mt, seed);
+  __syncthreads();
+  for (uint32_t blk = 0; blk * rng::kN < need; ++blk) {
+    rng::twist_block(S.mt);
+    for (uint32_t t = threadIdx.x; t < rng::kN; t += blockDim.x) {
+      const uint32_t k = blk * rng::kN + t;
+      if (k < need)
+        col[k] = clampf(__fadd_rn(col[k], rng::uniform_real(rng::temper(S.mt[t]), -0.1f, 0.1f)),
+                        0.0f, 1.0f);
+    }
+    __syncthreads();
+  }
+  return kOk;
+}
+
+// Ordered compaction of the points passing `keep(i)` into ix[0]; returns m.
+template <typename Pred>
+__device__ uint32_t compact(Cloud& c, Smem& S, uint32_t n, Pred keep) {
+  int32_t* out = c.ix[0];
+  uint32_t base = 0;
+  for (uint32_t t0 = 0; t0 < n; t0 += blockDim.x) {
+    const uint32_t i = t0 + threadIdx.x;
+    const bool k = i < n && keep(i);
+    uint32_t tot;
+    const uint32_t r = dev::block_scan_excl(k ? 1u : 0u, &tot, S.red);
+    if (k) out[base + r] = (int32_t)i;
+    base += tot;
+  }
+  __syncthreads();
+  return base;
+}
+
+// random_crop (transforms.cpp:220-271).
+__device__ int32_t op_random_crop(const WaveArgs& a, Cloud& c, Smem& S, uint64_t seed) {
+  const float* d = F(c, a.role_data);
+  const uint32_t n = c.n[a.role_data];
+  // bbox: sequential std::min/std::max from pts[0]: equal values keep the
+  // earliest, NaN never replaces, a NaN pts[0] poisons the axis.
+  float lo[3], hi[3];
+  for (int k = 0; k < 3; ++k) {
+    float l = INFINITY, h = -INFINITY;
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+      const float v = d[3 * i + k];
+      l = fminf(l, v);
+      h = fmaxf(h, v);
+    }
+    lo[k] = dev::block_reduce(l, [](float x, float y) { return fminf(x, y); }, INFINITY, S.red);
+    hi[k] = dev::block_reduce(h, [](float x, float y) { return fmaxf(x, y); }, -INFINITY, S.red);
+    const float p0 = d[k];
+    if (isnan(p0)) lo[k] = hi[k] = p0;
+    // -0/+0 ties: the sequential min keeps the first of equal values
+    if (lo[k] == 0.0f) lo[k] = (p0 == 0.0f) ? p0 : 0.0f;
+    if (hi[k] == 0.0f) hi[k] = (p0 == 0.0f) ? p0 : 0.0f;
+  }
+  __syncthreads();
+  // the "first zero" rule above is exact only when pts[0] is that zero; a
+  // later signed zero can only matter for the box start, which is computed
+  // from lo + positive terms — +0 and -0 give the same sums unless all terms
+  // are zero.  Handled exactly by the rescan below.
+  for (int k = 0; k < 3; ++k) {
+    if (lo[k] == 0.0f && d[k] != 0.0f) {
+      if (threadIdx.x == 0) {
+        float z = 0.0f;
+        for (uint32_t i = 0; i < n; ++i)
+          if (d[3 * i + k] == 0.0f) { z = d[3 * i + k]; break; }
+        S.f32s[k] = z;
+      }
+      __syncthreads();
+      lo[k] = S.f32s[k];
+      __syncthreads();
+    }
+    if (hi[k] == 0.0f && d[k] != 0.0f) {
+      if (threadIdx.x == 0) {
+        float z = 0.0f;
+        for (uint32_t i = 0; i < n; ++i)
+          if (d[3 * i + k] == 0.0f) { z = d[3 * i + k]; break; }
+        S.f32s[k + 3] = z;
+      }
+      __syncthreads();
+      hi[k] = S.f32s[k + 3];
+      __syncthreads();
+    }
+  }
+  uint64_t u[6];
+  first_draws(S, seed, 6, u);
+  float blo[3], bhi[3];
+  for (int k = 0; k < 3; ++k) {
+    const float ext = __fsub_rn(hi[k], lo[k]);
+    const float f = rng::uniform_real(u[2 * k], 0.7f, 1.0f);
+    const float uu = rng::uniform_real(u[2 * k + 1], 0.0f, 1.0f);
+    blo[k] = __fadd_rn(lo[k], __fmul_rn(__fmul_rn(uu, ext), __fsub_rn(1.0f, f)));
+    bhi[k] = __fadd_rn(blo[k], __fmul_rn(ext, f));
+  }
+  const uint32_t m = compact(c, S, n, [&](uint32_t i) {
+    const float x = d[3 * i], y = d[3 * i + 1], z = d[3 * i + 2];
+    return x >= blo[0] && x <= bhi[0] && y >= blo[1] && y <= bhi[1] && z >= blo[2] && z <= bhi[2];
+  });
+  if (m == 0) return kOk;  // fall back to the full cloud (:246)
+  const uint32_t mm = move_mask(a, c, false, 0);
+  const int32_t st = check_move(a, c, mm);
+  if (st) return st;
+  // intensity: only when it has at least as many entries as kept points,
+  // keeping entries whose index exists (:257-269)
+  if (has(c, a.role_intensity) && c.n[a.role_intensity] >= m) {
+    const int fi = a.role_intensity;
+    const uint32_t ni = c.n[fi];
+    const int32_t* keep = c.ix[0];
+    uint32_t* dst = reinterpret_cast<uint32_t*>(c.alt[fi]);
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(c.cur[fi]);
+    uint32_t base = 0;
+    for (uint32_t t0 = 0; t0 < m; t0 += blockDim.x) {
+      const uint32_t k = t0 + threadIdx.x;
+      const bool ok = k < m && (uint32_t)keep[k] < ni;
+      uint32_t tot;
+      const uint32_t r = dev::block_scan_excl(ok ? 1u : 0u, &tot, S.red);
+      if (ok) dst[base + r] = src[keep[k]];
+      base += tot;
+    }
+    __syncthreads();
+    c.cur[fi] = c.alt[fi];
+    c.alt[fi] = reinterpret_cast<uint8_t*>(const_cast<uint32_t*>(src));
+    c.n[fi] = base;
+  }
+  gather_mask_fields(a, c, mm, c.ix[0], m);
+  return kOk;
+}
+
+__device__ int32_t op_downsample(const WaveArgs& a, Cloud& c, Smem& S, const OpDesc& op,
+                                 uint64_t seed) {
+  if (op.num_points <= 0) return kOutOfBounds;
+  const uint32_t T = (uint32_t)op.num_points;
+  const uint32_t N = c.n[a.role_data];
+  if (T > c.cap) return kOutOfBounds;
+  const uint32_t mm = move_mask(a, c, false, op.gather_mask);
+  const int32_t st = check_move(a, c, mm);
+  if (st) return st;
+  const bool fast = downsample_draws(c, S, seed, N, T) && !a.force_serial_fy;
+  if (fast) {
+    if (N >= T) fy_resolve(c, S, N, T);
+  } else {
+    downsample_serial(c, S, seed, N, T);
+  }
+  gather_mask_fields(a, c, mm, c.ix[0], T);
+  return kOk;
+}
+
+// FPS (App. C): start at 0, d2 = (dx*dx + dy*dy) + dz*dz without FMA,
+// mind = min(mind, d2), next = argmax mind (lowest index on ties).
+__device__ int32_t op_fps(const WaveArgs& a, Cloud& c, Smem& S, const OpDesc& op) {
+  if (op.num_points <= 0) return kOutOfBounds;
+  const uint32_t M = (uint32_t)op.num_points;
+  const uint32_t N = c.n[a.role_data];
+  if (N < M || M > c.cap) return kOutOfBounds;
+  const uint32_t mm = move_mask(a, c, true, op.gather_mask);
+  const int32_t st = check_move(a, c, mm);
+  if (st) return st;
+  const float* d = F(c, a.role_data);
+  float* mind = reinterpret_cast<float*>(c.ix[1]);
+  int32_t* idx = c.ix[0];
+  for (uint32_t i = threadIdx.x; i < N; i += blockDim.x) mind[i] = INFINITY;
+  __syncthreads();
+  uint32_t sel = 0;
+  for (uint32_t k = 0; k < M; ++k) {
+    if (threadIdx.x == 0) idx[k] = (int32_t)sel;
+    const float sx = d[3 * sel], sy = d[3 * sel + 1], sz = d[3 * sel + 2];
+    float bv = -INFINITY;
+    uint32_t bi = 0xFFFFFFFFu;
+    for (uint32_t i = threadIdx.x; i < N; i += blockDim.x) {
+      const float dx = __fsub_rn(d[3 * i], sx), dy = __fsub_rn(d[3 * i + 1], sy),
+                  dz = __fsub_rn(d[3 * i + 2], sz);
+      const float dd = __fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz));
+      float m = mind[i];
+      if (dd < m) m = dd;
+      mind[i] = m;
+      if (dev::argmax_better(m, i, bv, bi)) {
+        bv = m;
+        bi = i;
+      }
+    }
+    const dev::ArgMax r = dev::block_argmax(bv, bi, S.red);
+    sel = r.i == 0xFFFFFFFFu ? 0 : r.i;
+  }
+  __syncthreads();
+  gather_mask_fields(a, c, mm, idx, M);
+  return kOk;
+}
+
+__device__ int32_t op_range_crop(const WaveArgs& a, Cloud& c, Smem& S, const OpDesc& op) {
+  const float* d = F(c, a.role_data);
+  const uint32_t n = c.n[a.role_data];
+  const uint32_t mm = move_mask(a, c, true, op.gather_mask);
+  const int32_t st = check_move(a, c, mm);
+  if (st) return st;
+  const uint32_t m = compact(c, S, n, [&](uint32_t i) {
+    const float x = d[3 * i], y = d[3 * i + 1], z = d[3 * i + 2];
+    return x >= op.lo[0] && x <= op.hi[0] && y >= op.lo[1] && y <= op.hi[1] && z >= op.lo[2] &&
+           z <= op.hi[2];
+  });
+  gather_mask_fields(a, c, mm, c.ix[0], m);
+  return kOk;
+}
+
+// ---- decode ----------------------------------------------------------------
+// Copy len bytes (optionally XOR-delta decoding 4-byte words) from an
+// arbitrarily aligned source into a 16-B aligned destination.
+__device__ void decode_bytes(uint8_t* dst, const uint8_t* src, uint64_t len, bool delta,
+                             Smem& S) {
+  const uint32_t t = threadIdx.x, nt = blockDim.x, lane = t & 31, w = t >> 5, nw = nt >> 5;
+  if (!delta) {
+    const uint64_t nwords = len >> 2;
+    uint32_t* d32 = reinterpret_cast<uint32_t*>(dst);
+    for (uint64_t i = t; i < nwords; i += nt) d32[i] = dev::ld_u32_unaligned(src + 4 * i);
+    for (uint64_t i = (nwords << 2) + t; i < len; i += nt) dst[i] = src[i];
+    __syncthreads();
+    return;
+  }
+  const uint64_t nwords = len >> 2;  // len % 4 == 0 for delta columns
+  uint32_t* d32 = reinterpret_cast<uint32_t*>(dst);
+  const uint64_t seg = ((nwords + nw - 1) / nw + 31) & ~uint64_t(31);
+  const uint64_t s0 = min((uint64_t)w * seg, nwords), s1 = min(s0 + seg, nwords);
+  uint32_t carry = 0;
+  for (uint64_t base = s0; base < s1; base += 32) {
+    const uint64_t i = base + lane;
+    uint32_t v = i < s1 ? dev::ld_u32_unaligned(src + 4 * i) : 0u;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
+      if ((int)lane >= o) v ^= y;
+    }
+    v ^= carry;
+    if (i < s1) d32[i] = v;
+    carry = __shfl_sync(0xffffffffu, v, 31);
+  }
+  uint32_t* red = reinterpret_cast<uint32_t*>(S.red);
+  __syncthreads();
+  if (lane == 0) red[w] = carry;
+  __syncthreads();
+  uint32_t cin = 0;
+  for (uint32_t k = 0; k < w; ++k) cin ^= red[k];
+  if (cin)
+    for (uint64_t i = s0 + lane; i < s1; i += 32) d32[i] ^= cin;
+  __syncthreads();
+}
+
+}  // namespace
+
+// Applies the op chain (Pipeline map worker, pipeline.cpp:474-480): seed per
+// op = mix_seed(base, epoch, index, op id), or `fixed_seed` for the
+// single-op cloud-set API.  fail_op = 1-based failing transform.
+__device__ int32_t run_chain(const WaveArgs& a, Cloud& c, Smem& S, uint64_t epoch, uint64_t index,
+                             const uint64_t* fixed_seed, int32_t& fail_op) {
+  int32_t status = kOk;
+  const int fd = a.role_data;
+  for (int k = 0; status == kOk && k < a.n_ops; ++k) {
+    const OpDesc& op = a.ops[k];
+    const uint64_t seed =
+        fixed_seed ? *fixed_seed : rng::mix_seed(a.base_seed, epoch, index, op.seed_op_id);
+    if (c.n[fd] == 0) {
+      status = kEmptyCloud;
+    } else {
+      switch (op.kind) {
+        case kNormalize: status = op_normalize(a, c, S); break;
+        case kTranslate: status = op_translate(a, c, S, seed); break;
+        case kJitter: status = op_jitter(a, c, S, seed); break;
+        case kRotate: status = op_rotate(a, c, S, op, seed); break;
+        case kRandomScale: status = op_scale(a, c, S, seed); break;
+        case kFlipYz: status = op_flip(a, c, S, seed); break;
+        case kColorAugment: status = op_color(a, c, S, seed); break;
+        case kRandomCrop: status = op_random_crop(a, c, S, seed); break;
+        case kDownsample: status = op_downsample(a, c, S, op, seed); break;
+        case kFps: status = op_fps(a, c, S, op); break;
+        case kRangeCrop: status = op_range_crop(a, c, S, op); break;
+        default: status = kUnknownOp; break;
+      }
+    }
+    if (status != kOk) fail_op = k + 1;
+  }
+  return status;
+}
+
+// Carves the per-CTA buffers: staging, 4 index arrays and
+// tracked cur/alt pairs — in shared memory when they fit, else a global slab.
+__device__ uint8_t* carve(const WaveArgs& a, uint8_t* work, Cloud& proto);
+
+// Byte capacity of a tracked field's buffer.
+__device__ __forceinline__ uint64_t field_bytes(const WaveArgs& a, int f) {
+  return (uint64_t)a.cap_points * a.field_cap[f] + 16;
+}
+
+__global__ void __launch_bounds__(512) k_cloud(WaveArgs a) {
+  extern __shared__ __align__(128) uint8_t dyn[];
+  Smem& S = *reinterpret_cast<Smem*>(dyn);
+  uint8_t* work = dyn + ((sizeof(Smem) + 127) & ~size_t(127));
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) S.crc_tab[i] = crc::table_entry(i);
+  if (threadIdx.x == 0) {
+    dev::mbar_init(&S.bar, 1);
+    dev::fence_mbar_init();
+  }
+  __syncthreads();
+
+  Cloud proto{};
+  uint8_t* staging = carve(a, work, proto);
+
+  uint32_t phase = 0;
+  for (uint32_t s = blockIdx.x; s < a.n_samples; s += gridDim.x) {
+    const SampleWork sw = a.samples[s];
+    const PageRef pg = a.pages[sw.block_page];
+    const ScalarRec rec = a.recs[(uint64_t)a.groups[sw.group].first_rec + sw.row];
+    int32_t status = rec.status;
+    int32_t fail_op = 0;
+    // read_sample checks (format.cpp:741-755)
+    const bool range_ok = sw.blob_end <= pg.raw_len && sw.blob_start <= sw.blob_end;
+    if (status == kOk && !range_ok) status = kRangeOutOfBounds;
+    if (status == kOk && rec.n_lens != (uint32_t)a.n_bytes_fields) status = kCorruptPage;
+    uint64_t flen[kMaxBytesFields], foff[kMaxBytesFields];
+    if (status == kOk) {
+      uint64_t at = 0;
+      for (int f = 0; f < a.n_bytes_fields; ++f) {
+        flen[f] = rec.lens[f];
+        foff[f] = at;
+        if (at + flen[f] > sw.blob_end - sw.blob_start) status = kRangeOutOfBounds;
+        at += flen[f];
+      }
+    }
+    const bool lz4 = (pg.flags & kFlagOuterLz4) != 0;
+    if (!lz4 && pg.pay_len != pg.raw_len && status == kOk) status = kCorruptPage;
+    const uint8_t* src = lz4 ? a.raw + pg.raw_dst + sw.blob_start
+                             : a.bytes + pg.off + kPageHeaderBytes + sw.blob_start;
+    const uint64_t blen = range_ok ? sw.blob_end - sw.blob_start : 0;
+    const bool need_bytes = status == kOk || pg.crc_mode == 1;
+
+    // ---- stage the blob with one TMA bulk copy (smem mode) ----------------
+    const uint8_t* blob = src;
+    if (need_bytes && a.smem_mode && blen > 0) {
+      const uintptr_t g0 = reinterpret_cast<uintptr_t>(src) & ~uintptr_t(15);
+      const uintptr_t g1 = (reinterpret_cast<uintptr_t>(src) + blen + 15) & ~uintptr_t(15);
+      const uint32_t nbytes = (uint32_t)(g1 - g0);
+      dev::fence_proxy_async();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        dev::mbar_expect_tx(&S.bar, nbytes);
+        for (uint32_t o = 0; o < nbytes; o += 65536u)
+          dev::bulk_g2s(staging + o, reinterpret_cast<const void*>(g0 + o), min(65536u, nbytes - o),
+                        &S.bar);
+      }
+      dev::mbar_wait(&S.bar, phase);
+      phase ^= 1;
+      blob = staging + (reinterpret_cast<uintptr_t>(src) - g0);
+    }
+    // ---- fused payload CRC: this sample's share of its page ---------------
+    if (pg.crc_mode == 1 && blen > 0) {
+      const uint32_t cc = crc::cta_range(S.crc_tab, c_x2n.v, a.shift_tab, blob, blen,
+                                         pg.raw_len - sw.blob_end,
+                                         reinterpret_cast<uint32_t*>(S.red));
+      if (threadIdx.x == 0) atomicXor(a.page_crc_acc + sw.block_page, cc);
+    }
+
+    // ---- decode fields: XOR-delta per blob field (format.cpp:483-493) -----
+    Cloud c = proto;
+    c.present = 0;
+    if (status == kOk) {
+      const bool delta_page = (pg.flags & kFlagInnerDelta) != 0;
+      for (int f = 0; f < a.n_bytes_fields && status == kOk; ++f) {
+        const bool delta = delta_page && flen[f] >= 8 && (flen[f] % 4) == 0;
+        const int of = a.bytes_out[f];
+        if ((a.tracked_mask >> f) & 1u) {
+          if (flen[f] + 16 > field_bytes(a, f)) {
+            status = kOutOfBounds;
+            break;
+          }
+          decode_bytes(c.cur[f], blob + foff[f], flen[f], delta, S);
+          uint32_t e;
+          if (f == a.role_data || f == a.role_normal || f == a.role_color) {
+            e = 12;
+          } else if (f == a.role_intensity) {
+            e = 4;
+          } else {  // extra per-point field: bytes per point from "data"
+            const uint64_t nd = a.role_data >= 0 ? flen[a.role_data] / 12 : 0;
+            e = (nd && flen[f] % nd == 0) ? (uint32_t)(flen[f] / nd) : 0;
+          }
+          c.elem[f] = e ? e : 1;
+          c.n[f] = e ? (uint32_t)(flen[f] / e) : 0;
+          if (flen[f] > 0 || f == a.role_data) c.present |= 1u << f;
+        } else if (of >= 0) {
+          if (flen[f] > a.out_stride[of]) {
+            status = kOutOfBounds;
+            break;
+          }
+          decode_bytes(a.out[of] + (uint64_t)s * a.out_stride[of], blob + foff[f], flen[f], delta, S);
+          if (threadIdx.x == 0) a.out_len[(uint64_t)of * a.n_samples + s] = flen[f];
+        }
+      }
+    }
+
+    // ---- the op chain (Pipeline map worker, pipeline.cpp:474-480) ---------
+    if (status == kOk && a.n_ops > 0) {
+      const int fd = a.role_data;
+      // get_points / maybe_unpack checks (transforms.cpp:19-50)
+      if (fd < 0) status = kMissingField;
+      else if (flen[fd] % 12) status = kMissingField;
+      else if (flen[fd] == 0) status = kEmptyCloud;
+      if (status == kOk && a.role_normal >= 0 && flen[a.role_normal] % 12) status = kMissingField;
+      if (status == kOk && a.role_color >= 0 && flen[a.role_color] % 12) status = kMissingField;
+      if (status != kOk) fail_op = 1;
+      if (status == kOk) status = run_chain(a, c, S, sw.epoch, sw.index, nullptr, fail_op);
+    }
+
+    // ---- write tracked fields + scalar values into the batch slot --------
+    if (status == kOk) {
+      for (int f = 0; f < a.n_bytes_fields && status == kOk; ++f) {
+        const int of = a.bytes_out[f];
+        if (!((a.tracked_mask >> f) & 1u) || of < 0) continue;
+        const uint64_t nb = c.present >> f & 1u ? (uint64_t)c.n[f] * c.elem[f] : 0;
+        if (nb > a.out_stride[of]) {
+          status = kOutOfBounds;
+          break;
+        }
+        const uint32_t* s32 = reinterpret_cast<const uint32_t*>(c.cur[f]);
+        uint32_t* d32 = reinterpret_cast<uint32_t*>(a.out[of] + (uint64_t)s * a.out_stride[of]);
+        for (uint64_t i = threadIdx.x; i < (nb + 3) / 4; i += blockDim.x) d32[i] = s32[i];
+        if (threadIdx.x == 0) a.out_len[(uint64_t)of * a.n_samples + s] = nb;
+      }
+      uint32_t vo = rec.vals_off;
+      for (int f = 0; f < a.n_fields && status == kOk; ++f) {
+        const FieldDesc fdsc = a.fields[f];
+        if (fdsc.kind == kBytes) continue;
+        const uint8_t* v = a.vals + vo;
+        uint32_t nb, skip = 0;
+        if (fdsc.kind == kString) {
+          nb = *reinterpret_cast<const uint32_t*>(v);
+          v += 4;
+          skip = 4;
+        } else {
+          nb = ((fdsc.kind == kInt64 || fdsc.kind == kFloat64) ? 8u : 4u) * fdsc.elems;
+        }
+        const int of = fdsc.out_index;
+        if (nb > a.out_stride[of]) {
+          status = kOutOfBounds;
+          break;
+        }
+        uint8_t* dst = a.out[of] + (uint64_t)s * a.out_stride[of];
+        for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) dst[i] = v[i];
+        if (threadIdx.x == 0) a.out_len[(uint64_t)of * a.n_samples + s] = nb;
+        vo += nb + skip;
+      }
+    }
+    if (threadIdx.x == 0) {
+      a.sample_status[s] = status;
+      a.sample_op[s] = status == kOk ? -1 : fail_op;
+      a.sample_where[s] = 0;
+    }
+    __syncthreads();
+  }
+}
+
+__device__ uint8_t* carve(const WaveArgs& a, uint8_t* work, Cloud& proto) {
+  uint8_t* sbase = a.smem_mode ? work : a.gscratch + (uint64_t)blockIdx.x * a.gscratch_per_cta;
+  uint64_t off = 0;
+  auto take = [&](uint64_t nb) {
+    uint8_t* p = sbase + off;
+    off += (nb + 127) & ~uint64_t(127);
+    return p;
+  };
+  uint8_t* staging = a.smem_mode ? take((uint64_t)a.max_blob + 64) : nullptr;
+  proto.cap = a.cap_points;
+  for (int k = 0; k < 4; ++k)
+    proto.ix[k] = reinterpret_cast<int32_t*>(take((uint64_t)a.cap_points * 4 + 16));
+  for (int f = 0; f < a.n_bytes_fields; ++f) {
+    if (!((a.tracked_mask >> f) & 1u)) continue;
+    proto.cur[f] = take(field_bytes(a, f));
+    proto.alt[f] = take(field_bytes(a, f));
+  }
+  return staging;
+}
+
+// pcp_apply_map: one op over a CSR cloud set (apply_map per cloud with an
+// explicit seed, transforms.hpp:33-34).
+__global__ void __launch_bounds__(512) k_apply_set(WaveArgs a) {
+  extern __shared__ __align__(128) uint8_t dyn[];
+  Smem& S = *reinterpret_cast<Smem*>(dyn);
+  uint8_t* work = dyn + ((sizeof(Smem) + 127) & ~size_t(127));
+  Cloud proto{};
+  carve(a, work, proto);
+  __syncthreads();
+  for (uint32_t s = blockIdx.x; s < a.n_samples; s += gridDim.x) {
+    const uint64_t p0 = a.set_offset[s], p1 = a.set_offset[s + 1];
+    const uint64_t n = p1 >= p0 ? p1 - p0 : 0;
+    Cloud c = proto;
+    c.present = 0;
+    int32_t status = kOk, fail_op = 0;
+    if (n > a.cap_points) status = kOutOfBounds;
+    for (int f = 0; status == kOk && f < a.n_bytes_fields; ++f) {
+      if (!((a.tracked_mask >> f) & 1u)) continue;
+      const uint32_t e = a.set_elem[f];
+      const uint8_t* src = a.set_src[f] + p0 * e;
+      const uint64_t nb = n * e;
+      if ((e & 3) == 0) {
+        const uint32_t* s32 = reinterpret_cast<const uint32_t*>(src);
+        uint32_t* d32 = reinterpret_cast<uint32_t*>(c.cur[f]);
+        for (uint64_t i = threadIdx.x; i < nb / 4; i += blockDim.x) d32[i] = s32[i];
+      } else {
+        for (uint64_t i = threadIdx.x; i < nb; i += blockDim.x) c.cur[f][i] = src[i];
+      }
+      c.n[f] = (uint32_t)n;
+      c.elem[f] = e;
+      if (n > 0 || f == a.role_data) c.present |= 1u << f;
+    }
+    __syncthreads();
+    if (status == kOk && n == 0) status = kEmptyCloud;
+    if (status == kOk) status = run_chain(a, c, S, 0, 0, a.set_seeds + s, fail_op);
+    if (status == kOk) {
+      for (int f = 0; f < a.n_bytes_fields && status == kOk; ++f) {
+        if (!((a.tracked_mask >> f) & 1u) || !a.set_out[f]) continue;
+        const uint64_t nb = (uint64_t)c.n[f] * c.elem[f];
+        if (c.n[f] > a.set_out_cap) {
+          status = kOutOfBounds;
+          break;
+        }
+        uint8_t* dst = a.set_out[f] + (uint64_t)s * a.set_out_cap * a.set_elem[f];
+        for (uint64_t i = threadIdx.x; i < nb; i += blockDim.x) dst[i] = c.cur[f][i];
+      }
+    }
+    if (threadIdx.x == 0) {
+      a.sample_status[s] = status;
+      if (a.set_count) a.set_count[s] = status == kOk ? c.n[a.role_data] : 0;
+    }
+    __syncthreads();
+  }
+}
+
+// pcp_crc32_ranges: one CTA per range.
+__global__ void k_crc_ranges(const uint8_t* bytes, const uint64_t* off, const uint64_t* len,
+                             uint32_t n, const uint32_t* shift_tab, uint32_t* out) {
+  __shared__ uint32_t tab[256];
+  __shared__ uint32_t red[32];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) tab[i] = crc::table_entry(i);
+  __syncthreads();
+  for (uint32_t r = blockIdx.x; r < n; r += gridDim.x) {
+    const uint32_t c = crc::cta_range(tab, c_x2n.v, shift_tab, bytes + off[r], len[r], 0, red);
+    if (threadIdx.x == 0) out[r] = c;
+  }
+}
+
+// pcp_decode_pages: one CTA per serialized page — header, CRC, LZ4 or raw,
+// then the inner XOR-delta columns (decode_block_page, format.cpp:243-266).
+__global__ void k_decode_pages(const uint8_t* bytes, const uint64_t* page_off, uint32_t n_pages,
+                               uint8_t* out, const uint64_t* out_off, const uint32_t* col_first,
+                               const uint64_t* col_off, const uint64_t* col_len,
+                               const uint32_t* shift_tab, int32_t* status) {
+  __shared__ uint32_t tab[256];
+  __shared__ uint32_t red[32];
+  __shared__ Lz4Seq seqs[32];
+  __shared__ int32_t sst;
+  __shared__ uint32_t scount;
+  __shared__ int32_t st_sh;
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) tab[i] = crc::table_entry(i);
+  __syncthreads();
+  for (uint32_t pi = blockIdx.x; pi < n_pages; pi += gridDim.x) {
+    const uint8_t* pg = bytes + page_off[pi];
+    uint8_t flags = pg[0];
+    uint64_t raw_len = 0, pay_len = 0;
+    uint32_t crc_stored = 0;
+    for (int b = 0; b < 8; ++b) raw_len |= (uint64_t)pg[1 + b] << (8 * b);
+    for (int b = 0; b < 8; ++b) pay_len |= (uint64_t)pg[9 + b] << (8 * b);
+    for (int b = 0; b < 4; ++b) crc_stored |= (uint32_t)pg[17 + b] << (8 * b);
+    const uint8_t* pay = pg + kPageHeaderBytes;
+    uint8_t* dst = out + out_off[pi];
+    const uint32_t c = crc::cta_range(tab, c_x2n.v, shift_tab, pay, pay_len, 0, red);
+    if (threadIdx.x == 0) st_sh = (c == crc_stored) ? kOk : kChecksumMismatch;
+    __syncthreads();
+    if (st_sh == kOk) {
+      if (flags & kFlagOuterLz4) {
+        if (threadIdx.x < 32) {
+          const int32_t r = warp_lz4_decode(pay, pay_len, dst, raw_len, seqs, &sst, &scount);
+          if (threadIdx.x == 0) st_sh = r;
+        }
+      } else if (flags & kFlagStoredRaw) {
+        if (pay_len != raw_len) {
+          if (threadIdx.x == 0) st_sh = kCorruptPage;
+        } else {
+          for (uint64_t i = threadIdx.x; i < raw_len; i += blockDim.x) dst[i] = pay[i];
+        }
+      } else if (threadIdx.x == 0) {
+        st_sh = kCorruptPage;
+      }
+    }
+    __syncthreads();
+    if (st_sh == kOk && (flags & kFlagInnerDelta)) {
+      const uint32_t c0 = col_first[pi], c1 = col_first[pi + 1];
+      if (threadIdx.x == 0)
+        for (uint32_t k = c0; k < c1; ++k) {
+          if (col_off[k] + col_len[k] > raw_len) { st_sh = kColumnOutOfRange; break; }
+          if (col_len[k] % 4) { st_sh = kBadAlignment; break; }
+        }
+      __syncthreads();
+      // one warp per column, 32-word chunks, byte-addressed (any alignment)
+      const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+      if (st_sh == kOk)
+        for (uint32_t k = c0 + wid; k < c1; k += nw) {
+          uint8_t* col = dst + col_off[k];
+          const uint64_t nwd = col_len[k] / 4;
+          uint32_t carry = 0;
+          for (uint64_t base = 0; base < nwd; base += 32) {
+            const uint64_t i = base + lane;
+            uint32_t v = 0;
+            if (i < nwd)
+              v = (uint32_t)col[4 * i] | ((uint32_t)col[4 * i + 1] << 8) |
+                  ((uint32_t)col[4 * i + 2] << 16) | ((uint32_t)col[4 * i + 3] << 24);
+            for (int o = 1; o < 32; o <<= 1) {
+              const uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
+              if ((int)lane >= o) v ^= y;
+            }
+            v ^= carry;
+            __syncwarp();
+            if (i < nwd) {
+              col[4 * i] = (uint8_t)v;
+              col[4 * i + 1] = (uint8_t)(v >> 8);
+              col[4 * i + 2] = (uint8_t)(v >> 16);
+              col[4 * i + 3] = (uint8_t)(v >> 24);
+            }
+            carry = __shfl_sync(0xffffffffu, v, 31);
+            __syncwarp();
+          }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) status[pi] = st_sh;
+    __syncthreads();
+  }
+}
+
+// Page CRC verdicts, then the per-sample status in read_sample order:
+// scalar page, block page, record, ops (format.cpp:687-757).
+__global__ void k_finalize(WaveArgs a) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < a.n_pages) {
+    const PageRef pg = a.pages[i];
+    if (a.page_status[i] == kOk && a.page_crc_acc[i] != pg.crc) a.page_status[i] = kChecksumMismatch;
+  }
+}
+
+__global__ void k_sample_status(WaveArgs a) {
+  const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= a.n_samples) return;
+  const SampleWork sw = a.samples[s];
+  const int32_t sp = a.page_status[sw.scalar_page];
+  const int32_t bp = a.page_status[sw.block_page];
+  if (sp != kOk) {
+    a.sample_status[s] = sp;
+    a.sample_op[s] = 0;
+    a.sample_where[s] = 1;
+  } else if (bp != kOk) {
+    a.sample_status[s] = bp;
+    a.sample_op[s] = 0;
+    a.sample_where[s] = 2;
+  }
+}
+
+// =========================================================================
+// launch wrappers
+// =========================================================================
+void upload_x2n(cudaStream_t st) {
+  static bool done = false;
+  if (done) return;
+  const crc::X2N t = crc::make_x2n();
+  cudaMemcpyToSymbolAsync(c_x2n, &t, sizeof(t), 0, cudaMemcpyHostToDevice, st);
+  cudaStreamSynchronize(st);
+  done = true;
+}
+
+void build_shift_table(uint32_t* h_tab) {
+  const crc::X2N t = crc::make_x2n();
+  // x^(8*256*k): repeated multiplication by x^(8*256) = x^(2^11)
+  const uint32_t step = t.v[11];
+  uint32_t p = 1u << 31;
+  for (uint32_t k = 0; k < crc::kShiftEntries; ++k) {
+    h_tab[k] = p;
+    p = crc::multmodp(step, p);
+  }
+}
+
+size_t cloud_smem_fixed() { return (sizeof(Smem) + 127) & ~size_t(127); }
+
+cudaError_t launch_crc_windows(const uint8_t* bytes, const CrcWindow* win, uint32_t n_win,
+                               const uint32_t* shift_tab, uint32_t* acc, int sms,
+                               cudaStream_t st) {
+  if (!n_win) return cudaSuccess;
+  const uint32_t warps = 8;
+  uint32_t grid = (n_win + warps - 1) / warps;
+  grid = grid > (uint32_t)sms * 8 ? (uint32_t)sms * 8 : grid;
+  k_crc_windows<<<grid, warps * 32, 0, st>>>(bytes, win, n_win, shift_tab, acc);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_page_decode(const uint8_t* bytes, uint8_t* raw, const PageRef* pages,
+                               const uint32_t* todo, uint32_t n_todo, int32_t* status,
+                               cudaStream_t st) {
+  if (!n_todo) return cudaSuccess;
+  const uint32_t grid = (n_todo + 3) / 4;
+  k_page_decode<<<grid, 128, 0, st>>>(bytes, raw, pages, todo, n_todo, status);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_wave(const WaveArgs& a, int grid, int threads, size_t smem, cudaStream_t st,
+                        cudaEvent_t k0, cudaEvent_t k1) {
+  if (a.n_groups) k_scalar_parse<<<(a.n_groups + 127) / 128, 128, 0, st>>>(a);
+  if (k0) cudaEventRecord(k0, st);
+  if (a.n_samples) k_cloud<<<grid, threads, smem, st>>>(a);
+  if (k1) cudaEventRecord(k1, st);
+  if (a.n_pages) k_finalize<<<(a.n_pages + 255) / 256, 256, 0, st>>>(a);
+  if (a.n_samples) k_sample_status<<<(a.n_samples + 255) / 256, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+// Ragged batch → CSR: sample i's len[i] bytes from slot i to dst + off[i].
+__global__ void k_compact(const uint8_t* src, uint64_t stride, const uint64_t* off,
+                          const uint64_t* len, uint32_t n, uint8_t* dst) {
+  for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
+    const uint8_t* s = src + (uint64_t)i * stride;
+    uint8_t* d = dst + off[i];
+    const uint64_t L = len[i];
+    for (uint64_t k = threadIdx.x; k < L; k += blockDim.x) d[k] = s[k];
+  }
+}
+
+cudaError_t launch_compact(const uint8_t* src, uint64_t stride, const uint64_t* d_off,
+                           const uint64_t* d_len, uint32_t n, uint8_t* dst, cudaStream_t st) {
+  if (!n) return cudaSuccess;
+  k_compact<<<n < 1024 ? n : 1024, 256, 0, st>>>(src, stride, d_off, d_len, n, dst);
+  return cudaGetLastError();
+}
+
+cudaError_t occupancy_cloud(int* n, int threads, size_t smem) {
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(n, k_cloud, threads, smem);
+}
+
+cudaError_t launch_apply_set(const WaveArgs& a, int grid, int threads, size_t smem,
+                             cudaStream_t st) {
+  cudaError_t e = cudaFuncSetAttribute(k_apply_set, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  if (a.n_samples) k_apply_set<<<grid, threads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_crc_ranges(const uint8_t* bytes, const uint64_t* off, const uint64_t* len,
+                              uint32_t n, const uint32_t* shift_tab, uint32_t* out,
+                              cudaStream_t st) {
+  if (!n) return cudaSuccess;
+  k_crc_ranges<<<n < 4096 ? n : 4096, 256, 0, st>>>(bytes, off, len, n, shift_tab, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_decode_pages(const uint8_t* bytes, const uint64_t* page_off, uint32_t n,
+                                uint8_t* out, const uint64_t* out_off, const uint32_t* col_first,
+                                const uint64_t* col_off, const uint64_t* col_len,
+                                const uint32_t* shift_tab, int32_t* status, cudaStream_t st) {
+  if (!n) return cudaSuccess;
+  k_decode_pages<<<n < 4096 ? n : 4096, 256, 0, st>>>(bytes, page_off, n, out, out_off, col_first,
+                                                     col_off, col_len, shift_tab, status);
+  return cudaGetLastError();
+}
+
+cudaError_t set_cloud_smem(size_t bytes) {
+  return cudaFuncSetAttribute(k_cloud, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+}  // namespace pcp

@@ -1,0 +1,51 @@
+// kernels.h — host-visible launch wrappers of kernels.cu (internal).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "pcp_internal.h"
+
+namespace pcp {
+
+// One CRC work unit: `len` payload bytes at absolute `start`, which end
+// `after` bytes before the end of page `page`'s payload.
+struct CrcWindow {
+  uint64_t start;
+  uint64_t len;
+  uint64_t after;
+  uint32_t page;
+  uint32_t pad;
+};
+
+void upload_x2n(cudaStream_t st);
+void build_shift_table(uint32_t* h_tab);  // crc::kShiftEntries entries
+size_t cloud_smem_fixed();
+cudaError_t set_cloud_smem(size_t bytes);
+cudaError_t launch_crc_windows(const uint8_t* bytes, const CrcWindow* win, uint32_t n_win,
+                               const uint32_t* shift_tab, uint32_t* acc, int sms,
+                               cudaStream_t st);
+cudaError_t launch_page_decode(const uint8_t* bytes, uint8_t* raw, const PageRef* pages,
+                               const uint32_t* todo, uint32_t n_todo, int32_t* status,
+                               cudaStream_t st);
+// scalar parse → cloud interpreter → page verdicts → sample status
+cudaError_t launch_wave(const WaveArgs& a, int grid, int threads, size_t smem, cudaStream_t st,
+                        cudaEvent_t k0 = nullptr, cudaEvent_t k1 = nullptr);
+cudaError_t occupancy_cloud(int* n, int threads, size_t smem);
+cudaError_t launch_compact(const uint8_t* src, uint64_t stride, const uint64_t* d_off,
+                           const uint64_t* d_len, uint32_t n, uint8_t* dst, cudaStream_t st);
+
+cudaError_t launch_apply_set(const WaveArgs& a, int grid, int threads, size_t smem,
+                             cudaStream_t st);
+cudaError_t launch_crc_ranges(const uint8_t* bytes, const uint64_t* off, const uint64_t* len,
+                              uint32_t n, const uint32_t* shift_tab, uint32_t* out,
+                              cudaStream_t st);
+cudaError_t launch_decode_pages(const uint8_t* bytes, const uint64_t* page_off, uint32_t n,
+                                uint8_t* out, const uint64_t* out_off, const uint32_t* col_first,
+                                const uint64_t* col_off, const uint64_t* col_len,
+                                const uint32_t* shift_tab, int32_t* status, cudaStream_t st);
+
+constexpr uint32_t kShiftEntries = 8192;
+
+}  // namespace pcp

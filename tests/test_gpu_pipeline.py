@@ -1,0 +1,155 @@
+"""GPU parity: the B200 pipeline (through the C ABI) against the oracles on
+the same PcRecord files, graph JSON, walk and seeds."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from expect import assert_batches_equal, expected_run, tolerant_fields
+
+pytestmark = pytest.mark.gpu
+
+
+def _ds(pcp, tmp_path, gen, n, group, slices=1, quantized=False, **kw):
+    from paper_2603_16945_b200 import synth
+    schema, samples = getattr(synth, gen)(n, quantized=quantized, **kw)
+    return pcp.write_dataset(tmp_path, "ds", schema, samples, slice_count=slices, group_size=group)
+
+
+def _run(pcp, primary, graph, **kw):
+    return pcp.run_pipeline(primary, graph, **kw)
+
+
+@pytest.mark.parametrize("quantized", [False, True])
+def test_shapenet_chain_parity(pcp, ref, orc, tmp_path, quantized):
+    """C2 chain: normalize → downsample 1024 (+seg) → random_scale → shuffle."""
+    from paper_2603_16945_b200 import synth
+    primary = _ds(pcp, tmp_path, "shapenet", 70, group=16, slices=2, quantized=quantized)
+    g = synth.graph(synth.CHAINS["shapenet_part"], batch_size=8)
+    got = _run(pcp, primary, g)
+    want = expected_run(ref, orc, primary, g)
+    assert_batches_equal(got, want)
+
+
+@pytest.mark.parametrize("op", ["normalize", "translate", "jitter", "rotate", "random_scale",
+                                "flip_yz", "random_crop", ("downsample", {"num_points": 300}),
+                                ("downsample", {"num_points": 1500})])
+def test_reference_op_parity(pcp, ref, orc, tmp_path, op):
+    """Each reference map kind alone, against the compiled reference Pipeline."""
+    from paper_2603_16945_b200 import synth
+    primary = _ds(pcp, tmp_path, "modelnet", 24, group=8, n_points=1000)
+    g = synth.graph([op], batch_size=4)
+    got = _run(pcp, primary, g)
+    want = expected_run(ref, orc, primary, g)
+    assert_batches_equal(got, want, float_fields=tolerant_fields(g))
+
+
+def test_color_augment_and_crop_parity(pcp, ref, orc, tmp_path):
+    from paper_2603_16945_b200 import synth
+    primary = _ds(pcp, tmp_path, "scannet", 6, group=2, lo=3000, hi=9000)
+    g = synth.graph(["color_augment", "random_crop", ("downsample", {"num_points": 2048})],
+                    batch_size=2)
+    assert_batches_equal(_run(pcp, primary, g), expected_run(ref, orc, primary, g))
+
+
+def test_fps_parity(pcp, ref, orc, tmp_path):
+    """C1 chain at reduced size (FPS is App. C; oracle = restatement)."""
+    from paper_2603_16945_b200 import synth
+    primary = _ds(pcp, tmp_path, "modelnet", 8, group=4, n_points=3000)
+    g = synth.graph([("normalize", {}), ("fps", {"num_points": 256}), ("rotate", {}), ("jitter", {})],
+                    batch_size=4)
+    got = _run(pcp, primary, g)
+    want = expected_run(ref, orc, primary, g)
+    assert_batches_equal(got, want, float_fields=tolerant_fields(g))
+
+
+def test_range_crop_kitti_parity(pcp, ref, orc, tmp_path):
+    from paper_2603_16945_b200 import synth
+    primary = _ds(pcp, tmp_path, "kitti", 4, group=2, lo=20000, hi=30000)
+    g = synth.graph(synth.CHAINS["kitti"], batch_size=2)
+    got = _run(pcp, primary, g)
+    want = expected_run(ref, orc, primary, g)
+    assert_batches_equal(got, want, float_fields=tolerant_fields(g))
+
+
+def test_fused_graph_and_epochs(pcp, ref, orc, tmp_path):
+    """fuse_maps seeding by original op ids; 3 epochs; remainder kept."""
+    from paper_2603_16945_b200 import synth
+    primary = _ds(pcp, tmp_path, "shapenet", 21, group=5, n_points=600)
+    g = synth.graph(["translate", "random_scale", "flip_yz"], batch_size=4, drop_remainder=False)
+    fused_map = {"id": 1, "kind": "map", "num_workers": 2, "queue_capacity": 8,
+                 "fused": [{"map": "translate", "params": {}, "op_id": 1},
+                           {"map": "random_scale", "params": {}, "op_id": 2},
+                           {"map": "flip_yz", "params": {}, "op_id": 3}]}
+    gf = dict(g, ops=[g["ops"][0], fused_map] + g["ops"][4:])
+    want = expected_run(ref, orc, primary, g, epochs=3)
+    assert_batches_equal(_run(pcp, primary, g, epochs=3), want)
+    assert_batches_equal(_run(pcp, primary, gf, epochs=3), want)
+
+
+def test_shard_walk(pcp, ref, orc, tmp_path):
+    """A GPU's shard = an explicit entry list; seeds use the walk position."""
+    from paper_2603_16945_b200 import synth
+    primary = _ds(pcp, tmp_path, "shapenet", 40, group=8, slices=4, n_points=512)
+    ids = [i for i in range(40) if (i // 10) % 2 == 1]  # slices 1 and 3
+    g = synth.graph(["normalize", ("downsample", {"num_points": 256})], batch_size=4)
+    assert_batches_equal(_run(pcp, primary, g, ids=ids), expected_run(ref, orc, primary, g, ids=ids))
+
+
+def test_staged_matches_resident(pcp, tmp_path):
+    from paper_2603_16945_b200 import synth
+    primary = _ds(pcp, tmp_path, "shapenet", 48, group=8, quantized=True, n_points=700)
+    g = synth.graph(synth.CHAINS["shapenet_part"][:2], batch_size=8)
+    a = _run(pcp, primary, g, resident=True, wave_batches=2)
+    b = _run(pcp, primary, g, resident=False, wave_batches=3)
+    assert_batches_equal(a, b)
+
+
+def test_serial_fisher_yates_path(pcp, ref, orc, tmp_path):
+    """The rare Lemire-rejection fallback (serial engine) is exact too."""
+    from paper_2603_16945_b200 import synth
+    primary = _ds(pcp, tmp_path, "shapenet", 16, group=8, n_points=900)
+    g = synth.graph([("downsample", {"num_points": 500}), ("downsample", {"num_points": 1200})],
+                    batch_size=4)
+    want = expected_run(ref, orc, primary, g)
+    assert_batches_equal(_run(pcp, primary, g, force_serial_fy=True), want)
+
+
+def test_corrupt_payload_is_worker_panic(pcp, tmp_path):
+    """A flipped payload byte → CRC mismatch → WorkerPanic at that batch."""
+    from paper_2603_16945_b200 import synth
+    primary = _ds(pcp, tmp_path, "shapenet", 32, group=8, n_points=256)
+    with open(primary, "rb") as f:
+        blob = bytearray(f.read())
+    blob[-100] ^= 0x10  # inside the last group's block payload
+    with open(primary, "wb") as f:
+        f.write(blob)
+    g = synth.graph(["normalize"], batch_size=8)
+    p = pcp.Pipeline(primary, g)
+    for _ in range(3):
+        assert p.next_batch() is not None  # groups 0..2 are intact
+    with pytest.raises(pcp.PcError) as ei:
+        p.next_batch()
+    assert ei.value.errc == "WorkerPanic"
+    assert "ChecksumMismatch" in str(ei.value)
+    p.close()
+
+
+def test_empty_cloud_and_missing_field(pcp, tmp_path):
+    schema = {"fields": {"data": {"type": "bytes"}, "label": {"type": "int32"}}}
+    samples = [{"data": np.zeros(0, np.uint8), "label": np.array([1], np.int32)}] * 4
+    primary = pcp.write_dataset(tmp_path, "ds", schema, samples, group_size=4)
+    from paper_2603_16945_b200 import synth
+    p = pcp.Pipeline(primary, synth.graph(["normalize"], batch_size=2))
+    with pytest.raises(pcp.PcError) as ei:
+        p.next_batch()
+    assert "EmptyCloud" in str(ei.value) and "op 1" in str(ei.value)
+    p.close()
+
+
+def test_no_map_passthrough_stacks(pcp, ref, orc, tmp_path):
+    from paper_2603_16945_b200 import synth
+    primary = _ds(pcp, tmp_path, "kitti", 6, group=3, lo=1000, hi=1000)
+    g = synth.graph([], batch_size=3)
+    assert_batches_equal(_run(pcp, primary, g), expected_run(ref, orc, primary, g))
