@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <filesystem>
 #include <map>
@@ -110,6 +111,7 @@ struct HostBuf {  // pinned
 };
 
 inline uint64_t align16(uint64_t v) { return (v + 15) & ~uint64_t(15); }
+inline uint64_t align4(uint64_t v) { return (v + 3) & ~uint64_t(3); }
 
 // ---------------------------------------------------------------- graph
 struct MapStep {
@@ -285,9 +287,12 @@ struct Wave {
   uint64_t first_batch = 0;  // batch index of the wave's first batch
   uint32_t n_batches = 0;
   bool launched = false;
+  cudaStream_t stream = nullptr;  // one stream per slot: consecutive waves overlap
   cudaEvent_t done = nullptr, k0 = nullptr, k1 = nullptr;
+  DevBuf gscratch;                // k_cloud global slab (smem_mode 0), per slot
   // device
-  DevBuf bytes_stage, raw, tables, outs, compact, compact_meta;
+  DevBuf bytes_stage, raw, tables, outs, compact, compact_meta, lz4_scratch, lz4_timing;
+  uint32_t n_todo = 0;
   HostBuf h_tables, h_res, h_compact_meta;
   std::vector<uint64_t> out_base;  // per output field: offset in outs
   // results (pinned, filled by D2H)
@@ -311,6 +316,8 @@ struct Pipeline {
   uint32_t wave_batches = 0;
   uint64_t epochs = 1;
   bool force_serial_fy = false;
+  bool lz4_timing = std::getenv("PCP_LZ4_TIMING") != nullptr;
+  std::vector<double> lz4_phase_cycles = std::vector<double>(4, 0.0);
   cudaStream_t stream = nullptr;        // wave compute (copies + kernels)
   cudaStream_t serve_stream = nullptr;  // batch views: compaction, user D2H
   // byte store: all slice data areas, 16-B aligned, 64 B slack each side
@@ -347,6 +354,7 @@ struct Pipeline {
 
   ~Pipeline() {
     for (auto& w : slots) {
+      if (w.stream) cudaStreamDestroy(w.stream);
       if (w.done) cudaEventDestroy(w.done);
       if (w.k0) cudaEventDestroy(w.k0);
       if (w.k1) cudaEventDestroy(w.k1);
@@ -391,8 +399,10 @@ struct Pipeline {
     d_shift.ensure(shift.size() * 4);
     CK(cudaMemcpyAsync(d_shift.p, shift.data(), shift.size() * 4, cudaMemcpyHostToDevice, stream));
     CK(cudaStreamSynchronize(stream));
-    slots.resize(2);
+    slots.resize(3);
     for (auto& w : slots) {
+      CK(cudaStreamCreateWithFlags(&w.stream, cudaStreamNonBlocking));
+      if (!proto.smem_mode) w.gscratch.ensure(proto.gscratch_per_cta * grid);
       CK(cudaEventCreate(&w.done));
       CK(cudaEventCreate(&w.k0));
       CK(cudaEventCreate(&w.k1));
@@ -549,20 +559,20 @@ struct Pipeline {
       if (bi >= 0) {
         if ((tracked >> bi) & 1u) {
           const uint64_t e = a.field_cap[bi];
-          if (state[bi] == 1) o.stride = align16(fixed_pts[bi] * e);
-          else if (state[bi] == 2) o.stride = align16(cap * e);
-          else o.stride = align16(std::max<uint64_t>(max_len[bi], 1));
+          if (state[bi] == 1) o.stride = align4(fixed_pts[bi] * e);
+          else if (state[bi] == 2) o.stride = align4(cap * e);
+          else o.stride = align4(std::max<uint64_t>(max_len[bi], 1));
         } else {
-          o.stride = align16(max_len[bi]);
+          o.stride = align4(max_len[bi]);
         }
         a.bytes_out[bi] = (int32_t)outs.size();
       } else if (h.schema[f].kind == kString) {
         o.stride = 4096;
       } else {
         const uint64_t es = (h.schema[f].kind == kInt64 || h.schema[f].kind == kFloat64) ? 8 : 4;
-        o.stride = align16(es * h.schema[f].elems());
+        o.stride = es * h.schema[f].elems();
       }
-      o.stride = std::max<uint64_t>(o.stride, 16);
+      o.stride = std::max<uint64_t>(o.stride, 4);
       a.fields[f].out_index = (int32_t)outs.size();
       outs.push_back(o);
     }
@@ -587,9 +597,7 @@ struct Pipeline {
       uint64_t per = 4 * rnd((uint64_t)cap * 4 + 16);
       for (size_t f = 0; f < bytes_fields.size(); ++f)
         if ((tracked >> f) & 1u) per += 2 * rnd((uint64_t)cap * a.field_cap[f] + 16);
-      a.gscratch_per_cta = per;
-      d_gscratch.ensure(per * grid);
-      a.gscratch = d_gscratch.as<uint8_t>();
+      a.gscratch_per_cta = per;  // slabs are allocated per wave slot
     }
     a.force_serial_fy = force_serial_fy ? 1 : 0;
   }
@@ -599,7 +607,14 @@ struct Pipeline {
     const uint64_t n = walk.size();
     const uint32_t B = g.batch_size;
     uint32_t wb = wave_batches;
-    if (!wb) wb = (uint32_t)std::max<uint64_t>(1, 8192 / B);
+    if (!wb) {
+      // default: >= 8192 samples and >= 2 pages (groups) per SM in flight, so
+      // every page's serial LZ4 chain runs concurrently
+      uint64_t gmax = 1;
+      for (const auto& gr : h.groups) gmax = std::max<uint64_t>(gmax, gr.sample_count);
+      const uint64_t want = std::max<uint64_t>(8192, 2ull * sms * gmax);
+      wb = (uint32_t)std::max<uint64_t>(1, (want + B - 1) / B);
+    }
     const uint64_t W = (uint64_t)wb * B;
     const uint64_t usable = g.drop_remainder ? (n / B) * B : n;
     for (uint64_t e = 0; e < epochs; ++e)
@@ -638,6 +653,13 @@ struct Pipeline {
     std::vector<PageRef> pages(2 * ng);
     std::vector<GroupWork> gw(ng);
     std::vector<uint32_t> todo;
+    std::vector<uint64_t> todo_scratch;
+    uint64_t scratch_at = 0;
+    auto add_todo = [&](uint32_t page, const PageHead& ph) {
+      todo.push_back(page);
+      todo_scratch.push_back(scratch_at);
+      if (ph.flags & kFlagOuterLz4) scratch_at = align16(scratch_at + lz4_scratch_bytes(ph.pay_len));
+    };
     std::vector<CrcWindow> wins;
     uint64_t raw_at = 0, vals_at = 0;
     uint32_t rec_at = 0;
@@ -674,7 +696,7 @@ struct Pipeline {
       sp.raw_dst = raw_at;
       raw_at = align16(raw_at + sh.raw_len) + 16;
       sp.crc_mode = 0;
-      todo.push_back(i);
+      add_todo(i, sh);
       PageRef& bp = pages[ng + i];
       bp.off = stage_off[ng + i];
       bp.raw_len = bh.raw_len;
@@ -685,7 +707,7 @@ struct Pipeline {
       if (bh.flags & kFlagOuterLz4) {
         bp.raw_dst = raw_at;
         raw_at = align16(raw_at + bh.raw_len) + 16;
-        todo.push_back(ng + i);
+        add_todo(ng + i, bh);
       }
       // fused CRC only when this wave's samples tile the stored-raw payload
       // exactly once
@@ -748,7 +770,8 @@ struct Pipeline {
     const uint64_t o_groups = o_pages + sz(pages.size() * sizeof(PageRef));
     const uint64_t o_samples = o_groups + sz(gw.size() * sizeof(GroupWork));
     const uint64_t o_todo = o_samples + sz(sw.size() * sizeof(SampleWork));
-    const uint64_t o_wins = o_todo + sz(todo.size() * 4);
+    const uint64_t o_tsc = o_todo + sz(todo.size() * 4);
+    const uint64_t o_wins = o_tsc + sz(todo.size() * 8);
     const uint64_t up_bytes = o_wins + sz(wins.size() * sizeof(CrcWindow));
     // device-only regions after the uploaded part
     const uint64_t o_recs = up_bytes;
@@ -766,6 +789,7 @@ struct Pipeline {
     std::memcpy(ht + o_groups, gw.data(), gw.size() * sizeof(GroupWork));
     std::memcpy(ht + o_samples, sw.data(), sw.size() * sizeof(SampleWork));
     std::memcpy(ht + o_todo, todo.data(), todo.size() * 4);
+    std::memcpy(ht + o_tsc, todo_scratch.data(), todo_scratch.size() * 8);
     std::memcpy(ht + o_wins, wins.data(), wins.size() * sizeof(CrcWindow));
     w.tables.ensure(total);
     uint8_t* dt = w.tables.as<uint8_t>();
@@ -776,15 +800,16 @@ struct Pipeline {
       uint64_t d_at = 64;
       for (const auto& r : runs) {
         CK(cudaMemcpyAsync(w.bytes_stage.as<uint8_t>() + d_at, h_store.as<uint8_t>() + r.first,
-                           r.second, cudaMemcpyHostToDevice, stream));
+                           r.second, cudaMemcpyHostToDevice, w.stream));
         d_at += r.second + 64;
       }
       bytes = w.bytes_stage.as<uint8_t>();
       for (const auto& r : runs) h2d_bytes += r.second;
     }
-    CK(cudaMemcpyAsync(dt, ht, up_bytes, cudaMemcpyHostToDevice, stream));
-    CK(cudaMemsetAsync(dt + o_acc, 0, o_len - o_acc, stream));
+    CK(cudaMemcpyAsync(dt, ht, up_bytes, cudaMemcpyHostToDevice, w.stream));
+    CK(cudaMemsetAsync(dt + o_acc, 0, o_len - o_acc, w.stream));
     w.raw.ensure(raw_at + 64);
+    w.lz4_scratch.ensure(scratch_at + 64);
     // outputs
     w.out_base.resize(outs.size());
     uint64_t out_total = 0;
@@ -811,16 +836,25 @@ struct Pipeline {
     a.sample_where = reinterpret_cast<int32_t*>(dt + o_swh);
     a.out_len = reinterpret_cast<uint64_t*>(dt + o_len);
     a.shift_tab = d_shift.as<uint32_t>();
+    if (!a.smem_mode) a.gscratch = w.gscratch.as<uint8_t>();
     for (size_t f = 0; f < outs.size(); ++f) {
       a.out[f] = w.outs.as<uint8_t>() + w.out_base[f];
       a.out_stride[f] = outs[f].stride;
     }
     // ---- kernels ---------------------------------------------------------------
     CK(launch_crc_windows(bytes, reinterpret_cast<const CrcWindow*>(dt + o_wins),
-                          (uint32_t)wins.size(), d_shift.as<uint32_t>(), a.page_crc_acc, sms, stream));
+                          (uint32_t)wins.size(), d_shift.as<uint32_t>(), a.page_crc_acc, sms, w.stream));
+    long long* tm = nullptr;
+    if (lz4_timing) {  // PCP_LZ4_TIMING=1: per-page phase clocks (diagnostics)
+      w.lz4_timing.ensure(todo.size() * 64);
+      CK(cudaMemsetAsync(w.lz4_timing.p, 0, todo.size() * 64, w.stream));
+      tm = w.lz4_timing.as<long long>();
+    }
     CK(launch_page_decode(bytes, a.raw, a.pages, reinterpret_cast<const uint32_t*>(dt + o_todo),
-                          (uint32_t)todo.size(), a.page_status, stream));
-    CK(launch_wave(a, grid, threads, smem, stream, w.k0, w.k1));
+                          reinterpret_cast<const uint64_t*>(dt + o_tsc), w.lz4_scratch.as<uint8_t>(),
+                          (uint32_t)todo.size(), a.page_status, w.stream, tm));
+    w.n_todo = (uint32_t)todo.size();
+    CK(launch_wave(a, grid, threads, smem, w.stream, w.k0, w.k1));
     launches += (wins.empty() ? 0 : 1) + (todo.empty() ? 0 : 1) + (ng ? 1 : 0) + 1 + 1 + 1;
     h2d_bytes += up_bytes;
     // ---- results back to pinned host -------------------------------------------
@@ -831,11 +865,11 @@ struct Pipeline {
     w.h_op = reinterpret_cast<int32_t*>(hr + align16(w.n * 4));
     w.h_where = reinterpret_cast<int32_t*>(hr + 2 * align16(w.n * 4));
     w.h_len = reinterpret_cast<uint64_t*>(hr + 3 * align16(w.n * 4));
-    CK(cudaMemcpyAsync(w.h_status, dt + o_sst, w.n * 4, cudaMemcpyDeviceToHost, stream));
-    CK(cudaMemcpyAsync(w.h_op, dt + o_sop, w.n * 4, cudaMemcpyDeviceToHost, stream));
-    CK(cudaMemcpyAsync(w.h_where, dt + o_swh, w.n * 4, cudaMemcpyDeviceToHost, stream));
-    CK(cudaMemcpyAsync(w.h_len, dt + o_len, outs.size() * w.n * 8, cudaMemcpyDeviceToHost, stream));
-    CK(cudaEventRecord(w.done, stream));
+    CK(cudaMemcpyAsync(w.h_status, dt + o_sst, w.n * 4, cudaMemcpyDeviceToHost, w.stream));
+    CK(cudaMemcpyAsync(w.h_op, dt + o_sop, w.n * 4, cudaMemcpyDeviceToHost, w.stream));
+    CK(cudaMemcpyAsync(w.h_where, dt + o_swh, w.n * 4, cudaMemcpyDeviceToHost, w.stream));
+    CK(cudaMemcpyAsync(w.h_len, dt + o_len, outs.size() * w.n * 8, cudaMemcpyDeviceToHost, w.stream));
+    CK(cudaEventRecord(w.done, w.stream));
     w.launched = true;
   }
 
@@ -862,10 +896,8 @@ struct Pipeline {
     if (failed) fail(fail_code, fail_msg);
     if (cur < 0 || served >= slots[cur].n_batches) {
       if (cur >= 0) ++waves_done;
-      if (next_plan >= plan.size() && !(next_plan < plan.size())) {
-        // nothing prefetched beyond?  check whether the other slot is in flight
-      }
-      const int nxt = cur < 0 ? 0 : 1 - cur;
+      const int ns = (int)slots.size();
+      const int nxt = cur < 0 ? 0 : (cur + 1) % ns;
       Wave& wn = slots[nxt];
       if (!wn.launched) {
         if (next_plan >= plan.size()) {
@@ -878,6 +910,14 @@ struct Pipeline {
       float ms = 0;
       CK(cudaEventElapsedTime(&ms, wn.k0, wn.k1));
       cloud_kernel_ms += ms;
+      if (lz4_timing && wn.n_todo) {
+        std::vector<long long> tm(wn.n_todo * 8);
+        CK(cudaMemcpy(tm.data(), wn.lz4_timing.p, tm.size() * 8, cudaMemcpyDeviceToHost));
+        for (uint32_t i = 0; i < wn.n_todo; ++i)
+          if (tm[i * 8 + 4])
+            for (int ph = 0; ph < 4; ++ph)
+              lz4_phase_cycles[ph] = std::max(lz4_phase_cycles[ph], (double)(tm[i * 8 + ph + 1] - tm[i * 8 + ph]));
+      }
       if (cur >= 0) slots[cur].launched = false;
       cur = nxt;
       served = 0;
@@ -887,8 +927,12 @@ struct Pipeline {
       alg_bytes += wn.in_payload_bytes;
       points_in += wn.in_points;
       payload_bytes += wn.in_payload_bytes;
-      // prefetch the following wave into the slot we just left
-      if (next_plan < plan.size()) launch(slots[1 - cur], next_plan++);
+      // keep slots-1 waves in flight ahead of the one being served (waves go
+      // to slots in ring order on per-slot streams, so they overlap)
+      for (int d = 1; d < ns && next_plan < plan.size(); ++d) {
+        Wave& wp = slots[(cur + d) % ns];
+        if (!wp.launched) launch(wp, next_plan++);
+      }
     }
     Wave& w = slots[cur];
     const uint32_t B = g.batch_size;
@@ -974,7 +1018,8 @@ struct Pipeline {
            {"smem_bytes", smem},
            {"smem_mode", proto.smem_mode},
            {"cap_points", proto.cap_points},
-           {"resident", resident}};
+           {"resident", resident},
+           {"lz4_max_phase_cycles", lz4_phase_cycles}};
     stats_json = j.dump();
     return stats_json.c_str();
   }
@@ -1043,8 +1088,27 @@ int pcp_decode_pages(const uint8_t* d_bytes, const uint64_t* d_page_off, uint32_
   return guarded([&] {
     auto st = (cudaStream_t)stream;
     DeviceCtx& c = device_ctx(st);
+    if (!n_pages) return;
+    // page heads → per-page LZ4 scratch slabs (convenience path: one D2H)
+    std::vector<uint64_t> off(n_pages), sc_off(n_pages);
+    CK(cudaMemcpyAsync(off.data(), d_page_off, n_pages * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    uint64_t total = 0;
+    for (uint32_t i = 0; i < n_pages; ++i) {
+      uint8_t head[kPageHeaderBytes];
+      CK(cudaMemcpy(head, d_bytes + off[i], kPageHeaderBytes, cudaMemcpyDeviceToHost));
+      uint64_t pay;
+      std::memcpy(&pay, head + 9, 8);
+      sc_off[i] = total;
+      if (head[0] & kFlagOuterLz4) total = align16(total + lz4_scratch_bytes(std::min<uint64_t>(pay, 1ull << 32)));
+    }
+    c.scratch.ensure(total + 128 + n_pages * 8);
+    uint64_t* d_sc_off = reinterpret_cast<uint64_t*>(c.scratch.as<uint8_t>() + align16(total + 64));
+    CK(cudaMemcpyAsync(d_sc_off, sc_off.data(), n_pages * 8, cudaMemcpyHostToDevice, st));
     CK(launch_decode_pages(d_bytes, d_page_off, n_pages, d_out, d_out_off, d_col_first, d_col_off,
-                           d_col_len, c.shift.as<uint32_t>(), d_status, st));
+                           d_col_len, c.shift.as<uint32_t>(), d_sc_off, c.scratch.as<uint8_t>(),
+                           d_status, st));
+    CK(cudaStreamSynchronize(st));
   });
 }
 

@@ -22,6 +22,7 @@
 #include "device_crc.cuh"
 #include "device_rng.cuh"
 #include "device_util.cuh"
+#include "lz4_parallel.cuh"
 #include "kernels.h"
 #include "pcp_internal.h"
 
@@ -160,33 +161,52 @@ __device__ int32_t warp_lz4_decode(const uint8_t* src, uint64_t n, uint8_t* dst,
   return status;
 }
 
-// One warp per page: LZ4 decode or stored-raw copy into the raw arena.
-__global__ void k_page_decode(const uint8_t* bytes, uint8_t* raw, const PageRef* pages,
-                              const uint32_t* todo, uint32_t n_todo, int32_t* page_status) {
-  constexpr int kWarps = 4;
-  __shared__ Lz4Seq seqs[kWarps][32];
-  __shared__ int32_t sst[kWarps];
-  __shared__ uint32_t scount[kWarps];
-  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-  for (uint32_t w = blockIdx.x * kWarps + wl; w < n_todo; w += gridDim.x * kWarps) {
+// One CTA per page: LZ4 pages use the CTA-parallel decoder (lz4_parallel.cuh)
+// with a per-page scratch slab; stored-raw pages are copied.  The rare page
+// whose match count exceeds the scratch falls back to the warp decoder.
+__global__ void __launch_bounds__(256) k_page_decode(const uint8_t* bytes, uint8_t* raw,
+                                                     const PageRef* pages, const uint32_t* todo,
+                                                     const uint64_t* scratch_off, uint8_t* scratch,
+                                                     uint32_t n_todo, int32_t* page_status,
+                                                     long long* timing) {
+  __shared__ uint32_t ctl[lz4p::kSmemWords];
+  __shared__ Lz4Seq seqs[32];
+  __shared__ int32_t sst;
+  __shared__ uint32_t scount;
+  __shared__ __align__(16) uint8_t ring[lz4p::kRing];
+  for (uint32_t w = blockIdx.x; w < n_todo; w += gridDim.x) {
     const uint32_t pi = todo[w];
     const PageRef pg = pages[pi];
     const uint8_t* src = bytes + pg.off + kPageHeaderBytes;
     uint8_t* dst = raw + pg.raw_dst;
     int32_t status = kOk;
     if (pg.flags & kFlagOuterLz4) {
-      status = warp_lz4_decode(src, pg.pay_len, dst, pg.raw_len, seqs[wl], &sst[wl], &scount[wl]);
+      if (pg.pay_len >= 0xFFFFFFF0ull || pg.raw_len >= 0xFFFFFFF0ull) {
+        status = kCorruptPage;
+      } else {
+        const lz4p::Scratch sc = lz4p::carve_scratch(scratch + scratch_off[w], pg.pay_len);
+        status = lz4p::decode_block(src, (uint32_t)pg.pay_len, dst, (uint32_t)pg.raw_len, sc, ctl,
+                                    ring, timing ? timing + 8 * (uint64_t)w : nullptr);
+        if (status < 0) {
+          if (threadIdx.x < 32) {
+            const int32_t r = warp_lz4_decode(src, pg.pay_len, dst, pg.raw_len, seqs, &sst, &scount);
+            if (threadIdx.x == 0) ctl[5] = (uint32_t)r;
+          }
+          __syncthreads();
+          status = (int32_t)ctl[5];
+        }
+      }
     } else if (pg.flags & kFlagStoredRaw) {
       if (pg.pay_len != pg.raw_len) {
         status = kCorruptPage;
       } else {
-        for (uint64_t i = lane; i < pg.raw_len; i += 32) dst[i] = src[i];
+        for (uint64_t i = threadIdx.x; i < pg.raw_len; i += blockDim.x) dst[i] = src[i];
       }
     } else {
       status = kCorruptPage;
     }
-    if (lane == 0 && status != kOk) page_status[pi] = status;
-    __syncwarp();
+    if (threadIdx.x == 0 && status != kOk) page_status[pi] = status;
+    __syncthreads();
   }
 }
 
@@ -1079,8 +1099,10 @@ __global__ void __launch_bounds__(512) k_cloud(WaveArgs a) {
           break;
         }
         const uint32_t* s32 = reinterpret_cast<const uint32_t*>(c.cur[f]);
-        uint32_t* d32 = reinterpret_cast<uint32_t*>(a.out[of] + (uint64_t)s * a.out_stride[of]);
-        for (uint64_t i = threadIdx.x; i < (nb + 3) / 4; i += blockDim.x) d32[i] = s32[i];
+        uint8_t* dst = a.out[of] + (uint64_t)s * a.out_stride[of];
+        uint32_t* d32 = reinterpret_cast<uint32_t*>(dst);
+        for (uint64_t i = threadIdx.x; i < nb / 4; i += blockDim.x) d32[i] = s32[i];
+        for (uint64_t i = (nb & ~3ull) + threadIdx.x; i < nb; i += blockDim.x) dst[i] = c.cur[f][i];
         if (threadIdx.x == 0) a.out_len[(uint64_t)of * a.n_samples + s] = nb;
       }
       uint32_t vo = rec.vals_off;
@@ -1209,13 +1231,16 @@ __global__ void k_crc_ranges(const uint8_t* bytes, const uint64_t* off, const ui
 __global__ void k_decode_pages(const uint8_t* bytes, const uint64_t* page_off, uint32_t n_pages,
                                uint8_t* out, const uint64_t* out_off, const uint32_t* col_first,
                                const uint64_t* col_off, const uint64_t* col_len,
-                               const uint32_t* shift_tab, int32_t* status) {
+                               const uint32_t* shift_tab, const uint64_t* scratch_off,
+                               uint8_t* scratch, int32_t* status) {
   __shared__ uint32_t tab[256];
   __shared__ uint32_t red[32];
+  __shared__ uint32_t ctl[lz4p::kSmemWords];
   __shared__ Lz4Seq seqs[32];
   __shared__ int32_t sst;
   __shared__ uint32_t scount;
   __shared__ int32_t st_sh;
+  __shared__ __align__(16) uint8_t ring[lz4p::kRing];
   for (int i = threadIdx.x; i < 256; i += blockDim.x) tab[i] = crc::table_entry(i);
   __syncthreads();
   for (uint32_t pi = blockIdx.x; pi < n_pages; pi += gridDim.x) {
@@ -1233,10 +1258,20 @@ __global__ void k_decode_pages(const uint8_t* bytes, const uint64_t* page_off, u
     __syncthreads();
     if (st_sh == kOk) {
       if (flags & kFlagOuterLz4) {
-        if (threadIdx.x < 32) {
-          const int32_t r = warp_lz4_decode(pay, pay_len, dst, raw_len, seqs, &sst, &scount);
-          if (threadIdx.x == 0) st_sh = r;
+        int32_t r = kCorruptPage;
+        if (pay_len < 0xFFFFFFF0ull && raw_len < 0xFFFFFFF0ull) {
+          const lz4p::Scratch sc = lz4p::carve_scratch(scratch + scratch_off[pi], pay_len);
+          r = lz4p::decode_block(pay, (uint32_t)pay_len, dst, (uint32_t)raw_len, sc, ctl, ring);
+          if (r < 0) {
+            if (threadIdx.x < 32) {
+              const int32_t q = warp_lz4_decode(pay, pay_len, dst, raw_len, seqs, &sst, &scount);
+              if (threadIdx.x == 0) ctl[5] = (uint32_t)q;
+            }
+            __syncthreads();
+            r = (int32_t)ctl[5];
+          }
         }
+        if (threadIdx.x == 0) st_sh = r;
       } else if (flags & kFlagStoredRaw) {
         if (pay_len != raw_len) {
           if (threadIdx.x == 0) st_sh = kCorruptPage;
@@ -1342,6 +1377,8 @@ void build_shift_table(uint32_t* h_tab) {
   }
 }
 
+uint64_t lz4_scratch_bytes(uint64_t pay) { return lz4p::scratch_bytes(pay); }
+
 size_t cloud_smem_fixed() { return (sizeof(Smem) + 127) & ~size_t(127); }
 
 cudaError_t launch_crc_windows(const uint8_t* bytes, const CrcWindow* win, uint32_t n_win,
@@ -1356,11 +1393,12 @@ cudaError_t launch_crc_windows(const uint8_t* bytes, const CrcWindow* win, uint3
 }
 
 cudaError_t launch_page_decode(const uint8_t* bytes, uint8_t* raw, const PageRef* pages,
-                               const uint32_t* todo, uint32_t n_todo, int32_t* status,
-                               cudaStream_t st) {
+                               const uint32_t* todo, const uint64_t* scratch_off,
+                               uint8_t* scratch, uint32_t n_todo, int32_t* status,
+                               cudaStream_t st, long long* timing) {
   if (!n_todo) return cudaSuccess;
-  const uint32_t grid = (n_todo + 3) / 4;
-  k_page_decode<<<grid, 128, 0, st>>>(bytes, raw, pages, todo, n_todo, status);
+  k_page_decode<<<n_todo, 256, 0, st>>>(bytes, raw, pages, todo, scratch_off, scratch, n_todo,
+                                        status, timing);
   return cudaGetLastError();
 }
 
@@ -1417,10 +1455,12 @@ cudaError_t launch_crc_ranges(const uint8_t* bytes, const uint64_t* off, const u
 cudaError_t launch_decode_pages(const uint8_t* bytes, const uint64_t* page_off, uint32_t n,
                                 uint8_t* out, const uint64_t* out_off, const uint32_t* col_first,
                                 const uint64_t* col_off, const uint64_t* col_len,
-                                const uint32_t* shift_tab, int32_t* status, cudaStream_t st) {
+                                const uint32_t* shift_tab, const uint64_t* scratch_off,
+                                uint8_t* scratch, int32_t* status, cudaStream_t st) {
   if (!n) return cudaSuccess;
   k_decode_pages<<<n < 4096 ? n : 4096, 256, 0, st>>>(bytes, page_off, n, out, out_off, col_first,
-                                                     col_off, col_len, shift_tab, status);
+                                                     col_off, col_len, shift_tab, scratch_off,
+                                                     scratch, status);
   return cudaGetLastError();
 }
 

@@ -27,8 +27,10 @@ cudaError_t launch_crc_windows(const uint8_t* bytes, const CrcWindow* win, uint3
                                const uint32_t* shift_tab, uint32_t* acc, int sms,
                                cudaStream_t st);
 cudaError_t launch_page_decode(const uint8_t* bytes, uint8_t* raw, const PageRef* pages,
-                               const uint32_t* todo, uint32_t n_todo, int32_t* status,
-                               cudaStream_t st);
+                               const uint32_t* todo, const uint64_t* scratch_off,
+                               uint8_t* scratch, uint32_t n_todo, int32_t* status,
+                               cudaStream_t st, long long* timing = nullptr);
+uint64_t lz4_scratch_bytes(uint64_t pay);  // per LZ4 page
 // scalar parse → cloud interpreter → page verdicts → sample status
 cudaError_t launch_wave(const WaveArgs& a, int grid, int threads, size_t smem, cudaStream_t st,
                         cudaEvent_t k0 = nullptr, cudaEvent_t k1 = nullptr);
@@ -44,7 +46,8 @@ cudaError_t launch_crc_ranges(const uint8_t* bytes, const uint64_t* off, const u
 cudaError_t launch_decode_pages(const uint8_t* bytes, const uint64_t* page_off, uint32_t n,
                                 uint8_t* out, const uint64_t* out_off, const uint32_t* col_first,
                                 const uint64_t* col_off, const uint64_t* col_len,
-                                const uint32_t* shift_tab, int32_t* status, cudaStream_t st);
+                                const uint32_t* shift_tab, const uint64_t* scratch_off,
+                                uint8_t* scratch, int32_t* status, cudaStream_t st);
 
 constexpr uint32_t kShiftEntries = 8192;
 

@@ -1,0 +1,213 @@
+"""GPU parity of the stateless C-ABI entry points against the compiled
+reference: page decode (CRC + CTA-parallel LZ4 + XOR-delta columns), CRC
+ranges, and apply_map over cloud sets."""
+import ctypes as C
+import json
+import struct
+import zlib
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _dev(torch, b: bytes, pad=64):
+    t = torch.zeros(len(b) + 2 * pad, dtype=torch.uint8, device="cuda")
+    if b:
+        t[pad:pad + len(b)] = torch.frombuffer(bytearray(b), dtype=torch.uint8).cuda()
+    return t, pad
+
+
+def _u64(torch, xs):
+    return torch.tensor(list(xs) or [0], dtype=torch.int64, device="cuda")
+
+
+def _decode_pages(pcp, pages, cols_per_page):
+    """pages: serialized EncodedPage bytes; returns [(status, bytes)]."""
+    import torch
+    blob = b""
+    offs = []
+    for p in pages:
+        offs.append(64 + len(blob))
+        blob += p + b"\0" * ((-len(p)) % 16)
+    d_bytes, _ = _dev(torch, blob)
+    raw_lens = [struct.unpack_from("<Q", p, 1)[0] for p in pages]
+    out_off, at = [], 0
+    for r in raw_lens:
+        out_off.append(at)
+        at += r + 64
+    d_out = torch.zeros(at + 64, dtype=torch.uint8, device="cuda")
+    first, co, cl = [0], [], []
+    for cols in cols_per_page:
+        for o, l in cols:
+            co.append(o)
+            cl.append(l)
+        first.append(len(co))
+    d_po, d_oo = _u64(torch, offs), _u64(torch, out_off)
+    d_first = torch.tensor(first, dtype=torch.int32, device="cuda")
+    d_co, d_cl = _u64(torch, co), _u64(torch, cl)
+    d_st = torch.zeros(len(pages), dtype=torch.int32, device="cuda")
+    L = pcp.lib()
+    st = L.pcp_decode_pages(C.c_void_p(d_bytes.data_ptr()), C.c_void_p(d_po.data_ptr()), len(pages),
+                            C.c_void_p(d_out.data_ptr()), C.c_void_p(d_oo.data_ptr()),
+                            C.c_void_p(d_first.data_ptr()), C.c_void_p(d_co.data_ptr()),
+                            C.c_void_p(d_cl.data_ptr()), C.c_void_p(d_st.data_ptr()), None)
+    assert st == 0, L.pcp_last_error()
+    torch.cuda.synchronize()
+    out = d_out.cpu().numpy().tobytes()
+    res = []
+    for i, s in enumerate(d_st.cpu().tolist()):
+        res.append((s, out[out_off[i]:out_off[i] + raw_lens[i]]))
+    return res
+
+
+def _ref_decode(ref, page, cols):
+    from oracle.ffi import OracleError
+    try:
+        return 0, ref.decode_page(page, cols)
+    except OracleError as e:
+        return e.code, None
+
+
+def _corpus(rng):
+    from paper_2603_16945_b200 import synth
+    out = [b"", b"\x00" * 5000, rng.integers(0, 256, 3000).astype(np.uint8).tobytes()]
+    for n in (13, 100, 4095, 4096, 4097, 70000, 300000):
+        out.append(rng.integers(0, 3, n).astype(np.uint8).tobytes())
+    walk = np.cumsum(rng.normal(0, 1e-3, 200000)).astype(np.float32)
+    out.append(np.round(walk, 3).astype(np.float32).tobytes())
+    schema, s = synth.shapenet(3, n_points=2048)
+    out.append(b"".join(x["data"].tobytes() + x["seg"].tobytes() for x in s))
+    schema, s = synth.kitti(1, lo=60000, hi=60000, quantized=True)
+    out.append(s[0]["data"].tobytes() + s[0]["intensity"].tobytes())
+    return out
+
+
+def test_decode_pages_matches_reference(pcp, ref, rng):
+    pages, cols = [], []
+    for raw in _corpus(rng):
+        c = [(0, len(raw) // 8 * 4)] if len(raw) >= 8 else []
+        pages.append(ref.encode_page(raw, c))
+        cols.append(c)
+    got = _decode_pages(pcp, pages, cols)
+    for p, c, (st, out) in zip(pages, cols, got):
+        rst, rout = _ref_decode(ref, p, c)
+        assert st == rst
+        assert out == rout
+
+
+def test_lz4_corruption_verdicts_match_reference(pcp, ref, rng):
+    """Mutated LZ4 payloads (CRC re-stamped so decode is reached): the device
+    verdict (CorruptPage or bytes) equals lz4::decompress's."""
+    from oracle.ffi import OracleError
+    raw = rng.integers(0, 256, 2048).astype(np.uint8).tobytes() + b"\x55" * 2048
+    raw += rng.integers(0, 4, 9000).astype(np.uint8).tobytes()
+    comp = ref.lz4_compress(raw)
+    pages, want = [], []
+    for k in range(240):
+        m = bytearray(comp)
+        for _ in range(1 + k % 3):
+            m[int(rng.integers(0, len(m)))] ^= int(rng.integers(1, 256))
+        if k % 17 == 0:
+            m = m[: int(rng.integers(0, len(m)))]
+        pay = bytes(m)
+        page = struct.pack("<BQQI", 1, len(raw), len(pay), zlib.crc32(pay)) + pay
+        pages.append(page)
+        try:
+            want.append((0, ref.lz4_decompress(pay, len(raw))))
+        except OracleError as e:
+            want.append((e.code, None))
+    got = _decode_pages(pcp, pages, [[]] * len(pages))
+    for i, ((gs, go), (ws, wo)) in enumerate(zip(got, want)):
+        assert gs == ws, (i, gs, ws)
+        if ws == 0:
+            assert go == wo, i
+
+
+def test_crc_ranges(pcp, rng):
+    import torch
+    data = rng.integers(0, 256, 3_000_000).astype(np.uint8).tobytes()
+    d, pad = _dev(torch, data)
+    ranges = [(0, 0), (0, 1), (5, 255), (1, 256), (17, 100000), (3, 2_999_990), (123, 2_500_001)]
+    d_off = _u64(torch, [pad + a for a, _ in ranges])
+    d_len = _u64(torch, [n for _, n in ranges])
+    d_crc = torch.zeros(len(ranges), dtype=torch.int32, device="cuda")
+    L = pcp.lib()
+    assert L.pcp_crc32_ranges(C.c_void_p(d.data_ptr()), C.c_void_p(d_off.data_ptr()),
+                              C.c_void_p(d_len.data_ptr()), len(ranges),
+                              C.c_void_p(d_crc.data_ptr()), None) == 0
+    torch.cuda.synchronize()
+    got = [x & 0xFFFFFFFF for x in d_crc.cpu().tolist()]
+    assert got == [zlib.crc32(data[a:a + n]) for a, n in ranges]
+
+
+class _Set(C.Structure):
+    _fields_ = [("n_clouds", C.c_uint32), ("d_offset", C.c_void_p), ("d_data", C.c_void_p),
+                ("d_normal", C.c_void_p), ("d_color", C.c_void_p), ("d_intensity", C.c_void_p),
+                ("d_extra", C.c_void_p * 4), ("extra_elem", C.c_uint32 * 4)]
+
+
+class _Out(C.Structure):
+    _fields_ = [("cap_points", C.c_uint32), ("d_data", C.c_void_p), ("d_normal", C.c_void_p),
+                ("d_color", C.c_void_p), ("d_intensity", C.c_void_p), ("d_extra", C.c_void_p * 4),
+                ("d_voxel_count", C.c_void_p), ("d_count", C.c_void_p)]
+
+
+@pytest.mark.parametrize("kind,params", [("normalize", {}), ("translate", {}), ("random_scale", {}),
+                                         ("flip_yz", {}), ("color_augment", {}),
+                                         ("random_crop", {}), ("downsample", {"num_points": 200}),
+                                         ("downsample", {"num_points": 900}),
+                                         ("fps", {"num_points": 64}), ("rotate", {}),
+                                         ("jitter", {})])
+def test_apply_map_cloud_set(pcp, ref, orc, rng, kind, params):
+    import torch
+    from oracle.ffi import cloud
+    sizes = [300, 1, 700, 513]
+    clouds = [rng.uniform(-2, 2, (n, 3)).astype(np.float32) for n in sizes]
+    normals = [rng.normal(0, 1, (n, 3)).astype(np.float32) for n in sizes]
+    colors = [rng.uniform(0, 1, (n, 3)).astype(np.float32) for n in sizes]
+    seeds = [int(x) for x in rng.integers(0, 2**63, len(sizes))]
+    off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    cap = max(max(sizes), params.get("num_points", 0))
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    d_data, d_nrm, d_col = t(np.concatenate(clouds)), t(np.concatenate(normals)), t(np.concatenate(colors))
+    d_off, d_seed = t(off), t(np.array(seeds, dtype=np.uint64).view(np.int64))
+    o_data = torch.zeros(len(sizes) * cap * 3, dtype=torch.float32, device="cuda")
+    o_nrm, o_col = torch.zeros_like(o_data), torch.zeros_like(o_data)
+    o_cnt = torch.zeros(len(sizes), dtype=torch.int32, device="cuda")
+    d_st = torch.zeros(len(sizes), dtype=torch.int32, device="cuda")
+    s = _Set(len(sizes), d_off.data_ptr(), d_data.data_ptr(), d_nrm.data_ptr(), d_col.data_ptr(), None)
+    o = _Out(cap, o_data.data_ptr(), o_nrm.data_ptr(), o_col.data_ptr(), None)
+    o.d_count = o_cnt.data_ptr()
+    L = pcp.lib()
+    L.pcp_apply_map.argtypes = [C.c_int, C.c_char_p, C.POINTER(_Set), C.POINTER(_Out), C.c_void_p,
+                                C.c_void_p, C.c_void_p]
+    rc = L.pcp_apply_map(pcp.map_kind_from_name(kind), json.dumps(params).encode(), C.byref(s),
+                         C.byref(o), d_seed.data_ptr(), d_st.data_ptr(), None)
+    assert rc == 0, L.pcp_last_error()
+    torch.cuda.synchronize()
+    st, cnt = d_st.cpu().numpy(), o_cnt.cpu().numpy()
+    od = o_data.cpu().numpy().reshape(len(sizes), cap, 3)
+    on = o_nrm.cpu().numpy().reshape(len(sizes), cap, 3)
+    oc = o_col.cpu().numpy().reshape(len(sizes), cap, 3)
+    tol = kind in ("rotate", "jitter")
+    for i in range(len(sizes)):
+        smp = {"data": cloud(clouds[i]), "normal": cloud(normals[i]), "color": cloud(colors[i])}
+        impl = ref if kind != "fps" else orc
+        from oracle.ffi import OracleError
+        try:
+            w = impl.apply_map(kind, params, smp, seeds[i])
+        except OracleError as e:
+            assert st[i] == e.code, (kind, i, st[i], e.code)
+            continue
+        assert st[i] == 0
+        wd = w["data"].view(np.float32).reshape(-1, 3)
+        assert cnt[i] == len(wd)
+        for got, name in ((od[i], "data"), (on[i], "normal"), (oc[i], "color")):
+            want = w[name].view(np.float32).reshape(-1, 3)
+            g = got[: len(want)]
+            if tol:
+                np.testing.assert_allclose(g, want, rtol=1e-5, atol=1e-6 * max(1, np.abs(want).max()))
+            else:
+                assert np.array_equal(g.view(np.uint32), want.view(np.uint32)), (kind, i, name)
