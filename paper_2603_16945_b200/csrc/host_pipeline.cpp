@@ -166,12 +166,19 @@ Graph parse_graph(const std::string& text) {
       n.batch = o.value("batch_size", 1u);
       if (n.kind == "map") {
         if (o.contains("fused")) {
-          for (const auto& f : o["fused"])
+          for (const auto& f : o["fused"]) {
             n.steps.push_back({map_kind_from_name(f.at("map").get<std::string>()), n.id,
                                f.at("op_id").get<uint32_t>(), f.value("params", json::object())});
+            if (f.at("map").get<std::string>() == "grid_subsample" &&
+                n.steps.back().params.is_object() && !n.steps.back().params.contains("counts"))
+              n.steps.back().params["counts"] = false;
+          }
         } else {
           n.steps.push_back({map_kind_from_name(o.at("map").get<std::string>()), n.id, n.id,
                              o.value("params", json::object())});
+          if (o.at("map").get<std::string>() == "grid_subsample" && n.steps.back().params.is_object() &&
+              !n.steps.back().params.contains("counts"))
+            n.steps.back().params["counts"] = false;
         }
       }
       nodes.push_back(std::move(n));
@@ -246,7 +253,7 @@ void parse_op_params(OpDesc& op, const json& p, IndexOf bytes_index_of) {
   }
   if ((op.kind == kDownsample || op.kind == kFps) && op.num_points <= 0)
     fail(kOutOfBounds, "num_points must be positive");
-  if (op.kind == kVoxel) fail(kUnknownOp, "voxel/grid_subsample is not in this build yet");
+  if (op.kind == kVoxel && !(op.voxel > 0.0f)) fail(kOutOfBounds, "voxel_size must be positive");
 }
 
 // Per-device state for the stateless entry points (codec + operator API).
@@ -544,6 +551,14 @@ struct Pipeline {
         }
       }
     }
+    bool any_voxel = false, any_counts = false;
+    for (int k = 0; k < a.n_ops; ++k)
+      if (a.ops[k].kind == kVoxel) {
+        any_voxel = true;
+        any_counts |= a.ops[k].counts != 0;
+      }
+    a.voxel_scratch = any_voxel ? 1 : 0;
+    a.count_out = -1;
     // outputs in std::map (name) order
     std::vector<int32_t> order(h.schema.size());
     for (size_t f = 0; f < order.size(); ++f) order[f] = (int32_t)f;
@@ -576,11 +591,29 @@ struct Pipeline {
       a.fields[f].out_index = (int32_t)outs.size();
       outs.push_back(o);
     }
+    if (any_counts) {  // synthesized "count" bytes field (int32 per voxel)
+      for (const auto& o : outs)
+        if (o.name == "count") fail(kSchemaConflict, "schema already has a 'count' field");
+      OutField o;
+      o.name = "count";
+      o.kind = kBytes;
+      o.schema_idx = -1;
+      o.stride = align4(cap * 4);
+      size_t pos = 0;
+      while (pos < outs.size() && outs[pos].name < o.name) ++pos;
+      outs.insert(outs.begin() + pos, o);
+      for (int f = 0; f < a.n_fields; ++f)
+        if (a.fields[f].out_index >= (int32_t)pos) ++a.fields[f].out_index;
+      for (int k = 0; k < kMaxBytesFields; ++k)
+        if (a.bytes_out[k] >= (int32_t)pos) ++a.bytes_out[k];
+      a.count_out = (int32_t)pos;
+    }
     if (outs.size() > (size_t)PCP_MAX_BATCH_FIELDS) fail(kOutOfBounds, "too many batch fields");
     a.n_out = (int32_t)outs.size();
     // shared-memory plan for k_cloud
     auto rnd = [](uint64_t v) { return (v + 127) & ~uint64_t(127); };
     uint64_t need = rnd(a.max_blob + 64) + 4 * rnd((uint64_t)cap * 4 + 16);
+    if (a.voxel_scratch) need += 2 * rnd((uint64_t)cap * 8 + 16) + rnd((uint64_t)cap * 4 + 16);
     for (size_t f = 0; f < bytes_fields.size(); ++f)
       if ((tracked >> f) & 1u) need += 2 * rnd((uint64_t)cap * a.field_cap[f] + 16);
     const size_t fixed = cloud_smem_fixed();
@@ -595,6 +628,7 @@ struct Pipeline {
     grid = std::max(1, per_sm) * sms;
     if (!a.smem_mode) {
       uint64_t per = 4 * rnd((uint64_t)cap * 4 + 16);
+      if (a.voxel_scratch) per += 2 * rnd((uint64_t)cap * 8 + 16) + rnd((uint64_t)cap * 4 + 16);
       for (size_t f = 0; f < bytes_fields.size(); ++f)
         if ((tracked >> f) & 1u) per += 2 * rnd((uint64_t)cap * a.field_cap[f] + 16);
       a.gscratch_per_cta = per;  // slabs are allocated per wave slot
@@ -1164,7 +1198,7 @@ int pcp_apply_map(int kind, const char* params_json, const pcp_cloud_set* in,
     });
     if (kind != kNormalize && kind != kTranslate && kind != kJitter && kind != kRotate &&
         kind != kRandomScale && kind != kFlipYz && kind != kColorAugment && kind != kRandomCrop &&
-        kind != kDownsample && kind != kFps && kind != kRangeCrop)
+        kind != kDownsample && kind != kFps && kind != kRangeCrop && kind != kVoxel)
       fail(kUnknownOp, "unknown map kind " + std::to_string(kind));
     a.n_ops = 1;
     a.cap_points = (uint32_t)std::max<uint64_t>({max_n, (uint64_t)std::max<int64_t>(op.num_points, 0), 1});
@@ -1174,8 +1208,12 @@ int pcp_apply_map(int kind, const char* params_json, const pcp_cloud_set* in,
     a.set_seeds = d_seeds;
     a.set_count = out->d_count;
     a.sample_status = d_status;
+    a.voxel_scratch = kind == kVoxel ? 1 : 0;
+    a.set_voxel_count = out->d_voxel_count;
+    a.count_out = -1;
     auto rnd = [](uint64_t v) { return (v + 127) & ~uint64_t(127); };
     uint64_t need = rnd(64) + 4 * rnd((uint64_t)a.cap_points * 4 + 16);
+    if (a.voxel_scratch) need += 2 * rnd((uint64_t)a.cap_points * 8 + 16) + rnd((uint64_t)a.cap_points * 4 + 16);
     for (int f = 0; f < 8; ++f)
       if ((a.tracked_mask >> f) & 1u) need += 2 * rnd((uint64_t)a.cap_points * a.field_cap[f] + 16);
     cudaDeviceProp prop;

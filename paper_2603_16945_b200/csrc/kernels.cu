@@ -291,6 +291,8 @@ namespace {
 constexpr int kRed = 64;  // reduction scratch words (8 B)
 
 struct Smem {
+  uint32_t rs_base[16];
+  uint32_t rs_wcnt[16][16];  // per-warp digit counts (radix sort tiles)
   uint32_t crc_tab[256];
   unsigned long long red[kRed];
   uint64_t mt[rng::kN];
@@ -310,6 +312,10 @@ struct Cloud {
   uint32_t present;                // tracked + present bits
   int32_t* ix[4];                  // index scratch, cap entries each
   uint32_t cap;
+  uint64_t* key[2];                // voxel sort keys (ping-pong)
+  int32_t* counts;                 // voxel counts (cap)
+  uint32_t n_counts;
+  int32_t has_counts;
 };
 
 __device__ __forceinline__ float* F(Cloud& c, int f) { return reinterpret_cast<float*>(c.cur[f]); }
@@ -927,6 +933,192 @@ __device__ void decode_bytes(uint8_t* dst, const uint8_t* src, uint64_t len, boo
 
 }  // namespace
 
+// Stable LSD radix sort of (key, val) by the low `bits` bits of key, 4-bit
+// digits, whole CTA.  Ping-pongs between (k0,v0) and (k1,v1); returns the
+// buffer index (0/1) holding the result.
+__device__ int radix_sort(uint64_t* k0, uint32_t* v0, uint64_t* k1, uint32_t* v1, uint32_t n,
+                          uint32_t bits, Smem& S) {
+  const uint32_t t = threadIdx.x, lane = t & 31, w = t >> 5, nw = blockDim.x >> 5;
+  uint64_t* ks[2] = {k0, k1};
+  uint32_t* vs[2] = {v0, v1};
+  int cur = 0;
+  for (uint32_t sh = 0; sh < bits; sh += 4) {
+    const uint64_t* kin = ks[cur];
+    const uint32_t* vin = vs[cur];
+    uint64_t* kout = ks[cur ^ 1];
+    uint32_t* vout = vs[cur ^ 1];
+    if (t < 16) S.rs_base[t] = 0;
+    __syncthreads();
+    for (uint32_t i = t; i < n; i += blockDim.x) atomicAdd(&S.rs_base[(kin[i] >> sh) & 15u], 1u);
+    __syncthreads();
+    if (t == 0) {
+      uint32_t acc = 0;
+      for (int d = 0; d < 16; ++d) {
+        const uint32_t c = S.rs_base[d];
+        S.rs_base[d] = acc;
+        acc += c;
+      }
+    }
+    __syncthreads();
+    for (uint32_t t0 = 0; t0 < n; t0 += blockDim.x) {
+      const uint32_t i = t0 + t;
+      const bool valid = i < n;
+      uint64_t key = 0;
+      uint32_t val = 0, d = 16;
+      if (valid) {
+        key = kin[i];
+        val = vin[i];
+        d = (uint32_t)(key >> sh) & 15u;
+      }
+      if (lane < 16) S.rs_wcnt[w][lane] = 0;
+      __syncwarp();
+      const uint32_t peers = __match_any_sync(0xffffffffu, d);
+      const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
+      if (valid && rank == 0) S.rs_wcnt[w][d] = __popc(peers);
+      __syncthreads();
+      if (valid) {
+        uint32_t off = S.rs_base[d] + rank;
+        for (uint32_t q = 0; q < w; ++q) off += S.rs_wcnt[q][d];
+        kout[off] = key;
+        vout[off] = val;
+      }
+      __syncthreads();
+      if (t < 16) {
+        uint32_t tot = 0;
+        for (uint32_t q = 0; q < nw; ++q) tot += S.rs_wcnt[q][t];
+        S.rs_base[t] += tot;
+      }
+      __syncthreads();
+    }
+    cur ^= 1;
+  }
+  return cur;
+}
+
+// Smallest coordinate per axis with the sequential `if (v < o) o = v`
+// semantics starting from point 0 (App. C voxel origin): NaN at point 0
+// poisons the axis; later NaNs never win; equal values keep the first.
+__device__ void seq_min3(const float* d, uint32_t n, Smem& S, float* lo) {
+  for (int k = 0; k < 3; ++k) {
+    float l = INFINITY;
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) l = fminf(l, d[3 * i + k]);
+    lo[k] = dev::block_reduce(l, [](float x, float y) { return fminf(x, y); }, INFINITY, S.red);
+    const float p0 = d[k];
+    if (isnan(p0)) lo[k] = p0;
+    else if (lo[k] == 0.0f) {  // first zero in point order keeps its sign
+      if (threadIdx.x == 0) {
+        float z = 0.0f;
+        for (uint32_t i = 0; i < n; ++i)
+          if (d[3 * i + k] == 0.0f) { z = d[3 * i + k]; break; }
+        S.f32s[k] = z;
+      }
+      __syncthreads();
+      lo[k] = S.f32s[k];
+      __syncthreads();
+    }
+  }
+}
+
+// voxel / grid subsample (App. C): k = (int32)floorf((p - o) / v) per axis,
+// key = kx | ky<<21 | kz<<42, stable order by key, per voxel the count and
+// the mean of every float field = (float)(sum in point order (double) / count);
+// extra gathered fields take the voxel's first point.  Output ascending key.
+__device__ int32_t op_voxel(const WaveArgs& a, Cloud& c, Smem& S, const OpDesc& op) {
+  const uint32_t n = c.n[a.role_data];
+  if (!(op.voxel > 0.0f)) return kOutOfBounds;
+  if (!c.key[0]) return kOutOfBounds;
+  const uint32_t mm = move_mask(a, c, true, op.gather_mask);
+  const int32_t st = check_move(a, c, mm);
+  if (st) return st;
+  const float* d = F(c, a.role_data);
+  float o[3];
+  if (op.has_origin) {
+    o[0] = op.origin[0]; o[1] = op.origin[1]; o[2] = op.origin[2];
+  } else {
+    seq_min3(d, n, S, o);
+  }
+  uint32_t* idx = reinterpret_cast<uint32_t*>(c.ix[0]);
+  uint32_t* idx2 = reinterpret_cast<uint32_t*>(c.ix[1]);
+  uint32_t bad = 0, mx[3] = {0, 0, 0};
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+    uint32_t kk[3];
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+      const float q = floorf(__fdiv_rn(__fsub_rn(d[3 * i + ax], o[ax]), op.voxel));
+      if (!(q >= 0.0f && q < 2097152.0f)) bad = 1;
+      kk[ax] = bad ? 0u : (uint32_t)q;
+      mx[ax] = max(mx[ax], kk[ax]);
+    }
+    c.key[0][i] = (uint64_t)kk[0] | ((uint64_t)kk[1] << 21) | ((uint64_t)kk[2] << 42);
+    idx[i] = i;
+  }
+  bad = dev::block_reduce(bad, dev::OpOr{}, 0u, S.red);
+  if (bad) return kOutOfBounds;
+  uint32_t bx[3];
+  for (int ax = 0; ax < 3; ++ax) {
+    const uint32_t m = dev::block_reduce(mx[ax], dev::OpMax{}, 0u, S.red);
+    bx[ax] = m ? 32u - __clz(m) : 0u;
+  }
+  // compact sort key, monotone in the App. C key (kz major, then ky, kx)
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const uint64_t K = c.key[0][i];
+    const uint64_t kx = K & 0x1FFFFF, ky = (K >> 21) & 0x1FFFFF, kz = K >> 42;
+    c.key[0][i] = kx | (ky << bx[0]) | (kz << (bx[0] + bx[1]));
+  }
+  __syncthreads();
+  const int r = radix_sort(c.key[0], idx, c.key[1], idx2, n, bx[0] + bx[1] + bx[2], S);
+  const uint64_t* K = c.key[r];
+  const uint32_t* P = r ? idx2 : idx;  // sorted original indices
+  uint32_t* seg = reinterpret_cast<uint32_t*>(c.ix[2]);
+  uint32_t base = 0;
+  for (uint32_t t0 = 0; t0 < n; t0 += blockDim.x) {
+    const uint32_t i = t0 + threadIdx.x;
+    const bool f = i < n && (i == 0 || K[i] != K[i - 1]);
+    uint32_t tot;
+    const uint32_t rk = dev::block_scan_excl(f ? 1u : 0u, &tot, S.red);
+    if (f) seg[base + rk] = i;
+    base += tot;
+  }
+  __syncthreads();
+  const uint32_t V = base;
+  for (uint32_t v = threadIdx.x; v < V; v += blockDim.x) {
+    const uint32_t s0 = seg[v], s1 = v + 1 < V ? seg[v + 1] : n;
+    const double cnt = (double)(s1 - s0);
+    for (int f = 0; f < a.n_bytes_fields; ++f) {
+      if (!((mm >> f) & 1u)) continue;
+      const bool avg = f == a.role_data || f == a.role_normal || f == a.role_color ||
+                       f == a.role_intensity;
+      if (avg) {
+        const uint32_t comps = c.elem[f] / 4;
+        const float* src = reinterpret_cast<const float*>(c.cur[f]);
+        float* dst = reinterpret_cast<float*>(c.alt[f]);
+        for (uint32_t q = 0; q < comps; ++q) {
+          double acc = 0.0;
+          for (uint32_t k = s0; k < s1; ++k) acc = __dadd_rn(acc, (double)src[(uint64_t)P[k] * comps + q]);
+          dst[(uint64_t)v * comps + q] = __double2float_rn(__ddiv_rn(acc, cnt));
+        }
+      } else {
+        const uint32_t es = c.elem[f];
+        for (uint32_t b = 0; b < es; ++b) c.alt[f][(uint64_t)v * es + b] = c.cur[f][(uint64_t)P[s0] * es + b];
+      }
+    }
+    if (c.counts) c.counts[v] = (int32_t)(s1 - s0);
+  }
+  __syncthreads();
+  for (int f = 0; f < a.n_bytes_fields; ++f) {
+    if (!((mm >> f) & 1u)) continue;
+    uint8_t* tmp = c.cur[f];
+    c.cur[f] = c.alt[f];
+    c.alt[f] = tmp;
+    c.n[f] = V;
+  }
+  if (op.counts) {
+    c.has_counts = 1;
+    c.n_counts = V;
+  }
+  return kOk;
+}
+
 // Applies the op chain (Pipeline map worker, pipeline.cpp:474-480): seed per
 // op = mix_seed(base, epoch, index, op id), or `fixed_seed` for the
 // single-op cloud-set API.  fail_op = 1-based failing transform.
@@ -953,6 +1145,7 @@ __device__ int32_t run_chain(const WaveArgs& a, Cloud& c, Smem& S, uint64_t epoc
         case kDownsample: status = op_downsample(a, c, S, op, seed); break;
         case kFps: status = op_fps(a, c, S, op); break;
         case kRangeCrop: status = op_range_crop(a, c, S, op); break;
+        case kVoxel: status = op_voxel(a, c, S, op); break;
         default: status = kUnknownOp; break;
       }
     }
@@ -1105,6 +1298,17 @@ __global__ void __launch_bounds__(512) k_cloud(WaveArgs a) {
         for (uint64_t i = (nb & ~3ull) + threadIdx.x; i < nb; i += blockDim.x) dst[i] = c.cur[f][i];
         if (threadIdx.x == 0) a.out_len[(uint64_t)of * a.n_samples + s] = nb;
       }
+      if (a.count_out >= 0) {  // synthesized "count" field (voxel counts, int32 bytes)
+        const int of = a.count_out;
+        const uint64_t nb = c.has_counts ? (uint64_t)c.n_counts * 4 : 0;
+        if (nb > a.out_stride[of]) {
+          status = kOutOfBounds;
+        } else {
+          int32_t* dst = reinterpret_cast<int32_t*>(a.out[of] + (uint64_t)s * a.out_stride[of]);
+          for (uint32_t i = threadIdx.x; i < nb / 4; i += blockDim.x) dst[i] = c.counts[i];
+          if (threadIdx.x == 0) a.out_len[(uint64_t)of * a.n_samples + s] = nb;
+        }
+      }
       uint32_t vo = rec.vals_off;
       for (int f = 0; f < a.n_fields && status == kOk; ++f) {
         const FieldDesc fdsc = a.fields[f];
@@ -1154,6 +1358,11 @@ __device__ uint8_t* carve(const WaveArgs& a, uint8_t* work, Cloud& proto) {
     if (!((a.tracked_mask >> f) & 1u)) continue;
     proto.cur[f] = take(field_bytes(a, f));
     proto.alt[f] = take(field_bytes(a, f));
+  }
+  if (a.voxel_scratch) {
+    proto.key[0] = reinterpret_cast<uint64_t*>(take((uint64_t)a.cap_points * 8 + 16));
+    proto.key[1] = reinterpret_cast<uint64_t*>(take((uint64_t)a.cap_points * 8 + 16));
+    proto.counts = reinterpret_cast<int32_t*>(take((uint64_t)a.cap_points * 4 + 16));
   }
   return staging;
 }
@@ -1205,6 +1414,9 @@ __global__ void __launch_bounds__(512) k_apply_set(WaveArgs a) {
         for (uint64_t i = threadIdx.x; i < nb; i += blockDim.x) dst[i] = c.cur[f][i];
       }
     }
+    if (status == kOk && a.set_voxel_count && c.has_counts)
+      for (uint32_t i = threadIdx.x; i < c.n_counts && i < a.set_out_cap; i += blockDim.x)
+        a.set_voxel_count[(uint64_t)s * a.set_out_cap + i] = c.counts[i];
     if (threadIdx.x == 0) {
       a.sample_status[s] = status;
       if (a.set_count) a.set_count[s] = status == kOk ? c.n[a.role_data] : 0;

@@ -23,6 +23,7 @@ enum Status : int32_t {
   kUnsupportedVersion = 12,
   kCorruptHeader = 13,
   kRangeOutOfBounds = 14,
+  kSchemaConflict = 15,
   kOutOfRange = 16,
   kNotPadded = 17,
   kShutdown = 23,
@@ -181,6 +182,10 @@ struct WaveArgs {
   uint32_t set_elem[kMaxBytesFields];
   uint32_t* set_count;                   // [n_samples]
   uint32_t set_out_cap;                  // output slot capacity (points)
+  // voxel / grid subsample
+  int32_t voxel_scratch;    // carve u64 sort keys (2 x cap) + counts (cap)
+  int32_t count_out;        // output index of the synthesized "count" field, -1 none
+  int32_t* set_voxel_count; // pcp_apply_map: [n_samples][set_out_cap]
 };
 
 }  // namespace pcp

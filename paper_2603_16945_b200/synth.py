@@ -178,7 +178,11 @@ CHAINS = {
                    ("jitter", {})],
     "shapenet_part": [("normalize", {}), ("downsample", {"num_points": 1024, "gather": ["seg"]}),
                       ("random_scale", {}), ("downsample", {"num_points": 1024, "gather": ["seg"]})],
-    "s3dis": [("random_crop", {}), ("downsample", {"num_points": 4096})],
-    "kitti": [("range_crop", {"lo": [0.0, -40.0, -3.0], "hi": [70.4, 40.0, 1.0]}), ("rotate", {}),
+    "s3dis": [("grid_subsample", {"voxel_size": 0.04}), ("random_crop", {}),
+              ("downsample", {"num_points": 4096})],
+    "kitti": [("range_crop", {"lo": [0.0, -40.0, -3.0], "hi": [70.4, 40.0, 1.0]}),
+              ("voxel", {"voxel_size": 0.05, "origin": [0.0, -40.0, -3.0]}), ("rotate", {}),
               ("flip_yz", {})],
+    "scannet": [("grid_subsample", {"voxel_size": 0.02}), ("downsample", {"num_points": 40000}),
+                ("fps", {"num_points": 20000})],
 }

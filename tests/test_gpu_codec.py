@@ -159,7 +159,8 @@ class _Out(C.Structure):
                                          ("random_crop", {}), ("downsample", {"num_points": 200}),
                                          ("downsample", {"num_points": 900}),
                                          ("fps", {"num_points": 64}), ("rotate", {}),
-                                         ("jitter", {})])
+                                         ("jitter", {}), ("grid_subsample", {"voxel_size": 0.3}),
+                                         ("range_crop", {"lo": [-1, -1, -1], "hi": [1, 0.5, 1]})])
 def test_apply_map_cloud_set(pcp, ref, orc, rng, kind, params):
     import torch
     from oracle.ffi import cloud
@@ -194,7 +195,7 @@ def test_apply_map_cloud_set(pcp, ref, orc, rng, kind, params):
     tol = kind in ("rotate", "jitter")
     for i in range(len(sizes)):
         smp = {"data": cloud(clouds[i]), "normal": cloud(normals[i]), "color": cloud(colors[i])}
-        impl = ref if kind != "fps" else orc
+        impl = orc if kind in ("fps", "voxel", "grid_subsample", "range_crop") else ref
         from oracle.ffi import OracleError
         try:
             w = impl.apply_map(kind, params, smp, seeds[i])

@@ -64,7 +64,8 @@ def test_fps_parity(pcp, ref, orc, tmp_path):
     assert_batches_equal(got, want, float_fields=tolerant_fields(g))
 
 
-def test_range_crop_kitti_parity(pcp, ref, orc, tmp_path):
+def test_kitti_chain_parity(pcp, ref, orc, tmp_path):
+    """C4: range crop → voxel 0.05 m (counts) → rotate → flip_yz (CSR batch)."""
     from paper_2603_16945_b200 import synth
     primary = _ds(pcp, tmp_path, "kitti", 4, group=2, lo=20000, hi=30000)
     g = synth.graph(synth.CHAINS["kitti"], batch_size=2)
@@ -152,4 +153,29 @@ def test_no_map_passthrough_stacks(pcp, ref, orc, tmp_path):
     from paper_2603_16945_b200 import synth
     primary = _ds(pcp, tmp_path, "kitti", 6, group=3, lo=1000, hi=1000)
     g = synth.graph([], batch_size=3)
+    assert_batches_equal(_run(pcp, primary, g), expected_run(ref, orc, primary, g))
+
+
+@pytest.mark.parametrize("quantized", [False, True])
+def test_s3dis_chain_parity(pcp, ref, orc, tmp_path, quantized):
+    """C3 at reduced size: grid 0.04 m → random_crop → downsample 4096."""
+    from paper_2603_16945_b200 import synth
+    primary = _ds(pcp, tmp_path, "s3dis", 4, group=1, quantized=quantized, mean_points=60000)
+    g = synth.graph(synth.CHAINS["s3dis"], batch_size=2)
+    assert_batches_equal(_run(pcp, primary, g), expected_run(ref, orc, primary, g))
+
+
+def test_scannet_chain_parity(pcp, ref, orc, tmp_path):
+    """C5 at reduced size: grid 0.02 m → downsample → FPS."""
+    from paper_2603_16945_b200 import synth
+    primary = _ds(pcp, tmp_path, "scannet", 4, group=2, lo=20000, hi=40000)
+    g = synth.graph([("grid_subsample", {"voxel_size": 0.02}), ("downsample", {"num_points": 6000}),
+                     ("fps", {"num_points": 500})], batch_size=2)
+    assert_batches_equal(_run(pcp, primary, g), expected_run(ref, orc, primary, g))
+
+
+def test_voxel_gathers_extra_field_and_counts(pcp, ref, orc, tmp_path):
+    from paper_2603_16945_b200 import synth
+    primary = _ds(pcp, tmp_path, "shapenet", 6, group=3, n_points=3000)
+    g = synth.graph([("voxel", {"voxel_size": 0.1, "gather": ["seg"]}), "random_scale"], batch_size=3)
     assert_batches_equal(_run(pcp, primary, g), expected_run(ref, orc, primary, g))
