@@ -90,9 +90,9 @@ __device__ inline void twist_block(uint64_t* st) {
 
 // The first k (<= 8) outputs of a freshly seeded engine, on ONE thread,
 // without materialising the whole state: output i needs new word i, i.e.
-// old words i, i+1 and i+156 (i < 156).
-__device__ inline void first_outputs(uint64_t seed, int k, uint64_t* out) {
-  uint64_t w[kM + 10];
+// old words i, i+1 and i+156 (i < 156).  `w` = >= 166 words of scratch
+// (shared memory: the engine state buffer).
+__device__ inline void first_outputs(uint64_t seed, int k, uint64_t* out, uint64_t* w) {
   uint64_t x = seed;
   w[0] = x;
   const int need = kM + k + 1;

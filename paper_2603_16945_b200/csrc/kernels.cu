@@ -290,19 +290,7 @@ namespace {
 
 constexpr int kRed = 64;  // reduction scratch words (8 B)
 
-struct Smem {
-  uint32_t rs_base[16];
-  uint32_t rs_wcnt[16][16];  // per-warp digit counts (radix sort tiles)
-  uint32_t crc_tab[256];
-  unsigned long long red[kRed];
-  uint64_t mt[rng::kN];
-  uint64_t bar;
-  int32_t status;
-  int32_t flag;
-  uint32_t u32s[8];
-  float f32s[8];
-  double f64s[8];
-};
+
 
 struct Cloud {
   uint8_t* cur[kMaxBytesFields];
@@ -316,6 +304,24 @@ struct Cloud {
   int32_t* counts;                 // voxel counts (cap)
   uint32_t n_counts;
   int32_t has_counts;
+};
+
+struct Smem {
+  uint32_t rs_base[16];
+  uint32_t rs_wcnt[16][16];  // per-warp digit counts (radix sort tiles)
+  uint32_t crc_tab[256];
+  unsigned long long red[kRed];
+  uint64_t mt[rng::kN];
+  uint64_t bar;
+  int32_t status;
+  int32_t flag;
+  uint32_t u32s[8];
+  float f32s[8];
+  double f64s[8];
+  Cloud cl;                   // the current sample's descriptor (single writer: thread 0)
+  Cloud proto;
+  uint64_t flen[kMaxBytesFields], foff[kMaxBytesFields];
+  int32_t pre_status;
 };
 
 __device__ __forceinline__ float* F(Cloud& c, int f) { return reinterpret_cast<float*>(c.cur[f]); }
@@ -357,10 +363,13 @@ __device__ void gather_field(Cloud& c, int f, const int32_t* idx, uint32_t m) {
     }
   }
   __syncthreads();
-  uint8_t* t = c.cur[f];
-  c.cur[f] = c.alt[f];
-  c.alt[f] = t;
-  c.n[f] = m;
+  if (threadIdx.x == 0) {
+    uint8_t* t = c.cur[f];
+    c.cur[f] = c.alt[f];
+    c.alt[f] = t;
+    c.n[f] = m;
+  }
+  __syncthreads();
 }
 
 // Mask of tracked fields an index op moves.
@@ -574,7 +583,7 @@ __device__ int32_t op_normalize(const WaveArgs& a, Cloud& c, Smem& S) {
 // Broadcast the first k (<= 8) engine outputs to S.u32s/f32s via thread 0.
 __device__ void first_draws(Smem& S, uint64_t seed, int k, uint64_t* out) {
   __shared__ uint64_t o[8];
-  if (threadIdx.x == 0) rng::first_outputs(seed, k, o);
+  if (threadIdx.x == 0) rng::first_outputs(seed, k, o, S.mt);
   __syncthreads();
   for (int i = 0; i < k; ++i) out[i] = o[i];
   __syncthreads();
@@ -807,9 +816,12 @@ __device__ int32_t op_random_crop(const WaveArgs& a, Cloud& c, Smem& S, uint64_t
       base += tot;
     }
     __syncthreads();
-    c.cur[fi] = c.alt[fi];
-    c.alt[fi] = reinterpret_cast<uint8_t*>(const_cast<uint32_t*>(src));
-    c.n[fi] = base;
+    if (threadIdx.x == 0) {
+      c.cur[fi] = c.alt[fi];
+      c.alt[fi] = reinterpret_cast<uint8_t*>(const_cast<uint32_t*>(src));
+      c.n[fi] = base;
+    }
+    __syncthreads();
   }
   gather_mask_fields(a, c, mm, c.ix[0], m);
   return kOk;
@@ -1105,17 +1117,20 @@ __device__ int32_t op_voxel(const WaveArgs& a, Cloud& c, Smem& S, const OpDesc& 
     if (c.counts) c.counts[v] = (int32_t)(s1 - s0);
   }
   __syncthreads();
-  for (int f = 0; f < a.n_bytes_fields; ++f) {
-    if (!((mm >> f) & 1u)) continue;
-    uint8_t* tmp = c.cur[f];
-    c.cur[f] = c.alt[f];
-    c.alt[f] = tmp;
-    c.n[f] = V;
+  if (threadIdx.x == 0) {
+    for (int f = 0; f < a.n_bytes_fields; ++f) {
+      if (!((mm >> f) & 1u)) continue;
+      uint8_t* tmp = c.cur[f];
+      c.cur[f] = c.alt[f];
+      c.alt[f] = tmp;
+      c.n[f] = V;
+    }
+    if (op.counts) {
+      c.has_counts = 1;
+      c.n_counts = V;
+    }
   }
-  if (op.counts) {
-    c.has_counts = 1;
-    c.n_counts = V;
-  }
+  __syncthreads();
   return kOk;
 }
 
@@ -1176,28 +1191,39 @@ __global__ void __launch_bounds__(512) k_cloud(WaveArgs a) {
 
   Cloud proto{};
   uint8_t* staging = carve(a, work, proto);
+  if (threadIdx.x == 0) S.proto = proto;
+  __syncthreads();
+  Cloud& c = S.cl;
 
   uint32_t phase = 0;
   for (uint32_t s = blockIdx.x; s < a.n_samples; s += gridDim.x) {
     const SampleWork sw = a.samples[s];
     const PageRef pg = a.pages[sw.block_page];
     const ScalarRec rec = a.recs[(uint64_t)a.groups[sw.group].first_rec + sw.row];
-    int32_t status = rec.status;
     int32_t fail_op = 0;
     // read_sample checks (format.cpp:741-755)
     const bool range_ok = sw.blob_end <= pg.raw_len && sw.blob_start <= sw.blob_end;
-    if (status == kOk && !range_ok) status = kRangeOutOfBounds;
-    if (status == kOk && rec.n_lens != (uint32_t)a.n_bytes_fields) status = kCorruptPage;
-    uint64_t flen[kMaxBytesFields], foff[kMaxBytesFields];
-    if (status == kOk) {
-      uint64_t at = 0;
-      for (int f = 0; f < a.n_bytes_fields; ++f) {
-        flen[f] = rec.lens[f];
-        foff[f] = at;
-        if (at + flen[f] > sw.blob_end - sw.blob_start) status = kRangeOutOfBounds;
-        at += flen[f];
+    uint64_t* flen = S.flen;
+    uint64_t* foff = S.foff;
+    if (threadIdx.x == 0) {
+      int32_t st0 = rec.status;
+      if (st0 == kOk && !range_ok) st0 = kRangeOutOfBounds;
+      if (st0 == kOk && rec.n_lens != (uint32_t)a.n_bytes_fields) st0 = kCorruptPage;
+      if (st0 == kOk) {
+        uint64_t at = 0;
+        for (int f = 0; f < a.n_bytes_fields; ++f) {
+          flen[f] = rec.lens[f];
+          foff[f] = at;
+          if (at + flen[f] > sw.blob_end - sw.blob_start) st0 = kRangeOutOfBounds;
+          at += flen[f];
+        }
       }
+      S.pre_status = st0;
+      S.cl = S.proto;
+      S.cl.present = 0;
     }
+    __syncthreads();
+    int32_t status = S.pre_status;
     const bool lz4 = (pg.flags & kFlagOuterLz4) != 0;
     if (!lz4 && pg.pay_len != pg.raw_len && status == kOk) status = kCorruptPage;
     const uint8_t* src = lz4 ? a.raw + pg.raw_dst + sw.blob_start
@@ -1232,8 +1258,6 @@ __global__ void __launch_bounds__(512) k_cloud(WaveArgs a) {
     }
 
     // ---- decode fields: XOR-delta per blob field (format.cpp:483-493) -----
-    Cloud c = proto;
-    c.present = 0;
     if (status == kOk) {
       const bool delta_page = (pg.flags & kFlagInnerDelta) != 0;
       for (int f = 0; f < a.n_bytes_fields && status == kOk; ++f) {
@@ -1254,9 +1278,11 @@ __global__ void __launch_bounds__(512) k_cloud(WaveArgs a) {
             const uint64_t nd = a.role_data >= 0 ? flen[a.role_data] / 12 : 0;
             e = (nd && flen[f] % nd == 0) ? (uint32_t)(flen[f] / nd) : 0;
           }
-          c.elem[f] = e ? e : 1;
-          c.n[f] = e ? (uint32_t)(flen[f] / e) : 0;
-          if (flen[f] > 0 || f == a.role_data) c.present |= 1u << f;
+          if (threadIdx.x == 0) {
+            c.elem[f] = e ? e : 1;
+            c.n[f] = e ? (uint32_t)(flen[f] / e) : 0;
+            if (flen[f] > 0 || f == a.role_data) c.present |= 1u << f;
+          }
         } else if (of >= 0) {
           if (flen[f] > a.out_stride[of]) {
             status = kOutOfBounds;
@@ -1268,6 +1294,7 @@ __global__ void __launch_bounds__(512) k_cloud(WaveArgs a) {
       }
     }
 
+    __syncthreads();
     // ---- the op chain (Pipeline map worker, pipeline.cpp:474-480) ---------
     if (status == kOk && a.n_ops > 0) {
       const int fd = a.role_data;
@@ -1375,12 +1402,17 @@ __global__ void __launch_bounds__(512) k_apply_set(WaveArgs a) {
   uint8_t* work = dyn + ((sizeof(Smem) + 127) & ~size_t(127));
   Cloud proto{};
   carve(a, work, proto);
+  if (threadIdx.x == 0) S.proto = proto;
   __syncthreads();
+  Cloud& c = S.cl;
   for (uint32_t s = blockIdx.x; s < a.n_samples; s += gridDim.x) {
     const uint64_t p0 = a.set_offset[s], p1 = a.set_offset[s + 1];
     const uint64_t n = p1 >= p0 ? p1 - p0 : 0;
-    Cloud c = proto;
-    c.present = 0;
+    if (threadIdx.x == 0) {
+      S.cl = S.proto;
+      S.cl.present = 0;
+    }
+    __syncthreads();
     int32_t status = kOk, fail_op = 0;
     if (n > a.cap_points) status = kOutOfBounds;
     for (int f = 0; status == kOk && f < a.n_bytes_fields; ++f) {
@@ -1395,9 +1427,11 @@ __global__ void __launch_bounds__(512) k_apply_set(WaveArgs a) {
       } else {
         for (uint64_t i = threadIdx.x; i < nb; i += blockDim.x) c.cur[f][i] = src[i];
       }
-      c.n[f] = (uint32_t)n;
-      c.elem[f] = e;
-      if (n > 0 || f == a.role_data) c.present |= 1u << f;
+      if (threadIdx.x == 0) {
+        c.n[f] = (uint32_t)n;
+        c.elem[f] = e;
+        if (n > 0 || f == a.role_data) c.present |= 1u << f;
+      }
     }
     __syncthreads();
     if (status == kOk && n == 0) status = kEmptyCloud;
