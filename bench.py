@@ -40,13 +40,18 @@ CONFIGS = {
                        points=10000, desc="ModelNet40-shaped 10k-pt clouds + normals: normalize, "
                        "FPS 1024, rotate, jitter; B 32"),
     "kitti": dict(gen="kitti", kw={}, clouds=512, group=16, batch=4, points=120000,
-                  desc="KITTI-shaped ~120k-pt XYZI frames: range crop, rotate, flip_yz; B 4"),
+                  desc="KITTI-shaped ~120k-pt XYZI frames: range crop, voxel 0.05 m (+counts), "
+                  "rotate, flip_yz; B 4 (CSR batches)"),
     "s3dis": dict(gen="s3dis", kw={"mean_points": 1_000_000}, clouds=64, group=1, batch=4,
-                  points=1_000_000, desc="S3DIS-shaped ~1M-pt XYZRGB rooms: random_crop, "
-                  "downsample 4096; B 4"),
+                  points=1_000_000, desc="S3DIS-shaped ~1M-pt XYZRGB rooms: grid 0.04 m, "
+                  "random_crop, downsample 4096; B 4"),
+    "scannet": dict(gen="scannet", kw={}, clouds=192, group=4, batch=4, points=275000,
+                    desc="ScanNet-shaped 50k-500k-pt XYZRGB scenes: grid 0.02 m, downsample "
+                    "40000, FPS 20000; B 4"),
 }
-CHAIN_OF = {"shapenet_part": "shapenet_part", "modelnet40": "modelnet40", "kitti": "kitti",
-            "s3dis": "s3dis"}
+CHAIN_OF = {k: k for k in CONFIGS}
+REF_OPS = {"normalize", "translate", "jitter", "rotate", "random_scale", "flip_yz",
+           "color_augment", "random_crop", "downsample"}
 SLICES = 8
 
 
@@ -77,49 +82,64 @@ def dataset(cfg_name, cfg, world, quantized, rank, barrier):
 
 
 class Clocks:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    """SM clocks and throttle reasons sampled every 20 ms during the timed
+    region (NVML; falls back to nvidia-smi -lms 200)."""
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
 
     def __init__(self, dev):
-        self.dev, self.rows, self.p = dev, [], None
+        self.dev, self.rows, self.stop, self.t, self.p = dev, [], False, None, None
+
+    def _nvml(self):
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(self.dev)
+        mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        while not self.stop:
+            sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+            rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+            self.rows.append((sm, mx, rs))
+            time.sleep(0.02)
 
     def __enter__(self):
         try:
-            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "200"],
-                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml  # noqa: F401
+            self.t = threading.Thread(target=self._nvml, daemon=True)
             self.t.start()
-        except OSError:
-            self.p = None
+        except Exception:
+            try:
+                q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active")
+                self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={q}",
+                                           "--format=csv,noheader,nounits", "-lms", "200"],
+                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                self.t = threading.Thread(target=self._smi, daemon=True)
+                self.t.start()
+            except OSError:
+                pass
         return self
 
-    def _read(self):
+    def _smi(self):
         for line in self.p.stdout:
             parts = [x.strip() for x in line.split(",")]
-            if len(parts) == 6:
-                self.rows.append(parts)
+            try:
+                self.rows.append((float(parts[0]), float(parts[1]), int(parts[2], 16)))
+            except (ValueError, IndexError):
+                pass
 
     def __exit__(self, *a):
+        self.stop = True
         if self.p:
             self.p.terminate()
-            try:
-                self.p.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.p.kill()
+        if self.t:
+            self.t.join(timeout=2)
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [r[0] for r in self.rows]
+        reasons = sorted({k for r in self.rows for k, bit in self.REASONS.items() if r[2] & bit})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(r[1] for r in self.rows),
+                "reasons": reasons, "samples": len(self.rows)}
 
 
 def peaks():
@@ -131,11 +151,11 @@ def peaks():
         return 6650.0, "fallback"
 
 
-def ncu_traffic(workload):
+def ncu_traffic(workload, kernel):
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
             s = json.load(f)
-        k = s.get(workload, {}).get("k_cloud", {})
+        k = s.get(workload, {}).get(kernel, {})
         return k.get("dram_bytes_per_launch"), k.get("alg_bytes_per_launch")
     except (OSError, ValueError):
         return None, None
@@ -148,29 +168,50 @@ def graph_for(cfg_name, cfg, workers=1):
 
 
 def cpu_reference(primary, graph, sample_ids, steps, warmup):
-    """The reference Pipeline (oracle/_ref: unmodified reference sources)
-    with all host threads, run_benchmark-style timing (bench.cpp:43-96)."""
-    from oracle.ffi import Ref
+    """CPU baseline on a bounded sample of the same dataset.
+
+    Graphs made only of reference ops run in the reference Pipeline
+    (oracle/_ref: unmodified reference sources) with all host threads,
+    run_benchmark-style timing (bench.cpp:43-96) -> kind "reference".
+    Graphs with App. C ops (fps / voxel / grid / range crop — absent from the
+    reference) run reference read_sample + reference ops + the C restatement
+    for the rest, one thread -> kind "port"."""
+    from oracle.ffi import Orc, Ref
     ref = Ref()
     ncpu = os.cpu_count() or 1
     g = json.loads(json.dumps(graph))
-    for o in g["ops"]:
-        if o["kind"] == "source":
-            o["num_workers"] = min(4, ncpu)
-        elif o["kind"] == "map":
-            o["num_workers"] = ncpu
+    steps_ops = [(o["map"], o.get("params", {}), o["id"]) for o in g["ops"] if o["kind"] == "map"]
+    if all(k in REF_OPS for k, _, _ in steps_ops):
+        for o in g["ops"]:
+            if o["kind"] == "source":
+                o["num_workers"] = min(4, ncpu)
+            elif o["kind"] == "map":
+                o["num_workers"] = ncpu
+        vals = []
+        for i in range(warmup + steps):
+            r = ref.bench_pipeline(primary, g, repeats=1, ids=sample_ids)
+            if i >= warmup:
+                vals.append(r["items"] / r["cost_time_s"])
+        return statistics.median(vals), ncpu, "reference"
+    orc = Orc()
     vals = []
     for i in range(warmup + steps):
-        r = ref.bench_pipeline(primary, g, repeats=1, ids=sample_ids)
+        t0 = time.perf_counter()
+        for k, smp in enumerate(ref.read_samples(primary, sample_ids)):
+            for kind, params, op_id in steps_ops:
+                seed = ref.mix_seed(g.get("base_seed", 0), 0, k, op_id)
+                impl = ref if kind in REF_OPS and "gather" not in params else orc
+                smp = impl.apply_map(kind, params, smp, seed)
+        dt = time.perf_counter() - t0
         if i >= warmup:
-            vals.append(r["items"] / r["cost_time_s"])
-    return statistics.median(vals), ncpu, g
+            vals.append(len(sample_ids) / dt)
+    return statistics.median(vals), 1, "port"
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="shapenet_part", choices=sorted(CONFIGS))
@@ -191,8 +232,8 @@ def main():
               "parallelism": f"record-sharded by slice, {world} independent pipelines",
               "l2": "inputs per step > 126 MB L2 (no flush needed)"}
     metric = "point clouds/sec (PcRecord -> training batch)"
-    cpu_sample = args.cpu_sample or {"shapenet_part": 4096, "modelnet40": 512, "kitti": 32,
-                                     "s3dis": 4}[args.config]
+    cpu_sample = args.cpu_sample or {"shapenet_part": 4096, "modelnet40": 64, "kitti": 16,
+                                     "s3dis": 2, "scannet": 2}[args.config]
 
     if args.impl == "reference":
         if rank != 0:
@@ -202,15 +243,15 @@ def main():
         from paper_2603_16945_b200 import shard
         idx = shard.read_index(primary)
         ids = np.arange(min(cpu_sample, len(idx)), dtype=np.uint64)
-        v, ncpu, _ = cpu_reference(primary, g, ids, args.steps, args.warmup)
+        v, ncpu, kind = cpu_reference(primary, g, ids, args.steps, args.warmup)
         line = {"metric": metric, "value": v, "unit": "clouds/s", "impl": "reference",
                 "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
                 "data": "synthetic", "config": config,
                 "mpoints_per_sec": v * cfg["points"] / 1e6,
-                "cpu_baseline": {"value": v, "unit": "clouds/s", "cores": ncpu, "kind": "reference",
-                                 "sample": f"{len(ids)} clouds per step (first entries), reference "
-                                           f"Pipeline, {ncpu} map workers"},
+                "cpu_baseline": {"value": v, "unit": "clouds/s", "cores": ncpu, "kind": kind,
+                                 "sample": f"{len(ids)} clouds per step (first entries); "
+                                           f"{'reference Pipeline, ' + str(ncpu) + ' map workers' if kind == 'reference' else 'reference reads/ops + C restatement for App. C ops, 1 thread'}"},
                 "e2e": {"value": v, "unit": "clouds/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
         if args.config == "shapenet_part":
@@ -276,19 +317,28 @@ def main():
         dist.all_reduce(tot)
     clouds_all, points_all = float(tot[0]), float(tot[1])
     value = clouds_all / (ms_max / 1e3)
-    # roofline of the dominant kernel (k_cloud), measured live with CUDA events
-    kms = st1["cloud_kernel_ms"] - st0["cloud_kernel_ms"]
-    kbytes = st1["cloud_kernel_alg_bytes"] - st0["cloud_kernel_alg_bytes"]
-    waves = max(1, st1["waves"] - st0["waves"] + 1)
+    # roofline of the dominant kernel, measured live with CUDA events on the
+    # wave streams (k_cloud and k_page_decode are both timed per wave)
     peak, peak_kind = peaks()
-    achieved = kbytes / (kms / 1e3) / 1e9 if kms > 0 else 0.0
-    dram, alg_per_launch = ncu_traffic(args.config)
-    roof = {"bound": "hbm", "kernel": "k_cloud", "achieved": achieved, "peak": peak,
-            "unit": "GB/s", "frac": achieved / peak, "peak_kind": peak_kind,
-            "traffic": dram, "alg_bytes_per_launch": kbytes / waves,
-            "kernel_ms_per_step": kms / args.steps,
-            "kernel_share_of_step": kms / ms if ms else None,
-            "step_hbm_gbs": kbytes / (ms / 1e3) / 1e9}
+    waves = max(1, st1["waves"] - st0["waves"])
+    kern = {}
+    for name, ms_key, by_key in (("k_cloud", "cloud_kernel_ms", "cloud_kernel_alg_bytes"),
+                                 ("k_page_decode", "decode_kernel_ms", "decode_kernel_alg_bytes")):
+        kms = st1[ms_key] - st0[ms_key]
+        kby = st1[by_key] - st0[by_key]
+        kern[name] = {"ms_per_step": kms / args.steps, "alg_bytes_per_step": kby / args.steps,
+                      "achieved_gbs": kby / (kms / 1e3) / 1e9 if kms > 0 else 0.0,
+                      "share_of_step": kms / ms if ms else None}
+    dom = max(kern, key=lambda k: kern[k]["ms_per_step"])
+    dram, alg_per_launch = ncu_traffic(args.config, dom)
+    achieved = kern[dom]["achieved_gbs"]
+    roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "peak_kind": peak_kind, "traffic": dram,
+            "alg_bytes_per_launch": kern[dom]["alg_bytes_per_step"] * args.steps / waves,
+            "kernels": kern}
+    if dom == "k_page_decode":
+        roof["note"] = ("latency-bound: one serial LZ4 token/match chain per page "
+                        "(DESIGN.md 4.2); HBM fraction reported for completeness")
     if dram is not None and alg_per_launch:
         roof["traffic_over_alg"] = dram / alg_per_launch
     e2e = None
@@ -309,10 +359,11 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         ids_cpu = np.arange(min(cpu_sample, len(idx)), dtype=np.uint64)
-        v, ncpu, _ = cpu_reference(primary, g, ids_cpu, 1, 0)
-        cpu = {"value": v, "unit": "clouds/s", "cores": ncpu, "kind": "reference",
-               "sample": f"{len(ids_cpu)} clouds of the same dataset, reference Pipeline "
-                         f"(oracle/_ref), {ncpu} map workers"}
+        v, ncpu, kind = cpu_reference(primary, g, ids_cpu, 1, 0)
+        cpu = {"value": v, "unit": "clouds/s", "cores": ncpu, "kind": kind,
+               "sample": f"{len(ids_cpu)} clouds of the same dataset; "
+                         + (f"reference Pipeline (oracle/_ref), {ncpu} map workers" if kind == "reference"
+                            else "reference reads/ops + C restatement for App. C ops, 1 thread")}
     if rank == 0:
         line = {"metric": metric, "value": value, "unit": "clouds/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,

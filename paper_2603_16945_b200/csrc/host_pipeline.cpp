@@ -295,7 +295,8 @@ struct Wave {
   uint32_t n_batches = 0;
   bool launched = false;
   cudaStream_t stream = nullptr;  // one stream per slot: consecutive waves overlap
-  cudaEvent_t done = nullptr, k0 = nullptr, k1 = nullptr;
+  cudaEvent_t done = nullptr, k0 = nullptr, k1 = nullptr, d0 = nullptr, d1 = nullptr;
+  uint64_t decode_alg_bytes = 0;  // payload + raw bytes of the pages k_page_decode handles
   DevBuf gscratch;                // k_cloud global slab (smem_mode 0), per slot
   // device
   DevBuf bytes_stage, raw, tables, outs, compact, compact_meta, lz4_scratch, lz4_timing;
@@ -356,7 +357,8 @@ struct Pipeline {
   // stats
   uint64_t clouds = 0, points_in = 0, payload_bytes = 0, batches = 0;
   uint64_t h2d_bytes = 0, launches = 0, alg_bytes = 0;
-  double kernel_ms = 0, cloud_kernel_ms = 0;
+  double kernel_ms = 0, cloud_kernel_ms = 0, decode_kernel_ms = 0;
+  uint64_t decode_alg_bytes = 0;
   uint32_t waves_done = 0;
 
   ~Pipeline() {
@@ -365,6 +367,8 @@ struct Pipeline {
       if (w.done) cudaEventDestroy(w.done);
       if (w.k0) cudaEventDestroy(w.k0);
       if (w.k1) cudaEventDestroy(w.k1);
+      if (w.d0) cudaEventDestroy(w.d0);
+      if (w.d1) cudaEventDestroy(w.d1);
     }
     if (stream) cudaStreamDestroy(stream);
     if (serve_stream) cudaStreamDestroy(serve_stream);
@@ -409,10 +413,13 @@ struct Pipeline {
     slots.resize(3);
     for (auto& w : slots) {
       CK(cudaStreamCreateWithFlags(&w.stream, cudaStreamNonBlocking));
+      for (size_t pi = 0; pi < plan.size() && plan[pi].first == 0; ++pi) launch(w, pi, true);
       if (!proto.smem_mode) w.gscratch.ensure(proto.gscratch_per_cta * grid);
       CK(cudaEventCreate(&w.done));
       CK(cudaEventCreate(&w.k0));
       CK(cudaEventCreate(&w.k1));
+      CK(cudaEventCreate(&w.d0));
+      CK(cudaEventCreate(&w.d1));
     }
   }
 
@@ -659,7 +666,7 @@ struct Pipeline {
   }
 
   // ---- wave construction ---------------------------------------------------
-  void launch(Wave& w, size_t pi) {
+  void launch(Wave& w, size_t pi, bool dry = false) {
     w.epoch = plan[pi].first;
     w.pos0 = plan[pi].second;
     w.n = plan_n[pi];
@@ -817,7 +824,29 @@ struct Pipeline {
     const uint64_t o_swh = o_sop + sz(w.n * 4);
     const uint64_t o_len = o_swh + sz(w.n * 4);
     const uint64_t total = o_len + sz(outs.size() * w.n * 8);
+    // size every buffer first (a dry run stops here: open() pre-sizes the
+    // slots for the largest planned wave so no cudaMalloc lands mid-run)
     w.h_tables.ensure(up_bytes);
+    w.tables.ensure(total);
+    if (!resident) w.bytes_stage.ensure(stage_at + 64);
+    w.raw.ensure(raw_at + 64);
+    w.lz4_scratch.ensure(scratch_at + 64);
+    w.out_base.resize(outs.size());
+    uint64_t out_total = 0;
+    for (size_t f = 0; f < outs.size(); ++f) {
+      w.out_base[f] = out_total;
+      out_total += align16(outs[f].stride * w.n) + 64;
+    }
+    w.outs.ensure(out_total);
+    w.h_res.ensure(3 * align16(w.n * 4) + outs.size() * w.n * 8);
+    {
+      uint64_t need = 0;
+      for (size_t q = 0; q < outs.size(); ++q) need += align16(outs[q].stride * B) + 64;
+      w.compact.ensure(need);
+      w.compact_meta.ensure(2 * (uint64_t)(B + 1) * 8 * outs.size());
+      w.h_compact_meta.ensure(2 * (uint64_t)(B + 1) * 8 * outs.size());
+    }
+    if (dry) return;
     uint8_t* ht = w.h_tables.as<uint8_t>();
     std::memcpy(ht + o_pages, pages.data(), pages.size() * sizeof(PageRef));
     std::memcpy(ht + o_groups, gw.data(), gw.size() * sizeof(GroupWork));
@@ -825,12 +854,10 @@ struct Pipeline {
     std::memcpy(ht + o_todo, todo.data(), todo.size() * 4);
     std::memcpy(ht + o_tsc, todo_scratch.data(), todo_scratch.size() * 8);
     std::memcpy(ht + o_wins, wins.data(), wins.size() * sizeof(CrcWindow));
-    w.tables.ensure(total);
     uint8_t* dt = w.tables.as<uint8_t>();
     // staged input bytes
     const uint8_t* bytes = d_store.as<uint8_t>();
     if (!resident) {
-      w.bytes_stage.ensure(stage_at + 64);
       uint64_t d_at = 64;
       for (const auto& r : runs) {
         CK(cudaMemcpyAsync(w.bytes_stage.as<uint8_t>() + d_at, h_store.as<uint8_t>() + r.first,
@@ -842,16 +869,6 @@ struct Pipeline {
     }
     CK(cudaMemcpyAsync(dt, ht, up_bytes, cudaMemcpyHostToDevice, w.stream));
     CK(cudaMemsetAsync(dt + o_acc, 0, o_len - o_acc, w.stream));
-    w.raw.ensure(raw_at + 64);
-    w.lz4_scratch.ensure(scratch_at + 64);
-    // outputs
-    w.out_base.resize(outs.size());
-    uint64_t out_total = 0;
-    for (size_t f = 0; f < outs.size(); ++f) {
-      w.out_base[f] = out_total;
-      out_total += align16(outs[f].stride * w.n) + 64;
-    }
-    w.outs.ensure(out_total);
     // ---- args ----------------------------------------------------------------
     a.bytes = bytes;
     a.raw = w.raw.as<uint8_t>();
@@ -884,16 +901,19 @@ struct Pipeline {
       CK(cudaMemsetAsync(w.lz4_timing.p, 0, todo.size() * 64, w.stream));
       tm = w.lz4_timing.as<long long>();
     }
+    CK(cudaEventRecord(w.d0, w.stream));
     CK(launch_page_decode(bytes, a.raw, a.pages, reinterpret_cast<const uint32_t*>(dt + o_todo),
                           reinterpret_cast<const uint64_t*>(dt + o_tsc), w.lz4_scratch.as<uint8_t>(),
                           (uint32_t)todo.size(), a.page_status, w.stream, tm));
+    CK(cudaEventRecord(w.d1, w.stream));
     w.n_todo = (uint32_t)todo.size();
+    w.decode_alg_bytes = 0;
+    for (uint32_t pi : todo) w.decode_alg_bytes += pages[pi].pay_len + pages[pi].raw_len;
     CK(launch_wave(a, grid, threads, smem, w.stream, w.k0, w.k1));
     launches += (wins.empty() ? 0 : 1) + (todo.empty() ? 0 : 1) + (ng ? 1 : 0) + 1 + 1 + 1;
     h2d_bytes += up_bytes;
     // ---- results back to pinned host -------------------------------------------
-    const uint64_t res = 3 * align16(w.n * 4) + outs.size() * w.n * 8;
-    w.h_res.ensure(res);
+
     uint8_t* hr = w.h_res.as<uint8_t>();
     w.h_status = reinterpret_cast<int32_t*>(hr);
     w.h_op = reinterpret_cast<int32_t*>(hr + align16(w.n * 4));
@@ -944,6 +964,9 @@ struct Pipeline {
       float ms = 0;
       CK(cudaEventElapsedTime(&ms, wn.k0, wn.k1));
       cloud_kernel_ms += ms;
+      CK(cudaEventElapsedTime(&ms, wn.d0, wn.d1));
+      decode_kernel_ms += ms;
+      decode_alg_bytes += wn.decode_alg_bytes;
       if (lz4_timing && wn.n_todo) {
         std::vector<long long> tm(wn.n_todo * 8);
         CK(cudaMemcpy(tm.data(), wn.lz4_timing.p, tm.size() * 8, cudaMemcpyDeviceToHost));
@@ -986,13 +1009,7 @@ struct Pipeline {
     out->n_samples = nb;
     out->n_fields = (uint32_t)outs.size();
     w.offsets.assign(outs.size(), std::vector<uint64_t>(nb + 1, 0));
-    {  // per-field CSR buffers for ragged batches live back to back in w.compact
-      uint64_t need = 0;
-      for (size_t q = 0; q < outs.size(); ++q) need += align16(outs[q].stride * B) + 64;
-      w.compact.ensure(need);
-      w.compact_meta.ensure(2 * (uint64_t)(B + 1) * 8 * outs.size());
-      w.h_compact_meta.ensure(2 * (uint64_t)(B + 1) * 8 * outs.size());
-    }
+
     for (size_t f = 0; f < outs.size(); ++f) {
       pcp_field& pf = out->fields[f];
       std::snprintf(pf.name, sizeof(pf.name), "%s", outs[f].name.c_str());
@@ -1045,6 +1062,8 @@ struct Pipeline {
            {"waves", waves_done},
            {"cloud_kernel_ms", cloud_kernel_ms},
            {"cloud_kernel_alg_bytes", alg_bytes},
+           {"decode_kernel_ms", decode_kernel_ms},
+           {"decode_kernel_alg_bytes", decode_alg_bytes},
            {"h2d_bytes", h2d_bytes},
            {"launches", launches},
            {"grid", grid},

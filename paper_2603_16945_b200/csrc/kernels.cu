@@ -16,6 +16,7 @@
 // output uses explicit _rn intrinsics (no FMA), like the reference build.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cfloat>
 #include <cstdint>
 
@@ -1660,20 +1661,32 @@ cudaError_t launch_wave(const WaveArgs& a, int grid, int threads, size_t smem, c
 }
 
 // Ragged batch → CSR: sample i's len[i] bytes from slot i to dst + off[i].
+// blockIdx.y = sample, blockIdx.x strides its bytes; 4-byte words when the
+// slot stride and the CSR offset allow (every float/int32 field does).
 __global__ void k_compact(const uint8_t* src, uint64_t stride, const uint64_t* off,
                           const uint64_t* len, uint32_t n, uint8_t* dst) {
-  for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
-    const uint8_t* s = src + (uint64_t)i * stride;
-    uint8_t* d = dst + off[i];
-    const uint64_t L = len[i];
-    for (uint64_t k = threadIdx.x; k < L; k += blockDim.x) d[k] = s[k];
+  const uint32_t i = blockIdx.y;
+  if (i >= n) return;
+  const uint8_t* s = src + (uint64_t)i * stride;
+  uint8_t* d = dst + off[i];
+  const uint64_t L = len[i];
+  const uint64_t step = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if ((((uintptr_t)s | (uintptr_t)d) & 3u) == 0) {
+    const uint32_t* s4 = reinterpret_cast<const uint32_t*>(s);
+    uint32_t* d4 = reinterpret_cast<uint32_t*>(d);
+    for (uint64_t k = t0; k < L / 4; k += step) d4[k] = s4[k];
+    for (uint64_t k = (L & ~3ull) + t0; k < L; k += step) d[k] = s[k];
+  } else {
+    for (uint64_t k = t0; k < L; k += step) d[k] = s[k];
   }
 }
 
 cudaError_t launch_compact(const uint8_t* src, uint64_t stride, const uint64_t* d_off,
                            const uint64_t* d_len, uint32_t n, uint8_t* dst, cudaStream_t st) {
   if (!n) return cudaSuccess;
-  k_compact<<<n < 1024 ? n : 1024, 256, 0, st>>>(src, stride, d_off, d_len, n, dst);
+  const uint32_t bx = (uint32_t)std::min<uint64_t>(64, (stride / 4 + 255) / 256 + 1);
+  k_compact<<<dim3(bx, n), 256, 0, st>>>(src, stride, d_off, d_len, n, dst);
   return cudaGetLastError();
 }
 
