@@ -256,6 +256,71 @@ void parse_op_params(OpDesc& op, const json& p, IndexOf bytes_index_of) {
   if (op.kind == kVoxel && !(op.voxel > 0.0f)) fail(kOutOfBounds, "voxel_size must be positive");
 }
 
+// Per-CTA buffer plan of k_cloud / k_apply_set (buffer ids in WaveArgs):
+// sizes follow what the op chain can need; shared memory is filled greedily
+// in priority order (coordinates first), everything else goes to the per-CTA
+// global slab (a.gscratch_per_cta).  Returns the shared bytes used.
+size_t plan_buffers(WaveArgs& a, bool want_staging, size_t smem_budget) {
+  uint64_t T = 0, M = 0;
+  bool ds = false, fps = false, crop = false, vox = false;
+  for (int k = 0; k < a.n_ops; ++k) {
+    const OpDesc& op = a.ops[k];
+    if (op.kind == kDownsample) ds = true, T = std::max<uint64_t>(T, (uint64_t)op.num_points);
+    if (op.kind == kFps) fps = true, M = std::max<uint64_t>(M, (uint64_t)op.num_points);
+    if (op.kind == kRandomCrop || op.kind == kRangeCrop) crop = true;
+    if (op.kind == kVoxel) vox = true;
+  }
+  const uint64_t cap = a.cap_points;
+  const uint64_t big = (crop || vox) ? cap : 0;
+  const uint64_t alt_pts = std::max({T, M, big});
+  auto with = [](uint64_t b) { return b ? b + 16 : 0; };
+  uint64_t* sz = a.buf_bytes;
+  for (int b = 0; b < 24; ++b) sz[b] = 0;
+  sz[0] = want_staging ? (uint64_t)a.max_blob + 64 : 0;
+  sz[1] = 4 * std::max<uint64_t>({T, M, big, 1}) + 16;
+  sz[2] = with(4 * ((ds || fps || vox) ? cap : 0));
+  sz[3] = with(4 * std::max<uint64_t>(ds ? T : 0, vox ? cap : 0));
+  sz[4] = with(4 * (ds ? T : 0));
+  for (int f = 0; f < a.n_bytes_fields; ++f) {
+    if (!((a.tracked_mask >> f) & 1u)) continue;
+    sz[5 + f] = cap * a.field_cap[f] + 16;
+    sz[13 + f] = with(alt_pts * a.field_cap[f]);
+  }
+  if (vox) {
+    sz[21] = sz[22] = 8 * cap + 16;
+    sz[23] = 4 * cap + 16;
+  }
+  std::vector<int> order;
+  const int rd = a.role_data;
+  if (rd >= 0) order.push_back(5 + rd);
+  for (int b : {1, 3, 4}) order.push_back(b);
+  if (rd >= 0) order.push_back(13 + rd);
+  order.push_back(2);
+  for (int f = 0; f < kMaxBytesFields; ++f)
+    if (f != rd) order.push_back(5 + f);
+  for (int f = 0; f < kMaxBytesFields; ++f)
+    if (f != rd) order.push_back(13 + f);
+  for (int b : {21, 22, 23, 0}) order.push_back(b);
+  auto rnd = [](uint64_t v) { return (v + 127) & ~uint64_t(127); };
+  size_t used = 0;
+  uint64_t gbytes = 0;
+  a.buf_smem_mask = 0;
+  for (int b : order) {
+    if (!sz[b]) continue;
+    if (used + rnd(sz[b]) <= smem_budget) {
+      used += rnd(sz[b]);
+      a.buf_smem_mask |= 1u << b;
+    } else if (b == 0) {
+      sz[0] = 0;  // no staging: decode reads the blob from global memory
+    } else {
+      gbytes += rnd(sz[b]);
+    }
+  }
+  a.smem_mode = a.buf_smem_mask ? 1 : 0;
+  a.gscratch_per_cta = gbytes;
+  return used;
+}
+
 // Per-device state for the stateless entry points (codec + operator API).
 struct DeviceCtx {
   int sms = 0;
@@ -414,7 +479,7 @@ struct Pipeline {
     for (auto& w : slots) {
       CK(cudaStreamCreateWithFlags(&w.stream, cudaStreamNonBlocking));
       for (size_t pi = 0; pi < plan.size() && plan[pi].first == 0; ++pi) launch(w, pi, true);
-      if (!proto.smem_mode) w.gscratch.ensure(proto.gscratch_per_cta * grid);
+      if (proto.gscratch_per_cta) w.gscratch.ensure(proto.gscratch_per_cta * grid);
       CK(cudaEventCreate(&w.done));
       CK(cudaEventCreate(&w.k0));
       CK(cudaEventCreate(&w.k1));
@@ -617,29 +682,22 @@ struct Pipeline {
     }
     if (outs.size() > (size_t)PCP_MAX_BATCH_FIELDS) fail(kOutOfBounds, "too many batch fields");
     a.n_out = (int32_t)outs.size();
-    // shared-memory plan for k_cloud
-    auto rnd = [](uint64_t v) { return (v + 127) & ~uint64_t(127); };
-    uint64_t need = rnd(a.max_blob + 64) + 4 * rnd((uint64_t)cap * 4 + 16);
-    if (a.voxel_scratch) need += 2 * rnd((uint64_t)cap * 8 + 16) + rnd((uint64_t)cap * 4 + 16);
-    for (size_t f = 0; f < bytes_fields.size(); ++f)
-      if ((tracked >> f) & 1u) need += 2 * rnd((uint64_t)cap * a.field_cap[f] + 16);
-    const size_t fixed = cloud_smem_fixed();
+    // per-CTA buffer plan for k_cloud (sizes from the op chain, shared
+    // memory by priority, the rest in a per-CTA global slab)
+    bool any_stored_raw = false;
+    for (const auto& bh : block_head) any_stored_raw |= !(bh.flags & kFlagOuterLz4);
     cudaDeviceProp prop;
     CK(cudaGetDeviceProperties(&prop, device));
-    const size_t limit = prop.sharedMemPerBlockOptin;
-    a.smem_mode = (fixed + need <= limit) ? 1 : 0;
-    smem = a.smem_mode ? fixed + need : fixed;
+    const size_t fixed = cloud_smem_fixed();
+    const size_t used = plan_buffers(a, any_stored_raw, prop.sharedMemPerBlockOptin - fixed);
+    smem = fixed + used;
     CK(set_cloud_smem(smem));
+    // two CTAs per SM when the shared footprint allows it (the 64-register
+    // build), otherwise one CTA with the 128-register build (FPS fast path)
+    a.min_blocks = (2 * smem <= prop.sharedMemPerMultiprocessor) ? 2 : 1;
     int per_sm = 0;
-    CK(occupancy_cloud(&per_sm, threads, smem));
+    CK(occupancy_cloud(&per_sm, threads, smem, a.min_blocks));
     grid = std::max(1, per_sm) * sms;
-    if (!a.smem_mode) {
-      uint64_t per = 4 * rnd((uint64_t)cap * 4 + 16);
-      if (a.voxel_scratch) per += 2 * rnd((uint64_t)cap * 8 + 16) + rnd((uint64_t)cap * 4 + 16);
-      for (size_t f = 0; f < bytes_fields.size(); ++f)
-        if ((tracked >> f) & 1u) per += 2 * rnd((uint64_t)cap * a.field_cap[f] + 16);
-      a.gscratch_per_cta = per;  // slabs are allocated per wave slot
-    }
     a.force_serial_fy = force_serial_fy ? 1 : 0;
   }
 
@@ -887,7 +945,7 @@ struct Pipeline {
     a.sample_where = reinterpret_cast<int32_t*>(dt + o_swh);
     a.out_len = reinterpret_cast<uint64_t*>(dt + o_len);
     a.shift_tab = d_shift.as<uint32_t>();
-    if (!a.smem_mode) a.gscratch = w.gscratch.as<uint8_t>();
+    a.gscratch = proto.gscratch_per_cta ? w.gscratch.as<uint8_t>() : nullptr;
     for (size_t f = 0; f < outs.size(); ++f) {
       a.out[f] = w.outs.as<uint8_t>() + w.out_base[f];
       a.out_stride[f] = outs[f].stride;
@@ -1230,23 +1288,16 @@ int pcp_apply_map(int kind, const char* params_json, const pcp_cloud_set* in,
     a.voxel_scratch = kind == kVoxel ? 1 : 0;
     a.set_voxel_count = out->d_voxel_count;
     a.count_out = -1;
-    auto rnd = [](uint64_t v) { return (v + 127) & ~uint64_t(127); };
-    uint64_t need = rnd(64) + 4 * rnd((uint64_t)a.cap_points * 4 + 16);
-    if (a.voxel_scratch) need += 2 * rnd((uint64_t)a.cap_points * 8 + 16) + rnd((uint64_t)a.cap_points * 4 + 16);
-    for (int f = 0; f < 8; ++f)
-      if ((a.tracked_mask >> f) & 1u) need += 2 * rnd((uint64_t)a.cap_points * a.field_cap[f] + 16);
     cudaDeviceProp prop;
     int dev = 0;
     CK(cudaGetDevice(&dev));
     CK(cudaGetDeviceProperties(&prop, dev));
     const size_t fixed = cloud_smem_fixed();
-    a.smem_mode = (fixed + need <= prop.sharedMemPerBlockOptin) ? 1 : 0;
-    const size_t smem = a.smem_mode ? fixed + need : fixed;
+    const size_t smem = fixed + plan_buffers(a, false, prop.sharedMemPerBlockOptin - fixed);
     int grid = ctx.sms * 2;
-    if (!a.smem_mode) {
-      a.gscratch_per_cta = need;
+    if (a.gscratch_per_cta) {
       grid = std::min<int>(grid, (int)n);
-      ctx.scratch.ensure(need * grid);
+      ctx.scratch.ensure(a.gscratch_per_cta * grid);
       a.gscratch = ctx.scratch.as<uint8_t>();
     }
     CK(launch_apply_set(a, grid, 512, smem, st));

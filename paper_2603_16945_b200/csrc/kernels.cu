@@ -849,6 +849,60 @@ __device__ int32_t op_downsample(const WaveArgs& a, Cloud& c, Smem& S, const OpD
 
 // FPS (App. C): start at 0, d2 = (dx*dx + dy*dy) + dz*dz without FMA,
 // mind = min(mind, d2), next = argmax mind (lowest index on ties).
+// FPS fast path (cloud in shared memory, N <= kFpsRegPts * blockDim): each
+// thread keeps the min-distances of points i = t + k*nt in registers, reads
+// coordinates with LDS through the dynamic-smem base, reduces (value, index)
+// with warp shuffles and publishes one candidate per warp into a parity
+// double-buffered slot, so each iteration needs ONE block barrier.
+constexpr uint32_t kFpsRegPts = 24;
+
+__device__ __forceinline__ uint64_t umax64(uint64_t a, uint64_t b) { return a > b ? a : b; }
+
+__device__ void fps_fast(const float* dg, uint32_t N, uint32_t M, int32_t* idx, Smem& S) {
+  extern __shared__ __align__(128) uint8_t dyn[];
+  const float* d = reinterpret_cast<const float*>(dyn + (reinterpret_cast<const uint8_t*>(dg) - dyn));
+  // (value, index) packed as value_bits << 32 | ~index: min-distances are
+  // >= +0 or +inf (a NaN distance never replaces mind), so unsigned order of
+  // the key = larger value first, then lower index — the App. C argmax.
+  uint64_t* slot = reinterpret_cast<uint64_t*>(S.rs_wcnt);  // [2][16]
+  const uint32_t t = threadIdx.x, nt = blockDim.x, lane = t & 31, w = t >> 5, nw = nt >> 5;
+  float mind[kFpsRegPts];
+#pragma unroll
+  for (int k = 0; k < (int)kFpsRegPts; ++k) mind[k] = INFINITY;
+  uint32_t sel = 0;
+  for (uint32_t it = 0; it < M; ++it) {
+    if (t == 0) idx[it] = (int32_t)sel;
+    const float sx = d[3 * sel], sy = d[3 * sel + 1], sz = d[3 * sel + 2];
+    uint64_t b0 = 0, b1 = 0;  // two independent chains (even / odd k)
+#pragma unroll
+    for (int k = 0; k < (int)kFpsRegPts; ++k) {
+      const uint32_t i = t + (uint32_t)k * nt;
+      if (i < N) {
+        const float dx = __fsub_rn(d[3 * i], sx), dy = __fsub_rn(d[3 * i + 1], sy),
+                    dz = __fsub_rn(d[3 * i + 2], sz);
+        const float dd =
+            __fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz));
+        const float m = dd < mind[k] ? dd : mind[k];
+        mind[k] = m;
+        const uint64_t key = ((uint64_t)__float_as_uint(m) << 32) | (0xFFFFFFFFu - i);
+        if (k & 1) b1 = umax64(b1, key);
+        else b0 = umax64(b0, key);
+      }
+    }
+    uint64_t best = umax64(b0, b1);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) best = umax64(best, __shfl_xor_sync(0xffffffffu, best, o));
+    const uint32_t par = it & 1u;
+    if (lane == 0) slot[par * 16 + w] = best;
+    __syncthreads();
+    uint64_t g = lane < nw ? slot[par * 16 + lane] : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) g = umax64(g, __shfl_xor_sync(0xffffffffu, g, o));
+    // g == 0 only if no candidate (N == 0): select index 0 like the oracle
+    sel = g ? 0xFFFFFFFFu - (uint32_t)(g & 0xFFFFFFFFu) : 0u;
+  }
+}
+
 __device__ int32_t op_fps(const WaveArgs& a, Cloud& c, Smem& S, const OpDesc& op) {
   if (op.num_points <= 0) return kOutOfBounds;
   const uint32_t M = (uint32_t)op.num_points;
@@ -858,8 +912,14 @@ __device__ int32_t op_fps(const WaveArgs& a, Cloud& c, Smem& S, const OpDesc& op
   const int32_t st = check_move(a, c, mm);
   if (st) return st;
   const float* d = F(c, a.role_data);
-  float* mind = reinterpret_cast<float*>(c.ix[1]);
   int32_t* idx = c.ix[0];
+  if (N <= kFpsRegPts * blockDim.x && __isShared(d)) {
+    fps_fast(d, N, M, idx, S);
+    __syncthreads();
+    gather_mask_fields(a, c, mm, idx, M);
+    return kOk;
+  }
+  float* mind = reinterpret_cast<float*>(c.ix[1]);
   for (uint32_t i = threadIdx.x; i < N; i += blockDim.x) mind[i] = INFINITY;
   __syncthreads();
   uint32_t sel = 0;
@@ -1179,7 +1239,10 @@ __device__ __forceinline__ uint64_t field_bytes(const WaveArgs& a, int f) {
   return (uint64_t)a.cap_points * a.field_cap[f] + 16;
 }
 
-__global__ void __launch_bounds__(512) k_cloud(WaveArgs a) {
+// MinBlocks = 1: up to 128 registers (FPS keeps min-distances in registers);
+// MinBlocks = 2: <= 64 registers, two CTAs per SM for global-slab clouds.
+template <int MinBlocks>
+__global__ void __launch_bounds__(512, MinBlocks) k_cloud(WaveArgs a) {
   extern __shared__ __align__(128) uint8_t dyn[];
   Smem& S = *reinterpret_cast<Smem*>(dyn);
   uint8_t* work = dyn + ((sizeof(Smem) + 127) & ~size_t(127));
@@ -1234,7 +1297,7 @@ __global__ void __launch_bounds__(512) k_cloud(WaveArgs a) {
 
     // ---- stage the blob with one TMA bulk copy (smem mode) ----------------
     const uint8_t* blob = src;
-    if (need_bytes && a.smem_mode && blen > 0) {
+    if (need_bytes && staging && blen > 0) {
       const uintptr_t g0 = reinterpret_cast<uintptr_t>(src) & ~uintptr_t(15);
       const uintptr_t g1 = (reinterpret_cast<uintptr_t>(src) + blen + 15) & ~uintptr_t(15);
       const uint32_t nbytes = (uint32_t)(g1 - g0);
@@ -1371,33 +1434,36 @@ __global__ void __launch_bounds__(512) k_cloud(WaveArgs a) {
 }
 
 __device__ uint8_t* carve(const WaveArgs& a, uint8_t* work, Cloud& proto) {
-  uint8_t* sbase = a.smem_mode ? work : a.gscratch + (uint64_t)blockIdx.x * a.gscratch_per_cta;
-  uint64_t off = 0;
-  auto take = [&](uint64_t nb) {
-    uint8_t* p = sbase + off;
-    off += (nb + 127) & ~uint64_t(127);
-    return p;
-  };
-  uint8_t* staging = a.smem_mode ? take((uint64_t)a.max_blob + 64) : nullptr;
+  uint8_t* gbase = a.gscratch ? a.gscratch + (uint64_t)blockIdx.x * a.gscratch_per_cta : nullptr;
+  uint64_t soff = 0, goff = 0;
+  uint8_t* ptr[24];
+  for (int b = 0; b < 24; ++b) {
+    const uint64_t nb = (a.buf_bytes[b] + 127) & ~uint64_t(127);
+    if (!nb) {
+      ptr[b] = nullptr;
+    } else if ((a.buf_smem_mask >> b) & 1u) {
+      ptr[b] = work + soff;
+      soff += nb;
+    } else {
+      ptr[b] = gbase + goff;
+      goff += nb;
+    }
+  }
   proto.cap = a.cap_points;
-  for (int k = 0; k < 4; ++k)
-    proto.ix[k] = reinterpret_cast<int32_t*>(take((uint64_t)a.cap_points * 4 + 16));
-  for (int f = 0; f < a.n_bytes_fields; ++f) {
-    if (!((a.tracked_mask >> f) & 1u)) continue;
-    proto.cur[f] = take(field_bytes(a, f));
-    proto.alt[f] = take(field_bytes(a, f));
+  for (int k = 0; k < 4; ++k) proto.ix[k] = reinterpret_cast<int32_t*>(ptr[1 + k]);
+  for (int f = 0; f < kMaxBytesFields; ++f) {
+    proto.cur[f] = ptr[5 + f];
+    proto.alt[f] = ptr[13 + f];
   }
-  if (a.voxel_scratch) {
-    proto.key[0] = reinterpret_cast<uint64_t*>(take((uint64_t)a.cap_points * 8 + 16));
-    proto.key[1] = reinterpret_cast<uint64_t*>(take((uint64_t)a.cap_points * 8 + 16));
-    proto.counts = reinterpret_cast<int32_t*>(take((uint64_t)a.cap_points * 4 + 16));
-  }
-  return staging;
+  proto.key[0] = reinterpret_cast<uint64_t*>(ptr[21]);
+  proto.key[1] = reinterpret_cast<uint64_t*>(ptr[22]);
+  proto.counts = reinterpret_cast<int32_t*>(ptr[23]);
+  return ptr[0];  // TMA staging buffer (shared) or nullptr
 }
 
 // pcp_apply_map: one op over a CSR cloud set (apply_map per cloud with an
 // explicit seed, transforms.hpp:33-34).
-__global__ void __launch_bounds__(512) k_apply_set(WaveArgs a) {
+__global__ void __launch_bounds__(512, 1) k_apply_set(WaveArgs a) {
   extern __shared__ __align__(128) uint8_t dyn[];
   Smem& S = *reinterpret_cast<Smem*>(dyn);
   uint8_t* work = dyn + ((sizeof(Smem) + 127) & ~size_t(127));
@@ -1653,7 +1719,10 @@ cudaError_t launch_wave(const WaveArgs& a, int grid, int threads, size_t smem, c
                         cudaEvent_t k0, cudaEvent_t k1) {
   if (a.n_groups) k_scalar_parse<<<(a.n_groups + 127) / 128, 128, 0, st>>>(a);
   if (k0) cudaEventRecord(k0, st);
-  if (a.n_samples) k_cloud<<<grid, threads, smem, st>>>(a);
+  if (a.n_samples) {
+    if (a.min_blocks == 2) k_cloud<2><<<grid, threads, smem, st>>>(a);
+    else k_cloud<1><<<grid, threads, smem, st>>>(a);
+  }
   if (k1) cudaEventRecord(k1, st);
   if (a.n_pages) k_finalize<<<(a.n_pages + 255) / 256, 256, 0, st>>>(a);
   if (a.n_samples) k_sample_status<<<(a.n_samples + 255) / 256, 256, 0, st>>>(a);
@@ -1690,8 +1759,9 @@ cudaError_t launch_compact(const uint8_t* src, uint64_t stride, const uint64_t* 
   return cudaGetLastError();
 }
 
-cudaError_t occupancy_cloud(int* n, int threads, size_t smem) {
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(n, k_cloud, threads, smem);
+cudaError_t occupancy_cloud(int* n, int threads, size_t smem, int min_blocks) {
+  return min_blocks == 2 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(n, k_cloud<2>, threads, smem)
+                         : cudaOccupancyMaxActiveBlocksPerMultiprocessor(n, k_cloud<1>, threads, smem);
 }
 
 cudaError_t launch_apply_set(const WaveArgs& a, int grid, int threads, size_t smem,
@@ -1724,7 +1794,9 @@ cudaError_t launch_decode_pages(const uint8_t* bytes, const uint64_t* page_off, 
 }
 
 cudaError_t set_cloud_smem(size_t bytes) {
-  return cudaFuncSetAttribute(k_cloud, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  cudaError_t e = cudaFuncSetAttribute(k_cloud<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_cloud<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
 }  // namespace pcp

@@ -168,7 +168,13 @@ struct WaveArgs {
   // per-CTA placement
   uint32_t cap_points;      // max points any tracked buffer must hold
   uint32_t max_blob;        // max blob bytes (staging)
-  int32_t smem_mode;        // 1: cloud lives in shared memory
+  int32_t smem_mode;        // 1: some per-CTA buffers live in shared memory
+  // per-CTA buffer plan (host: plan_buffers): 0 staging, 1..4 index arrays,
+  // 5..12 cur per bytes field, 13..20 alt per bytes field, 21/22 voxel keys,
+  // 23 voxel counts.  Bytes (0 = absent) and shared-memory placement bits.
+  uint64_t buf_bytes[24];
+  uint32_t buf_smem_mask;
+  int32_t min_blocks;       // k_cloud instantiation: 1 (128 regs) or 2 (64 regs)
   uint8_t* gscratch;        // global scratch (smem_mode 0), per CTA
   uint64_t gscratch_per_cta;
   uint32_t force_serial_fy; // test hook: take the serial Fisher-Yates path
