@@ -955,8 +955,8 @@ struct Pipeline {
                           (uint32_t)wins.size(), d_shift.as<uint32_t>(), a.page_crc_acc, sms, w.stream));
     long long* tm = nullptr;
     if (lz4_timing) {  // PCP_LZ4_TIMING=1: per-page phase clocks (diagnostics)
-      w.lz4_timing.ensure(todo.size() * 64);
-      CK(cudaMemsetAsync(w.lz4_timing.p, 0, todo.size() * 64, w.stream));
+      w.lz4_timing.ensure(todo.size() * 128);
+      CK(cudaMemsetAsync(w.lz4_timing.p, 0, todo.size() * 128, w.stream));
       tm = w.lz4_timing.as<long long>();
     }
     CK(cudaEventRecord(w.d0, w.stream));
@@ -1026,12 +1026,12 @@ struct Pipeline {
       decode_kernel_ms += ms;
       decode_alg_bytes += wn.decode_alg_bytes;
       if (lz4_timing && wn.n_todo) {
-        std::vector<long long> tm(wn.n_todo * 8);
+        std::vector<long long> tm(wn.n_todo * 16);
         CK(cudaMemcpy(tm.data(), wn.lz4_timing.p, tm.size() * 8, cudaMemcpyDeviceToHost));
         for (uint32_t i = 0; i < wn.n_todo; ++i)
-          if (tm[i * 8 + 4])
+          if (tm[i * 16 + 4])
             for (int ph = 0; ph < 4; ++ph)
-              lz4_phase_cycles[ph] = std::max(lz4_phase_cycles[ph], (double)(tm[i * 8 + ph + 1] - tm[i * 8 + ph]));
+              lz4_phase_cycles[ph] = std::max(lz4_phase_cycles[ph], (double)(tm[i * 16 + ph + 1] - tm[i * 16 + ph]));
       }
       if (cur >= 0) slots[cur].launched = false;
       cur = nxt;

@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(256) k_page_decode(const uint8_t* bytes, uint8
       } else {
         const lz4p::Scratch sc = lz4p::carve_scratch(scratch + scratch_off[w], pg.pay_len);
         status = lz4p::decode_block(src, (uint32_t)pg.pay_len, dst, (uint32_t)pg.raw_len, sc, ctl,
-                                    ring, timing ? timing + 8 * (uint64_t)w : nullptr);
+                                    ring, timing ? timing + 16 * (uint64_t)w : nullptr);
         if (status < 0) {
           if (threadIdx.x < 32) {
             const int32_t r = warp_lz4_decode(src, pg.pay_len, dst, pg.raw_len, seqs, &sst, &scount);

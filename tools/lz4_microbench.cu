@@ -33,11 +33,11 @@ int main(int argc, char** argv) {
   cudaMalloc(&d_src, pay.size() + 64);
   cudaMalloc(&d_dst, raw + 64);
   cudaMalloc(&d_scr, lz4p::scratch_bytes(pay.size()));
-  cudaMalloc(&d_tm, 64);
+  cudaMalloc(&d_tm, 128);
   cudaMalloc(&d_st, 4);
   cudaMemcpy(d_src, pay.data(), pay.size(), cudaMemcpyHostToDevice);
   for (int it = 0; it < 3; ++it) {
-    cudaMemset(d_tm, 0, 64);
+    cudaMemset(d_tm, 0, 128);
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
@@ -47,12 +47,12 @@ int main(int argc, char** argv) {
     cudaEventSynchronize(b);
     float ms;
     cudaEventElapsedTime(&ms, a, b);
-    long long tm[8];
+    long long tm[16];
     int st;
-    cudaMemcpy(tm, d_tm, 64, cudaMemcpyDeviceToHost);
+    cudaMemcpy(tm, d_tm, 128, cudaMemcpyDeviceToHost);
     cudaMemcpy(&st, d_st, 4, cudaMemcpyDeviceToHost);
-    printf("status %d  %.3f ms  skim %lld  phase3 %lld  matches %lld cycles  fast %lld slow %lld\n", st, ms,
-           tm[2] - tm[0], tm[3] - tm[2], tm[4] - tm[3], tm[5], tm[6]);
+    printf("status %d  %.3f ms  skim %lld (walk %lld fill %lld)  phase3 %lld  matches %lld (ring %lld dep %lld waves %lld n_waves %lld) fast %lld slow %lld\n",
+           st, ms, tm[2] - tm[0], tm[8], tm[9], tm[3] - tm[2], tm[4] - tm[3], tm[13], tm[11], tm[12], tm[14], tm[5], tm[6]);
   }
   std::vector<uint8_t> out(raw);
   cudaMemcpy(out.data(), d_dst, raw, cudaMemcpyDeviceToHost);
