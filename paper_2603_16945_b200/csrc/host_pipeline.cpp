@@ -531,6 +531,7 @@ struct Pipeline {
   void plan_schema() {
     WaveArgs& a = proto;
     std::memset(&a, 0, sizeof(a));
+    a.neg_zero = -0.0f;
     if (h.schema.size() > (size_t)kMaxFields) fail(kOutOfBounds, "too many schema fields");
     a.n_fields = (int32_t)h.schema.size();
     for (size_t f = 0; f < h.schema.size(); ++f) {
@@ -693,8 +694,11 @@ struct Pipeline {
     smem = fixed + used;
     CK(set_cloud_smem(smem));
     // two CTAs per SM when the shared footprint allows it (the 64-register
-    // build), otherwise one CTA with the 128-register build (FPS fast path)
-    a.min_blocks = (2 * smem <= prop.sharedMemPerMultiprocessor) ? 2 : 1;
+    // build), otherwise (or with FPS: register-resident points) one CTA with
+    // the 128-register build
+    bool any_fps = false;
+    for (int k = 0; k < a.n_ops; ++k) any_fps |= a.ops[k].kind == kFps;
+    a.min_blocks = (2 * smem <= prop.sharedMemPerMultiprocessor && !any_fps) ? 2 : 1;
     int per_sm = 0;
     CK(occupancy_cloud(&per_sm, threads, smem, a.min_blocks));
     grid = std::max(1, per_sm) * sms;
@@ -1239,6 +1243,7 @@ int pcp_apply_map(int kind, const char* params_json, const pcp_cloud_set* in,
     for (uint32_t i = 0; i < n; ++i) max_n = std::max<uint64_t>(max_n, off[i + 1] - off[i]);
     WaveArgs a;
     std::memset(&a, 0, sizeof(a));
+    a.neg_zero = -0.0f;
     a.set_mode = 1;
     a.n_bytes_fields = kMaxBytesFields;
     a.role_data = 0;

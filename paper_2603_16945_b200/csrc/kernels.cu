@@ -849,60 +849,99 @@ __device__ int32_t op_downsample(const WaveArgs& a, Cloud& c, Smem& S, const OpD
 
 // FPS (App. C): start at 0, d2 = (dx*dx + dy*dy) + dz*dz without FMA,
 // mind = min(mind, d2), next = argmax mind (lowest index on ties).
-// FPS fast path (cloud in shared memory, N <= kFpsRegPts * blockDim): each
-// thread keeps the min-distances of points i = t + k*nt in registers, reads
-// coordinates with LDS through the dynamic-smem base, reduces (value, index)
-// with warp shuffles and publishes one candidate per warp into a parity
-// double-buffered slot, so each iteration needs ONE block barrier.
-constexpr uint32_t kFpsRegPts = 24;
+// Paired FP32 (sm_100 FADD2/FFMA2): two independent IEEE round-to-nearest
+// operations per instruction, so the no-FMA distance below is bit-identical
+// to the scalar form at half the FMA-pipe issue cost.
+__device__ __forceinline__ uint64_t f2_pack(float lo, float hi) {
+  return (uint64_t)__float_as_uint(lo) | ((uint64_t)__float_as_uint(hi) << 32);
+}
+__device__ __forceinline__ uint64_t f2_sub(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+// x*x as fma(x, x, nz) with nz = -0.0f known only at run time: ptxas 12.9
+// contracts mul.rn.f32x2 + add.rn.f32x2 into FFMA2 despite the explicit
+// rounding modifiers; an FFMA2 result cannot be fused again, and
+// fma(x, x, -0) == mul(x, x) for every x (including +-0, inf, NaN).
+__device__ __forceinline__ uint64_t f2_sq(uint64_t a, uint64_t nz2) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(d) : "l"(a), "l"(nz2));
+  return d;
+}
+__device__ __forceinline__ uint64_t f2_add(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
 
-__device__ __forceinline__ uint64_t umax64(uint64_t a, uint64_t b) { return a > b ? a : b; }
+// Register-resident FPS: thread t owns points i = t + k*nt (k < P), packed
+// in pairs (k = 2j, 2j+1) with their min-distances in registers.  Per
+// iteration the argmax (largest min-distance, lowest index on ties) is two
+// warp redux.sync ops — max of the distance bits (distances are >= +0, so
+// the unsigned order of their bits is the float order; padding carries -inf
+// and contributes key 0 with index ~0u), then min of the tied indices — plus
+// one block barrier through a parity double-buffered per-warp slot.
+constexpr uint32_t kFpsRegPts = 20;
 
-__device__ void fps_fast(const float* dg, uint32_t N, uint32_t M, int32_t* idx, Smem& S) {
-  extern __shared__ __align__(128) uint8_t dyn[];
-  const float* d = reinterpret_cast<const float*>(dyn + (reinterpret_cast<const uint8_t*>(dg) - dyn));
-  // (value, index) packed as value_bits << 32 | ~index: min-distances are
-  // >= +0 or +inf (a NaN distance never replaces mind), so unsigned order of
-  // the key = larger value first, then lower index — the App. C argmax.
+template <int P>
+__device__ void fps_reg(const float* d, uint32_t N, uint32_t M, int32_t* idx, Smem& S, float nz) {
+  static_assert(P % 2 == 0, "points are processed in pairs");
   uint64_t* slot = reinterpret_cast<uint64_t*>(S.rs_wcnt);  // [2][16]
   const uint32_t t = threadIdx.x, nt = blockDim.x, lane = t & 31, w = t >> 5, nw = nt >> 5;
-  float mind[kFpsRegPts];
+  uint64_t X[P / 2], Y[P / 2], Z[P / 2];
+  float mind[P];
 #pragma unroll
-  for (int k = 0; k < (int)kFpsRegPts; ++k) mind[k] = INFINITY;
+  for (int j = 0; j < P / 2; ++j) {
+    float v[2][3];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t i = t + (uint32_t)(2 * j + h) * nt;
+      const bool ok = i < N;
+      v[h][0] = ok ? d[3 * i] : 0.f;
+      v[h][1] = ok ? d[3 * i + 1] : 0.f;
+      v[h][2] = ok ? d[3 * i + 2] : 0.f;
+      mind[2 * j + h] = ok ? INFINITY : -INFINITY;
+    }
+    X[j] = f2_pack(v[0][0], v[1][0]);
+    Y[j] = f2_pack(v[0][1], v[1][1]);
+    Z[j] = f2_pack(v[0][2], v[1][2]);
+  }
+  const uint64_t NZ = f2_pack(nz, nz);
   uint32_t sel = 0;
   for (uint32_t it = 0; it < M; ++it) {
     if (t == 0) idx[it] = (int32_t)sel;
     const float sx = d[3 * sel], sy = d[3 * sel + 1], sz = d[3 * sel + 2];
-    uint64_t b0 = 0, b1 = 0;  // two independent chains (even / odd k)
+    const uint64_t SX = f2_pack(sx, sx), SY = f2_pack(sy, sy), SZ = f2_pack(sz, sz);
+    float bv = -INFINITY;
 #pragma unroll
-    for (int k = 0; k < (int)kFpsRegPts; ++k) {
-      const uint32_t i = t + (uint32_t)k * nt;
-      if (i < N) {
-        const float dx = __fsub_rn(d[3 * i], sx), dy = __fsub_rn(d[3 * i + 1], sy),
-                    dz = __fsub_rn(d[3 * i + 2], sz);
-        const float dd =
-            __fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz));
-        const float m = dd < mind[k] ? dd : mind[k];
-        mind[k] = m;
-        const uint64_t key = ((uint64_t)__float_as_uint(m) << 32) | (0xFFFFFFFFu - i);
-        if (k & 1) b1 = umax64(b1, key);
-        else b0 = umax64(b0, key);
-      }
+    for (int j = 0; j < P / 2; ++j) {
+      const uint64_t dx = f2_sub(X[j], SX), dy = f2_sub(Y[j], SY), dz = f2_sub(Z[j], SZ);
+      const uint64_t dd = f2_add(f2_add(f2_sq(dx, NZ), f2_sq(dy, NZ)), f2_sq(dz, NZ));
+      // fminf == (dd < mind ? dd : mind) here: dd is >= +0 or NaN (-> mind)
+      mind[2 * j] = fminf(__uint_as_float((uint32_t)dd), mind[2 * j]);
+      mind[2 * j + 1] = fminf(__uint_as_float((uint32_t)(dd >> 32)), mind[2 * j + 1]);
+      bv = fmaxf(bv, fmaxf(mind[2 * j], mind[2 * j + 1]));
     }
-    uint64_t best = umax64(b0, b1);
+    uint32_t bk = P;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) best = umax64(best, __shfl_xor_sync(0xffffffffu, best, o));
+    for (int k = P - 1; k >= 0; --k) bk = mind[k] == bv ? (uint32_t)k : bk;
+    const uint32_t vb = bv >= 0.f ? __float_as_uint(bv) : 0u;
+    const uint32_t bi = bv >= 0.f ? t + bk * nt : 0xFFFFFFFFu;
+    const uint32_t wmax = __reduce_max_sync(0xffffffffu, vb);
+    const uint32_t wi = __reduce_min_sync(0xffffffffu, vb == wmax ? bi : 0xFFFFFFFFu);
     const uint32_t par = it & 1u;
-    if (lane == 0) slot[par * 16 + w] = best;
+    if (lane == 0) slot[par * 16 + w] = ((uint64_t)wmax << 32) | wi;
     __syncthreads();
-    uint64_t g = lane < nw ? slot[par * 16 + lane] : 0ull;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) g = umax64(g, __shfl_xor_sync(0xffffffffu, g, o));
-    // g == 0 only if no candidate (N == 0): select index 0 like the oracle
-    sel = g ? 0xFFFFFFFFu - (uint32_t)(g & 0xFFFFFFFFu) : 0u;
+    const uint64_t g = lane < nw ? slot[par * 16 + lane] : 0ull;
+    const uint32_t gv = (uint32_t)(g >> 32);
+    const uint32_t gmax = __reduce_max_sync(0xffffffffu, gv);
+    sel = __reduce_min_sync(0xffffffffu, (lane < nw && gv == gmax) ? (uint32_t)g : 0xFFFFFFFFu);
+    if (sel == 0xFFFFFFFFu) sel = 0;  // no candidate at all (N == 0): index 0 like the oracle
   }
 }
 
+template <int MinBlocks>
 __device__ int32_t op_fps(const WaveArgs& a, Cloud& c, Smem& S, const OpDesc& op) {
   if (op.num_points <= 0) return kOutOfBounds;
   const uint32_t M = (uint32_t)op.num_points;
@@ -913,8 +952,19 @@ __device__ int32_t op_fps(const WaveArgs& a, Cloud& c, Smem& S, const OpDesc& op
   if (st) return st;
   const float* d = F(c, a.role_data);
   int32_t* idx = c.ix[0];
-  if (N <= kFpsRegPts * blockDim.x && __isShared(d)) {
-    fps_fast(d, N, M, idx, S);
+  // register-resident paths (MinBlocks = 1 builds have 128 registers)
+  bool done = false;
+  if (N <= 8 * blockDim.x) {
+    fps_reg<8>(d, N, M, idx, S, a.neg_zero);
+    done = true;
+  } else if (MinBlocks == 1 && N <= 16 * blockDim.x) {
+    fps_reg<16>(d, N, M, idx, S, a.neg_zero);
+    done = true;
+  } else if (MinBlocks == 1 && N <= kFpsRegPts * blockDim.x) {
+    fps_reg<kFpsRegPts>(d, N, M, idx, S, a.neg_zero);
+    done = true;
+  }
+  if (done) {
     __syncthreads();
     gather_mask_fields(a, c, mm, idx, M);
     return kOk;
@@ -1198,6 +1248,7 @@ __device__ int32_t op_voxel(const WaveArgs& a, Cloud& c, Smem& S, const OpDesc& 
 // Applies the op chain (Pipeline map worker, pipeline.cpp:474-480): seed per
 // op = mix_seed(base, epoch, index, op id), or `fixed_seed` for the
 // single-op cloud-set API.  fail_op = 1-based failing transform.
+template <int MinBlocks>
 __device__ int32_t run_chain(const WaveArgs& a, Cloud& c, Smem& S, uint64_t epoch, uint64_t index,
                              const uint64_t* fixed_seed, int32_t& fail_op) {
   int32_t status = kOk;
@@ -1219,7 +1270,7 @@ __device__ int32_t run_chain(const WaveArgs& a, Cloud& c, Smem& S, uint64_t epoc
         case kColorAugment: status = op_color(a, c, S, seed); break;
         case kRandomCrop: status = op_random_crop(a, c, S, seed); break;
         case kDownsample: status = op_downsample(a, c, S, op, seed); break;
-        case kFps: status = op_fps(a, c, S, op); break;
+        case kFps: status = op_fps<MinBlocks>(a, c, S, op); break;
         case kRangeCrop: status = op_range_crop(a, c, S, op); break;
         case kVoxel: status = op_voxel(a, c, S, op); break;
         default: status = kUnknownOp; break;
@@ -1369,7 +1420,7 @@ __global__ void __launch_bounds__(512, MinBlocks) k_cloud(WaveArgs a) {
       if (status == kOk && a.role_normal >= 0 && flen[a.role_normal] % 12) status = kMissingField;
       if (status == kOk && a.role_color >= 0 && flen[a.role_color] % 12) status = kMissingField;
       if (status != kOk) fail_op = 1;
-      if (status == kOk) status = run_chain(a, c, S, sw.epoch, sw.index, nullptr, fail_op);
+      if (status == kOk) status = run_chain<MinBlocks>(a, c, S, sw.epoch, sw.index, nullptr, fail_op);
     }
 
     // ---- write tracked fields + scalar values into the batch slot --------
@@ -1502,7 +1553,7 @@ __global__ void __launch_bounds__(512, 1) k_apply_set(WaveArgs a) {
     }
     __syncthreads();
     if (status == kOk && n == 0) status = kEmptyCloud;
-    if (status == kOk) status = run_chain(a, c, S, 0, 0, a.set_seeds + s, fail_op);
+    if (status == kOk) status = run_chain<1>(a, c, S, 0, 0, a.set_seeds + s, fail_op);
     if (status == kOk) {
       for (int f = 0; f < a.n_bytes_fields && status == kOk; ++f) {
         if (!((a.tracked_mask >> f) & 1u) || !a.set_out[f]) continue;

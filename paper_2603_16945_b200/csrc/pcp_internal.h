@@ -178,6 +178,7 @@ struct WaveArgs {
   uint8_t* gscratch;        // global scratch (smem_mode 0), per CTA
   uint64_t gscratch_per_cta;
   uint32_t force_serial_fy; // test hook: take the serial Fisher-Yates path
+  float neg_zero;           // -0.0f, opaque to ptxas (FPS paired squares, kernels.cu)
   // cloud-set mode (pcp_apply_map): clouds come from CSR arrays instead of
   // pages; bytes-field slots 0..7 = data, normal, color, intensity, extra0..3
   int32_t set_mode;

@@ -212,3 +212,93 @@ def test_apply_map_cloud_set(pcp, ref, orc, rng, kind, params):
                 np.testing.assert_allclose(g, want, rtol=1e-5, atol=1e-6 * max(1, np.abs(want).max()))
             else:
                 assert np.array_equal(g.view(np.uint32), want.view(np.uint32)), (kind, i, name)
+
+
+def _adversarial_fps_pairs(n_pairs, seed=7):
+    """Point pairs (P1, P2) whose squared distances to the origin order one way
+    with the App. C rounding ((dx*dx + dy*dy) + dz*dz, every op rounded) and
+    the other way if the squares were fused into the adds (FMA contraction)."""
+    r = np.random.default_rng(seed)
+    p = r.uniform(0.5, 1.0, (400000, 3)).astype(np.float32)
+    p /= np.linalg.norm(p.astype(np.float64), axis=1, keepdims=True).astype(np.float32)
+    sq = p * p  # float32, rounded
+    unf = (sq[:, 0] + sq[:, 1]) + sq[:, 2]
+    p64 = p.astype(np.float64)
+    fus = (p64[:, 2] ** 2 + (p64[:, 1] ** 2 + sq[:, 0].astype(np.float64)).astype(np.float32)).astype(np.float32)
+    # on the unit sphere the rounded distances take a few ulp-spaced levels;
+    # pair a point of a lower level with a point of a higher one whose fused
+    # value is not larger
+    out = []
+    levels = np.unique(unf)
+    for lo_v, hi_v in zip(levels[:-1], levels[1:]):
+        A = np.flatnonzero(unf == lo_v)
+        B = np.flatnonzero(unf == hi_v)
+        A = A[np.argsort(-fus[A], kind="stable")]
+        B = B[np.argsort(fus[B], kind="stable")]
+        for a, b in zip(A, B):
+            if fus[a] < fus[b]:
+                break
+            out.append((p[a], p[b]))
+            if len(out) == n_pairs:
+                return out
+    return out
+
+
+def _apply_set(pcp, kind, params, clouds, seeds=None):
+    import torch
+    sizes = [len(c) for c in clouds]
+    off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    cap = max(max(sizes), params.get("num_points", 0))
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    d_data, d_off = t(np.concatenate(clouds)), t(off)
+    seeds = seeds or [0] * len(clouds)
+    d_seed = t(np.array(seeds, dtype=np.uint64).view(np.int64))
+    o_data = torch.zeros(len(sizes) * cap * 3, dtype=torch.float32, device="cuda")
+    o_cnt = torch.zeros(len(sizes), dtype=torch.int32, device="cuda")
+    d_st = torch.zeros(len(sizes), dtype=torch.int32, device="cuda")
+    s = _Set(len(sizes), d_off.data_ptr(), d_data.data_ptr(), None, None, None)
+    o = _Out(cap, o_data.data_ptr(), None, None, None)
+    o.d_count = o_cnt.data_ptr()
+    L = pcp.lib()
+    L.pcp_apply_map.argtypes = [C.c_int, C.c_char_p, C.POINTER(_Set), C.POINTER(_Out), C.c_void_p,
+                                C.c_void_p, C.c_void_p]
+    rc = L.pcp_apply_map(pcp.map_kind_from_name(kind), json.dumps(params).encode(), C.byref(s),
+                         C.byref(o), d_seed.data_ptr(), d_st.data_ptr(), None)
+    assert rc == 0, L.pcp_last_error()
+    torch.cuda.synchronize()
+    od = o_data.cpu().numpy().reshape(len(sizes), cap, 3)
+    return d_st.cpu().numpy(), o_cnt.cpu().numpy(), od
+
+
+def test_fps_no_fma_contraction(pcp, orc):
+    """FPS distances must be computed without FMA (App. C): on these clouds a
+    contracted distance picks the other point."""
+    from oracle.ffi import cloud
+    pairs = _adversarial_fps_pairs(48)
+    assert len(pairs) >= 16
+    clouds = [np.stack([np.zeros(3, np.float32), a, b]) for a, b in pairs]
+    st, cnt, od = _apply_set(pcp, "fps", {"num_points": 2}, clouds)
+    for i, c in enumerate(clouds):
+        want = orc.apply_map("fps", {"num_points": 2}, {"data": cloud(c)}, 0)["data"]
+        want = want.view(np.float32).reshape(-1, 3)
+        assert st[i] == 0 and cnt[i] == 2
+        assert np.array_equal(want[1], c[2])  # the restatement picks P2 ...
+        assert np.array_equal(od[i, :2].view(np.uint32), want.view(np.uint32)), i  # ... and so must we
+
+
+@pytest.mark.parametrize("n,m", [(3000, 700), (7000, 512), (10000, 1024), (12000, 300), (40000, 256)])
+def test_fps_sizes_bit_exact(pcp, orc, rng, n, m):
+    """Every FPS path (register P = 8 / 16 / 20, and the large-cloud path)
+    against the restatement, including duplicated points (exact ties)."""
+    from oracle.ffi import cloud
+    clouds = []
+    for k in range(3):
+        c = rng.uniform(-1, 1, (n, 3)).astype(np.float32)
+        c[n // 2:n // 2 + 50] = c[:50]  # exact duplicates -> tied distances
+        clouds.append(c)
+    st, cnt, od = _apply_set(pcp, "fps", {"num_points": m}, clouds)
+    for i, c in enumerate(clouds):
+        want = orc.apply_map("fps", {"num_points": m}, {"data": cloud(c)}, 0)["data"]
+        want = want.view(np.float32).reshape(-1, 3)
+        assert st[i] == 0 and cnt[i] == m
+        assert np.array_equal(od[i, :m].view(np.uint32), want.view(np.uint32)), i
