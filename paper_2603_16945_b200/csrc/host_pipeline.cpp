@@ -260,6 +260,35 @@ void parse_op_params(OpDesc& op, const json& p, IndexOf bytes_index_of) {
 // sizes follow what the op chain can need; shared memory is filled greedily
 // in priority order (coordinates first), everything else goes to the per-CTA
 // global slab (a.gscratch_per_cta).  Returns the shared bytes used.
+// Cluster FPS plan: a static bound on the points any FPS op
+// sees — the cloud capacity, or T after a downsample / M after an FPS (both
+// leave exactly that many points; crops and voxel never grow a cloud).  A
+// bound above one CTA's register capacity (kFpsRegPts x threads) splits the
+// cloud over a thread-block cluster of up to 8 CTAs; beyond that the
+// global-memory FPS path runs in one CTA.
+void plan_fps_cluster(WaveArgs& a, uint32_t threads) {
+  uint64_t bound = a.cap_points, need = 0;
+  for (int k = 0; k < a.n_ops; ++k) {
+    const OpDesc& op = a.ops[k];
+    if (op.kind == kFps) {
+      need = std::max(need, bound);
+      bound = (uint64_t)std::max<int64_t>(op.num_points, 0);
+    } else if (op.kind == kDownsample) {
+      bound = (uint64_t)std::max<int64_t>(op.num_points, 0);
+    }
+  }
+  const uint64_t per_cta = (uint64_t)kFpsRegPts * threads;
+  a.fps_cluster = 1;
+  a.fps_slice_pts = 0;
+  if (need > per_cta) {
+    const uint64_t C = (need + per_cta - 1) / per_cta;
+    if (C <= 8) {
+      a.fps_cluster = (uint32_t)C;
+      a.fps_slice_pts = (uint32_t)((need + C - 1) / C);
+    }
+  }
+}
+
 size_t plan_buffers(WaveArgs& a, bool want_staging, size_t smem_budget) {
   uint64_t T = 0, M = 0;
   bool ds = false, fps = false, crop = false, vox = false;
@@ -275,7 +304,8 @@ size_t plan_buffers(WaveArgs& a, bool want_staging, size_t smem_budget) {
   const uint64_t alt_pts = std::max({T, M, big});
   auto with = [](uint64_t b) { return b ? b + 16 : 0; };
   uint64_t* sz = a.buf_bytes;
-  for (int b = 0; b < 24; ++b) sz[b] = 0;
+  for (int b = 0; b < 25; ++b) sz[b] = 0;
+  if (a.fps_cluster > 1) sz[24] = kFpsMailBytes + 12ull * a.fps_slice_pts + 16;
   sz[0] = want_staging ? (uint64_t)a.max_blob + 64 : 0;
   sz[1] = 4 * std::max<uint64_t>({T, M, big, 1}) + 16;
   sz[2] = with(4 * ((ds || fps || vox) ? cap : 0));
@@ -291,6 +321,7 @@ size_t plan_buffers(WaveArgs& a, bool want_staging, size_t smem_budget) {
     sz[23] = 4 * cap + 16;
   }
   std::vector<int> order;
+  if (sz[24]) order.push_back(24);  // cluster-FPS slice + mailbox first (latency-critical)
   const int rd = a.role_data;
   if (rd >= 0) order.push_back(5 + rd);
   for (int b : {1, 3, 4}) order.push_back(b);
@@ -690,6 +721,7 @@ struct Pipeline {
     cudaDeviceProp prop;
     CK(cudaGetDeviceProperties(&prop, device));
     const size_t fixed = cloud_smem_fixed();
+    plan_fps_cluster(a, (uint32_t)threads);
     const size_t used = plan_buffers(a, any_stored_raw, prop.sharedMemPerBlockOptin - fixed);
     smem = fixed + used;
     CK(set_cloud_smem(smem));
@@ -699,9 +731,16 @@ struct Pipeline {
     bool any_fps = false;
     for (int k = 0; k < a.n_ops; ++k) any_fps |= a.ops[k].kind == kFps;
     a.min_blocks = (2 * smem <= prop.sharedMemPerMultiprocessor && !any_fps) ? 2 : 1;
-    int per_sm = 0;
-    CK(occupancy_cloud(&per_sm, threads, smem, a.min_blocks));
-    grid = std::max(1, per_sm) * sms;
+    if (a.fps_cluster > 1) {  // one cloud per cluster of fps_cluster CTAs
+      int clusters = 0;
+      CK(occupancy_cloud_clusters(&clusters, threads, smem, a.fps_cluster, false));
+      if (clusters < 1) fail(kOutOfBounds, "no room for a cluster of " + std::to_string(a.fps_cluster) + " CTAs");
+      grid = clusters * (int)a.fps_cluster;
+    } else {
+      int per_sm = 0;
+      CK(occupancy_cloud(&per_sm, threads, smem, a.min_blocks));
+      grid = std::max(1, per_sm) * sms;
+    }
     a.force_serial_fy = force_serial_fy ? 1 : 0;
   }
 
@@ -1298,10 +1337,18 @@ int pcp_apply_map(int kind, const char* params_json, const pcp_cloud_set* in,
     CK(cudaGetDevice(&dev));
     CK(cudaGetDeviceProperties(&prop, dev));
     const size_t fixed = cloud_smem_fixed();
+    plan_fps_cluster(a, 512);
     const size_t smem = fixed + plan_buffers(a, false, prop.sharedMemPerBlockOptin - fixed);
+    CK(set_apply_smem(smem));
     int grid = ctx.sms * 2;
+    if (a.fps_cluster > 1) {
+      int clusters = 0;
+      CK(occupancy_cloud_clusters(&clusters, 512, smem, a.fps_cluster, true));
+      if (clusters < 1) fail(kOutOfBounds, "no room for a cluster of " + std::to_string(a.fps_cluster) + " CTAs");
+      grid = std::min<int>(clusters, (int)n) * (int)a.fps_cluster;
+    }
     if (a.gscratch_per_cta) {
-      grid = std::min<int>(grid, (int)n);
+      if (a.fps_cluster <= 1) grid = std::min<int>(grid, (int)n);
       ctx.scratch.ensure(a.gscratch_per_cta * grid);
       a.gscratch = ctx.scratch.as<uint8_t>();
     }

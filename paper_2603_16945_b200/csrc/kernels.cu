@@ -305,6 +305,7 @@ struct Cloud {
   int32_t* counts;                 // voxel counts (cap)
   uint32_t n_counts;
   int32_t has_counts;
+  uint8_t* fps_buf;                // cluster FPS: mailbox + this CTA's slice (buffer 24)
 };
 
 struct Smem {
@@ -314,6 +315,7 @@ struct Smem {
   unsigned long long red[kRed];
   uint64_t mt[rng::kN];
   uint64_t bar;
+  uint64_t fbar[2];           // cluster-FPS mailbox barriers (per parity)
   int32_t status;
   int32_t flag;
   uint32_t u32s[8];
@@ -882,8 +884,6 @@ __device__ __forceinline__ uint64_t f2_add(uint64_t a, uint64_t b) {
 // the unsigned order of their bits is the float order; padding carries -inf
 // and contributes key 0 with index ~0u), then min of the tied indices — plus
 // one block barrier through a parity double-buffered per-warp slot.
-constexpr uint32_t kFpsRegPts = 20;
-
 template <int P>
 __device__ void fps_reg(const float* d, uint32_t N, uint32_t M, int32_t* idx, Smem& S, float nz) {
   static_assert(P % 2 == 0, "points are processed in pairs");
@@ -941,6 +941,123 @@ __device__ void fps_reg(const float* d, uint32_t N, uint32_t M, int32_t* idx, Sm
   }
 }
 
+// Cluster FPS for clouds above one CTA's register capacity:
+// the points are split over the C CTAs of a thread-block cluster (CTA r owns
+// [r*per, r*per + per)), each holding its slice in registers as in fps_reg
+// plus an AoS copy in shared memory for its candidates' coordinates.  Per
+// iteration every warp sends its candidate (distance bits, index, x, y, z)
+// to every CTA of the cluster with st.async into a parity double-buffered
+// mailbox whose mbarrier counts the bytes — one DSMEM hop and an mbarrier
+// wait instead of a cluster barrier (which would also flush L1) — then every
+// CTA reduces the same 16*C records to the same `sel`.  Reuse is safe: a CTA
+// can send iteration it+2's records only after completing it+1, which needs
+// it+1 records from every warp of every CTA, each sent after that warp read
+// iteration it's mailbox.
+template <int P>
+__device__ void fps_cluster(const float* d, uint32_t N, uint32_t M, int32_t* idx, Smem& S,
+                            float nz, uint8_t* buf, uint32_t C) {
+  static_assert(P % 2 == 0, "points are processed in pairs");
+  const uint32_t t = threadIdx.x, nt = blockDim.x, lane = t & 31, w = t >> 5, nw = nt >> 5;
+  const uint32_t r = dev::cluster_rank();
+  const uint32_t per = (N + C - 1) / C;
+  const uint32_t base = min(r * per, N), nloc = min(per, N - base);
+  uint32_t* mail = reinterpret_cast<uint32_t*>(buf);         // [2][128][8] words
+  float* sp = reinterpret_cast<float*>(buf + kFpsMailBytes);  // [nloc][3]
+  for (uint32_t k = t; k < 3 * nloc; k += nt) sp[k] = d[3 * (uint64_t)base + k];
+  if (t == 0) {
+    dev::mbar_init(&S.fbar[0], 1);
+    dev::mbar_init(&S.fbar[1], 1);
+    dev::fence_mbar_init();
+  }
+  __syncthreads();
+  uint64_t X[P / 2], Y[P / 2], Z[P / 2];
+  float mind[P];
+#pragma unroll
+  for (int j = 0; j < P / 2; ++j) {
+    float v[2][3];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t i = t + (uint32_t)(2 * j + h) * nt;
+      const bool ok = i < nloc;
+      v[h][0] = ok ? sp[3 * i] : 0.f;
+      v[h][1] = ok ? sp[3 * i + 1] : 0.f;
+      v[h][2] = ok ? sp[3 * i + 2] : 0.f;
+      mind[2 * j + h] = ok ? INFINITY : -INFINITY;
+    }
+    X[j] = f2_pack(v[0][0], v[1][0]);
+    Y[j] = f2_pack(v[0][1], v[1][1]);
+    Z[j] = f2_pack(v[0][2], v[1][2]);
+  }
+  dev::cluster_sync_all();  // every CTA's mailbox barriers are initialised
+  const uint32_t nrec = C * nw;
+  const uint32_t tx = nrec * 20;  // bytes per phase (16 + 4 per record)
+  if (t == 0) {
+    dev::mbar_expect_tx(&S.fbar[0], tx);
+    dev::mbar_expect_tx(&S.fbar[1], tx);
+  }
+  const uint64_t NZ = f2_pack(nz, nz);
+  uint32_t sel = 0;
+  float sx = d[0], sy = d[1], sz = d[2];
+  for (uint32_t it = 0; it < M; ++it) {
+    if (t == 0) idx[it] = (int32_t)sel;
+    const uint64_t SX = f2_pack(sx, sx), SY = f2_pack(sy, sy), SZ = f2_pack(sz, sz);
+    float bv = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < P / 2; ++j) {
+      const uint64_t dx = f2_sub(X[j], SX), dy = f2_sub(Y[j], SY), dz = f2_sub(Z[j], SZ);
+      const uint64_t dd = f2_add(f2_add(f2_sq(dx, NZ), f2_sq(dy, NZ)), f2_sq(dz, NZ));
+      mind[2 * j] = fminf(__uint_as_float((uint32_t)dd), mind[2 * j]);
+      mind[2 * j + 1] = fminf(__uint_as_float((uint32_t)(dd >> 32)), mind[2 * j + 1]);
+      bv = fmaxf(bv, fmaxf(mind[2 * j], mind[2 * j + 1]));
+    }
+    uint32_t bk = P;
+#pragma unroll
+    for (int k = P - 1; k >= 0; --k) bk = mind[k] == bv ? (uint32_t)k : bk;
+    const uint32_t vb = bv >= 0.f ? __float_as_uint(bv) : 0u;
+    const uint32_t bi = bv >= 0.f ? base + t + bk * nt : 0xFFFFFFFFu;
+    const uint32_t wmax = __reduce_max_sync(0xffffffffu, vb);
+    const uint32_t wi = __reduce_min_sync(0xffffffffu, vb == wmax ? bi : 0xFFFFFFFFu);
+    const uint32_t par = it & 1u;
+    if (lane < C) {  // lane q sends this warp's candidate to CTA q
+      float x = 0.f, y = 0.f, z = 0.f;
+      if (wi != 0xFFFFFFFFu) {
+        const uint32_t j = wi - base;
+        x = sp[3 * j];
+        y = sp[3 * j + 1];
+        z = sp[3 * j + 2];
+      }
+      const uint32_t* rec = mail + (par * 128 + r * nw + w) * 8;
+      const uint32_t ra = dev::mapa(rec, lane), rb = dev::mapa(&S.fbar[par], lane);
+      dev::st_async_v4(ra, wmax, wi, __float_as_uint(x), __float_as_uint(y), rb);
+      dev::st_async_b32(ra + 16, __float_as_uint(z), rb);
+    }
+    dev::mbar_wait_cluster(&S.fbar[par], (it >> 1) & 1u);
+    if (t == 0 && it + 2 < M) dev::mbar_expect_tx(&S.fbar[par], tx);
+    const uint32_t* mb = mail + par * 128 * 8;
+    uint32_t lv = 0, li = 0xFFFFFFFFu, lq = 0;
+    for (uint32_t q = lane; q < nrec; q += 32) {
+      const uint32_t v = mb[q * 8], i = mb[q * 8 + 1];
+      if (v > lv || (v == lv && i < li)) {
+        lv = v;
+        li = i;
+        lq = q;
+      }
+    }
+    const uint32_t gmax = __reduce_max_sync(0xffffffffu, lv);
+    sel = __reduce_min_sync(0xffffffffu, lv == gmax ? li : 0xFFFFFFFFu);
+    if (sel == 0xFFFFFFFFu) {  // no candidate at all: index 0 like the oracle
+      sel = 0;
+      sx = d[0], sy = d[1], sz = d[2];
+    } else {
+      const uint32_t bal = __ballot_sync(0xffffffffu, lv == gmax && li == sel);
+      const uint32_t q = __shfl_sync(0xffffffffu, lq, __ffs(bal) - 1);
+      sx = __uint_as_float(mb[q * 8 + 2]);
+      sy = __uint_as_float(mb[q * 8 + 3]);
+      sz = __uint_as_float(mb[q * 8 + 4]);
+    }
+  }
+}
+
 template <int MinBlocks>
 __device__ int32_t op_fps(const WaveArgs& a, Cloud& c, Smem& S, const OpDesc& op) {
   if (op.num_points <= 0) return kOutOfBounds;
@@ -962,6 +1079,11 @@ __device__ int32_t op_fps(const WaveArgs& a, Cloud& c, Smem& S, const OpDesc& op
     done = true;
   } else if (MinBlocks == 1 && N <= kFpsRegPts * blockDim.x) {
     fps_reg<kFpsRegPts>(d, N, M, idx, S, a.neg_zero);
+    done = true;
+  } else if (MinBlocks == 1 && a.fps_cluster > 1 && c.fps_buf &&
+             N <= a.fps_cluster * a.fps_slice_pts && N <= a.fps_cluster * kFpsRegPts * blockDim.x) {
+    // every CTA of the cluster takes this branch for the same sample
+    fps_cluster<kFpsRegPts>(d, N, M, idx, S, a.neg_zero, c.fps_buf, a.fps_cluster);
     done = true;
   }
   if (done) {
@@ -1310,8 +1432,12 @@ __global__ void __launch_bounds__(512, MinBlocks) k_cloud(WaveArgs a) {
   __syncthreads();
   Cloud& c = S.cl;
 
+  // cluster FPS: the fps_cluster CTAs of a cluster run the same sample (the
+  // chain redundantly, FPS split over them); only rank 0 writes results
+  const uint32_t CL = a.fps_cluster > 1 ? a.fps_cluster : 1;
+  const bool leader = (blockIdx.x % CL) == 0;
   uint32_t phase = 0;
-  for (uint32_t s = blockIdx.x; s < a.n_samples; s += gridDim.x) {
+  for (uint32_t s = blockIdx.x / CL; s < a.n_samples; s += gridDim.x / CL) {
     const SampleWork sw = a.samples[s];
     const PageRef pg = a.pages[sw.block_page];
     const ScalarRec rec = a.recs[(uint64_t)a.groups[sw.group].first_rec + sw.row];
@@ -1369,7 +1495,7 @@ __global__ void __launch_bounds__(512, MinBlocks) k_cloud(WaveArgs a) {
       const uint32_t cc = crc::cta_range(S.crc_tab, c_x2n.v, a.shift_tab, blob, blen,
                                          pg.raw_len - sw.blob_end,
                                          reinterpret_cast<uint32_t*>(S.red));
-      if (threadIdx.x == 0) atomicXor(a.page_crc_acc + sw.block_page, cc);
+      if (threadIdx.x == 0 && leader) atomicXor(a.page_crc_acc + sw.block_page, cc);
     }
 
     // ---- decode fields: XOR-delta per blob field (format.cpp:483-493) -----
@@ -1403,8 +1529,10 @@ __global__ void __launch_bounds__(512, MinBlocks) k_cloud(WaveArgs a) {
             status = kOutOfBounds;
             break;
           }
-          decode_bytes(a.out[of] + (uint64_t)s * a.out_stride[of], blob + foff[f], flen[f], delta, S);
-          if (threadIdx.x == 0) a.out_len[(uint64_t)of * a.n_samples + s] = flen[f];
+          if (leader) {
+            decode_bytes(a.out[of] + (uint64_t)s * a.out_stride[of], blob + foff[f], flen[f], delta, S);
+            if (threadIdx.x == 0) a.out_len[(uint64_t)of * a.n_samples + s] = flen[f];
+          }
         }
       }
     }
@@ -1424,7 +1552,7 @@ __global__ void __launch_bounds__(512, MinBlocks) k_cloud(WaveArgs a) {
     }
 
     // ---- write tracked fields + scalar values into the batch slot --------
-    if (status == kOk) {
+    if (status == kOk && leader) {
       for (int f = 0; f < a.n_bytes_fields && status == kOk; ++f) {
         const int of = a.bytes_out[f];
         if (!((a.tracked_mask >> f) & 1u) || of < 0) continue;
@@ -1475,7 +1603,7 @@ __global__ void __launch_bounds__(512, MinBlocks) k_cloud(WaveArgs a) {
         vo += nb + skip;
       }
     }
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && leader) {
       a.sample_status[s] = status;
       a.sample_op[s] = status == kOk ? -1 : fail_op;
       a.sample_where[s] = 0;
@@ -1487,8 +1615,8 @@ __global__ void __launch_bounds__(512, MinBlocks) k_cloud(WaveArgs a) {
 __device__ uint8_t* carve(const WaveArgs& a, uint8_t* work, Cloud& proto) {
   uint8_t* gbase = a.gscratch ? a.gscratch + (uint64_t)blockIdx.x * a.gscratch_per_cta : nullptr;
   uint64_t soff = 0, goff = 0;
-  uint8_t* ptr[24];
-  for (int b = 0; b < 24; ++b) {
+  uint8_t* ptr[25];
+  for (int b = 0; b < 25; ++b) {
     const uint64_t nb = (a.buf_bytes[b] + 127) & ~uint64_t(127);
     if (!nb) {
       ptr[b] = nullptr;
@@ -1509,6 +1637,7 @@ __device__ uint8_t* carve(const WaveArgs& a, uint8_t* work, Cloud& proto) {
   proto.key[0] = reinterpret_cast<uint64_t*>(ptr[21]);
   proto.key[1] = reinterpret_cast<uint64_t*>(ptr[22]);
   proto.counts = reinterpret_cast<int32_t*>(ptr[23]);
+  proto.fps_buf = ptr[24];
   return ptr[0];  // TMA staging buffer (shared) or nullptr
 }
 
@@ -1523,7 +1652,9 @@ __global__ void __launch_bounds__(512, 1) k_apply_set(WaveArgs a) {
   if (threadIdx.x == 0) S.proto = proto;
   __syncthreads();
   Cloud& c = S.cl;
-  for (uint32_t s = blockIdx.x; s < a.n_samples; s += gridDim.x) {
+  const uint32_t CL = a.fps_cluster > 1 ? a.fps_cluster : 1;
+  const bool leader = (blockIdx.x % CL) == 0;
+  for (uint32_t s = blockIdx.x / CL; s < a.n_samples; s += gridDim.x / CL) {
     const uint64_t p0 = a.set_offset[s], p1 = a.set_offset[s + 1];
     const uint64_t n = p1 >= p0 ? p1 - p0 : 0;
     if (threadIdx.x == 0) {
@@ -1554,7 +1685,7 @@ __global__ void __launch_bounds__(512, 1) k_apply_set(WaveArgs a) {
     __syncthreads();
     if (status == kOk && n == 0) status = kEmptyCloud;
     if (status == kOk) status = run_chain<1>(a, c, S, 0, 0, a.set_seeds + s, fail_op);
-    if (status == kOk) {
+    if (status == kOk && leader) {
       for (int f = 0; f < a.n_bytes_fields && status == kOk; ++f) {
         if (!((a.tracked_mask >> f) & 1u) || !a.set_out[f]) continue;
         const uint64_t nb = (uint64_t)c.n[f] * c.elem[f];
@@ -1566,10 +1697,10 @@ __global__ void __launch_bounds__(512, 1) k_apply_set(WaveArgs a) {
         for (uint64_t i = threadIdx.x; i < nb; i += blockDim.x) dst[i] = c.cur[f][i];
       }
     }
-    if (status == kOk && a.set_voxel_count && c.has_counts)
+    if (status == kOk && leader && a.set_voxel_count && c.has_counts)
       for (uint32_t i = threadIdx.x; i < c.n_counts && i < a.set_out_cap; i += blockDim.x)
         a.set_voxel_count[(uint64_t)s * a.set_out_cap + i] = c.counts[i];
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && leader) {
       a.sample_status[s] = status;
       if (a.set_count) a.set_count[s] = status == kOk ? c.n[a.role_data] : 0;
     }
@@ -1766,13 +1897,39 @@ cudaError_t launch_page_decode(const uint8_t* bytes, uint8_t* raw, const PageRef
   return cudaGetLastError();
 }
 
+namespace {
+template <typename K>
+cudaError_t launch_clustered(K kern, const WaveArgs& a, int grid, int threads, size_t smem,
+                             cudaStream_t st) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = a.fps_cluster;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, a);
+}
+}  // namespace
+
 cudaError_t launch_wave(const WaveArgs& a, int grid, int threads, size_t smem, cudaStream_t st,
                         cudaEvent_t k0, cudaEvent_t k1) {
   if (a.n_groups) k_scalar_parse<<<(a.n_groups + 127) / 128, 128, 0, st>>>(a);
   if (k0) cudaEventRecord(k0, st);
   if (a.n_samples) {
-    if (a.min_blocks == 2) k_cloud<2><<<grid, threads, smem, st>>>(a);
-    else k_cloud<1><<<grid, threads, smem, st>>>(a);
+    if (a.fps_cluster > 1) {
+      const cudaError_t e = launch_clustered(k_cloud<1>, a, grid, threads, smem, st);
+      if (e != cudaSuccess) return e;
+    } else if (a.min_blocks == 2) {
+      k_cloud<2><<<grid, threads, smem, st>>>(a);
+    } else {
+      k_cloud<1><<<grid, threads, smem, st>>>(a);
+    }
   }
   if (k1) cudaEventRecord(k1, st);
   if (a.n_pages) k_finalize<<<(a.n_pages + 255) / 256, 256, 0, st>>>(a);
@@ -1817,10 +1974,11 @@ cudaError_t occupancy_cloud(int* n, int threads, size_t smem, int min_blocks) {
 
 cudaError_t launch_apply_set(const WaveArgs& a, int grid, int threads, size_t smem,
                              cudaStream_t st) {
-  cudaError_t e = cudaFuncSetAttribute(k_apply_set, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
+  cudaError_t e = set_apply_smem(smem);
   if (e != cudaSuccess) return e;
-  if (a.n_samples) k_apply_set<<<grid, threads, smem, st>>>(a);
+  if (!a.n_samples) return cudaSuccess;
+  if (a.fps_cluster > 1) return launch_clustered(k_apply_set, a, grid, threads, smem, st);
+  k_apply_set<<<grid, threads, smem, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -1842,6 +2000,27 @@ cudaError_t launch_decode_pages(const uint8_t* bytes, const uint64_t* page_off, 
                                                      col_off, col_len, shift_tab, scratch_off,
                                                      scratch, status);
   return cudaGetLastError();
+}
+
+cudaError_t set_apply_smem(size_t bytes) {
+  return cudaFuncSetAttribute(k_apply_set, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+
+cudaError_t occupancy_cloud_clusters(int* n, int threads, size_t smem, uint32_t cluster, bool apply) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(cluster * 64);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cluster;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return apply ? cudaOccupancyMaxActiveClusters(n, k_apply_set, &cfg)
+               : cudaOccupancyMaxActiveClusters(n, k_cloud<1>, &cfg);
 }
 
 cudaError_t set_cloud_smem(size_t bytes) {

@@ -35,6 +35,9 @@ uint64_t lz4_scratch_bytes(uint64_t pay);  // per LZ4 page
 cudaError_t launch_wave(const WaveArgs& a, int grid, int threads, size_t smem, cudaStream_t st,
                         cudaEvent_t k0 = nullptr, cudaEvent_t k1 = nullptr);
 cudaError_t occupancy_cloud(int* n, int threads, size_t smem, int min_blocks);
+// Max co-resident clusters of `cluster` CTAs (k_cloud<1>, or k_apply_set).
+cudaError_t occupancy_cloud_clusters(int* n, int threads, size_t smem, uint32_t cluster, bool apply);
+cudaError_t set_apply_smem(size_t bytes);
 cudaError_t launch_compact(const uint8_t* src, uint64_t stride, const uint64_t* d_off,
                            const uint64_t* d_len, uint32_t n, uint8_t* dst, cudaStream_t st);
 

@@ -62,6 +62,8 @@ enum FieldKind : int32_t { kBytes = 0, kInt32, kInt64, kFloat32, kFloat64, kStri
 
 constexpr int kMaxFields = 16;      // schema fields
 constexpr int kMaxBytesFields = 8;  // bytes fields per sample
+constexpr uint32_t kFpsRegPts = 20;  // FPS points per thread held in registers (kernels.cu)
+constexpr uint32_t kFpsMailBytes = 2 * 128 * 32;  // cluster-FPS mailbox: [parity][<= 8 x 16 warps] x 32 B
 constexpr int kMaxOps = 16;         // map transforms per pipeline
 
 // One serialized EncodedPage used by a wave (absolute offsets into the
@@ -171,14 +173,17 @@ struct WaveArgs {
   int32_t smem_mode;        // 1: some per-CTA buffers live in shared memory
   // per-CTA buffer plan (host: plan_buffers): 0 staging, 1..4 index arrays,
   // 5..12 cur per bytes field, 13..20 alt per bytes field, 21/22 voxel keys,
-  // 23 voxel counts.  Bytes (0 = absent) and shared-memory placement bits.
-  uint64_t buf_bytes[24];
+  // 23 voxel counts, 24 cluster-FPS slice + mailbox.  Bytes (0 = absent)
+  // and shared-memory placement bits.
+  uint64_t buf_bytes[25];
   uint32_t buf_smem_mask;
   int32_t min_blocks;       // k_cloud instantiation: 1 (128 regs) or 2 (64 regs)
   uint8_t* gscratch;        // global scratch (smem_mode 0), per CTA
   uint64_t gscratch_per_cta;
   uint32_t force_serial_fy; // test hook: take the serial Fisher-Yates path
   float neg_zero;           // -0.0f, opaque to ptxas (FPS paired squares, kernels.cu)
+  uint32_t fps_cluster;     // CTAs per cloud (thread-block cluster) for large-cloud FPS; 1 = none
+  uint32_t fps_slice_pts;   // points per CTA slice in cluster FPS (buffer 24 sizing)
   // cloud-set mode (pcp_apply_map): clouds come from CSR arrays instead of
   // pages; bytes-field slots 0..7 = data, normal, color, intensity, extra0..3
   int32_t set_mode;

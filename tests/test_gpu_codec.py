@@ -286,9 +286,11 @@ def test_fps_no_fma_contraction(pcp, orc):
         assert np.array_equal(od[i, :2].view(np.uint32), want.view(np.uint32)), i  # ... and so must we
 
 
-@pytest.mark.parametrize("n,m", [(3000, 700), (7000, 512), (10000, 1024), (12000, 300), (40000, 256)])
+@pytest.mark.parametrize("n,m", [(3000, 700), (7000, 512), (10000, 1024), (12000, 300), (25000, 900),
+                                 (40000, 256), (90000, 64)])
 def test_fps_sizes_bit_exact(pcp, orc, rng, n, m):
-    """Every FPS path (register P = 8 / 16 / 20, and the large-cloud path)
+    """Every FPS path (register P = 8 / 16 / 20, clusters of 2..8 CTAs, and
+    the single-CTA global-memory path beyond 8 x 10240 points)
     against the restatement, including duplicated points (exact ties)."""
     from oracle.ffi import cloud
     clouds = []

@@ -179,3 +179,15 @@ def test_voxel_gathers_extra_field_and_counts(pcp, ref, orc, tmp_path):
     primary = _ds(pcp, tmp_path, "shapenet", 6, group=3, n_points=3000)
     g = synth.graph([("voxel", {"voxel_size": 0.1, "gather": ["seg"]}), "random_scale"], batch_size=3)
     assert_batches_equal(_run(pcp, primary, g), expected_run(ref, orc, primary, g))
+
+
+def test_cluster_fps_chain_parity(pcp, ref, orc, tmp_path):
+    """FPS input above one CTA's registers (downsample 24000 -> cluster of 3
+    CTAs): chain prefix run redundantly per CTA, FPS split over the cluster."""
+    from paper_2603_16945_b200 import synth
+    primary = _ds(pcp, tmp_path, "scannet", 5, group=2, lo=30000, hi=45000)
+    g = synth.graph([("grid_subsample", {"voxel_size": 0.01}), ("downsample", {"num_points": 24000}),
+                     ("fps", {"num_points": 700}), "rotate"], batch_size=2, drop_remainder=False)
+    got = _run(pcp, primary, g)
+    want = expected_run(ref, orc, primary, g)
+    assert_batches_equal(got, want, float_fields=tolerant_fields(g))
