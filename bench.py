@@ -374,6 +374,13 @@ def main():
                 "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
                 "gpu_launches": st1["launches"] - st0["launches"],
                 "batches_per_step": nb / args.steps}
+        if "op_cycles" in st1:  # PCP_OP_TIMING=1 diagnostics: share of k_cloud CTA time
+            oc = st1["op_cycles"]
+            from paper_2603_16945_b200 import synth
+            names = (["stage+decode"] + [o if isinstance(o, str) else o[0]
+                                         for o in synth.CHAINS[CHAIN_OF[args.config]]] + ["writes"])
+            tot_c = max(1, sum(oc))
+            line["op_cycle_share"] = {n: round(c / tot_c, 4) for n, c in zip(names, oc)}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

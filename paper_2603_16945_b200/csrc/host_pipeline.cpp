@@ -421,6 +421,8 @@ struct Pipeline {
   uint64_t epochs = 1;
   bool force_serial_fy = false;
   bool lz4_timing = std::getenv("PCP_LZ4_TIMING") != nullptr;
+  bool op_timing = std::getenv("PCP_OP_TIMING") != nullptr;  // per-op SM cycles (diagnostics)
+  DevBuf d_op_cycles;
   std::vector<double> lz4_phase_cycles = std::vector<double>(4, 0.0);
   cudaStream_t stream = nullptr;        // wave compute (copies + kernels)
   cudaStream_t serve_stream = nullptr;  // batch views: compaction, user D2H
@@ -722,6 +724,11 @@ struct Pipeline {
     CK(cudaGetDeviceProperties(&prop, device));
     const size_t fixed = cloud_smem_fixed();
     plan_fps_cluster(a, (uint32_t)threads);
+    if (op_timing) {
+      d_op_cycles.ensure((kMaxOps + 2) * 8);
+      CK(cudaMemset(d_op_cycles.p, 0, (kMaxOps + 2) * 8));
+      a.op_cycles = d_op_cycles.as<unsigned long long>();
+    }
     const size_t used = plan_buffers(a, any_stored_raw, prop.sharedMemPerBlockOptin - fixed);
     smem = fixed + used;
     CK(set_cloud_smem(smem));
@@ -1174,6 +1181,13 @@ struct Pipeline {
            {"cap_points", proto.cap_points},
            {"resident", resident},
            {"lz4_max_phase_cycles", lz4_phase_cycles}};
+    if (op_timing && d_op_cycles.p) {  // summed over CTAs: [stage+decode, ops..., writes]
+      std::vector<unsigned long long> oc(kMaxOps + 2);
+      CK(cudaDeviceSynchronize());
+      CK(cudaMemcpy(oc.data(), d_op_cycles.p, oc.size() * 8, cudaMemcpyDeviceToHost));
+      oc.resize(proto.n_ops + 2);
+      j["op_cycles"] = oc;
+    }
     stats_json = j.dump();
     return stats_json.c_str();
   }

@@ -877,18 +877,50 @@ __device__ __forceinline__ uint64_t f2_add(uint64_t a, uint64_t b) {
   return d;
 }
 
+// CTA argmax of the min-distances for one FPS iteration: the largest value,
+// lowest point index on ties (App. C).  Values first — warp redux.sync max
+// of the distance bits (distances are >= +0, so the unsigned order of their
+// bits is the float order; padding carries -inf and contributes 0), one
+// block barrier through per-warp parity slots — then only the warp(s)
+// holding the maximum look up which of their points it is (a min-tree over
+// k, off every other warp's issue slots), and a second barrier publishes
+// the lowest index.  Returns base + t + k*nt of the winner, or ~0u if the
+// CTA has no point.  `slot`: >= 64 words of shared memory.
+template <int P>
+__device__ __forceinline__ uint32_t fps_argmax(const float (&mind)[P], float bv, uint32_t base,
+                                               uint32_t* slot, uint32_t it, uint32_t& gmax_out) {
+  const uint32_t t = threadIdx.x, nt = blockDim.x, lane = t & 31, w = t >> 5, nw = nt >> 5;
+  const uint32_t par = it & 1u;
+  const uint32_t vb = bv >= 0.f ? __float_as_uint(bv) : 0u;
+  const uint32_t wmax = __reduce_max_sync(0xffffffffu, vb);
+  if (lane == 0) slot[par * 16 + w] = wmax;
+  __syncthreads();
+  const uint32_t gv = lane < nw ? slot[par * 16 + lane] : 0u;
+  const uint32_t gmax = __reduce_max_sync(0xffffffffu, gv);
+  gmax_out = gmax;
+  if (wmax == gmax) {  // warp-uniform
+    uint32_t bk = 31;
+    if (vb == gmax && bv >= 0.f) {
+#pragma unroll
+      for (int k = 0; k < P; ++k) bk = min(bk, mind[k] == bv ? (uint32_t)k : 31u);
+    }
+    const uint32_t bi = bk < 31 ? base + t + bk * nt : 0xFFFFFFFFu;
+    const uint32_t wi = __reduce_min_sync(0xffffffffu, bi);
+    if (lane == 0) slot[32 + par * 16 + w] = wi;
+  }
+  __syncthreads();
+  return __reduce_min_sync(0xffffffffu,
+                           (lane < nw && gv == gmax) ? slot[32 + par * 16 + lane] : 0xFFFFFFFFu);
+}
+
 // Register-resident FPS: thread t owns points i = t + k*nt (k < P), packed
-// in pairs (k = 2j, 2j+1) with their min-distances in registers.  Per
-// iteration the argmax (largest min-distance, lowest index on ties) is two
-// warp redux.sync ops — max of the distance bits (distances are >= +0, so
-// the unsigned order of their bits is the float order; padding carries -inf
-// and contributes key 0 with index ~0u), then min of the tied indices — plus
-// one block barrier through a parity double-buffered per-warp slot.
+// in pairs (k = 2j, 2j+1) with their min-distances in registers; the argmax
+// per iteration is fps_argmax.
 template <int P>
 __device__ void fps_reg(const float* d, uint32_t N, uint32_t M, int32_t* idx, Smem& S, float nz) {
   static_assert(P % 2 == 0, "points are processed in pairs");
-  uint64_t* slot = reinterpret_cast<uint64_t*>(S.rs_wcnt);  // [2][16]
-  const uint32_t t = threadIdx.x, nt = blockDim.x, lane = t & 31, w = t >> 5, nw = nt >> 5;
+  uint32_t* slot = &S.rs_wcnt[0][0];  // [2][16] values, [2][16] indices
+  const uint32_t t = threadIdx.x, nt = blockDim.x;
   uint64_t X[P / 2], Y[P / 2], Z[P / 2];
   float mind[P];
 #pragma unroll
@@ -923,20 +955,8 @@ __device__ void fps_reg(const float* d, uint32_t N, uint32_t M, int32_t* idx, Sm
       mind[2 * j + 1] = fminf(__uint_as_float((uint32_t)(dd >> 32)), mind[2 * j + 1]);
       bv = fmaxf(bv, fmaxf(mind[2 * j], mind[2 * j + 1]));
     }
-    uint32_t bk = P;
-#pragma unroll
-    for (int k = P - 1; k >= 0; --k) bk = mind[k] == bv ? (uint32_t)k : bk;
-    const uint32_t vb = bv >= 0.f ? __float_as_uint(bv) : 0u;
-    const uint32_t bi = bv >= 0.f ? t + bk * nt : 0xFFFFFFFFu;
-    const uint32_t wmax = __reduce_max_sync(0xffffffffu, vb);
-    const uint32_t wi = __reduce_min_sync(0xffffffffu, vb == wmax ? bi : 0xFFFFFFFFu);
-    const uint32_t par = it & 1u;
-    if (lane == 0) slot[par * 16 + w] = ((uint64_t)wmax << 32) | wi;
-    __syncthreads();
-    const uint64_t g = lane < nw ? slot[par * 16 + lane] : 0ull;
-    const uint32_t gv = (uint32_t)(g >> 32);
-    const uint32_t gmax = __reduce_max_sync(0xffffffffu, gv);
-    sel = __reduce_min_sync(0xffffffffu, (lane < nw && gv == gmax) ? (uint32_t)g : 0xFFFFFFFFu);
+    uint32_t gmax;
+    sel = fps_argmax<P>(mind, bv, 0, slot, it, gmax);
     if (sel == 0xFFFFFFFFu) sel = 0;  // no candidate at all (N == 0): index 0 like the oracle
   }
 }
@@ -945,14 +965,15 @@ __device__ void fps_reg(const float* d, uint32_t N, uint32_t M, int32_t* idx, Sm
 // the points are split over the C CTAs of a thread-block cluster (CTA r owns
 // [r*per, r*per + per)), each holding its slice in registers as in fps_reg
 // plus an AoS copy in shared memory for its candidates' coordinates.  Per
-// iteration every warp sends its candidate (distance bits, index, x, y, z)
-// to every CTA of the cluster with st.async into a parity double-buffered
-// mailbox whose mbarrier counts the bytes — one DSMEM hop and an mbarrier
-// wait instead of a cluster barrier (which would also flush L1) — then every
-// CTA reduces the same 16*C records to the same `sel`.  Reuse is safe: a CTA
-// can send iteration it+2's records only after completing it+1, which needs
-// it+1 records from every warp of every CTA, each sent after that warp read
-// iteration it's mailbox.
+// iteration each CTA reduces its warps' candidates (one block barrier, as
+// fps_reg), then warp 0 sends the CTA's candidate (distance bits, index,
+// x, y, z) to every CTA of the cluster with st.async into a parity
+// double-buffered mailbox whose mbarrier counts the bytes — one DSMEM hop
+// and an mbarrier wait instead of a cluster barrier (which would also flush
+// L1) — and every CTA reduces the same C records to the same `sel`.  Reuse
+// is safe: a CTA sends iteration it+2's record only after completing it+1,
+// which needs every CTA's it+1 record, each sent after that CTA's block
+// barrier of it+1, i.e. after all its threads read iteration it's mailbox.
 template <int P>
 __device__ void fps_cluster(const float* d, uint32_t N, uint32_t M, int32_t* idx, Smem& S,
                             float nz, uint8_t* buf, uint32_t C) {
@@ -963,6 +984,7 @@ __device__ void fps_cluster(const float* d, uint32_t N, uint32_t M, int32_t* idx
   const uint32_t base = min(r * per, N), nloc = min(per, N - base);
   uint32_t* mail = reinterpret_cast<uint32_t*>(buf);         // [2][128][8] words
   float* sp = reinterpret_cast<float*>(buf + kFpsMailBytes);  // [nloc][3]
+  const uint32_t mail_s = dev::smem_u32(mail), sp_s = dev::smem_u32(sp);  // buf is in shared memory
   for (uint32_t k = t; k < 3 * nloc; k += nt) sp[k] = d[3 * (uint64_t)base + k];
   if (t == 0) {
     dev::mbar_init(&S.fbar[0], 1);
@@ -989,8 +1011,8 @@ __device__ void fps_cluster(const float* d, uint32_t N, uint32_t M, int32_t* idx
     Z[j] = f2_pack(v[0][2], v[1][2]);
   }
   dev::cluster_sync_all();  // every CTA's mailbox barriers are initialised
-  const uint32_t nrec = C * nw;
-  const uint32_t tx = nrec * 20;  // bytes per phase (16 + 4 per record)
+  uint32_t* slot = &S.rs_wcnt[0][0];  // fps_argmax slots
+  const uint32_t tx = C * 20;  // bytes per phase: one record (16 + 4 B) from each CTA
   if (t == 0) {
     dev::mbar_expect_tx(&S.fbar[0], tx);
     dev::mbar_expect_tx(&S.fbar[1], tx);
@@ -1010,38 +1032,31 @@ __device__ void fps_cluster(const float* d, uint32_t N, uint32_t M, int32_t* idx
       mind[2 * j + 1] = fminf(__uint_as_float((uint32_t)(dd >> 32)), mind[2 * j + 1]);
       bv = fmaxf(bv, fmaxf(mind[2 * j], mind[2 * j + 1]));
     }
-    uint32_t bk = P;
-#pragma unroll
-    for (int k = P - 1; k >= 0; --k) bk = mind[k] == bv ? (uint32_t)k : bk;
-    const uint32_t vb = bv >= 0.f ? __float_as_uint(bv) : 0u;
-    const uint32_t bi = bv >= 0.f ? base + t + bk * nt : 0xFFFFFFFFu;
-    const uint32_t wmax = __reduce_max_sync(0xffffffffu, vb);
-    const uint32_t wi = __reduce_min_sync(0xffffffffu, vb == wmax ? bi : 0xFFFFFFFFu);
     const uint32_t par = it & 1u;
-    if (lane < C) {  // lane q sends this warp's candidate to CTA q
+    uint32_t cmax;
+    const uint32_t ci = fps_argmax<P>(mind, bv, base, slot, it, cmax);
+    if (w == 0 && lane < C) {  // warp 0 sends the CTA's candidate to every CTA of the cluster
       float x = 0.f, y = 0.f, z = 0.f;
-      if (wi != 0xFFFFFFFFu) {
-        const uint32_t j = wi - base;
-        x = sp[3 * j];
-        y = sp[3 * j + 1];
-        z = sp[3 * j + 2];
+      if (ci != 0xFFFFFFFFu) {
+        const uint32_t j = sp_s + 12 * (ci - base);
+        x = dev::lds_f32(j);
+        y = dev::lds_f32(j + 4);
+        z = dev::lds_f32(j + 8);
       }
-      const uint32_t* rec = mail + (par * 128 + r * nw + w) * 8;
+      const uint32_t* rec = mail + (par * 128 + r) * 8;
       const uint32_t ra = dev::mapa(rec, lane), rb = dev::mapa(&S.fbar[par], lane);
-      dev::st_async_v4(ra, wmax, wi, __float_as_uint(x), __float_as_uint(y), rb);
+      dev::st_async_v4(ra, ci != 0xFFFFFFFFu ? cmax : 0u, ci, __float_as_uint(x), __float_as_uint(y), rb);
       dev::st_async_b32(ra + 16, __float_as_uint(z), rb);
     }
-    dev::mbar_wait_cluster(&S.fbar[par], (it >> 1) & 1u);
+    // CTA-scope wait: st.async data is visible once its complete_tx lands
+    // (an .acquire.cluster wait would also invalidate L1 every iteration)
+    dev::mbar_wait(&S.fbar[par], (it >> 1) & 1u);
     if (t == 0 && it + 2 < M) dev::mbar_expect_tx(&S.fbar[par], tx);
-    const uint32_t* mb = mail + par * 128 * 8;
-    uint32_t lv = 0, li = 0xFFFFFFFFu, lq = 0;
-    for (uint32_t q = lane; q < nrec; q += 32) {
-      const uint32_t v = mb[q * 8], i = mb[q * 8 + 1];
-      if (v > lv || (v == lv && i < li)) {
-        lv = v;
-        li = i;
-        lq = q;
-      }
+    const uint32_t mb = mail_s + par * 128 * 32;
+    uint32_t lv = 0, li = 0xFFFFFFFFu;
+    if (lane < C) {
+      lv = dev::lds_u32(mb + lane * 32);
+      li = dev::lds_u32(mb + lane * 32 + 4);
     }
     const uint32_t gmax = __reduce_max_sync(0xffffffffu, lv);
     sel = __reduce_min_sync(0xffffffffu, lv == gmax ? li : 0xFFFFFFFFu);
@@ -1049,11 +1064,11 @@ __device__ void fps_cluster(const float* d, uint32_t N, uint32_t M, int32_t* idx
       sel = 0;
       sx = d[0], sy = d[1], sz = d[2];
     } else {
-      const uint32_t bal = __ballot_sync(0xffffffffu, lv == gmax && li == sel);
-      const uint32_t q = __shfl_sync(0xffffffffu, lq, __ffs(bal) - 1);
-      sx = __uint_as_float(mb[q * 8 + 2]);
-      sy = __uint_as_float(mb[q * 8 + 3]);
-      sz = __uint_as_float(mb[q * 8 + 4]);
+      const uint32_t bal = __ballot_sync(0xffffffffu, lane < C && lv == gmax && li == sel);
+      const uint32_t q = __ffs(bal) - 1;
+      sx = dev::lds_f32(mb + q * 32 + 8);
+      sy = dev::lds_f32(mb + q * 32 + 12);
+      sz = dev::lds_f32(mb + q * 32 + 16);
     }
   }
 }
@@ -1080,7 +1095,7 @@ __device__ int32_t op_fps(const WaveArgs& a, Cloud& c, Smem& S, const OpDesc& op
   } else if (MinBlocks == 1 && N <= kFpsRegPts * blockDim.x) {
     fps_reg<kFpsRegPts>(d, N, M, idx, S, a.neg_zero);
     done = true;
-  } else if (MinBlocks == 1 && a.fps_cluster > 1 && c.fps_buf &&
+  } else if (MinBlocks == 1 && a.fps_cluster > 1 && c.fps_buf && __isShared(c.fps_buf) &&
              N <= a.fps_cluster * a.fps_slice_pts && N <= a.fps_cluster * kFpsRegPts * blockDim.x) {
     // every CTA of the cluster takes this branch for the same sample
     fps_cluster<kFpsRegPts>(d, N, M, idx, S, a.neg_zero, c.fps_buf, a.fps_cluster);
@@ -1375,6 +1390,7 @@ __device__ int32_t run_chain(const WaveArgs& a, Cloud& c, Smem& S, uint64_t epoc
                              const uint64_t* fixed_seed, int32_t& fail_op) {
   int32_t status = kOk;
   const int fd = a.role_data;
+  long long t0 = (a.op_cycles && threadIdx.x == 0) ? clock64() : 0;
   for (int k = 0; status == kOk && k < a.n_ops; ++k) {
     const OpDesc& op = a.ops[k];
     const uint64_t seed =
@@ -1399,6 +1415,11 @@ __device__ int32_t run_chain(const WaveArgs& a, Cloud& c, Smem& S, uint64_t epoc
       }
     }
     if (status != kOk) fail_op = k + 1;
+    if (a.op_cycles && threadIdx.x == 0) {
+      const long long t1 = clock64();
+      atomicAdd(a.op_cycles + 1 + k, (unsigned long long)(t1 - t0));
+      t0 = t1;
+    }
   }
   return status;
 }
@@ -1442,6 +1463,7 @@ __global__ void __launch_bounds__(512, MinBlocks) k_cloud(WaveArgs a) {
     const PageRef pg = a.pages[sw.block_page];
     const ScalarRec rec = a.recs[(uint64_t)a.groups[sw.group].first_rec + sw.row];
     int32_t fail_op = 0;
+    const long long tc0 = (a.op_cycles && threadIdx.x == 0) ? clock64() : 0;
     // read_sample checks (format.cpp:741-755)
     const bool range_ok = sw.blob_end <= pg.raw_len && sw.blob_start <= sw.blob_end;
     uint64_t* flen = S.flen;
@@ -1538,6 +1560,7 @@ __global__ void __launch_bounds__(512, MinBlocks) k_cloud(WaveArgs a) {
     }
 
     __syncthreads();
+    if (a.op_cycles && threadIdx.x == 0) atomicAdd(a.op_cycles, (unsigned long long)(clock64() - tc0));
     // ---- the op chain (Pipeline map worker, pipeline.cpp:474-480) ---------
     if (status == kOk && a.n_ops > 0) {
       const int fd = a.role_data;
@@ -1552,6 +1575,7 @@ __global__ void __launch_bounds__(512, MinBlocks) k_cloud(WaveArgs a) {
     }
 
     // ---- write tracked fields + scalar values into the batch slot --------
+    const long long tc2 = (a.op_cycles && threadIdx.x == 0) ? clock64() : 0;
     if (status == kOk && leader) {
       for (int f = 0; f < a.n_bytes_fields && status == kOk; ++f) {
         const int of = a.bytes_out[f];
@@ -1608,6 +1632,8 @@ __global__ void __launch_bounds__(512, MinBlocks) k_cloud(WaveArgs a) {
       a.sample_op[s] = status == kOk ? -1 : fail_op;
       a.sample_where[s] = 0;
     }
+    if (a.op_cycles && threadIdx.x == 0)
+      atomicAdd(a.op_cycles + a.n_ops + 1, (unsigned long long)(clock64() - tc2));
     __syncthreads();
   }
 }

@@ -184,6 +184,7 @@ struct WaveArgs {
   float neg_zero;           // -0.0f, opaque to ptxas (FPS paired squares, kernels.cu)
   uint32_t fps_cluster;     // CTAs per cloud (thread-block cluster) for large-cloud FPS; 1 = none
   uint32_t fps_slice_pts;   // points per CTA slice in cluster FPS (buffer 24 sizing)
+  unsigned long long* op_cycles;  // PCP_OP_TIMING: [0] stage+decode, [1..n_ops] ops, [n_ops+1] writes
   // cloud-set mode (pcp_apply_map): clouds come from CSR arrays instead of
   // pages; bytes-field slots 0..7 = data, normal, color, intensity, extra0..3
   int32_t set_mode;
