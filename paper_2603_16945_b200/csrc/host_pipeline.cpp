@@ -757,8 +757,9 @@ struct Pipeline {
     const uint32_t B = g.batch_size;
     uint32_t wb = wave_batches;
     if (!wb) {
-      // default: >= 8192 samples and >= 2 pages (groups) per SM in flight, so
-      // every page's serial LZ4 chain runs concurrently
+      // default: >= 8192 samples and >= 2 pages (groups) per SM per wave, so
+      // with two waves in flight every decoder slot (4 per SM) holds a page
+      // whose serial LZ4 chain runs concurrently
       uint64_t gmax = 1;
       for (const auto& gr : h.groups) gmax = std::max<uint64_t>(gmax, gr.sample_count);
       const uint64_t want = std::max<uint64_t>(8192, 2ull * sms * gmax);
@@ -1018,7 +1019,7 @@ struct Pipeline {
     w.decode_alg_bytes = 0;
     for (uint32_t pi : todo) w.decode_alg_bytes += pages[pi].pay_len + pages[pi].raw_len;
     CK(launch_wave(a, grid, threads, smem, w.stream, w.k0, w.k1));
-    launches += (wins.empty() ? 0 : 1) + (todo.empty() ? 0 : 1) + (ng ? 1 : 0) + 1 + 1 + 1;
+    launches += (wins.empty() ? 0 : 1) + (todo.empty() ? 0 : 2) + (ng ? 1 : 0) + 1 + 1 + 1;
     h2d_bytes += up_bytes;
     // ---- results back to pinned host -------------------------------------------
 
@@ -1080,8 +1081,11 @@ struct Pipeline {
         CK(cudaMemcpy(tm.data(), wn.lz4_timing.p, tm.size() * 8, cudaMemcpyDeviceToHost));
         for (uint32_t i = 0; i < wn.n_todo; ++i)
           if (tm[i * 16 + 4])
-            for (int ph = 0; ph < 4; ++ph)
-              lz4_phase_cycles[ph] = std::max(lz4_phase_cycles[ph], (double)(tm[i * 16 + ph + 1] - tm[i * 16 + ph]));
+            for (int ph = 0; ph < 4; ++ph) {  // phase 4 runs in k_page_matches: its own clocks
+              const long long* q = &tm[i * 16];
+              const double c = ph < 3 ? (double)(q[ph + 1] - q[ph]) : (double)(q[12] - q[11]);
+              lz4_phase_cycles[ph] = std::max(lz4_phase_cycles[ph], c);
+            }
       }
       if (cur >= 0) slots[cur].launched = false;
       cur = nxt;

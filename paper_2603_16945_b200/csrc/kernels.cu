@@ -165,16 +165,20 @@ __device__ int32_t warp_lz4_decode(const uint8_t* src, uint64_t n, uint8_t* dst,
 // One CTA per page: LZ4 pages use the CTA-parallel decoder (lz4_parallel.cuh)
 // with a per-page scratch slab; stored-raw pages are copied.  The rare page
 // whose match count exceeds the scratch falls back to the warp decoder.
-__global__ void __launch_bounds__(256) k_page_decode(const uint8_t* bytes, uint8_t* raw,
+// CTA size of the page decoder (phases 1-3): 256 threads x 64 registers =
+// 4 pages per SM.  128-thread CTAs (8 per SM) measured slower: the fill and
+// phase-3 throughput per page matters as much as pages in flight.
+constexpr uint32_t kDecodeThreads = 256;
+
+__global__ void __launch_bounds__(kDecodeThreads, 1024 / kDecodeThreads) k_page_decode(const uint8_t* bytes, uint8_t* raw,
                                                      const PageRef* pages, const uint32_t* todo,
                                                      const uint64_t* scratch_off, uint8_t* scratch,
                                                      uint32_t n_todo, int32_t* page_status,
                                                      long long* timing) {
-  __shared__ uint32_t ctl[lz4p::kSmemWords];
+  __shared__ __align__(16) uint32_t ctl[lz4p::kSmemWords];
   __shared__ Lz4Seq seqs[32];
   __shared__ int32_t sst;
   __shared__ uint32_t scount;
-  __shared__ __align__(16) uint8_t ring[lz4p::kRing];
   for (uint32_t w = blockIdx.x; w < n_todo; w += gridDim.x) {
     const uint32_t pi = todo[w];
     const PageRef pg = pages[pi];
@@ -182,12 +186,18 @@ __global__ void __launch_bounds__(256) k_page_decode(const uint8_t* bytes, uint8
     uint8_t* dst = raw + pg.raw_dst;
     int32_t status = kOk;
     if (pg.flags & kFlagOuterLz4) {
+      const lz4p::Scratch sc = lz4p::carve_scratch(scratch + scratch_off[w], pg.pay_len);
       if (pg.pay_len >= 0xFFFFFFF0ull || pg.raw_len >= 0xFFFFFFF0ull) {
         status = kCorruptPage;
+        if (threadIdx.x == 0) sc.hdr[1] = 0;
       } else {
-        const lz4p::Scratch sc = lz4p::carve_scratch(scratch + scratch_off[w], pg.pay_len);
-        status = lz4p::decode_block(src, (uint32_t)pg.pay_len, dst, (uint32_t)pg.raw_len, sc, ctl,
-                                    ring, timing ? timing + 16 * (uint64_t)w : nullptr);
+        // phases 1-3 here; phase 4 (one warp per page) in k_page_matches
+        status = lz4p::decode_prefix(src, (uint32_t)pg.pay_len, dst, (uint32_t)pg.raw_len, sc, ctl,
+                                     timing ? timing + 16 * (uint64_t)w : nullptr);
+        if (threadIdx.x == 0) {
+          sc.hdr[0] = ctl[1];
+          sc.hdr[1] = status == kOk ? 1u : 0u;
+        }
         if (status < 0) {
           if (threadIdx.x < 32) {
             const int32_t r = warp_lz4_decode(src, pg.pay_len, dst, pg.raw_len, seqs, &sst, &scount);
@@ -208,6 +218,25 @@ __global__ void __launch_bounds__(256) k_page_decode(const uint8_t* bytes, uint8
     }
     if (threadIdx.x == 0 && status != kOk) page_status[pi] = status;
     __syncthreads();
+  }
+}
+
+// Phase 4 of the LZ4 pages k_page_decode left pending: one warp per page
+// (the match chains are serial; a 32-thread CTA with a 16 KB ring lets ~13
+// pages per SM resolve at once instead of idling seven warps per page).
+__global__ void __launch_bounds__(32) k_page_matches(uint8_t* raw, const PageRef* pages,
+                                                     const uint32_t* todo, const uint64_t* scratch_off,
+                                                     uint8_t* scratch, uint32_t n_todo,
+                                                     long long* timing) {
+  __shared__ __align__(16) uint8_t ring[lz4p::kRing];
+  for (uint32_t w = blockIdx.x; w < n_todo; w += gridDim.x) {
+    const PageRef pg = pages[todo[w]];
+    if (!(pg.flags & kFlagOuterLz4)) continue;
+    const lz4p::Scratch sc = lz4p::carve_scratch(scratch + scratch_off[w], pg.pay_len);
+    if (sc.hdr[1] != 1u) continue;
+    long long* tm = timing ? timing + 16 * (uint64_t)w + 8 : nullptr;  // [11] start, [12] end
+    if (tm && threadIdx.x == 0) tm[3] = clock64();
+    lz4p::decode_matches(raw + pg.raw_dst, (uint32_t)pg.raw_len, sc, sc.hdr[0], ring, tm);
   }
 }
 
@@ -1756,7 +1785,7 @@ __global__ void k_decode_pages(const uint8_t* bytes, const uint64_t* page_off, u
                                uint8_t* scratch, int32_t* status) {
   __shared__ uint32_t tab[256];
   __shared__ uint32_t red[32];
-  __shared__ uint32_t ctl[lz4p::kSmemWords];
+  __shared__ __align__(16) uint32_t ctl[lz4p::kSmemWords];
   __shared__ Lz4Seq seqs[32];
   __shared__ int32_t sst;
   __shared__ uint32_t scount;
@@ -1918,8 +1947,14 @@ cudaError_t launch_page_decode(const uint8_t* bytes, uint8_t* raw, const PageRef
                                uint8_t* scratch, uint32_t n_todo, int32_t* status,
                                cudaStream_t st, long long* timing) {
   if (!n_todo) return cudaSuccess;
-  k_page_decode<<<n_todo, 256, 0, st>>>(bytes, raw, pages, todo, scratch_off, scratch, n_todo,
+  static bool carve = [] {  // static shared memory only: ask for the max carveout
+    cudaFuncSetAttribute(k_page_decode, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    return true;
+  }();
+  (void)carve;
+  k_page_decode<<<n_todo, kDecodeThreads, 0, st>>>(bytes, raw, pages, todo, scratch_off, scratch, n_todo,
                                         status, timing);
+  k_page_matches<<<n_todo, 32, 0, st>>>(raw, pages, todo, scratch_off, scratch, n_todo, timing);
   return cudaGetLastError();
 }
 

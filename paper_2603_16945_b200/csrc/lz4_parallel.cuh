@@ -28,6 +28,7 @@
 
 #include <cstdint>
 
+#include "device_util.cuh"
 #include "pcp_internal.h"
 
 namespace pcp {
@@ -35,9 +36,9 @@ namespace lz4p {
 
 constexpr uint32_t kChunk = 2048;      // compressed bytes per skim window / parse chunk
 constexpr uint32_t kRing = 16384;      // shared-memory output window (bytes)
-constexpr uint32_t kStageTail = 64;    // staged bytes past a window for its last tokens
-constexpr uint32_t kStageBytes = kChunk + kStageTail + 16;  // + alignment slack
-constexpr uint32_t kSmemWords = 72 + 2 * kChunk + (2 * kStageBytes) / 4 + kChunk;
+constexpr uint32_t kStageTail = 128;   // staged bytes past a window for its last tokens
+constexpr uint32_t kStageBytes = kChunk + kStageTail + 32;  // + 16-B alignment slack (TMA)
+constexpr uint32_t kSmemWords = 72 + 2 * kChunk + (2 * kStageBytes) / 4;
 constexpr uint32_t kRingChunk = 4096;  // refill granule
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 
@@ -48,22 +49,13 @@ __host__ __device__ inline uint32_t n_chunks(uint64_t pay) {
 __host__ __device__ inline uint64_t match_capacity(uint64_t pay) { return pay / 6 + 64; }
 
 __host__ __device__ inline uint64_t scratch_bytes(uint64_t pay) {
-  const uint64_t nch = n_chunks(pay) + 1;
-  return nch * (kChunk / 8)     // bitmaps
-         + nch * 4 * 8          // per-chunk words (8 u32)
-         + match_capacity(pay) * 16 + 256;
+  return 64 + match_capacity(pay) * 16 + 256;
 }
 
+// Per-page scratch: a header (phase-4 hand-off between k_page_decode and
+// k_page_matches), match records and the token positions of the skim.
 struct Scratch {
-  uint32_t* bitmap;    // [nch][kChunk/32]
-  uint32_t* spec_exit; // speculative exit position
-  uint32_t* spec_flag; // bit0: chain ended with the last sequence, bit1: error
-  uint32_t* walk_exit; // exit when walking from the assumed entry
-  uint32_t* walk_flag; // bit0 last, bit1 error, bit2 converged
-  uint32_t* entry;     // verified true entry
-  uint32_t* cnt_out;   // output bytes of the chunk's true sequences
-  uint32_t* cnt_match; // matches in the chunk
-  uint32_t* base_out;  // exclusive scans
+  uint32_t* hdr;       // [0] matches M, [1] 1 = phase 4 pending
   uint32_t* m_mo;      // match output start
   uint32_t* m_ml;      // match length
   uint16_t* m_off;     // offset
@@ -71,19 +63,9 @@ struct Scratch {
 };
 
 __device__ inline Scratch carve_scratch(uint8_t* p, uint64_t pay) {
-  const uint32_t nch = n_chunks(pay) + 1;
   Scratch s;
-  s.bitmap = reinterpret_cast<uint32_t*>(p);
-  uint32_t* w = s.bitmap + (uint64_t)nch * (kChunk / 32);
-  s.spec_exit = w;
-  s.spec_flag = w + nch;
-  s.walk_exit = w + 2 * nch;
-  s.walk_flag = w + 3 * nch;
-  s.entry = w + 4 * nch;
-  s.cnt_out = w + 5 * nch;
-  s.cnt_match = w + 6 * nch;
-  s.base_out = w + 7 * nch;
-  uint32_t* m = w + 8 * nch;
+  s.hdr = reinterpret_cast<uint32_t*>(p);
+  uint32_t* m = s.hdr + 16;
   const uint64_t cap = match_capacity(pay);
   s.m_mo = m;
   s.m_ml = m + cap;
@@ -99,19 +81,58 @@ struct Seq {
   bool last;
 };
 
+// LZ4 length extension (lz4_block.cpp:123-129 / :143-149): acc += bytes
+// until the first byte != 255 (inclusive) or acc reaches 0x7fffffff; false
+// if the stream ends first.  Raw-float pages carry literal runs of megabytes
+// whose length field is thousands of 255 bytes, so 16-B aligned stretches
+// are scanned 128 bytes per step with eight independent loads; the guard
+// and the truncation point are exactly the byte loop's.
+__device__ __forceinline__ bool ext_len(const uint8_t* __restrict__ src, uint32_t n, uint32_t& ip,
+                                        uint32_t& acc) {
+  while (true) {
+    if (ip >= n) return false;
+    // the 128-B block of 16-B aligned words starting at or below ip (reads
+    // <= 15 bytes before ip, inside the page header / payload)
+    const uint32_t sh = (uint32_t)((reinterpret_cast<uintptr_t>(src) + ip) & 15u);
+    if (ip + 128 - sh <= n && acc < 0x7fffffffu - 255u * 128u) {
+      const uint4* q = reinterpret_cast<const uint4*>(src + ip - sh);
+      uint4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = q[u];
+      uint32_t j = 128;  // first byte != 255 at or after offset sh
+#pragma unroll
+      for (int u = 7; u >= 0; --u) {
+        const uint32_t w4[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+        for (int e = 3; e >= 0; --e) {
+          uint32_t x = ~w4[e];  // nonzero bytes = bytes != 255
+          const int b0 = 16 * u + 4 * e;
+          if (b0 + 4 <= (int)sh) x = 0;  // word entirely before ip
+          else if (b0 < (int)sh) x &= 0xFFFFFFFFu << (8 * (sh - b0));
+          if (x) j = b0 + (__ffs(x) - 1) / 8;
+        }
+      }
+      if (j == 128) {
+        acc += 255u * (128u - sh);
+        ip += 128u - sh;
+        continue;
+      }
+      acc += 255u * (j - sh) + src[ip - sh + j];
+      ip += j - sh + 1;
+      return true;
+    }
+    const uint32_t b = src[ip++];
+    acc += b;
+    if (b != 255 || acc >= 0x7fffffffu) return true;
+  }
+}
+
 __device__ __forceinline__ bool parse_seq(const uint8_t* __restrict__ src, uint32_t n, uint32_t ip,
                                           Seq& s) {
   if (ip >= n) return false;
   const uint32_t token = src[ip++];
   uint32_t lit = token >> 4;
-  if (lit == 15) {
-    uint32_t b;
-    do {
-      if (ip >= n) return false;
-      b = src[ip++];
-      lit += b;
-    } while (b == 255 && lit < 0x7fffffffu);
-  }
+  if (lit == 15 && !ext_len(src, n, ip, lit)) return false;
   if ((uint64_t)ip + lit > n) return false;
   s.lit_src = ip;
   s.lit_len = lit;
@@ -128,14 +149,7 @@ __device__ __forceinline__ bool parse_seq(const uint8_t* __restrict__ src, uint3
   ip += 2;
   if (s.offset == 0) return false;
   uint32_t ml = token & 15;
-  if (ml == 15) {
-    uint32_t b;
-    do {
-      if (ip >= n) return false;
-      b = src[ip++];
-      ml += b;
-    } while (b == 255 && ml < 0x7fffffffu);
-  }
+  if (ml == 15 && !ext_len(src, n, ip, ml)) return false;
   s.match_len = ml + 4;
   s.last = false;
   s.next = ip;
@@ -189,42 +203,60 @@ __device__ __forceinline__ bool parse_seq_staged(const uint8_t* buf, uint32_t c0
   return true;
 }
 
+// parse_seq over a staged window (bytes [c0, se) in shared memory) without
+// touching global memory: 0 malformed, 1 parsed, 2 needs a byte in [se, n)
+// (the walker then parses that position from global).  Checks in
+// parse_seq's order, so verdicts 0/1 are parse_seq's.
+__device__ __forceinline__ int parse_seq_win(const uint8_t* buf, uint32_t c0, uint32_t se,
+                                             uint32_t n, uint32_t ip, Seq& s) {
+  if (ip >= n) return 0;
+  if (ip >= se) return 2;
+  const uint32_t token = buf[ip++ - c0];
+  uint32_t lit = token >> 4;
+  if (lit == 15) {
+    uint32_t b;
+    do {
+      if (ip >= n) return 0;
+      if (ip >= se) return 2;
+      b = buf[ip++ - c0];
+      lit += b;
+    } while (b == 255 && lit < 0x7fffffffu);
+  }
+  if ((uint64_t)ip + lit > n) return 0;
+  s.lit_src = ip;
+  s.lit_len = lit;
+  ip += lit;
+  if (ip == n) {
+    s.last = true;
+    s.match_len = 0;
+    s.offset = 0;
+    s.next = n;
+    return 1;
+  }
+  if (ip + 2 > n) return 0;
+  if (ip + 2 > se) return 2;
+  s.offset = (uint32_t)buf[ip - c0] | ((uint32_t)buf[ip + 1 - c0] << 8);
+  ip += 2;
+  if (s.offset == 0) return 0;
+  uint32_t ml = token & 15;
+  if (ml == 15) {
+    uint32_t b;
+    do {
+      if (ip >= n) return 0;
+      if (ip >= se) return 2;
+      b = buf[ip++ - c0];
+      ml += b;
+    } while (b == 255 && ml < 0x7fffffffu);
+  }
+  s.match_len = ml + 4;
+  s.last = false;
+  s.next = ip;
+  return 1;
+}
+
 // Barrier among the fill warps only (warps 1..), id 1.
 __device__ __forceinline__ void named_sync_fill(uint32_t nthreads) {
   asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
-}
-
-__device__ __forceinline__ bool bit(const uint32_t* bm, uint32_t i) {
-  return (bm[i >> 5] >> (i & 31)) & 1u;
-}
-
-// Walk the chain from `pos` inside chunk k until a position marked in the
-// chunk's bitmap (converged), the chunk end, the last sequence or an error.
-__device__ inline uint32_t walk(const uint8_t* src, uint32_t n, uint32_t k, uint32_t pos,
-                                const uint32_t* bm, uint32_t& flag) {
-  const uint32_t c0 = k * kChunk, c1 = min(c0 + kChunk, n);
-  flag = 0;
-  if (pos < c0) {  // entry assumed from an errored speculative chain
-    flag = 2;
-    return pos;
-  }
-  while (pos < c1) {
-    if (bit(bm, pos - c0)) {
-      flag = 4;
-      return pos;
-    }
-    Seq s;
-    if (!parse_seq(src, n, pos, s)) {
-      flag = 2;
-      return pos;
-    }
-    if (s.last) {
-      flag = 1;
-      return n;
-    }
-    pos = s.next;
-  }
-  return pos;
 }
 
 // Copy `len` bytes src→dst (both arbitrary alignment), one thread.
@@ -246,11 +278,13 @@ __device__ __forceinline__ void copy_bytes(uint8_t* __restrict__ dst, const uint
   for (; i < len; ++i) dst[i] = src[i];
 }
 
-// Decode one page with the whole CTA.  `ctl` is >= 8 words of shared memory.
-// Returns the status (same on all threads).
-__device__ inline int32_t decode_block(const uint8_t* __restrict__ src, uint32_t n,
-                                       uint8_t* __restrict__ dst, uint32_t raw_len, Scratch sc,
-                                       uint32_t* ctl, uint8_t* ring, long long* tm = nullptr) {
+// Phases 1-3 of one page with the whole CTA (`ctl`: kSmemWords of shared
+// memory).  Returns the status (same on all threads): kOk with ctl[1] =
+// matches left for phase 4, kCorruptPage, or -1 (scratch too small: the
+// caller falls back to the warp decoder).
+__device__ inline int32_t decode_prefix(const uint8_t* __restrict__ src, uint32_t n,
+                                        uint8_t* __restrict__ dst, uint32_t raw_len, Scratch sc,
+                                        uint32_t* ctl, long long* tm = nullptr) {
 #define PCP_T(i) \
   if (tm && threadIdx.x == 0) tm[i] = clock64();
   const uint32_t t = threadIdx.x, nt = blockDim.x;
@@ -260,107 +294,177 @@ __device__ inline int32_t decode_block(const uint8_t* __restrict__ src, uint32_t
   if (n == 0) return kCorruptPage;   // "truncated stream" (:134)
   PCP_T(0)
   // ---- phases 1+2: skim the token chain ------------------------------------
-  // Window w = compressed bytes [w*kChunk, (w+1)*kChunk).  All warps but
-  // warp 0 fill the jump table of window w+1 — d[p] = distance from p to the
-  // next token if a token started at p (bit 30: last sequence, bit 31:
-  // malformed) — while warp 0's lane 0 walks the true chain through window w
-  // with one shared-memory lookup per sequence, recording each window's
-  // entry (first true token >= window start).
+  // Window w = compressed bytes [w*kChunk, (w+1)*kChunk).  Warps 1.. fill the
+  // jump table of window w+1 — d[p] = distance from p to the next token if a
+  // token started at p (bit 31: malformed, bit 30: last sequence, bit 29:
+  // header runs past the staged bytes) — while warp 0's lane 0 walks the
+  // true chain through window w with one shared-memory lookup per sequence,
+  // writing each token position straight to global.  Window bytes arrive by
+  // TMA bulk copy one window ahead (mbarrier per buffer), so neither side
+  // waits on HBM.
   {
-    uint32_t* jt = ctl + 72;  // two windows of kChunk words, after ctl[0..71]
-    uint8_t* wb = reinterpret_cast<uint8_t*>(jt + 2 * kChunk);  // 2 x kStageBytes bytes
-    uint32_t* tbuf = jt + 2 * kChunk + (2 * kStageBytes) / 4;    // window token positions
-    if (t == 0) {
-      ctl[5] = 0;
-      ctl[6] = 0;
-    }
-    // staged copy of window w: aligned 4-byte words of [c0 - sh, e) with
-    // sh = misalignment of src + c0; all loads issued before the stores.
-    // Readers use buf0 + sh.  Reads up to 3 bytes outside the payload on
-    // either side; every byte store carries >= 16 B of slack.
-    auto stage = [&](uint32_t w, uint8_t* buf0, uint32_t tid, uint32_t nthr) {
-      const uint32_t c0 = w * kChunk, e = min(c0 + kChunk + kStageTail, n);
-      const uintptr_t base = reinterpret_cast<uintptr_t>(src) + c0;
-      const uint32_t sh = (uint32_t)(base & 3u);
-      const uint32_t* g = reinterpret_cast<const uint32_t*>(base - sh);
-      const uint32_t nw = (sh + (e - c0) + 3) / 4;
-      uint32_t* b32 = reinterpret_cast<uint32_t*>(buf0);
-      uint32_t v[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const uint32_t k = tid + u * nthr;
-        v[u] = k < nw ? g[k] : 0u;
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const uint32_t k = tid + u * nthr;
-        if (k < nw) b32[k] = v[u];
-      }
+    // per window buffer b: jt[b][kChunk] u32 = d (low 16 bits) | d2 << 16
+    uint32_t* jt = ctl + 72;
+    uint8_t* wb = reinterpret_cast<uint8_t*>(ctl + 72 + 2 * kChunk);  // 2 x kStageBytes bytes
+    uint64_t* sbar = reinterpret_cast<uint64_t*>(ctl + 64);     // stage barriers (ctl[64..67])
+    const uintptr_t sbase = reinterpret_cast<uintptr_t>(src);
+    // window w's bytes [c0, min(c0 + kChunk + kStageTail, n)) as the 16-B
+    // aligned superset; readers index buf0 + ((src + c0) & 15)
+    auto stage_async = [&](uint32_t w) {  // one thread
+      const uint32_t b = w & 1u;
+      const uint32_t e = min(w * kChunk + kChunk + kStageTail, n);
+      const uintptr_t g0 = (sbase + w * kChunk) & ~uintptr_t(15);
+      const uintptr_t g1 = (sbase + e + 15) & ~uintptr_t(15);
+      const uint32_t bytes = (uint32_t)(g1 - g0);
+      dev::mbar_expect_tx(&sbar[b], bytes);
+      dev::bulk_g2s(wb + b * kStageBytes, reinterpret_cast<const void*>(g0), bytes, &sbar[b]);
     };
-    auto fill = [&](uint32_t w, uint32_t* tab, const uint8_t* buf0, uint32_t tid, uint32_t nthr) {
+    // jump-table fill: the common header (every byte inside the staged
+    // window, no 255-continued length) in two levels of independent
+    // shared-memory loads; anything else goes through parse_seq_win.
+    auto fill = [&](uint32_t w, uint32_t* tab32, uint32_t tid, uint32_t nthr) {
+      uint16_t* tab = reinterpret_cast<uint16_t*>(tab32);  // low halves: tab[2 * lp]
       const uint32_t c0 = w * kChunk, c1 = min(c0 + kChunk, n);
-      const uint8_t* buf = buf0 + ((reinterpret_cast<uintptr_t>(src) + c0) & 3u);
+      const uint8_t* buf = wb + (w & 1u) * kStageBytes + ((sbase + c0) & 15u);
       const uint32_t se = min(c0 + kChunk + kStageTail, n);
       for (uint32_t p = c0 + tid; p < c1; p += nthr) {
-        Seq sq;
-        uint32_t v;
-        if (!parse_seq_staged(buf, c0, se, src, n, p, sq)) v = 0x80000000u;
-        else if (sq.last) v = 0x40000000u | (n - p);
-        else v = min(sq.next - p, 0x3FFFFFFFu);
-        tab[p - c0] = v;
+        const uint32_t lp = p - c0;
+        const uint32_t tok = buf[lp];
+        const uint32_t e1 = p + 1 < se ? buf[lp + 1] : 255u;
+        uint32_t lit = tok >> 4, hdr = 1;
+        if (lit == 15) {
+          lit += e1;
+          hdr = 2;
+        }
+        const uint32_t ip = p + hdr + lit;  // offset position (if not the last sequence)
+        uint32_t v = 0;
+        bool general = !(!(tok >= 0xF0u && e1 == 255u) && ip + 3 <= se && ip + 3 <= n);
+        if (!general) {
+          const uint32_t o = ip - c0;
+          const uint32_t off = (uint32_t)buf[o] | ((uint32_t)buf[o + 1] << 8);
+          const bool ml15 = (tok & 15u) == 15u;
+          if (ml15 && buf[o + 2] == 255u) general = true;  // long match-length run
+          else v = off == 0 ? 0x80000000u : (ip + 2 + (ml15 ? 1u : 0u)) - p;
+        }
+        if (general) {
+          Seq sq;
+          const int r = parse_seq_win(buf, c0, se, n, p, sq);
+          v = r == 0 ? 0x80000000u : r == 2 ? 0x20000000u : sq.last ? 0x40000000u : sq.next - p;
+        }
+        // u16 entry: distance, or 0xFFFF = walker parses this position from
+        // global (malformed / last / past the stage / distance >= 0xFFFF)
+        tab[2 * lp] = (v & 0xE0000000u) || v >= 0xFFFFu ? (uint16_t)0xFFFFu : (uint16_t)v;
       }
     };
-    stage(0, wb, t, nt);
+    // two-token jumps: d2[p] = d[p] + d[p + d[p]] when both hops are plain
+    // and the second token starts in this window, else 0
+    auto fill2 = [&](uint32_t w, uint32_t* tab32, uint32_t tid, uint32_t nthr) {
+      const uint16_t* tab = reinterpret_cast<const uint16_t*>(tab32);
+      uint16_t* tab2 = reinterpret_cast<uint16_t*>(tab32) + 1;  // high halves
+      const uint32_t c0 = w * kChunk, len = min(c0 + kChunk, n) - c0;
+      for (uint32_t lp = tid; lp < len; lp += nthr) {
+        const uint32_t a = tab[2 * lp];
+        uint32_t r = 0;
+        if (a != 0xFFFFu && lp + a < len) {
+          const uint32_t b = tab[2 * (lp + a)];
+          if (b != 0xFFFFu && a + b < 0xFFFFu) r = a + b;
+        }
+        tab2[2 * lp] = (uint16_t)r;
+      }
+    };
+    if (t == 0) {
+      dev::mbar_init(&sbar[0], 1);
+      dev::mbar_init(&sbar[1], 1);
+      dev::fence_mbar_init();
+    }
     __syncthreads();
-    fill(0, jt, wb, t, nt);
-    if (nch > 1) stage(1, wb + kStageBytes, t, nt);
+    if (t == 0) {
+      stage_async(0);
+      if (nch > 1) stage_async(1);
+    }
+    dev::mbar_wait(&sbar[0], 0);
+    fill(0, jt, t, nt);
     __syncthreads();
+    fill2(0, jt, t, nt);
+    __syncthreads();
+    long long a_walk = 0, a_fill = 0;  // PCP_LZ4_TIMING
     uint32_t pos = 0;  // walker state (thread 0)
     uint32_t err = 0, done = 0, nseq = 0;
     const uint32_t cap_seq = (uint32_t)match_capacity(n);
     for (uint32_t w = 0; w < nch; ++w) {
+#ifdef PCP_EXP_TRACE
+      if (tm && t == 0 && w < 1000) {
+        tm[16 + w] = clock64();
+        tm[1040 + w] = nseq;
+        tm[2064 + w] = pos;
+      }
+#endif
       if (t >= 32) {
-        // fill window w+1 from its staged bytes, then stage window w+2 into
-        // the buffer window w used (the walker only reads the jump table)
-        if (w + 1 < nch)
-          fill(w + 1, jt + ((w + 1) & 1) * kChunk, wb + ((w + 1) & 1) * kStageBytes,
-               t - 32, nt - 32);
-        named_sync_fill(nt - 32);
-        if (w + 2 < nch) stage(w + 2, wb + (w & 1) * kStageBytes, t - 32, nt - 32);
-      } else if (t == 0) {
-        const uint32_t* tab = jt + (w & 1) * kChunk;
-        const uint32_t c0 = w * kChunk, c1 = min(c0 + kChunk, n);
-        sc.entry[w] = pos;
-        uint32_t k = 0, acc = 0;
-        if (!done) {
-          while (pos < c1) {  // branch-free body: one LDS + one STS per token
-            const uint32_t v = tab[pos - c0];
-            acc |= v;
-            tbuf[k++] = pos;
-            pos += v & 0x3FFFFFFFu;
-            if (v & 0xC0000000u) break;  // malformed or last
-          }
-          if (acc & 0x80000000u) err = 1;
-          if (acc & 0xC0000000u) done = 1;
+        const long long f0 = (tm && t == 32) ? clock64() : 0;
+        // window w's buffer was last read by fill(w) before the previous
+        // barrier: refill it with window w+2 (async), then fill window w+1
+        if (t == 32 && w + 2 < nch) {
+          dev::fence_proxy_async();
+          stage_async(w + 2);
         }
-        ctl[5] = k;  // tokens found in this window (flushed by all threads)
+        if (w + 1 < nch) {
+          uint32_t* tb = jt + ((w + 1) & 1u) * kChunk;
+          dev::mbar_wait(&sbar[(w + 1) & 1u], ((w + 1) >> 1) & 1u);
+          fill(w + 1, tb, t - 32, nt - 32);
+          named_sync_fill(nt - 32);
+          fill2(w + 1, tb, t - 32, nt - 32);
+        }
+        if (tm && t == 32) a_fill += clock64() - f0;
+      } else if (t == 0) {
+        const long long w0 = tm ? clock64() : 0;
+        const uint32_t* tab = jt + (w & 1u) * kChunk;
+        const uint32_t c0 = w * kChunk, len = min(c0 + kChunk, n) - c0;
+        if (!done && pos < c0 + len) {
+          uint32_t* tp = sc.tokpos;
+          uint32_t lp = pos - c0;
+          while (true) {
+            // hot loop: one LDS per one or two tokens, no taken branch
+            uint32_t x = tab[lp];
+            while ((x & 0xFFFFu) != 0xFFFFu) {
+              const uint32_t a = x & 0xFFFFu, b = x >> 16;
+              if (nseq < cap_seq) tp[nseq] = c0 + lp;
+              if (b && nseq + 1 < cap_seq) tp[nseq + 1] = c0 + lp + a;
+              nseq += b ? 2u : 1u;
+              lp += b ? b : a;
+#ifdef PCP_EXP_TRACE
+              if (tm && w < 1000) tm[3088 + w] += b ? 1 : 0x100000;
+#endif
+              if (lp >= len) break;
+              x = tab[lp];
+            }
+            if (lp >= len) break;
+            // entry 0xFFFF: parse this position exactly from global
+#ifdef PCP_EXP_TRACE
+            if (tm && w < 1000) tm[3088 + w] += 1ll << 40;
+#endif
+            if (nseq < cap_seq) tp[nseq] = c0 + lp;
+            ++nseq;
+            Seq sq;
+            if (!parse_seq(src, n, c0 + lp, sq)) {
+              err = done = 1;
+              break;
+            }
+            if (sq.last) {
+              done = 1;
+              break;
+            }
+            lp = sq.next - c0;
+            if (lp >= len) break;
+          }
+          pos = done ? n : c0 + lp;
+        }
+        if (tm) a_walk += clock64() - w0;
       }
       __syncthreads();
-      {  // flush this window's token positions to global (coalesced)
-        const uint32_t k = ctl[5];
-        const uint32_t nb = ctl[6];
-        for (uint32_t i = t; i < k; i += nt)
-          if (nb + i < cap_seq) sc.tokpos[nb + i] = tbuf[i];
-        __syncthreads();
-        if (t == 0) {
-          ctl[6] = nb + k;
-          ctl[5] = 0;
-        }
-      }
     }
+    if (tm && t == 0) tm[8] = a_walk;
+    if (tm && t == 32) tm[9] = a_fill;
     if (t == 0) {
-      nseq = ctl[6];
-      sc.entry[nch] = pos;
       ctl[0] = (err || !done) ? 1u : 0u;  // no last sequence → truncated stream
       ctl[1] = nseq;
       ctl[3] = nseq > cap_seq ? 1u : 0u;  // scratch too small: caller falls back
@@ -462,15 +566,18 @@ __device__ inline int32_t decode_block(const uint8_t* __restrict__ src, uint32_t
   }
   if (ctl[0]) return kCorruptPage;
   PCP_T(3)
-  // ---- phase 4: matches, in order, by warp 0 through a shared-memory ring --
-  // Match dependency chains on these pages are thousands deep (DESIGN.md
-  // §4.2), so matches are resolved in stream order by one warp; the other
-  // warps of the SM belong to other pages' CTAs.  The ring holds output
-  // bytes [hi - kRing, hi); chunks are pulled in from global (literals are
-  // final after phase 3) ahead of the match being resolved; sources older
-  // than the ring are read back from global (already final).
-  const uint32_t M = ctl[1];
-  if (t < 32) {
+#undef PCP_T
+  return kOk;
+}
+
+// Phase 4 of one page by ONE warp (lane = threadIdx.x & 31): the M matches
+// recorded by decode_prefix, in order, through a shared-memory ring (`ring`:
+// kRing bytes).
+__device__ inline void decode_matches(uint8_t* __restrict__ dst, uint32_t raw_len, Scratch sc,
+                                      uint32_t M, uint8_t* ring, long long* tm = nullptr) {
+  const uint32_t t = threadIdx.x & 31u;
+  {
+
     uint32_t hi = 0, fl = 0;  // ring holds [hi - kRing, hi); global final below fl
     auto move_chunk = [&](uint32_t from, uint32_t end, bool to_ring) {
       if (end - from == kRingChunk && ((uintptr_t)(dst + from) & 15u) == 0) {
@@ -633,9 +740,18 @@ __device__ inline int32_t decode_block(const uint8_t* __restrict__ src, uint32_t
       }
     }
   }
+  __syncwarp();
+  if (tm && t == 0) tm[4] = clock64();
+}
+
+// Whole page with the whole CTA (phases 1-4; phase 4 on warp 0).
+__device__ inline int32_t decode_block(const uint8_t* __restrict__ src, uint32_t n,
+                                       uint8_t* __restrict__ dst, uint32_t raw_len, Scratch sc,
+                                       uint32_t* ctl, uint8_t* ring, long long* tm = nullptr) {
+  const int32_t st = decode_prefix(src, n, dst, raw_len, sc, ctl, tm);
+  if (st != kOk) return st;
+  if (threadIdx.x < 32) decode_matches(dst, raw_len, sc, ctl[1], ring, tm);
   __syncthreads();
-  PCP_T(4)
-#undef PCP_T
   return kOk;
 }
 

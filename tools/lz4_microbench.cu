@@ -5,13 +5,14 @@
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
+#include <algorithm>
 #include "../paper_2603_16945_b200/csrc/lz4_parallel.cuh"
 
 using namespace pcp;
 
 __global__ void k(const uint8_t* src, uint32_t n, uint8_t* dst, uint32_t raw, uint8_t* scr,
                   long long* tm, int* st) {
-  __shared__ uint32_t ctl[lz4p::kSmemWords];
+  __shared__ __align__(16) uint32_t ctl[lz4p::kSmemWords];
   __shared__ __align__(16) uint8_t ring[lz4p::kRing];
   lz4p::Scratch sc = lz4p::carve_scratch(scr, n);
   int r = lz4p::decode_block(src, n, dst, raw, sc, ctl, ring, tm);
@@ -33,11 +34,11 @@ int main(int argc, char** argv) {
   cudaMalloc(&d_src, pay.size() + 64);
   cudaMalloc(&d_dst, raw + 64);
   cudaMalloc(&d_scr, lz4p::scratch_bytes(pay.size()));
-  cudaMalloc(&d_tm, 128);
+  cudaMalloc(&d_tm, 8 * 8192);
   cudaMalloc(&d_st, 4);
   cudaMemcpy(d_src, pay.data(), pay.size(), cudaMemcpyHostToDevice);
   for (int it = 0; it < 3; ++it) {
-    cudaMemset(d_tm, 0, 128);
+    cudaMemset(d_tm, 0, 8 * 8192);
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
@@ -51,9 +52,26 @@ int main(int argc, char** argv) {
     int st;
     cudaMemcpy(tm, d_tm, 128, cudaMemcpyDeviceToHost);
     cudaMemcpy(&st, d_st, 4, cudaMemcpyDeviceToHost);
-    printf("status %d  %.3f ms  skim %lld (walk %lld fill %lld)  phase3 %lld  matches %lld (ring %lld dep %lld waves %lld n_waves %lld) fast %lld slow %lld\n",
-           st, ms, tm[2] - tm[0], tm[8], tm[9], tm[3] - tm[2], tm[4] - tm[3], tm[13], tm[11], tm[12], tm[14], tm[5], tm[6]);
+    printf("status %d  %.3f ms  skim %lld (walk %lld fill %lld)  phase3 %lld  matches %lld fast %lld slow %lld\n",
+           st, ms, tm[2] - tm[0], tm[8], tm[9], tm[3] - tm[2], tm[4] - tm[3], tm[5], tm[6]);
   }
+#ifdef PCP_EXP_TRACE
+  {
+    std::vector<long long> tr(4096);
+    cudaMemcpy(tr.data(), d_tm, 8 * 4096, cudaMemcpyDeviceToHost);
+    std::vector<long long> d;
+    for (int w = 1; w < 900; ++w) d.push_back(tr[16 + w] - tr[15 + w]);
+    std::vector<long long> srt = d;
+    std::sort(srt.begin(), srt.end());
+    long long sum = 0;
+    for (auto x : d) sum += x;
+    printf("window cycles: sum %lld median %lld p90 %lld p99 %lld max %lld\n", sum, srt[srt.size() / 2],
+           srt[srt.size() * 9 / 10], srt[srt.size() * 99 / 100], srt.back());
+    for (int w = 8; w < 32; ++w)
+      printf("w%d: %lld cyc, tokens %lld, pos %lld (window start %d) steps2 %lld steps1 %lld specials %lld\n", w, tr[17 + w] - tr[16 + w],
+             tr[1041 + w] - tr[1040 + w], tr[2064 + w], w * 2048, tr[3088 + w] & 0xFFFFF, (tr[3088 + w] >> 20) & 0xFFFFF, tr[3088 + w] >> 40);
+  }
+#endif
   std::vector<uint8_t> out(raw);
   cudaMemcpy(out.data(), d_dst, raw, cudaMemcpyDeviceToHost);
   FILE* o = fopen("/tmp/lz4_out.bin", "wb");
