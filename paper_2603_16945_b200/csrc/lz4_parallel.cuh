@@ -503,13 +503,19 @@ __device__ inline int32_t decode_prefix(const uint8_t* __restrict__ src, uint32_
         tot += wsum[k];
       }
       const uint64_t op = b0 + x - len;
-      // tile tables for the cooperative literal copy (reuse the jump tables)
+      // tile tables for the cooperative literal copy (reuse the jump tables):
+      // each literal is cut into 16-B aligned output chunks; a chunk prefix
+      // over the tile maps thread work items to (sequence, chunk)
       uint32_t* t_op = ctl + 72;
       uint32_t* t_src = t_op + nt;
-      uint32_t* t_lp = t_src + nt;  // exclusive prefix of literal lengths
-      uint32_t lit = (i < S && op + len <= raw_len) ? sq.lit_len : 0u;
+      uint32_t* t_len = t_src + nt;
+      uint32_t* t_cp = t_len + nt;  // exclusive prefix of chunk counts
+      const uint32_t lit = (i < S && op + len <= raw_len) ? sq.lit_len : 0u;
+      // chunk boundaries on absolute addresses (dst may be unaligned)
+      const uint32_t doff = (uint32_t)(reinterpret_cast<uintptr_t>(dst) & 15u);
+      const uint32_t nck = lit ? (uint32_t)((op + doff + lit + 15) / 16 - (op + doff) / 16) : 0u;
       {
-        uint32_t y = lit;
+        uint32_t y = nck;
         for (int o = 1; o < 32; o <<= 1) {
           const uint32_t z = __shfl_up_sync(0xffffffffu, y, o);
           if ((int)lane >= o) y += z;
@@ -524,22 +530,43 @@ __device__ inline int32_t decode_prefix(const uint8_t* __restrict__ src, uint32_
         }
         t_op[t] = (uint32_t)op;
         t_src[t] = sq.lit_src;
-        t_lp[t] = lb + y - lit;
+        t_len[t] = lit;
+        t_cp[t] = lb + y - nck;
         if (t == 0) ctl[7] = lt;
       }
       __syncthreads();
       {
-        const uint32_t L = ctl[7];
+        const uint32_t C = ctl[7];
         const uint32_t ns = min(nt, S - s0);
-        for (uint32_t b = t; b < L; b += nt) {
-          uint32_t lo = 0, hi = ns;  // last sequence with t_lp <= b
+        for (uint32_t c = t; c < C; c += nt) {
+          uint32_t lo = 0, hi = ns;  // last sequence with t_cp <= c
           while (hi - lo > 1) {
             const uint32_t mid = (lo + hi) >> 1;
-            if (t_lp[mid] <= b) lo = mid;
+            if (t_cp[mid] <= c) lo = mid;
             else hi = mid;
           }
-          const uint32_t k = b - t_lp[lo];
-          dst[t_op[lo] + k] = src[t_src[lo] + k];
+          const uint32_t d = t_op[lo], L = t_len[lo];
+          // this chunk's aligned start, in dst + doff coordinates
+          const uint32_t a0 = ((d + doff) / 16 + (c - t_cp[lo])) * 16;
+          const uint32_t b0 = max(a0, d + doff) - doff, b1 = min(a0 + 16, d + doff + L) - doff;
+          const uint8_t* sp = src + t_src[lo] + (b0 - d);
+          if (b1 - b0 == 16) {  // full chunk: one aligned 16-B store at dst + b0
+            const uintptr_t sa = reinterpret_cast<uintptr_t>(sp);
+            const uint32_t sh = (uint32_t)(sa & 3u) * 8u;
+            const uint32_t* q = reinterpret_cast<const uint32_t*>(sa & ~uintptr_t(3));
+            const uint32_t w0 = q[0], w1 = q[1], w2 = q[2], w3 = q[3];
+            uint4 v;
+            if (sh) {
+              const uint32_t w4 = q[4];  // <= 3 bytes past the literal (payload slack)
+              v = make_uint4(__funnelshift_r(w0, w1, sh), __funnelshift_r(w1, w2, sh),
+                             __funnelshift_r(w2, w3, sh), __funnelshift_r(w3, w4, sh));
+            } else {
+              v = make_uint4(w0, w1, w2, w3);
+            }
+            *reinterpret_cast<uint4*>(dst + b0) = v;
+          } else {
+            for (uint32_t b = b0; b < b1; ++b) dst[b] = sp[b - b0];
+          }
         }
       }
       if (i < S) {
