@@ -156,7 +156,7 @@ def ncu_traffic(workload, kernel):
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
             s = json.load(f)
         k = s.get(workload, {}).get(kernel, {})
-        return k.get("dram_bytes_per_launch"), k.get("alg_bytes_per_launch")
+        return k.get("dram_bytes_per_launch"), k.get("clouds_per_launch")
     except (OSError, ValueError):
         return None, None
 
@@ -330,13 +330,18 @@ def main():
                       "achieved_gbs": kby / (kms / 1e3) / 1e9 if kms > 0 else 0.0,
                       "share_of_step": kms / ms if ms else None}
     dom = max(kern, key=lambda k: kern[k]["ms_per_step"])
-    dram, alg_per_launch = ncu_traffic(args.config, dom)
+    # the decode events bracket k_page_decode + k_page_matches (phase 4)
+    dram, cap_clouds = ncu_traffic(args.config, "k_page_decode+k_page_matches" if dom == "k_page_decode" else dom)
+    alg_per_launch = kern[dom]["alg_bytes_per_step"] * args.steps / waves
+    if dram is not None and cap_clouds:  # capture wave -> this run's wave (per-cloud traffic)
+        dram = dram / cap_clouds * (clouds_rank / waves)
     achieved = kern[dom]["achieved_gbs"]
     roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "peak_kind": peak_kind, "traffic": dram,
             "alg_bytes_per_launch": kern[dom]["alg_bytes_per_step"] * args.steps / waves,
             "kernels": kern}
     if dom == "k_page_decode":
+        roof["kernel"] = "k_page_decode + k_page_matches"
         roof["note"] = ("latency-bound: one serial LZ4 token/match chain per page "
                         "(DESIGN.md 4.2); HBM fraction reported for completeness")
     if dram is not None and alg_per_launch:
