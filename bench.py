@@ -42,7 +42,7 @@ CONFIGS = {
     "kitti": dict(gen="kitti", kw={}, clouds=512, group=16, batch=4, points=120000,
                   desc="KITTI-shaped ~120k-pt XYZI frames: range crop, voxel 0.05 m (+counts), "
                   "rotate, flip_yz; B 4 (CSR batches)"),
-    "s3dis": dict(gen="s3dis", kw={"mean_points": 1_000_000}, clouds=64, group=1, batch=4,
+    "s3dis": dict(gen="s3dis", kw={"mean_points": 1_000_000}, clouds=256, group=1, batch=4,
                   points=1_000_000, desc="S3DIS-shaped ~1M-pt XYZRGB rooms: grid 0.04 m, "
                   "random_crop, downsample 4096; B 4"),
     "scannet": dict(gen="scannet", kw={}, clouds=192, group=4, batch=4, points=275000,
