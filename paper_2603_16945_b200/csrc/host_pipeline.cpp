@@ -304,8 +304,9 @@ size_t plan_buffers(WaveArgs& a, bool want_staging, size_t smem_budget) {
   const uint64_t alt_pts = std::max({T, M, big});
   auto with = [](uint64_t b) { return b ? b + 16 : 0; };
   uint64_t* sz = a.buf_bytes;
-  for (int b = 0; b < 25; ++b) sz[b] = 0;
+  for (int b = 0; b < 26; ++b) sz[b] = 0;
   if (a.fps_cluster > 1) sz[24] = kFpsMailBytes + 12ull * a.fps_slice_pts + 16;
+  if (vox) sz[25] = kSortScratchBytes;
   sz[0] = want_staging ? (uint64_t)a.max_blob + 64 : 0;
   sz[1] = 4 * std::max<uint64_t>({T, M, big, 1}) + 16;
   sz[2] = with(4 * ((ds || fps || vox) ? cap : 0));
@@ -322,6 +323,7 @@ size_t plan_buffers(WaveArgs& a, bool want_staging, size_t smem_budget) {
   }
   std::vector<int> order;
   if (sz[24]) order.push_back(24);  // cluster-FPS slice + mailbox first (latency-critical)
+  if (sz[25]) order.push_back(25);  // voxel sort scratch: smem atomics / per-warp counts
   const int rd = a.role_data;
   if (rd >= 0) order.push_back(5 + rd);
   for (int b : {1, 3, 4}) order.push_back(b);

@@ -335,6 +335,7 @@ struct Cloud {
   uint32_t n_counts;
   int32_t has_counts;
   uint8_t* fps_buf;                // cluster FPS: mailbox + this CTA's slice (buffer 24)
+  uint32_t* sort_buf;              // voxel sort scratch (buffer 25, kSortScratchBytes)
 };
 
 struct Smem {
@@ -1284,6 +1285,89 @@ __device__ int radix_sort(uint64_t* k0, uint32_t* v0, uint64_t* k1, uint32_t* v1
   return cur;
 }
 
+// Stable LSD radix sort of 64-bit words on bits [lo, hi), 8-bit digits
+// (voxel keys packed above the point index, so the words carry their own
+// payload).  One read computes every pass's digit histogram; each pass then
+// reads and writes the words once: tiles of blockDim words are ranked stably
+// with __match_any_sync inside a warp and per-warp digit counts turned into
+// exclusive prefixes in place, against double-buffered bucket bases (two
+// barriers per tile).  `scr`: kSortScratchBytes.  Returns 1 if the result
+// is in w1, 0 if in w0.
+__device__ int radix_sort8(uint64_t* w0, uint64_t* w1, uint32_t n, uint32_t lo, uint32_t hi,
+                           uint32_t* scr) {
+  uint32_t* hist = scr;               // [8][256]
+  uint32_t* wcnt = scr + 8 * 256;     // [16][256]
+  uint32_t* base = wcnt + 16 * 256;   // [2][256]
+  const uint32_t t = threadIdx.x, nt = blockDim.x, lane = t & 31, w = t >> 5, nw = nt >> 5;
+  const uint32_t np = (hi - lo + 7) / 8;
+  for (uint32_t i = t; i < np * 256; i += nt) hist[i] = 0;
+  __syncthreads();
+  for (uint32_t i = t; i < n; i += nt) {
+    const uint64_t x = w0[i];
+    for (uint32_t p = 0; p < np; ++p) atomicAdd(&hist[p * 256 + (uint32_t)((x >> (lo + 8 * p)) & 255u)], 1u);
+  }
+  __syncthreads();
+  if (w < np) {  // exclusive scan of pass w's histogram: 8 bins per lane
+    uint32_t* h = hist + w * 256;
+    uint32_t v[8], sum = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      v[k] = h[lane * 8 + k];
+      sum += v[k];
+    }
+    uint32_t x = sum;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if ((int)lane >= o) x += y;
+    }
+    uint32_t acc = x - sum;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      h[lane * 8 + k] = acc;
+      acc += v[k];
+    }
+  }
+  __syncthreads();
+  uint64_t* src = w0;
+  uint64_t* dst = w1;
+  const uint32_t lt = (1u << lane) - 1u;
+  for (uint32_t p = 0; p < np; ++p) {
+    const uint32_t sh = lo + 8 * p;
+    for (uint32_t d = t; d < 256; d += nt) base[d] = hist[p * 256 + d];
+    uint32_t cb = 0;
+    __syncthreads();
+    for (uint32_t t0 = 0; t0 < n; t0 += nt) {
+      const uint32_t i = t0 + t;
+      const bool valid = i < n;
+      const uint64_t x = valid ? src[i] : 0ull;
+      const uint32_t d = valid ? (uint32_t)((x >> sh) & 255u) : 256u;
+      for (uint32_t k = lane; k < 256; k += 32) wcnt[w * 256 + k] = 0;
+      __syncwarp();
+      const uint32_t peers = __match_any_sync(0xffffffffu, d);
+      const uint32_t rank = __popc(peers & lt);
+      if (valid && rank == 0) wcnt[w * 256 + d] = __popc(peers);
+      __syncthreads();
+      for (uint32_t dd = t; dd < 256; dd += nt) {  // per digit: warps' exclusive prefix
+        uint32_t acc = 0;
+        for (uint32_t q = 0; q < nw; ++q) {
+          const uint32_t c = wcnt[q * 256 + dd];
+          wcnt[q * 256 + dd] = acc;
+          acc += c;
+        }
+        base[(cb ^ 1u) * 256 + dd] = base[cb * 256 + dd] + acc;
+      }
+      __syncthreads();
+      if (valid) dst[base[cb * 256 + d] + wcnt[w * 256 + d] + rank] = x;
+      cb ^= 1u;
+    }
+    __syncthreads();
+    uint64_t* tmp = src;
+    src = dst;
+    dst = tmp;
+  }
+  return (int)(np & 1u);
+}
+
 // Smallest coordinate per axis with the sequential `if (v < o) o = v`
 // semantics starting from point 0 (App. C voxel origin): NaN at point 0
 // poisons the axis; later NaNs never win; equal values keep the first.
@@ -1328,18 +1412,19 @@ __device__ int32_t op_voxel(const WaveArgs& a, Cloud& c, Smem& S, const OpDesc& 
   }
   uint32_t* idx = reinterpret_cast<uint32_t*>(c.ix[0]);
   uint32_t* idx2 = reinterpret_cast<uint32_t*>(c.ix[1]);
+  auto axis_key = [&](uint32_t i, int ax, uint32_t& bad) -> uint32_t {
+    const float q = floorf(__fdiv_rn(__fsub_rn(d[3 * i + ax], o[ax]), op.voxel));
+    if (!(q >= 0.0f && q < 2097152.0f)) {
+      bad = 1;
+      return 0u;
+    }
+    return (uint32_t)q;
+  };
+  // pass 1: range check and per-axis extent (no stores)
   uint32_t bad = 0, mx[3] = {0, 0, 0};
   for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-    uint32_t kk[3];
 #pragma unroll
-    for (int ax = 0; ax < 3; ++ax) {
-      const float q = floorf(__fdiv_rn(__fsub_rn(d[3 * i + ax], o[ax]), op.voxel));
-      if (!(q >= 0.0f && q < 2097152.0f)) bad = 1;
-      kk[ax] = bad ? 0u : (uint32_t)q;
-      mx[ax] = max(mx[ax], kk[ax]);
-    }
-    c.key[0][i] = (uint64_t)kk[0] | ((uint64_t)kk[1] << 21) | ((uint64_t)kk[2] << 42);
-    idx[i] = i;
+    for (int ax = 0; ax < 3; ++ax) mx[ax] = max(mx[ax], axis_key(i, ax, bad));
   }
   bad = dev::block_reduce(bad, dev::OpOr{}, 0u, S.red);
   if (bad) return kOutOfBounds;
@@ -1349,20 +1434,40 @@ __device__ int32_t op_voxel(const WaveArgs& a, Cloud& c, Smem& S, const OpDesc& 
     bx[ax] = m ? 32u - __clz(m) : 0u;
   }
   // compact sort key, monotone in the App. C key (kz major, then ky, kx)
+  const uint32_t kb = bx[0] + bx[1] + bx[2];
+  const uint32_t ib = n > 1 ? 32u - __clz(n - 1) : 0u;  // point-index bits
+  const bool packed = c.sort_buf && kb + ib <= 64;
+  const uint64_t* K = nullptr;  // 64-bit path: sorted keys
+  const uint32_t* P = nullptr;  //              sorted original indices
+  const uint64_t* W = nullptr;  // packed path: sorted (key << ib | index)
   for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-    const uint64_t K = c.key[0][i];
-    const uint64_t kx = K & 0x1FFFFF, ky = (K >> 21) & 0x1FFFFF, kz = K >> 42;
-    c.key[0][i] = kx | (ky << bx[0]) | (kz << (bx[0] + bx[1]));
+    uint32_t b2 = 0;
+    const uint64_t kx = axis_key(i, 0, b2), ky = axis_key(i, 1, b2), kz = axis_key(i, 2, b2);
+    const uint64_t key = kx | (ky << bx[0]) | (kz << (bx[0] + bx[1]));
+    if (packed) {
+      c.key[0][i] = (key << ib) | i;
+    } else {
+      c.key[0][i] = key;
+      idx[i] = i;
+    }
   }
   __syncthreads();
-  const int r = radix_sort(c.key[0], idx, c.key[1], idx2, n, bx[0] + bx[1] + bx[2], S);
-  const uint64_t* K = c.key[r];
-  const uint32_t* P = r ? idx2 : idx;  // sorted original indices
+  if (packed) {
+    const int r = radix_sort8(c.key[0], c.key[1], n, ib, ib + kb, c.sort_buf);
+    W = c.key[r];
+  } else {
+    const int r = radix_sort(c.key[0], idx, c.key[1], idx2, n, kb, S);
+    K = c.key[r];
+    P = r ? idx2 : idx;
+  }
+  const uint64_t imask = ib ? ((1ull << ib) - 1) : 0ull;
+  auto key_at = [&](uint32_t k) -> uint64_t { return packed ? W[k] >> ib : K[k]; };
+  auto pt_at = [&](uint32_t k) -> uint32_t { return packed ? (uint32_t)(W[k] & imask) : P[k]; };
   uint32_t* seg = reinterpret_cast<uint32_t*>(c.ix[2]);
   uint32_t base = 0;
   for (uint32_t t0 = 0; t0 < n; t0 += blockDim.x) {
     const uint32_t i = t0 + threadIdx.x;
-    const bool f = i < n && (i == 0 || K[i] != K[i - 1]);
+    const bool f = i < n && (i == 0 || key_at(i) != key_at(i - 1));
     uint32_t tot;
     const uint32_t rk = dev::block_scan_excl(f ? 1u : 0u, &tot, S.red);
     if (f) seg[base + rk] = i;
@@ -1383,12 +1488,13 @@ __device__ int32_t op_voxel(const WaveArgs& a, Cloud& c, Smem& S, const OpDesc& 
         float* dst = reinterpret_cast<float*>(c.alt[f]);
         for (uint32_t q = 0; q < comps; ++q) {
           double acc = 0.0;
-          for (uint32_t k = s0; k < s1; ++k) acc = __dadd_rn(acc, (double)src[(uint64_t)P[k] * comps + q]);
+          for (uint32_t k = s0; k < s1; ++k) acc = __dadd_rn(acc, (double)src[(uint64_t)pt_at(k) * comps + q]);
           dst[(uint64_t)v * comps + q] = __double2float_rn(__ddiv_rn(acc, cnt));
         }
       } else {
         const uint32_t es = c.elem[f];
-        for (uint32_t b = 0; b < es; ++b) c.alt[f][(uint64_t)v * es + b] = c.cur[f][(uint64_t)P[s0] * es + b];
+        const uint64_t p0 = pt_at(s0);
+        for (uint32_t b = 0; b < es; ++b) c.alt[f][(uint64_t)v * es + b] = c.cur[f][p0 * es + b];
       }
     }
     if (c.counts) c.counts[v] = (int32_t)(s1 - s0);
@@ -1670,8 +1776,8 @@ __global__ void __launch_bounds__(512, MinBlocks) k_cloud(WaveArgs a) {
 __device__ uint8_t* carve(const WaveArgs& a, uint8_t* work, Cloud& proto) {
   uint8_t* gbase = a.gscratch ? a.gscratch + (uint64_t)blockIdx.x * a.gscratch_per_cta : nullptr;
   uint64_t soff = 0, goff = 0;
-  uint8_t* ptr[25];
-  for (int b = 0; b < 25; ++b) {
+  uint8_t* ptr[26];
+  for (int b = 0; b < 26; ++b) {
     const uint64_t nb = (a.buf_bytes[b] + 127) & ~uint64_t(127);
     if (!nb) {
       ptr[b] = nullptr;
@@ -1693,6 +1799,7 @@ __device__ uint8_t* carve(const WaveArgs& a, uint8_t* work, Cloud& proto) {
   proto.key[1] = reinterpret_cast<uint64_t*>(ptr[22]);
   proto.counts = reinterpret_cast<int32_t*>(ptr[23]);
   proto.fps_buf = ptr[24];
+  proto.sort_buf = reinterpret_cast<uint32_t*>(ptr[25]);
   return ptr[0];  // TMA staging buffer (shared) or nullptr
 }
 

@@ -64,6 +64,8 @@ constexpr int kMaxFields = 16;      // schema fields
 constexpr int kMaxBytesFields = 8;  // bytes fields per sample
 constexpr uint32_t kFpsRegPts = 20;  // FPS points per thread held in registers (kernels.cu)
 constexpr uint32_t kFpsMailBytes = 2 * 128 * 32;  // cluster-FPS mailbox: [parity][<= 8 x 16 warps] x 32 B
+// voxel sort scratch (u32): hist[8 passes][256] + wcnt[16 warps][256] + base[2][256]
+constexpr uint32_t kSortScratchBytes = (8 * 256 + 16 * 256 + 2 * 256) * 4;
 constexpr int kMaxOps = 16;         // map transforms per pipeline
 
 // One serialized EncodedPage used by a wave (absolute offsets into the
@@ -173,9 +175,10 @@ struct WaveArgs {
   int32_t smem_mode;        // 1: some per-CTA buffers live in shared memory
   // per-CTA buffer plan (host: plan_buffers): 0 staging, 1..4 index arrays,
   // 5..12 cur per bytes field, 13..20 alt per bytes field, 21/22 voxel keys,
-  // 23 voxel counts, 24 cluster-FPS slice + mailbox.  Bytes (0 = absent)
-  // and shared-memory placement bits.
-  uint64_t buf_bytes[25];
+  // 23 voxel counts, 24 cluster-FPS slice + mailbox, 25 voxel sort scratch
+  // (digit histograms + per-warp counts).  Bytes (0 = absent) and
+  // shared-memory placement bits.
+  uint64_t buf_bytes[26];
   uint32_t buf_smem_mask;
   int32_t min_blocks;       // k_cloud instantiation: 1 (128 regs) or 2 (64 regs)
   uint8_t* gscratch;        // global scratch (smem_mode 0), per CTA

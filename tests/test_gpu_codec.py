@@ -304,3 +304,20 @@ def test_fps_sizes_bit_exact(pcp, orc, rng, n, m):
         want = want.view(np.float32).reshape(-1, 3)
         assert st[i] == 0 and cnt[i] == m
         assert np.array_equal(od[i, :m].view(np.uint32), want.view(np.uint32)), i
+
+
+@pytest.mark.parametrize("vs,extent", [(0.05, 4.0), (1e-5, 20.0)])
+def test_voxel_sort_paths(pcp, orc, rng, vs, extent):
+    """Voxel/grid through both sorts: packed (key << index bits | index) words
+    with 8-bit digits, and the 64-bit key/index fallback when the keys need
+    ~21 bits per axis (1e-5 m voxels over 20 m)."""
+    from oracle.ffi import cloud
+    clouds = [rng.uniform(0, extent, (n, 3)).astype(np.float32) for n in (5000, 777, 1)]
+    clouds[0][100:200] = clouds[0][:100]  # duplicates share voxels
+    for kind in ("voxel", "grid_subsample"):
+        st, cnt, od = _apply_set(pcp, kind, {"voxel_size": vs, "origin": [0, 0, 0]}, clouds)
+        for i, c in enumerate(clouds):
+            want = orc.apply_map(kind, {"voxel_size": vs, "origin": [0, 0, 0]}, {"data": cloud(c)}, 0)["data"]
+            want = want.view(np.float32).reshape(-1, 3)
+            assert st[i] == 0 and cnt[i] == len(want), (kind, i)
+            assert np.array_equal(od[i, :len(want)].view(np.uint32), want.view(np.uint32)), (kind, i)
