@@ -424,6 +424,7 @@ struct Pipeline {
   bool force_serial_fy = false;
   bool lz4_timing = std::getenv("PCP_LZ4_TIMING") != nullptr;
   bool op_timing = std::getenv("PCP_OP_TIMING") != nullptr;  // per-op SM cycles (diagnostics)
+  bool no_fused_crc = std::getenv("PCP_NO_FUSED_CRC") != nullptr;  // experiment switch
   DevBuf d_op_cycles;
   std::vector<double> lz4_phase_cycles = std::vector<double>(4, 0.0);
   cudaStream_t stream = nullptr;        // wave compute (copies + kernels)
@@ -863,7 +864,7 @@ struct Pipeline {
       }
       // fused CRC only when this wave's samples tile the stored-raw payload
       // exactly once
-      bool fused = !(bh.flags & kFlagOuterLz4) && bh.pay_len == bh.raw_len;
+      bool fused = !(bh.flags & kFlagOuterLz4) && bh.pay_len == bh.raw_len && !no_fused_crc;
       uint64_t at = 0;
       for (uint32_t r = 0; fused && r < gr.sample_count; ++r) {
         if (hits[i][r] != 1 || gr.blob_ranges[r][0] != at) fused = false;

@@ -1187,10 +1187,40 @@ __device__ void decode_bytes(uint8_t* dst, const uint8_t* src, uint64_t len, boo
                              Smem& S) {
   const uint32_t t = threadIdx.x, nt = blockDim.x, lane = t & 31, w = t >> 5, nw = nt >> 5;
   if (!delta) {
-    const uint64_t nwords = len >> 2;
-    uint32_t* d32 = reinterpret_cast<uint32_t*>(dst);
-    for (uint64_t i = t; i < nwords; i += nt) d32[i] = dev::ld_u32_unaligned(src + 4 * i);
-    for (uint64_t i = (nwords << 2) + t; i < len; i += nt) dst[i] = src[i];
+    // 16-B stores built from aligned 4-B loads (funnel shift for the source
+    // misalignment), 4 per thread in flight: a CTA streaming a multi-MB blob
+    // is bound by loads in flight per SM, not by instructions
+    const uint64_t h0 = (16u - (reinterpret_cast<uintptr_t>(dst) & 15u)) & 15u;
+    const uint64_t head = h0 < len ? h0 : len;
+    for (uint64_t i = t; i < head; i += nt) dst[i] = src[i];  // dst may be 4-B aligned (output slots)
+    dst += head;
+    src += head;
+    len -= head;
+    const uintptr_t sa = reinterpret_cast<uintptr_t>(src);
+    const uint32_t sh = (uint32_t)(sa & 3u) * 8u;
+    const uint32_t* sw = reinterpret_cast<const uint32_t*>(sa & ~uintptr_t(3));
+    const uint64_t n16 = len >> 4;
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
+    for (uint64_t k0 = t; k0 < n16; k0 += 4 * (uint64_t)nt) {
+      uint32_t v[4][5];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint64_t k = k0 + (uint64_t)u * nt;
+        if (k < n16) {
+#pragma unroll
+          for (int e = 0; e < 5; ++e) v[u][e] = (e < 4 || sh) ? sw[4 * k + e] : 0u;  // <= 3 B past
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint64_t k = k0 + (uint64_t)u * nt;
+        if (k < n16)
+          d4[k] = sh ? make_uint4(__funnelshift_r(v[u][0], v[u][1], sh), __funnelshift_r(v[u][1], v[u][2], sh),
+                                  __funnelshift_r(v[u][2], v[u][3], sh), __funnelshift_r(v[u][3], v[u][4], sh))
+                     : make_uint4(v[u][0], v[u][1], v[u][2], v[u][3]);
+      }
+    }
+    for (uint64_t i = (n16 << 4) + t; i < len; i += nt) dst[i] = src[i];
     __syncthreads();
     return;
   }
