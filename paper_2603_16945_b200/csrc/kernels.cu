@@ -229,6 +229,7 @@ __global__ void __launch_bounds__(32) k_page_matches(uint8_t* raw, const PageRef
                                                      uint8_t* scratch, uint32_t n_todo,
                                                      long long* timing) {
   __shared__ __align__(16) uint8_t ring[lz4p::kRing];
+  __shared__ uint32_t pidx[lz4p::kDoubleSpan];
   for (uint32_t w = blockIdx.x; w < n_todo; w += gridDim.x) {
     const PageRef pg = pages[todo[w]];
     if (!(pg.flags & kFlagOuterLz4)) continue;
@@ -236,7 +237,7 @@ __global__ void __launch_bounds__(32) k_page_matches(uint8_t* raw, const PageRef
     if (sc.hdr[1] != 1u) continue;
     long long* tm = timing ? timing + 16 * (uint64_t)w + 8 : nullptr;  // [11] start, [12] end
     if (tm && threadIdx.x == 0) tm[3] = clock64();
-    lz4p::decode_matches(raw + pg.raw_dst, (uint32_t)pg.raw_len, sc, sc.hdr[0], ring, tm);
+    lz4p::decode_matches(raw + pg.raw_dst, (uint32_t)pg.raw_len, sc, sc.hdr[0], ring, pidx, tm);
   }
 }
 

@@ -41,6 +41,7 @@ constexpr uint32_t kStageBytes = kChunk + kStageTail + 32;  // + 16-B alignment 
 constexpr uint32_t kSmemWords = 72 + 2 * kChunk + (2 * kStageBytes) / 4;
 constexpr uint32_t kRingChunk = 4096;  // refill granule
 constexpr uint32_t kNone = 0xFFFFFFFFu;
+constexpr uint32_t kDoubleSpan = 2048;  // group output span resolved by pointer jumping
 
 // Per-page scratch layout (host computes the size with scratch_bytes()).
 __host__ __device__ inline uint32_t n_chunks(uint64_t pay) {
@@ -601,7 +602,8 @@ __device__ inline int32_t decode_prefix(const uint8_t* __restrict__ src, uint32_
 // recorded by decode_prefix, in order, through a shared-memory ring (`ring`:
 // kRing bytes).
 __device__ inline void decode_matches(uint8_t* __restrict__ dst, uint32_t raw_len, Scratch sc,
-                                      uint32_t M, uint8_t* ring, long long* tm = nullptr) {
+                                      uint32_t M, uint8_t* ring, uint32_t* pidx,
+                                      long long* tm = nullptr) {
   const uint32_t t = threadIdx.x & 31u;
   {
 
@@ -625,13 +627,26 @@ __device__ inline void decode_matches(uint8_t* __restrict__ dst, uint32_t raw_le
         }
       }
     };
+    // match records are prefetched one group ahead (their global-load
+    // latency would otherwise open every group)
+    uint32_t n_mo = 0, n_ml = 0, n_off = 1;
+    if (t < M) {
+      n_mo = sc.m_mo[t];
+      n_ml = sc.m_ml[t];
+      n_off = sc.m_off[t];
+    }
     for (uint32_t base = 0; base < M; base += 32) {
-      const uint32_t q = base + t;
-      uint32_t r_mo = 0, r_ml = 0, r_off = 1;
-      if (q < M) {
-        r_mo = sc.m_mo[q];
-        r_ml = sc.m_ml[q];
-        r_off = sc.m_off[q];
+      const uint32_t r_mo = n_mo, r_ml = n_ml, r_off = n_off;
+      {
+        const uint32_t nq = base + 32 + t;
+        n_mo = 0;
+        n_ml = 0;
+        n_off = 1;
+        if (nq < M) {
+          n_mo = sc.m_mo[nq];
+          n_ml = sc.m_ml[nq];
+          n_off = sc.m_off[nq];
+        }
       }
       const uint32_t cnt = min(32u, M - base);
       // ---- group fast path: one match per lane, in dependency waves -------
@@ -667,6 +682,56 @@ __device__ inline void decode_matches(uint8_t* __restrict__ dst, uint32_t raw_le
         const uint32_t a = r_mo - r_off;
         // every lane's source must be in the ring for the fast path
         const bool src_ok = !act || (a >= lo && r_mo + r_ml <= hi);
+        if (span_ok && __all_sync(0xffffffffu, src_ok) && pidx && g_end - g_first <= kDoubleSpan) {
+          // dense group: byte-level pointer jumping over its output span.
+          // src(b) = b - off inside a match (the forward copy's semantics,
+          // self-overlap included), b for literals; bytes below the span are
+          // final in the ring.  Doubling until every pointer reaches a final
+          // byte takes log2(chain depth) rounds instead of one wave per link.
+          const uint32_t g0 = g_first, L = g_end - g_first;
+          for (uint32_t b = t; b < L; b += 32) pidx[b] = g0 + b;
+          __syncwarp();
+          if (act)
+            for (uint32_t j = 0; j < r_ml; ++j) pidx[r_mo - g0 + j] = a + j;
+          __syncwarp();
+          for (int round = 0; round < 16; ++round) {  // depth <= L <= 2^11
+            bool ch = false;
+            for (uint32_t b0 = t; b0 < L; b0 += 128) {  // 4 bytes per lane in flight
+              uint32_t p[4], q[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const uint32_t b = b0 + 32 * u;
+                p[u] = b < L ? pidx[b] : 0u;
+              }
+#pragma unroll
+              for (int u = 0; u < 4; ++u) q[u] = (b0 + 32 * u < L && p[u] >= g0) ? pidx[p[u] - g0] : p[u];
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                if (q[u] != p[u]) {
+                  pidx[b0 + 32 * u] = q[u];
+                  ch = true;
+                }
+            }
+            __syncwarp();
+            if (!__any_sync(0xffffffffu, ch)) break;
+          }
+          // every final source is a literal of the span or a byte below it:
+          // those never change, so the gather has no read/write hazard
+          for (uint32_t b0 = t; b0 < L; b0 += 128) {
+            uint32_t p[4];
+            uint8_t v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) p[u] = b0 + 32 * u < L ? pidx[b0 + 32 * u] : g0 + b0 + 32 * u;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = p[u] != g0 + b0 + 32 * u ? ring[p[u] & (kRing - 1)] : 0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (p[u] != g0 + b0 + 32 * u) ring[(g0 + b0 + 32 * u) & (kRing - 1)] = v[u];
+          }
+          __syncwarp();
+          if (tm && t == 0) tm[7] += 1;
+          continue;
+        }
         if (span_ok && __all_sync(0xffffffffu, src_ok)) {
           const uint32_t ext_end = min(r_mo, a + r_ml);  // bytes read from earlier output
           uint32_t dep = 0;
@@ -777,7 +842,8 @@ __device__ inline int32_t decode_block(const uint8_t* __restrict__ src, uint32_t
                                        uint32_t* ctl, uint8_t* ring, long long* tm = nullptr) {
   const int32_t st = decode_prefix(src, n, dst, raw_len, sc, ctl, tm);
   if (st != kOk) return st;
-  if (threadIdx.x < 32) decode_matches(dst, raw_len, sc, ctl[1], ring, tm);
+  // phase 4 on warp 0; the skim's tables (ctl + 72) are free for the jump index
+  if (threadIdx.x < 32) decode_matches(dst, raw_len, sc, ctl[1], ring, ctl + 72, tm);
   __syncthreads();
   return kOk;
 }

@@ -52,8 +52,8 @@ int main(int argc, char** argv) {
     int st;
     cudaMemcpy(tm, d_tm, 128, cudaMemcpyDeviceToHost);
     cudaMemcpy(&st, d_st, 4, cudaMemcpyDeviceToHost);
-    printf("status %d  %.3f ms  skim %lld (walk %lld fill %lld)  phase3 %lld  matches %lld fast %lld slow %lld\n",
-           st, ms, tm[2] - tm[0], tm[8], tm[9], tm[3] - tm[2], tm[4] - tm[3], tm[5], tm[6]);
+    printf("status %d  %.3f ms  skim %lld (walk %lld fill %lld)  phase3 %lld  matches %lld jump %lld (rounds %lld, span bytes %lld) waves %lld slow %lld\n",
+           st, ms, tm[2] - tm[0], tm[8], tm[9], tm[3] - tm[2], tm[4] - tm[3], tm[7], tm[10], tm[11], tm[5], tm[6]);
   }
 #ifdef PCP_EXP_TRACE
   {
