@@ -627,108 +627,141 @@ __device__ inline void decode_matches(uint8_t* __restrict__ dst, uint32_t raw_le
         }
       }
     };
-    // match records are prefetched one group ahead (their global-load
-    // latency would otherwise open every group)
-    uint32_t n_mo = 0, n_ml = 0, n_off = 1;
-    if (t < M) {
-      n_mo = sc.m_mo[t];
-      n_ml = sc.m_ml[t];
-      n_off = sc.m_off[t];
-    }
-    for (uint32_t base = 0; base < M; base += 32) {
-      const uint32_t r_mo = n_mo, r_ml = n_ml, r_off = n_off;
-      {
-        const uint32_t nq = base + 32 + t;
-        n_mo = 0;
-        n_ml = 0;
-        n_off = 1;
-        if (nq < M) {
-          n_mo = sc.m_mo[nq];
-          n_ml = sc.m_ml[nq];
-          n_off = sc.m_off[nq];
-        }
+    // flush final chunks below g_first, refill the ring up to g_end; false if
+    // [g_first, g_end) cannot sit in the ring together with its sources
+    auto ensure_ring = [&](uint32_t g_first, uint32_t g_end) -> bool {
+      bool moved = false;
+      while (fl + kRingChunk <= g_first && fl + kRingChunk <= hi) {
+        move_chunk(fl, fl + kRingChunk, false);
+        fl += kRingChunk;
+        moved = true;
       }
-      const uint32_t cnt = min(32u, M - base);
-      // ---- group fast path: one match per lane, in dependency waves -------
-      {
-        const uint32_t g_lo = __shfl_sync(0xffffffffu, r_mo - r_off, 0);  // lowest source start (approx)
-        const uint32_t g_end = __shfl_sync(0xffffffffu, r_mo + r_ml, cnt - 1);
-        const uint32_t g_first = __shfl_sync(0xffffffffu, r_mo, 0);
-        // ensure ring holds [.., g_end): flush final chunks, refill
-        bool moved = false;
-        while (fl + kRingChunk <= g_first && fl + kRingChunk <= hi) {
-          move_chunk(fl, fl + kRingChunk, false);
-          fl += kRingChunk;
+      const bool span_ok = g_end - g_first + kRingChunk * 3 <= kRing;
+      if (span_ok) {
+        while (hi < g_end) {
+          const uint32_t end = min(hi + kRingChunk, raw_len);
+          while (fl + kRing < end) {
+            move_chunk(fl, fl + kRingChunk, false);
+            fl += kRingChunk;
+          }
+          __syncwarp();
+          move_chunk(hi, end, true);
+          hi = end;
           moved = true;
         }
-        const bool span_ok = g_end - g_first + kRingChunk * 3 <= kRing;
-        if (span_ok) {
-          while (hi < g_end) {
-            const uint32_t end = min(hi + kRingChunk, raw_len);
-            while (fl + kRing < end) {
-              move_chunk(fl, fl + kRingChunk, false);
-              fl += kRingChunk;
+      }
+      if (moved) __syncwarp();
+      return span_ok;
+    };
+    // byte-level pointer jumping over the output span [g0, g0 + L): src(b) =
+    // b - off inside a match (the forward copy's semantics, self-overlap
+    // included), b for literals; bytes below the span are final in the ring.
+    // Doubling until every pointer reaches a final byte takes log2(chain
+    // depth) rounds instead of one dependency wave per link.  The caller
+    // fills pidx with the matches' pointers after init_span.
+    auto init_span = [&](uint32_t g0, uint32_t L) {
+      for (uint32_t b = t; b < L; b += 32) pidx[b] = g0 + b;
+      __syncwarp();
+    };
+    auto jump_span = [&](uint32_t g0, uint32_t L) {
+      __syncwarp();
+      for (int round = 0; round < 16; ++round) {  // depth <= L <= 2^11
+        bool ch = false;
+        for (uint32_t b0 = t; b0 < L; b0 += 128) {  // 4 bytes per lane in flight
+          uint32_t p[4], q[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const uint32_t b = b0 + 32 * u;
+            p[u] = b < L ? pidx[b] : 0u;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) q[u] = (b0 + 32 * u < L && p[u] >= g0) ? pidx[p[u] - g0] : p[u];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (q[u] != p[u]) {
+              pidx[b0 + 32 * u] = q[u];
+              ch = true;
             }
-            __syncwarp();
-            move_chunk(hi, end, true);
-            hi = end;
-            moved = true;
+        }
+        __syncwarp();
+        if (!__any_sync(0xffffffffu, ch)) break;
+      }
+      // every final source is a literal of the span or a byte below it:
+      // those never change, so the gather has no read/write hazard
+      for (uint32_t b0 = t; b0 < L; b0 += 128) {
+        uint32_t p[4];
+        uint8_t v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) p[u] = b0 + 32 * u < L ? pidx[b0 + 32 * u] : g0 + b0 + 32 * u;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = p[u] != g0 + b0 + 32 * u ? ring[p[u] & (kRing - 1)] : 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (p[u] != g0 + b0 + 32 * u) ring[(g0 + b0 + 32 * u) & (kRing - 1)] = v[u];
+      }
+      __syncwarp();
+    };
+    uint32_t step = 32;
+    for (uint32_t base = 0; base < M; base += step) {
+      step = 32;
+      // ---- super-group: up to 8 x 32 consecutive matches in one jump pass
+      // when their output span is <= kDoubleSpan (dense label regions)
+      uint32_t smo[8], sml[8], soff[8];
+      const uint32_t cntS = min(256u, M - base);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t q = base + 32 * k + t;
+        const bool v = q < base + cntS;
+        smo[k] = v ? sc.m_mo[q] : 0u;
+        sml[k] = v ? sc.m_ml[q] : 0u;
+        soff[k] = v ? sc.m_off[q] : 1u;
+      }
+      if (pidx && cntS > 32) {
+        const uint32_t lastk = (cntS - 1) >> 5, lastl = (cntS - 1) & 31u;
+        uint32_t e_last = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if ((uint32_t)k == lastk) e_last = smo[k] + sml[k];
+        const uint32_t s_end = __shfl_sync(0xffffffffu, e_last, lastl);
+        const uint32_t s_first = __shfl_sync(0xffffffffu, smo[0], 0);
+        if (s_end - s_first <= kDoubleSpan && ensure_ring(s_first, s_end)) {
+          const uint32_t lo = hi > kRing ? hi - kRing : 0u;
+          bool ok = true;
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            if (32u * k + t < cntS) ok = ok && smo[k] - soff[k] >= lo && smo[k] + sml[k] <= hi;
+          if (__all_sync(0xffffffffu, ok)) {
+            const uint32_t L = s_end - s_first;
+            init_span(s_first, L);
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              if (32u * k + t < cntS)
+                for (uint32_t j = 0; j < sml[k]; ++j) pidx[smo[k] - s_first + j] = smo[k] - soff[k] + j;
+            jump_span(s_first, L);
+            if (tm && t == 0) tm[7] += 1;
+            step = cntS;
+            continue;
           }
         }
-        if (moved) __syncwarp();
-        (void)g_lo;
+      }
+      const uint32_t r_mo = smo[0], r_ml = sml[0], r_off = soff[0];
+      const uint32_t cnt = min(32u, M - base);
+      // ---- group fast path: one match per lane ----------------------------
+      {
+        const uint32_t g_end = __shfl_sync(0xffffffffu, r_mo + r_ml, cnt - 1);
+        const uint32_t g_first = __shfl_sync(0xffffffffu, r_mo, 0);
+        const bool span_ok = ensure_ring(g_first, g_end);
         const uint32_t lo = hi > kRing ? hi - kRing : 0u;
         const bool act = t < cnt;
         const uint32_t a = r_mo - r_off;
         // every lane's source must be in the ring for the fast path
         const bool src_ok = !act || (a >= lo && r_mo + r_ml <= hi);
         if (span_ok && __all_sync(0xffffffffu, src_ok) && pidx && g_end - g_first <= kDoubleSpan) {
-          // dense group: byte-level pointer jumping over its output span.
-          // src(b) = b - off inside a match (the forward copy's semantics,
-          // self-overlap included), b for literals; bytes below the span are
-          // final in the ring.  Doubling until every pointer reaches a final
-          // byte takes log2(chain depth) rounds instead of one wave per link.
-          const uint32_t g0 = g_first, L = g_end - g_first;
-          for (uint32_t b = t; b < L; b += 32) pidx[b] = g0 + b;
-          __syncwarp();
+          // dense group: pointer jumping (see jump_span)
+          init_span(g_first, g_end - g_first);
           if (act)
-            for (uint32_t j = 0; j < r_ml; ++j) pidx[r_mo - g0 + j] = a + j;
-          __syncwarp();
-          for (int round = 0; round < 16; ++round) {  // depth <= L <= 2^11
-            bool ch = false;
-            for (uint32_t b0 = t; b0 < L; b0 += 128) {  // 4 bytes per lane in flight
-              uint32_t p[4], q[4];
-#pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                const uint32_t b = b0 + 32 * u;
-                p[u] = b < L ? pidx[b] : 0u;
-              }
-#pragma unroll
-              for (int u = 0; u < 4; ++u) q[u] = (b0 + 32 * u < L && p[u] >= g0) ? pidx[p[u] - g0] : p[u];
-#pragma unroll
-              for (int u = 0; u < 4; ++u)
-                if (q[u] != p[u]) {
-                  pidx[b0 + 32 * u] = q[u];
-                  ch = true;
-                }
-            }
-            __syncwarp();
-            if (!__any_sync(0xffffffffu, ch)) break;
-          }
-          // every final source is a literal of the span or a byte below it:
-          // those never change, so the gather has no read/write hazard
-          for (uint32_t b0 = t; b0 < L; b0 += 128) {
-            uint32_t p[4];
-            uint8_t v[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) p[u] = b0 + 32 * u < L ? pidx[b0 + 32 * u] : g0 + b0 + 32 * u;
-#pragma unroll
-            for (int u = 0; u < 4; ++u) v[u] = p[u] != g0 + b0 + 32 * u ? ring[p[u] & (kRing - 1)] : 0;
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-              if (p[u] != g0 + b0 + 32 * u) ring[(g0 + b0 + 32 * u) & (kRing - 1)] = v[u];
-          }
-          __syncwarp();
+            for (uint32_t j = 0; j < r_ml; ++j) pidx[r_mo - g_first + j] = a + j;
+          jump_span(g_first, g_end - g_first);
           if (tm && t == 0) tm[7] += 1;
           continue;
         }
