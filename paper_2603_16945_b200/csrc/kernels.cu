@@ -1928,7 +1928,6 @@ __global__ void k_decode_pages(const uint8_t* bytes, const uint64_t* page_off, u
   __shared__ int32_t sst;
   __shared__ uint32_t scount;
   __shared__ int32_t st_sh;
-  __shared__ __align__(16) uint8_t ring[lz4p::kRing];
   for (int i = threadIdx.x; i < 256; i += blockDim.x) tab[i] = crc::table_entry(i);
   __syncthreads();
   for (uint32_t pi = blockIdx.x; pi < n_pages; pi += gridDim.x) {
@@ -1949,7 +1948,7 @@ __global__ void k_decode_pages(const uint8_t* bytes, const uint64_t* page_off, u
         int32_t r = kCorruptPage;
         if (pay_len < 0xFFFFFFF0ull && raw_len < 0xFFFFFFF0ull) {
           const lz4p::Scratch sc = lz4p::carve_scratch(scratch + scratch_off[pi], pay_len);
-          r = lz4p::decode_block(pay, (uint32_t)pay_len, dst, (uint32_t)raw_len, sc, ctl, ring);
+          r = lz4p::decode_block(pay, (uint32_t)pay_len, dst, (uint32_t)raw_len, sc, ctl);
           if (r < 0) {
             if (threadIdx.x < 32) {
               const int32_t q = warp_lz4_decode(pay, pay_len, dst, raw_len, seqs, &sst, &scount);

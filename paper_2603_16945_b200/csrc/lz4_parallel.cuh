@@ -38,7 +38,9 @@ constexpr uint32_t kChunk = 2048;      // compressed bytes per skim window / par
 constexpr uint32_t kRing = 16384;      // shared-memory output window (bytes)
 constexpr uint32_t kStageTail = 128;   // staged bytes past a window for its last tokens
 constexpr uint32_t kStageBytes = kChunk + kStageTail + 32;  // + 16-B alignment slack (TMA)
-constexpr uint32_t kSmemWords = 72 + 2 * kChunk + (2 * kStageBytes) / 4;
+// ctl[0..72) control; jump tables d|d2 [2][kChunk] u32; stage buffers; d4
+// tables [2][kChunk] u16; window token positions [2][kChunk] u16
+constexpr uint32_t kSmemWords = 72 + 2 * kChunk + (2 * kStageBytes) / 4 + kChunk + kChunk;
 constexpr uint32_t kRingChunk = 4096;  // refill granule
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 constexpr uint32_t kDoubleSpan = 2048;  // group output span resolved by pointer jumping
@@ -307,6 +309,12 @@ __device__ inline int32_t decode_prefix(const uint8_t* __restrict__ src, uint32_
     // per window buffer b: jt[b][kChunk] u32 = d (low 16 bits) | d2 << 16
     uint32_t* jt = ctl + 72;
     uint8_t* wb = reinterpret_cast<uint8_t*>(ctl + 72 + 2 * kChunk);  // 2 x kStageBytes bytes
+    // four-token jumps d4 = d2(p) + d2(p + d2(p)) (u16, 0 = none): [2][kChunk]
+    uint16_t* j4 = reinterpret_cast<uint16_t*>(ctl + 72 + 2 * kChunk + (2 * kStageBytes) / 4);
+    // window-relative token positions [2][kChunk] (u16): the walker writes
+    // window w's, the fill warps copy them to sc.tokpos (coalesced) after the
+    // next barrier — a lone thread's global stores would bound the walk
+    uint16_t* tw = j4 + 2 * kChunk;
     uint64_t* sbar = reinterpret_cast<uint64_t*>(ctl + 64);     // stage barriers (ctl[64..67])
     const uintptr_t sbase = reinterpret_cast<uintptr_t>(src);
     // window w's bytes [c0, min(c0 + kChunk + kStageTail, n)) as the 16-B
@@ -373,6 +381,18 @@ __device__ inline int32_t decode_prefix(const uint8_t* __restrict__ src, uint32_
         tab2[2 * lp] = (uint16_t)r;
       }
     };
+    auto fill4 = [&](uint32_t w, const uint32_t* tab32, uint16_t* t4, uint32_t tid, uint32_t nthr) {
+      const uint32_t c0 = w * kChunk, len = min(c0 + kChunk, n) - c0;
+      for (uint32_t lp = tid; lp < len; lp += nthr) {
+        const uint32_t b = tab32[lp] >> 16;
+        uint32_t r = 0;
+        if (b && lp + b < len) {
+          const uint32_t b2 = tab32[lp + b] >> 16;
+          if (b2 && b + b2 < 0xFFFFu) r = b + b2;
+        }
+        t4[lp] = (uint16_t)r;
+      }
+    };
     if (t == 0) {
       dev::mbar_init(&sbar[0], 1);
       dev::mbar_init(&sbar[1], 1);
@@ -388,20 +408,21 @@ __device__ inline int32_t decode_prefix(const uint8_t* __restrict__ src, uint32_
     __syncthreads();
     fill2(0, jt, t, nt);
     __syncthreads();
+    fill4(0, jt, j4, t, nt);
+    __syncthreads();
     long long a_walk = 0, a_fill = 0;  // PCP_LZ4_TIMING
     uint32_t pos = 0;  // walker state (thread 0)
     uint32_t err = 0, done = 0, nseq = 0;
     const uint32_t cap_seq = (uint32_t)match_capacity(n);
     for (uint32_t w = 0; w < nch; ++w) {
-#ifdef PCP_EXP_TRACE
-      if (tm && t == 0 && w < 1000) {
-        tm[16 + w] = clock64();
-        tm[1040 + w] = nseq;
-        tm[2064 + w] = pos;
-      }
-#endif
       if (t >= 32) {
         const long long f0 = (tm && t == 32) ? clock64() : 0;
+        if (w > 0) {  // window w-1's token positions -> global
+          const uint32_t pb = (w - 1) & 1u, cnt = ctl[50 + pb], base = ctl[52 + pb];
+          const uint32_t c0p = (w - 1) * kChunk;
+          for (uint32_t i = t - 32; i < cnt; i += nt - 32)
+            if (base + i < cap_seq) sc.tokpos[base + i] = c0p + tw[pb * kChunk + i];
+        }
         // window w's buffer was last read by fill(w) before the previous
         // barrier: refill it with window w+2 (async), then fill window w+1
         if (t == 32 && w + 2 < nch) {
@@ -414,37 +435,45 @@ __device__ inline int32_t decode_prefix(const uint8_t* __restrict__ src, uint32_
           fill(w + 1, tb, t - 32, nt - 32);
           named_sync_fill(nt - 32);
           fill2(w + 1, tb, t - 32, nt - 32);
+          named_sync_fill(nt - 32);
+          fill4(w + 1, tb, j4 + ((w + 1) & 1u) * kChunk, t - 32, nt - 32);
         }
         if (tm && t == 32) a_fill += clock64() - f0;
       } else if (t == 0) {
         const long long w0 = tm ? clock64() : 0;
         const uint32_t* tab = jt + (w & 1u) * kChunk;
+        const uint16_t* t4 = j4 + (w & 1u) * kChunk;
         const uint32_t c0 = w * kChunk, len = min(c0 + kChunk, n) - c0;
+        uint16_t* tr = tw + (w & 1u) * kChunk;
+        uint32_t k = 0;  // tokens of this window (all start inside it)
         if (!done && pos < c0 + len) {
-          uint32_t* tp = sc.tokpos;
           uint32_t lp = pos - c0;
           while (true) {
-            // hot loop: one LDS per one or two tokens, no taken branch
+            // hot loop: one dependent LDS per one, two or four tokens
             uint32_t x = tab[lp];
             while ((x & 0xFFFFu) != 0xFFFFu) {
               const uint32_t a = x & 0xFFFFu, b = x >> 16;
-              if (nseq < cap_seq) tp[nseq] = c0 + lp;
-              if (b && nseq + 1 < cap_seq) tp[nseq + 1] = c0 + lp + a;
-              nseq += b ? 2u : 1u;
-              lp += b ? b : a;
-#ifdef PCP_EXP_TRACE
-              if (tm && w < 1000) tm[3088 + w] += b ? 1 : 0x100000;
-#endif
+              const uint32_t f = t4[lp];  // four-token jump (0: none)
+              if (f) {  // tokens lp, lp+a, lp+b, lp+b+d(lp+b); next at lp+f
+                const uint32_t a2 = tab[lp + b] & 0xFFFFu;  // off the lp chain
+                tr[k] = (uint16_t)lp;
+                tr[k + 1] = (uint16_t)(lp + a);
+                tr[k + 2] = (uint16_t)(lp + b);
+                tr[k + 3] = (uint16_t)(lp + b + a2);
+                k += 4;
+                lp += f;
+              } else {
+                tr[k] = (uint16_t)lp;
+                if (b) tr[k + 1] = (uint16_t)(lp + a);
+                k += b ? 2u : 1u;
+                lp += b ? b : a;
+              }
               if (lp >= len) break;
               x = tab[lp];
             }
             if (lp >= len) break;
             // entry 0xFFFF: parse this position exactly from global
-#ifdef PCP_EXP_TRACE
-            if (tm && w < 1000) tm[3088 + w] += 1ll << 40;
-#endif
-            if (nseq < cap_seq) tp[nseq] = c0 + lp;
-            ++nseq;
+            tr[k++] = (uint16_t)lp;
             Seq sq;
             if (!parse_seq(src, n, c0 + lp, sq)) {
               err = done = 1;
@@ -459,9 +488,17 @@ __device__ inline int32_t decode_prefix(const uint8_t* __restrict__ src, uint32_
           }
           pos = done ? n : c0 + lp;
         }
+        ctl[50 + (w & 1u)] = k;
+        ctl[52 + (w & 1u)] = nseq;
+        nseq += k;
         if (tm) a_walk += clock64() - w0;
       }
       __syncthreads();
+    }
+    {  // the last window's token positions -> global
+      const uint32_t pb = (nch - 1) & 1u, cnt = ctl[50 + pb], base = ctl[52 + pb];
+      for (uint32_t i = t; i < cnt; i += nt)
+        if (base + i < cap_seq) sc.tokpos[base + i] = (nch - 1) * kChunk + tw[pb * kChunk + i];
     }
     if (tm && t == 0) tm[8] = a_walk;
     if (tm && t == 32) tm[9] = a_fill;
@@ -869,13 +906,16 @@ __device__ inline void decode_matches(uint8_t* __restrict__ dst, uint32_t raw_le
   if (tm && t == 0) tm[4] = clock64();
 }
 
-// Whole page with the whole CTA (phases 1-4; phase 4 on warp 0).
+// Whole page with the whole CTA (phases 1-4; phase 4 on warp 0).  Phase 4
+// reuses the skim's tables (dead by then): the jump index at ctl + 72, the
+// ring after it.
+static_assert(72 + kDoubleSpan + kRing / 4 <= kSmemWords, "phase-4 ring must fit in ctl");
 __device__ inline int32_t decode_block(const uint8_t* __restrict__ src, uint32_t n,
                                        uint8_t* __restrict__ dst, uint32_t raw_len, Scratch sc,
-                                       uint32_t* ctl, uint8_t* ring, long long* tm = nullptr) {
+                                       uint32_t* ctl, long long* tm = nullptr) {
   const int32_t st = decode_prefix(src, n, dst, raw_len, sc, ctl, tm);
   if (st != kOk) return st;
-  // phase 4 on warp 0; the skim's tables (ctl + 72) are free for the jump index
+  uint8_t* ring = reinterpret_cast<uint8_t*>(ctl + 72 + kDoubleSpan);
   if (threadIdx.x < 32) decode_matches(dst, raw_len, sc, ctl[1], ring, ctl + 72, tm);
   __syncthreads();
   return kOk;

@@ -13,9 +13,8 @@ using namespace pcp;
 __global__ void k(const uint8_t* src, uint32_t n, uint8_t* dst, uint32_t raw, uint8_t* scr,
                   long long* tm, int* st) {
   __shared__ __align__(16) uint32_t ctl[lz4p::kSmemWords];
-  __shared__ __align__(16) uint8_t ring[lz4p::kRing];
   lz4p::Scratch sc = lz4p::carve_scratch(scr, n);
-  int r = lz4p::decode_block(src, n, dst, raw, sc, ctl, ring, tm);
+  int r = lz4p::decode_block(src, n, dst, raw, sc, ctl, tm);
   if (threadIdx.x == 0) *st = r;
 }
 
