@@ -420,6 +420,8 @@ struct Pipeline {
   std::vector<Entry> index, walk;
   bool resident = true;
   uint32_t wave_batches = 0;
+  uint32_t n_slots = 4;  // wave slots (streams): n_slots - 1 waves in flight while one is served
+  bool slots_set = false;
   uint64_t epochs = 1;
   bool force_serial_fy = false;
   bool lz4_timing = std::getenv("PCP_LZ4_TIMING") != nullptr;
@@ -486,6 +488,10 @@ struct Pipeline {
       epochs = o.value("epochs", uint64_t{1});
       resident = o.value("resident", true);
       wave_batches = o.value("wave_batches", 0u);
+      if (o.contains("slots")) {
+        n_slots = std::max(2u, std::min(8u, o.value("slots", n_slots)));
+        slots_set = true;
+      }
       force_serial_fy = o.value("force_serial_fy", false);
     }
     h = read_header(primary);
@@ -511,7 +517,16 @@ struct Pipeline {
     d_shift.ensure(shift.size() * 4);
     CK(cudaMemcpyAsync(d_shift.p, shift.data(), shift.size() * 4, cudaMemcpyHostToDevice, stream));
     CK(cudaStreamSynchronize(stream));
-    slots.resize(3);
+    if (const char* e = std::getenv("PCP_SLOTS")) {
+      n_slots = std::max(2, std::min(8, std::atoi(e)));
+      slots_set = true;
+    }
+    // default: 4 slots (3 waves in flight: the LZ4 match phase of one wave
+    // overlaps the decode / k_cloud of the others), fewer when the per-CTA
+    // global slabs of large-cloud chains would exceed ~48 GB
+    if (!slots_set && proto.gscratch_per_cta)
+      while (n_slots > 2 && (uint64_t)n_slots * proto.gscratch_per_cta * grid > (48ull << 30)) --n_slots;
+    slots.resize(n_slots);
     for (auto& w : slots) {
       CK(cudaStreamCreateWithFlags(&w.stream, cudaStreamNonBlocking));
       for (size_t pi = 0; pi < plan.size() && plan[pi].first == 0; ++pi) launch(w, pi, true);
@@ -1183,6 +1198,7 @@ struct Pipeline {
            {"launches", launches},
            {"grid", grid},
            {"threads", threads},
+           {"slots", (uint64_t)slots.size()},
            {"smem_bytes", smem},
            {"smem_mode", proto.smem_mode},
            {"cap_points", proto.cap_points},
