@@ -402,6 +402,7 @@ __device__ inline int32_t decode_prefix(const uint8_t* __restrict__ src, uint32_
     if (t == 0) {
       stage_async(0);
       if (nch > 1) stage_async(1);
+      ctl[54] = 0;  // walker position at the start of window w: ctl[54 + (w & 1)]
     }
     dev::mbar_wait(&sbar[0], 0);
     fill(0, jt, t, nt);
@@ -429,9 +430,14 @@ __device__ inline int32_t decode_prefix(const uint8_t* __restrict__ src, uint32_
           dev::fence_proxy_async();
           stage_async(w + 2);
         }
-        if (w + 1 < nch) {
+        // a window the walker has already passed (inside a long literal, or
+        // after the last sequence) is never read: skip its tables
+        // (uniform across the fill warps: the walker publishes the next
+        // window's start position in the other parity slot)
+        const bool need = ctl[54 + (w & 1u)] < (w + 2) * kChunk;
+        if (w + 1 < nch) dev::mbar_wait(&sbar[(w + 1) & 1u], ((w + 1) >> 1) & 1u);
+        if (w + 1 < nch && need) {
           uint32_t* tb = jt + ((w + 1) & 1u) * kChunk;
-          dev::mbar_wait(&sbar[(w + 1) & 1u], ((w + 1) >> 1) & 1u);
           fill(w + 1, tb, t - 32, nt - 32);
           named_sync_fill(nt - 32);
           fill2(w + 1, tb, t - 32, nt - 32);
@@ -491,6 +497,7 @@ __device__ inline int32_t decode_prefix(const uint8_t* __restrict__ src, uint32_
         ctl[50 + (w & 1u)] = k;
         ctl[52 + (w & 1u)] = nseq;
         nseq += k;
+        ctl[54 + ((w + 1) & 1u)] = pos;  // read by the fill warps in iteration w+1
         if (tm) a_walk += clock64() - w0;
       }
       __syncthreads();
