@@ -196,6 +196,11 @@ int pcp_malloc(void** d_ptr, size_t n);
 int pcp_free(void* d_ptr);
 int pcp_memcpy_h2d(void* d_dst, const void* h_src, size_t n, void* stream);
 int pcp_memcpy_d2h(void* h_dst, const void* d_src, size_t n, void* stream);
+/* Asynchronous variant: enqueues the copy on `stream` (use the batch's
+ * pcp_batch.stream / pcp_pipeline_stream) and returns; the data is in h_dst
+ * after pcp_stream_sync(stream).  The pipeline will not reuse a batch's
+ * device buffers before copies enqueued on its serve stream complete. */
+int pcp_memcpy_d2h_async(void* h_dst, const void* d_src, size_t n, void* stream);
 int pcp_stream_sync(void* stream);
 
 #ifdef __cplusplus

@@ -81,6 +81,7 @@ def lib():
         L.pcp_pipeline_stats.argtypes = [C.c_void_p]
         L.pcp_pipeline_close.argtypes = [C.c_void_p]
         L.pcp_memcpy_d2h.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]
+        L.pcp_memcpy_d2h_async.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]
         L.pcp_memcpy_h2d.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]
         L.pcp_device_info.argtypes = [C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int),
                                       C.POINTER(C.c_int)]

@@ -394,6 +394,7 @@ struct Wave {
   bool launched = false;
   cudaStream_t stream = nullptr;  // one stream per slot: consecutive waves overlap
   cudaEvent_t done = nullptr, k0 = nullptr, k1 = nullptr, d0 = nullptr, d1 = nullptr;
+  cudaEvent_t served = nullptr;  // serve stream passed this wave's last batch (user copies enqueued)
   uint64_t decode_alg_bytes = 0;  // payload + raw bytes of the pages k_page_decode handles
   DevBuf gscratch;                // k_cloud global slab (smem_mode 0), per slot
   // device
@@ -472,6 +473,7 @@ struct Pipeline {
       if (w.k1) cudaEventDestroy(w.k1);
       if (w.d0) cudaEventDestroy(w.d0);
       if (w.d1) cudaEventDestroy(w.d1);
+      if (w.served) cudaEventDestroy(w.served);
     }
     if (stream) cudaStreamDestroy(stream);
     if (serve_stream) cudaStreamDestroy(serve_stream);
@@ -536,6 +538,8 @@ struct Pipeline {
       CK(cudaEventCreate(&w.k1));
       CK(cudaEventCreate(&w.d0));
       CK(cudaEventCreate(&w.d1));
+      CK(cudaEventCreateWithFlags(&w.served, cudaEventDisableTiming));
+      CK(cudaEventRecord(w.served, serve_stream));
     }
   }
 
@@ -794,6 +798,9 @@ struct Pipeline {
 
   // ---- wave construction ---------------------------------------------------
   void launch(Wave& w, size_t pi, bool dry = false) {
+    // the slot's previous wave may still be read by copies the user enqueued
+    // on the serve stream (pcp_memcpy_d2h_async): overwrite after them
+    if (!dry && w.served) CK(cudaStreamWaitEvent(w.stream, w.served, 0));
     w.epoch = plan[pi].first;
     w.pos0 = plan[pi].second;
     w.n = plan_n[pi];
@@ -831,23 +838,40 @@ struct Pipeline {
     std::vector<CrcWindow> wins;
     uint64_t raw_at = 0, vals_at = 0;
     uint32_t rec_at = 0;
-    // staged mode: copy the wave's pages into a device staging buffer
-    std::vector<std::pair<uint64_t, uint64_t>> runs;  // (store off, len)
+    // staged mode: copy the wave's pages into a device staging buffer.  A
+    // wave's pages are consecutive groups of a few slices, so their byte
+    // ranges are sorted and merged (gaps <= 64 KiB copied along): a handful
+    // of large H2D copies per wave instead of two per group.
+    std::vector<std::pair<uint64_t, uint64_t>> runs;  // (store off, len), 16-B aligned
     auto page_src = [&](uint32_t slice, uint64_t off) { return slice_base[slice] + off; };
     uint64_t stage_at = 64;
     std::vector<uint64_t> stage_off(2 * ng);
+    struct PRun {
+      uint64_t lo, hi;
+      uint32_t page;
+    };
+    std::vector<PRun> prs;
     for (uint32_t i = 0; i < ng; ++i) {
       const Group& gr = h.groups[groups[i]];
       for (int kind = 0; kind < 2; ++kind) {
         const uint64_t so = page_src(gr.slice, kind ? gr.block_off : gr.scalar_off);
         const uint64_t len = kind ? gr.block_len : gr.scalar_len;
-        if (!resident) {
-          stage_off[kind * ng + i] = stage_at + (so & 15);
-          runs.push_back({so & ~uint64_t(15), align16((so & 15) + len)});
-          stage_at += align16((so & 15) + len) + 64;
-        } else {
-          stage_off[kind * ng + i] = so;
-        }
+        if (!resident) prs.push_back({so, so + len, (uint32_t)(kind * ng + i)});
+        else stage_off[kind * ng + i] = so;
+      }
+    }
+    if (!resident && !prs.empty()) {
+      std::sort(prs.begin(), prs.end(), [](const PRun& x, const PRun& y) { return x.lo < y.lo; });
+      size_t k = 0;
+      while (k < prs.size()) {
+        const uint64_t lo = prs[k].lo & ~uint64_t(15);
+        uint64_t hi = align16(prs[k].hi);
+        size_t e = k + 1;
+        while (e < prs.size() && prs[e].lo <= hi + 65536) hi = std::max(hi, align16(prs[e].hi)), ++e;
+        for (size_t q = k; q < e; ++q) stage_off[prs[q].page] = stage_at + (prs[q].lo - lo);
+        runs.push_back({lo, hi - lo});
+        stage_at += (hi - lo) + 64;
+        k = e;
       }
     }
     for (uint32_t i = 0; i < ng; ++i) {
@@ -1105,7 +1129,10 @@ struct Pipeline {
               lz4_phase_cycles[ph] = std::max(lz4_phase_cycles[ph], c);
             }
       }
-      if (cur >= 0) slots[cur].launched = false;
+      if (cur >= 0) {
+        CK(cudaEventRecord(slots[cur].served, serve_stream));
+        slots[cur].launched = false;
+      }
       cur = nxt;
       served = 0;
       clouds += wn.n;
@@ -1475,6 +1502,9 @@ int pcp_memcpy_d2h(void* h, const void* d, size_t n, void* st) {
     CK(cudaMemcpyAsync(h, d, n, cudaMemcpyDeviceToHost, (cudaStream_t)st));
     CK(cudaStreamSynchronize((cudaStream_t)st));
   });
+}
+int pcp_memcpy_d2h_async(void* h, const void* d, size_t n, void* st) {
+  return guarded([&] { CK(cudaMemcpyAsync(h, d, n, cudaMemcpyDeviceToHost, (cudaStream_t)st)); });
 }
 int pcp_stream_sync(void* st) {
   return guarded([&] { CK(cudaStreamSynchronize((cudaStream_t)st)); });
