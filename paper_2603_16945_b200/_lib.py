@@ -189,11 +189,15 @@ class Pipeline:
     path).  ``graph`` is the reference graph JSON (dict or str)."""
 
     def __init__(self, primary, graph, ids=None, device: int = 0, epochs: int = 1,
-                 resident: bool = True, wave_batches: int = 0, force_serial_fy: bool = False):
+                 resident: bool = True, wave_batches: int = 0, force_serial_fy: bool = False,
+                 slots: int | None = None):
         L = lib()
         g = graph if isinstance(graph, str) else json.dumps(graph)
-        opts = json.dumps({"epochs": epochs, "resident": resident, "wave_batches": wave_batches,
-                           "force_serial_fy": force_serial_fy})
+        o = {"epochs": epochs, "resident": resident, "wave_batches": wave_batches,
+             "force_serial_fy": force_serial_fy}
+        if slots is not None:
+            o["slots"] = slots
+        opts = json.dumps(o)
         h = C.c_void_p()
         if ids is None:
             p, n = None, 0

@@ -191,3 +191,33 @@ def test_cluster_fps_chain_parity(pcp, ref, orc, tmp_path):
     got = _run(pcp, primary, g)
     want = expected_run(ref, orc, primary, g)
     assert_batches_equal(got, want, float_fields=tolerant_fields(g))
+
+
+@pytest.mark.parametrize("slots", [2, 4])
+def test_async_d2h_matches_sync(pcp, tmp_path, slots):
+    """pcp_memcpy_d2h_async of every batch with one sync at the end equals the
+    synchronous copies: small waves and few slots force slot reuse while
+    copies of older batches are still queued (the 'served' event guard)."""
+    import torch
+    from paper_2603_16945_b200 import synth
+    primary = _ds(pcp, tmp_path, "shapenet", 96, group=8, n_points=700)
+    g = synth.graph(synth.CHAINS["shapenet_part"][:3], batch_size=4)
+    want = [b.to_host() for b in pcp.Pipeline(primary, g, wave_batches=2, slots=slots)]
+    L = pcp.lib()
+    got, keep = [], []
+    p = pcp.Pipeline(primary, g, wave_batches=2, slots=slots)
+    for b in p:
+        host = {}
+        for name, (kind, ptr, nbytes, offs, _) in b.fields.items():
+            buf = torch.empty(max(nbytes, 1), dtype=torch.uint8, pin_memory=True)  # truly async
+            assert L.pcp_memcpy_d2h_async(buf.data_ptr(), ptr, nbytes, b.stream) == 0
+            host[name] = (buf, nbytes, offs)
+            keep.append(buf)
+        got.append(host)
+    assert L.pcp_stream_sync(p.stream) == 0
+    p.close()
+    assert len(got) == len(want)
+    for gb, wb in zip(got, want):
+        for name in wb:
+            buf, nbytes, _ = gb[name]
+            assert np.array_equal(buf.numpy()[:nbytes], wb[name][0].view(np.uint8)), name
