@@ -220,8 +220,11 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=0, help="clouds per CPU step")
+    ap.add_argument("--batch", type=int, default=0, help="override the config's batch size (diagnostics)")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
+    if args.batch:
+        cfg["batch"] = args.batch
     if args.clouds_per_gpu:
         cfg["clouds"] = args.clouds_per_gpu
     rank, world, local = env()

@@ -1333,9 +1333,15 @@ __device__ int radix_sort8(uint64_t* w0, uint64_t* w1, uint32_t n, uint32_t lo, 
   const uint32_t np = (hi - lo + 7) / 8;
   for (uint32_t i = t; i < np * 256; i += nt) hist[i] = 0;
   __syncthreads();
-  for (uint32_t i = t; i < n; i += nt) {
-    const uint64_t x = w0[i];
-    for (uint32_t p = 0; p < np; ++p) atomicAdd(&hist[p * 256 + (uint32_t)((x >> (lo + 8 * p)) & 255u)], 1u);
+  for (uint32_t i0 = t; i0 < n; i0 += 4 * nt) {  // 4 words per thread in flight
+    uint64_t x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) x[u] = i0 + u * nt < n ? w0[i0 + u * nt] : 0ull;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (i0 + u * nt < n)
+        for (uint32_t p = 0; p < np; ++p)
+          atomicAdd(&hist[p * 256 + (uint32_t)((x[u] >> (lo + 8 * p)) & 255u)], 1u);
   }
   __syncthreads();
   if (w < np) {  // exclusive scan of pass w's histogram: 8 bins per lane
@@ -1367,16 +1373,33 @@ __device__ int radix_sort8(uint64_t* w0, uint64_t* w1, uint32_t n, uint32_t lo, 
     for (uint32_t d = t; d < 256; d += nt) base[d] = hist[p * 256 + d];
     uint32_t cb = 0;
     __syncthreads();
-    for (uint32_t t0 = 0; t0 < n; t0 += nt) {
-      const uint32_t i = t0 + t;
-      const bool valid = i < n;
-      const uint64_t x = valid ? src[i] : 0ull;
-      const uint32_t d = valid ? (uint32_t)((x >> sh) & 255u) : 256u;
+    // tiles of 4 x blockDim words; warp w owns the contiguous 128 words
+    // [t0 + 128w, t0 + 128w + 128), ranked in four 32-word sub-tiles with a
+    // running per-warp digit count, so the tile order (warp, sub-tile, lane)
+    // is element order and the sort stays stable
+    const uint32_t tile = 4 * nt;
+    for (uint32_t t0 = 0; t0 < n; t0 += tile) {
       for (uint32_t k = lane; k < 256; k += 32) wcnt[w * 256 + k] = 0;
       __syncwarp();
-      const uint32_t peers = __match_any_sync(0xffffffffu, d);
-      const uint32_t rank = __popc(peers & lt);
-      if (valid && rank == 0) wcnt[w * 256 + d] = __popc(peers);
+      uint64_t x[4];
+      uint32_t d[4], lr[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t i = t0 + 128 * w + 32 * u + lane;
+        x[u] = i < n ? src[i] : 0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t i = t0 + 128 * w + 32 * u + lane;
+        const bool valid = i < n;
+        d[u] = valid ? (uint32_t)((x[u] >> sh) & 255u) : 256u;
+        const uint32_t peers = __match_any_sync(0xffffffffu, d[u]);
+        const uint32_t rank = __popc(peers & lt);
+        lr[u] = (valid ? wcnt[w * 256 + d[u]] : 0u) + rank;
+        __syncwarp();
+        if (valid && rank == 0) wcnt[w * 256 + d[u]] += __popc(peers);
+        __syncwarp();
+      }
       __syncthreads();
       for (uint32_t dd = t; dd < 256; dd += nt) {  // per digit: warps' exclusive prefix
         uint32_t acc = 0;
@@ -1388,7 +1411,9 @@ __device__ int radix_sort8(uint64_t* w0, uint64_t* w1, uint32_t n, uint32_t lo, 
         base[(cb ^ 1u) * 256 + dd] = base[cb * 256 + dd] + acc;
       }
       __syncthreads();
-      if (valid) dst[base[cb * 256 + d] + wcnt[w * 256 + d] + rank] = x;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (d[u] < 256u) dst[base[cb * 256 + d[u]] + wcnt[w * 256 + d[u]] + lr[u]] = x[u];
       cb ^= 1u;
     }
     __syncthreads();
@@ -1403,10 +1428,20 @@ __device__ int radix_sort8(uint64_t* w0, uint64_t* w1, uint32_t n, uint32_t lo, 
 // semantics starting from point 0 (App. C voxel origin): NaN at point 0
 // poisons the axis; later NaNs never win; equal values keep the first.
 __device__ void seq_min3(const float* d, uint32_t n, Smem& S, float* lo) {
+  float l3[3] = {INFINITY, INFINITY, INFINITY};
+  for (uint32_t i0 = threadIdx.x; i0 < n; i0 += 4 * blockDim.x) {  // all axes, 4 points in flight
+    float v[4][3];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) v[u][k] = i0 + u * blockDim.x < n ? d[3 * (i0 + u * blockDim.x) + k] : INFINITY;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) l3[k] = fminf(l3[k], v[u][k]);
+  }
   for (int k = 0; k < 3; ++k) {
-    float l = INFINITY;
-    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) l = fminf(l, d[3 * i + k]);
-    lo[k] = dev::block_reduce(l, [](float x, float y) { return fminf(x, y); }, INFINITY, S.red);
+    lo[k] = dev::block_reduce(l3[k], [](float x, float y) { return fminf(x, y); }, INFINITY, S.red);
     const float p0 = d[k];
     if (isnan(p0)) lo[k] = p0;
     else if (lo[k] == 0.0f) {  // first zero in point order keeps its sign
@@ -1443,19 +1478,24 @@ __device__ int32_t op_voxel(const WaveArgs& a, Cloud& c, Smem& S, const OpDesc& 
   }
   uint32_t* idx = reinterpret_cast<uint32_t*>(c.ix[0]);
   uint32_t* idx2 = reinterpret_cast<uint32_t*>(c.ix[1]);
-  auto axis_key = [&](uint32_t i, int ax, uint32_t& bad) -> uint32_t {
-    const float q = floorf(__fdiv_rn(__fsub_rn(d[3 * i + ax], o[ax]), op.voxel));
-    if (!(q >= 0.0f && q < 2097152.0f)) {
-      bad = 1;
-      return 0u;
-    }
-    return (uint32_t)q;
-  };
   // pass 1: range check and per-axis extent (no stores)
   uint32_t bad = 0, mx[3] = {0, 0, 0};
-  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+  for (uint32_t i0 = threadIdx.x; i0 < n; i0 += 4 * blockDim.x) {  // 4 points in flight
+    float v[4][3];
 #pragma unroll
-    for (int ax = 0; ax < 3; ++ax) mx[ax] = max(mx[ax], axis_key(i, ax, bad));
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t i = i0 + u * blockDim.x;
+#pragma unroll
+      for (int ax = 0; ax < 3; ++ax) v[u][ax] = i < n ? d[3 * i + ax] : o[ax];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int ax = 0; ax < 3; ++ax) {
+        const float q = floorf(__fdiv_rn(__fsub_rn(v[u][ax], o[ax]), op.voxel));
+        if (!(q >= 0.0f && q < 2097152.0f)) bad = 1;
+        else mx[ax] = max(mx[ax], (uint32_t)q);
+      }
   }
   bad = dev::block_reduce(bad, dev::OpOr{}, 0u, S.red);
   if (bad) return kOutOfBounds;
@@ -1471,15 +1511,28 @@ __device__ int32_t op_voxel(const WaveArgs& a, Cloud& c, Smem& S, const OpDesc& 
   const uint64_t* K = nullptr;  // 64-bit path: sorted keys
   const uint32_t* P = nullptr;  //              sorted original indices
   const uint64_t* W = nullptr;  // packed path: sorted (key << ib | index)
-  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-    uint32_t b2 = 0;
-    const uint64_t kx = axis_key(i, 0, b2), ky = axis_key(i, 1, b2), kz = axis_key(i, 2, b2);
-    const uint64_t key = kx | (ky << bx[0]) | (kz << (bx[0] + bx[1]));
-    if (packed) {
-      c.key[0][i] = (key << ib) | i;
-    } else {
-      c.key[0][i] = key;
-      idx[i] = i;
+  for (uint32_t i0 = threadIdx.x; i0 < n; i0 += 4 * blockDim.x) {  // 4 points in flight
+    float v[4][3];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t i = i0 + u * blockDim.x;
+#pragma unroll
+      for (int ax = 0; ax < 3; ++ax) v[u][ax] = i < n ? d[3 * i + ax] : o[ax];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t i = i0 + u * blockDim.x;
+      if (i >= n) break;
+      uint64_t kk[3];
+#pragma unroll
+      for (int ax = 0; ax < 3; ++ax) kk[ax] = (uint64_t)floorf(__fdiv_rn(__fsub_rn(v[u][ax], o[ax]), op.voxel));
+      const uint64_t key = kk[0] | (kk[1] << bx[0]) | (kk[2] << (bx[0] + bx[1]));
+      if (packed) {
+        c.key[0][i] = (key << ib) | i;
+      } else {
+        c.key[0][i] = key;
+        idx[i] = i;
+      }
     }
   }
   __syncthreads();
