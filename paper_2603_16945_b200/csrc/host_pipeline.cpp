@@ -399,6 +399,7 @@ struct Wave {
   DevBuf gscratch;                // k_cloud global slab (smem_mode 0), per slot
   // device
   DevBuf bytes_stage, raw, tables, outs, compact, compact_meta, lz4_scratch, lz4_timing;
+  DevBuf handoff;  // chain split: the clouds between the prefix and the cluster launch
   uint32_t n_todo = 0;
   HostBuf h_tables, h_res, h_compact_meta;
   std::vector<uint64_t> out_base;  // per output field: offset in outs
@@ -445,7 +446,7 @@ struct Pipeline {
   std::vector<int32_t> bytes_fields;  // schema index per bytes field
   std::vector<OutField> outs;
   WaveArgs proto{};
-  int threads = 512, grid = 0;
+  int threads = 512, grid = 0, grid_pre = 0;
   size_t smem = 0;
   // iteration
   std::vector<Wave> slots;
@@ -527,12 +528,13 @@ struct Pipeline {
     // overlaps the decode / k_cloud of the others), fewer when the per-CTA
     // global slabs of large-cloud chains would exceed ~48 GB
     if (!slots_set && proto.gscratch_per_cta)
-      while (n_slots > 2 && (uint64_t)n_slots * proto.gscratch_per_cta * grid > (48ull << 30)) --n_slots;
+      while (n_slots > 2 && (uint64_t)n_slots * proto.gscratch_per_cta * std::max(grid, grid_pre) > (48ull << 30))
+        --n_slots;
     slots.resize(n_slots);
     for (auto& w : slots) {
       CK(cudaStreamCreateWithFlags(&w.stream, cudaStreamNonBlocking));
       for (size_t pi = 0; pi < plan.size() && plan[pi].first == 0; ++pi) launch(w, pi, true);
-      if (proto.gscratch_per_cta) w.gscratch.ensure(proto.gscratch_per_cta * grid);
+      if (proto.gscratch_per_cta) w.gscratch.ensure(proto.gscratch_per_cta * std::max(grid, grid_pre));
       CK(cudaEventCreate(&w.done));
       CK(cudaEventCreate(&w.k0));
       CK(cudaEventCreate(&w.k1));
@@ -746,6 +748,24 @@ struct Pipeline {
     CK(cudaGetDeviceProperties(&prop, device));
     const size_t fixed = cloud_smem_fixed();
     plan_fps_cluster(a, (uint32_t)threads);
+    a.op_begin = 0;
+    a.op_end = a.n_ops;
+    a.split_at = 0;
+    if (a.fps_cluster > 1) {  // run the ops before the first FPS one CTA per cloud
+      int f = 0;
+      while (f < a.n_ops && a.ops[f].kind != kFps) ++f;
+      if (f > 0 && f < a.n_ops) {
+        a.split_at = f;
+        uint64_t at = 128;  // header: status, present, n[8], elem[8], has_counts, n_counts
+        for (int k = 0; k < kMaxBytesFields; ++k) {
+          a.handoff_off[k] = at;
+          if ((a.tracked_mask >> k) & 1u) at = align16(at + (uint64_t)a.cap_points * a.field_cap[k]);
+        }
+        a.handoff_off[kMaxBytesFields] = at;
+        if (a.voxel_scratch) at = align16(at + 4ull * a.cap_points);
+        a.handoff_stride = at;
+      }
+    }
     if (op_timing) {
       d_op_cycles.ensure((kMaxOps + 2) * 8);
       CK(cudaMemset(d_op_cycles.p, 0, (kMaxOps + 2) * 8));
@@ -765,6 +785,9 @@ struct Pipeline {
       CK(occupancy_cloud_clusters(&clusters, threads, smem, a.fps_cluster, false));
       if (clusters < 1) fail(kOutOfBounds, "no room for a cluster of " + std::to_string(a.fps_cluster) + " CTAs");
       grid = clusters * (int)a.fps_cluster;
+      int per_sm = 0;  // the split's prefix launch: one CTA per cloud
+      CK(occupancy_cloud(&per_sm, threads, smem, 1));
+      grid_pre = std::max(1, per_sm) * sms;
     } else {
       int per_sm = 0;
       CK(occupancy_cloud(&per_sm, threads, smem, a.min_blocks));
@@ -989,6 +1012,7 @@ struct Pipeline {
       out_total += align16(outs[f].stride * w.n) + 64;
     }
     w.outs.ensure(out_total);
+    if (proto.split_at) w.handoff.ensure(proto.handoff_stride * w.n);
     w.h_res.ensure(3 * align16(w.n * 4) + outs.size() * w.n * 8);
     {
       uint64_t need = 0;
@@ -1039,6 +1063,7 @@ struct Pipeline {
     a.out_len = reinterpret_cast<uint64_t*>(dt + o_len);
     a.shift_tab = d_shift.as<uint32_t>();
     a.gscratch = proto.gscratch_per_cta ? w.gscratch.as<uint8_t>() : nullptr;
+    a.handoff = proto.split_at ? w.handoff.as<uint8_t>() : nullptr;
     for (size_t f = 0; f < outs.size(); ++f) {
       a.out[f] = w.outs.as<uint8_t>() + w.out_base[f];
       a.out_stride[f] = outs[f].stride;
@@ -1060,7 +1085,7 @@ struct Pipeline {
     w.n_todo = (uint32_t)todo.size();
     w.decode_alg_bytes = 0;
     for (uint32_t pi : todo) w.decode_alg_bytes += pages[pi].pay_len + pages[pi].raw_len;
-    CK(launch_wave(a, grid, threads, smem, w.stream, w.k0, w.k1));
+    CK(launch_wave(a, grid, grid_pre, threads, smem, w.stream, w.k0, w.k1));
     launches += (wins.empty() ? 0 : 1) + (todo.empty() ? 0 : 2) + (ng ? 1 : 0) + 1 + 1 + 1;
     h2d_bytes += up_bytes;
     // ---- results back to pinned host -------------------------------------------

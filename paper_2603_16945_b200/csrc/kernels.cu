@@ -1606,11 +1606,11 @@ __device__ int32_t op_voxel(const WaveArgs& a, Cloud& c, Smem& S, const OpDesc& 
 // single-op cloud-set API.  fail_op = 1-based failing transform.
 template <int MinBlocks>
 __device__ int32_t run_chain(const WaveArgs& a, Cloud& c, Smem& S, uint64_t epoch, uint64_t index,
-                             const uint64_t* fixed_seed, int32_t& fail_op) {
+                             const uint64_t* fixed_seed, int32_t& fail_op, int op_begin, int op_end) {
   int32_t status = kOk;
   const int fd = a.role_data;
   long long t0 = (a.op_cycles && threadIdx.x == 0) ? clock64() : 0;
-  for (int k = 0; status == kOk && k < a.n_ops; ++k) {
+  for (int k = op_begin; status == kOk && k < op_end; ++k) {
     const OpDesc& op = a.ops[k];
     const uint64_t seed =
         fixed_seed ? *fixed_seed : rng::mix_seed(a.base_seed, epoch, index, op.seed_op_id);
@@ -1652,6 +1652,86 @@ __device__ __forceinline__ uint64_t field_bytes(const WaveArgs& a, int f) {
   return (uint64_t)a.cap_points * a.field_cap[f] + 16;
 }
 
+// Tracked fields and the synthesized "count" field into the sample's batch
+// slots (leader CTA).
+__device__ void write_tracked(const WaveArgs& a, const Cloud& c, uint32_t s, int32_t& status) {
+  for (int f = 0; f < a.n_bytes_fields && status == kOk; ++f) {
+    const int of = a.bytes_out[f];
+    if (!((a.tracked_mask >> f) & 1u) || of < 0) continue;
+    const uint64_t nb = c.present >> f & 1u ? (uint64_t)c.n[f] * c.elem[f] : 0;
+    if (nb > a.out_stride[of]) {
+      status = kOutOfBounds;
+      break;
+    }
+    const uint32_t* s32 = reinterpret_cast<const uint32_t*>(c.cur[f]);
+    uint8_t* dst = a.out[of] + (uint64_t)s * a.out_stride[of];
+    uint32_t* d32 = reinterpret_cast<uint32_t*>(dst);
+    for (uint64_t i = threadIdx.x; i < nb / 4; i += blockDim.x) d32[i] = s32[i];
+    for (uint64_t i = (nb & ~3ull) + threadIdx.x; i < nb; i += blockDim.x) dst[i] = c.cur[f][i];
+    if (threadIdx.x == 0) a.out_len[(uint64_t)of * a.n_samples + s] = nb;
+  }
+  if (status == kOk && a.count_out >= 0) {  // synthesized "count" field (voxel counts, int32 bytes)
+    const int of = a.count_out;
+    const uint64_t nb = c.has_counts ? (uint64_t)c.n_counts * 4 : 0;
+    if (nb > a.out_stride[of]) {
+      status = kOutOfBounds;
+    } else {
+      int32_t* dst = reinterpret_cast<int32_t*>(a.out[of] + (uint64_t)s * a.out_stride[of]);
+      for (uint32_t i = threadIdx.x; i < nb / 4; i += blockDim.x) dst[i] = c.counts[i];
+      if (threadIdx.x == 0) a.out_len[(uint64_t)of * a.n_samples + s] = nb;
+    }
+  }
+}
+
+// 16-B aligned copy (chain-split hand-off), whole CTA.
+__device__ __forceinline__ void copy16(uint8_t* dst, const uint8_t* src, uint64_t nb) {
+  const uint4* s4 = reinterpret_cast<const uint4*>(src);
+  uint4* d4 = reinterpret_cast<uint4*>(dst);
+  for (uint64_t i = threadIdx.x; i < nb / 16; i += blockDim.x) d4[i] = s4[i];
+  for (uint64_t i = (nb & ~15ull) + threadIdx.x; i < nb; i += blockDim.x) dst[i] = src[i];
+}
+
+// Chain split: the cloud after the prefix ops, to / from the hand-off slot
+// [header: status, present, n[8], elem[8], has_counts, n_counts | fields | counts].
+__device__ void handoff_store(const WaveArgs& a, const Cloud& c, uint8_t* hb) {
+  for (int f = 0; f < a.n_bytes_fields; ++f)
+    if (((a.tracked_mask >> f) & 1u) && ((c.present >> f) & 1u))
+      copy16(hb + a.handoff_off[f], c.cur[f], (uint64_t)c.n[f] * c.elem[f]);
+  if (c.has_counts) copy16(hb + a.handoff_off[kMaxBytesFields], reinterpret_cast<const uint8_t*>(c.counts),
+                           (uint64_t)c.n_counts * 4);
+  if (threadIdx.x == 0) {
+    uint32_t* h = reinterpret_cast<uint32_t*>(hb);
+    h[1] = c.present;
+    for (int f = 0; f < kMaxBytesFields; ++f) {
+      h[2 + f] = c.n[f];
+      h[10 + f] = c.elem[f];
+    }
+    h[18] = (uint32_t)c.has_counts;
+    h[19] = c.n_counts;
+  }
+}
+
+__device__ void handoff_load(const WaveArgs& a, Cloud& c, Smem& S, const uint8_t* hb) {
+  const uint32_t* h = reinterpret_cast<const uint32_t*>(hb);
+  if (threadIdx.x == 0) {
+    S.cl = S.proto;
+    S.cl.present = h[1];
+    for (int f = 0; f < kMaxBytesFields; ++f) {
+      S.cl.n[f] = h[2 + f];
+      S.cl.elem[f] = h[10 + f];
+    }
+    S.cl.has_counts = (int32_t)h[18];
+    S.cl.n_counts = h[19];
+  }
+  __syncthreads();
+  for (int f = 0; f < a.n_bytes_fields; ++f)
+    if (((a.tracked_mask >> f) & 1u) && ((c.present >> f) & 1u))
+      copy16(c.cur[f], hb + a.handoff_off[f], (uint64_t)c.n[f] * c.elem[f]);
+  if (c.has_counts) copy16(reinterpret_cast<uint8_t*>(c.counts), hb + a.handoff_off[kMaxBytesFields],
+                           (uint64_t)c.n_counts * 4);
+  __syncthreads();
+}
+
 // MinBlocks = 1: up to 128 registers (FPS keeps min-distances in registers);
 // MinBlocks = 2: <= 64 registers, two CTAs per SM for global-slab clouds.
 template <int MinBlocks>
@@ -1679,6 +1759,23 @@ __global__ void __launch_bounds__(512, MinBlocks) k_cloud(WaveArgs a) {
   uint32_t phase = 0;
   for (uint32_t s = blockIdx.x / CL; s < a.n_samples; s += gridDim.x / CL) {
     const SampleWork sw = a.samples[s];
+    if (a.handoff_mode == 2) {
+      // chain split, second launch: the cloud after the prefix ops; a failed
+      // prefix already wrote the (final) status
+      const uint8_t* hb = a.handoff + (uint64_t)s * a.handoff_stride;
+      if (reinterpret_cast<const uint32_t*>(hb)[0] != (uint32_t)kOk) continue;  // uniform
+      handoff_load(a, c, S, hb);
+      int32_t fail_op = 0;
+      int32_t status = run_chain<MinBlocks>(a, c, S, sw.epoch, sw.index, nullptr, fail_op, a.op_begin, a.op_end);
+      if (status == kOk && leader) write_tracked(a, c, s, status);
+      if (threadIdx.x == 0 && leader) {
+        a.sample_status[s] = status;
+        a.sample_op[s] = status == kOk ? -1 : fail_op;
+        a.sample_where[s] = 0;
+      }
+      __syncthreads();
+      continue;
+    }
     const PageRef pg = a.pages[sw.block_page];
     const ScalarRec rec = a.recs[(uint64_t)a.groups[sw.group].first_rec + sw.row];
     int32_t fail_op = 0;
@@ -1790,38 +1887,17 @@ __global__ void __launch_bounds__(512, MinBlocks) k_cloud(WaveArgs a) {
       if (status == kOk && a.role_normal >= 0 && flen[a.role_normal] % 12) status = kMissingField;
       if (status == kOk && a.role_color >= 0 && flen[a.role_color] % 12) status = kMissingField;
       if (status != kOk) fail_op = 1;
-      if (status == kOk) status = run_chain<MinBlocks>(a, c, S, sw.epoch, sw.index, nullptr, fail_op);
+      if (status == kOk)
+        status = run_chain<MinBlocks>(a, c, S, sw.epoch, sw.index, nullptr, fail_op, a.op_begin, a.op_end);
     }
 
+    // ---- chain split, first launch: hand the cloud to the cluster launch ---
+    uint8_t* hb = a.handoff_mode == 1 ? a.handoff + (uint64_t)s * a.handoff_stride : nullptr;
+    if (hb && status == kOk) handoff_store(a, c, hb);
     // ---- write tracked fields + scalar values into the batch slot --------
     const long long tc2 = (a.op_cycles && threadIdx.x == 0) ? clock64() : 0;
     if (status == kOk && leader) {
-      for (int f = 0; f < a.n_bytes_fields && status == kOk; ++f) {
-        const int of = a.bytes_out[f];
-        if (!((a.tracked_mask >> f) & 1u) || of < 0) continue;
-        const uint64_t nb = c.present >> f & 1u ? (uint64_t)c.n[f] * c.elem[f] : 0;
-        if (nb > a.out_stride[of]) {
-          status = kOutOfBounds;
-          break;
-        }
-        const uint32_t* s32 = reinterpret_cast<const uint32_t*>(c.cur[f]);
-        uint8_t* dst = a.out[of] + (uint64_t)s * a.out_stride[of];
-        uint32_t* d32 = reinterpret_cast<uint32_t*>(dst);
-        for (uint64_t i = threadIdx.x; i < nb / 4; i += blockDim.x) d32[i] = s32[i];
-        for (uint64_t i = (nb & ~3ull) + threadIdx.x; i < nb; i += blockDim.x) dst[i] = c.cur[f][i];
-        if (threadIdx.x == 0) a.out_len[(uint64_t)of * a.n_samples + s] = nb;
-      }
-      if (a.count_out >= 0) {  // synthesized "count" field (voxel counts, int32 bytes)
-        const int of = a.count_out;
-        const uint64_t nb = c.has_counts ? (uint64_t)c.n_counts * 4 : 0;
-        if (nb > a.out_stride[of]) {
-          status = kOutOfBounds;
-        } else {
-          int32_t* dst = reinterpret_cast<int32_t*>(a.out[of] + (uint64_t)s * a.out_stride[of]);
-          for (uint32_t i = threadIdx.x; i < nb / 4; i += blockDim.x) dst[i] = c.counts[i];
-          if (threadIdx.x == 0) a.out_len[(uint64_t)of * a.n_samples + s] = nb;
-        }
-      }
+      if (a.handoff_mode != 1) write_tracked(a, c, s, status);
       uint32_t vo = rec.vals_off;
       for (int f = 0; f < a.n_fields && status == kOk; ++f) {
         const FieldDesc fdsc = a.fields[f];
@@ -1846,11 +1922,12 @@ __global__ void __launch_bounds__(512, MinBlocks) k_cloud(WaveArgs a) {
         vo += nb + skip;
       }
     }
-    if (threadIdx.x == 0 && leader) {
+    if (threadIdx.x == 0 && leader && (!hb || status != kOk)) {  // split: the second launch reports success
       a.sample_status[s] = status;
       a.sample_op[s] = status == kOk ? -1 : fail_op;
       a.sample_where[s] = 0;
     }
+    if (hb && threadIdx.x == 0) reinterpret_cast<uint32_t*>(hb)[0] = (uint32_t)status;
     if (a.op_cycles && threadIdx.x == 0)
       atomicAdd(a.op_cycles + a.n_ops + 1, (unsigned long long)(clock64() - tc2));
     __syncthreads();
@@ -1930,7 +2007,7 @@ __global__ void __launch_bounds__(512, 1) k_apply_set(WaveArgs a) {
     }
     __syncthreads();
     if (status == kOk && n == 0) status = kEmptyCloud;
-    if (status == kOk) status = run_chain<1>(a, c, S, 0, 0, a.set_seeds + s, fail_op);
+    if (status == kOk) status = run_chain<1>(a, c, S, 0, 0, a.set_seeds + s, fail_op, 0, a.n_ops);
     if (status == kOk && leader) {
       for (int f = 0; f < a.n_bytes_fields && status == kOk; ++f) {
         if (!((a.tracked_mask >> f) & 1u) || !a.set_out[f]) continue;
@@ -2168,12 +2245,25 @@ cudaError_t launch_clustered(K kern, const WaveArgs& a, int grid, int threads, s
 }
 }  // namespace
 
-cudaError_t launch_wave(const WaveArgs& a, int grid, int threads, size_t smem, cudaStream_t st,
-                        cudaEvent_t k0, cudaEvent_t k1) {
+cudaError_t launch_wave(const WaveArgs& a, int grid, int grid_pre, int threads, size_t smem,
+                        cudaStream_t st, cudaEvent_t k0, cudaEvent_t k1) {
   if (a.n_groups) k_scalar_parse<<<(a.n_groups + 127) / 128, 128, 0, st>>>(a);
   if (k0) cudaEventRecord(k0, st);
   if (a.n_samples) {
-    if (a.fps_cluster > 1) {
+    if (a.fps_cluster > 1 && a.split_at > 0) {
+      // chain split: ops [0, split_at) one CTA per cloud, then the cluster
+      WaveArgs pre = a, post = a;
+      pre.fps_cluster = 1;
+      pre.op_begin = 0;
+      pre.op_end = a.split_at;
+      pre.handoff_mode = 1;
+      post.op_begin = a.split_at;
+      post.op_end = a.n_ops;
+      post.handoff_mode = 2;
+      k_cloud<1><<<grid_pre, threads, smem, st>>>(pre);
+      const cudaError_t e = launch_clustered(k_cloud<1>, post, grid, threads, smem, st);
+      if (e != cudaSuccess) return e;
+    } else if (a.fps_cluster > 1) {
       const cudaError_t e = launch_clustered(k_cloud<1>, a, grid, threads, smem, st);
       if (e != cudaSuccess) return e;
     } else if (a.min_blocks == 2) {

@@ -32,7 +32,8 @@ cudaError_t launch_page_decode(const uint8_t* bytes, uint8_t* raw, const PageRef
                                cudaStream_t st, long long* timing = nullptr);
 uint64_t lz4_scratch_bytes(uint64_t pay);  // per LZ4 page
 // scalar parse → cloud interpreter → page verdicts → sample status
-cudaError_t launch_wave(const WaveArgs& a, int grid, int threads, size_t smem, cudaStream_t st,
+// grid_pre: the prefix launch of a split chain (a.split_at > 0), one CTA per cloud
+cudaError_t launch_wave(const WaveArgs& a, int grid, int grid_pre, int threads, size_t smem, cudaStream_t st,
                         cudaEvent_t k0 = nullptr, cudaEvent_t k1 = nullptr);
 cudaError_t occupancy_cloud(int* n, int threads, size_t smem, int min_blocks);
 // Max co-resident clusters of `cluster` CTAs (k_cloud<1>, or k_apply_set).

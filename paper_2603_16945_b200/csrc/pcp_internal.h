@@ -188,6 +188,15 @@ struct WaveArgs {
   uint32_t fps_cluster;     // CTAs per cloud (thread-block cluster) for large-cloud FPS; 1 = none
   uint32_t fps_slice_pts;   // points per CTA slice in cluster FPS (buffer 24 sizing)
   unsigned long long* op_cycles;  // PCP_OP_TIMING: [0] stage+decode, [1..n_ops] ops, [n_ops+1] writes
+  // chain split for cluster FPS: ops [0, split_at) run in a
+  // one-CTA-per-cloud launch that hands the cloud to the cluster launch
+  // through a per-sample buffer; split_at = 0: no split
+  int32_t split_at;
+  int32_t op_begin, op_end;       // this launch's op range
+  int32_t handoff_mode;           // 0 none, 1 write the cloud after op_end, 2 read it before op_begin
+  uint8_t* handoff;               // [n_samples][handoff_stride]
+  uint64_t handoff_stride;
+  uint64_t handoff_off[kMaxBytesFields + 1];  // per tracked field, [kMaxBytesFields] = counts
   // cloud-set mode (pcp_apply_map): clouds come from CSR arrays instead of
   // pages; bytes-field slots 0..7 = data, normal, color, intensity, extra0..3
   int32_t set_mode;
