@@ -278,10 +278,11 @@ def main():
     g = graph_for(args.config, cfg)
     points_per_step = 0
 
+    pinned = {}  # (field, ring slot) -> pinned host buffer, power-of-two size classes
+
     def timed(resident, steps, d2h):
         p = P.Pipeline(primary, g, ids=ids, device=local, epochs=steps, resident=resident)
         st0 = p.stats()
-        pinned = {}
         d2h_bytes = 0
         barrier()
         torch.cuda.synchronize()
@@ -298,8 +299,8 @@ def main():
                     for name, (kind, ptr, nbytes, offs, uni) in b.fields.items():
                         key = (name, nb % 64)
                         if key not in pinned or pinned[key].numel() < nbytes:
-                            pinned[key] = torch.empty(max(nbytes, 1), dtype=torch.uint8,
-                                                      pin_memory=True)
+                            cls = 1 << max(12, (max(nbytes, 1) - 1).bit_length())
+                            pinned[key] = torch.empty(cls, dtype=torch.uint8, pin_memory=True)
                         P.lib().pcp_memcpy_d2h_async(pinned[key].data_ptr(), ptr, nbytes, b.stream)
                         d2h_bytes += nbytes
             torch.cuda.synchronize()
@@ -355,6 +356,7 @@ def main():
         roof["traffic_over_alg"] = dram / alg_per_launch
     e2e = None
     if not args.no_e2e:
+        timed(False, 1, True)  # untimed: allocate the pinned host buffers
         ems, est0, est1, enb, d2h, _ = timed(False, args.steps, True)
         te = torch.tensor([ems], dtype=torch.float64, device="cuda")
         if world > 1:
