@@ -1184,6 +1184,9 @@ __device__ int32_t op_range_crop(const WaveArgs& a, Cloud& c, Smem& S, const OpD
 // ---- decode ----------------------------------------------------------------
 // Copy len bytes (optionally XOR-delta decoding 4-byte words) from an
 // arbitrarily aligned source into a 16-B aligned destination.
+// U: 16-B chunks per thread in flight (4 in the 128-register build; 1 with
+// 64 registers, where deeper unrolling spills to local memory)
+template <int U>
 __device__ void decode_bytes(uint8_t* dst, const uint8_t* src, uint64_t len, bool delta,
                              Smem& S) {
   const uint32_t t = threadIdx.x, nt = blockDim.x, lane = t & 31, w = t >> 5, nw = nt >> 5;
@@ -1202,10 +1205,10 @@ __device__ void decode_bytes(uint8_t* dst, const uint8_t* src, uint64_t len, boo
     const uint32_t* sw = reinterpret_cast<const uint32_t*>(sa & ~uintptr_t(3));
     const uint64_t n16 = len >> 4;
     uint4* d4 = reinterpret_cast<uint4*>(dst);
-    for (uint64_t k0 = t; k0 < n16; k0 += 4 * (uint64_t)nt) {
-      uint32_t v[4][5];
+    for (uint64_t k0 = t; k0 < n16; k0 += U * (uint64_t)nt) {
+      uint32_t v[U][5];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < U; ++u) {
         const uint64_t k = k0 + (uint64_t)u * nt;
         if (k < n16) {
 #pragma unroll
@@ -1213,7 +1216,7 @@ __device__ void decode_bytes(uint8_t* dst, const uint8_t* src, uint64_t len, boo
         }
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < U; ++u) {
         const uint64_t k = k0 + (uint64_t)u * nt;
         if (k < n16)
           d4[k] = sh ? make_uint4(__funnelshift_r(v[u][0], v[u][1], sh), __funnelshift_r(v[u][1], v[u][2], sh),
@@ -1324,6 +1327,7 @@ __device__ int radix_sort(uint64_t* k0, uint32_t* v0, uint64_t* k1, uint32_t* v1
 // exclusive prefixes in place, against double-buffered bucket bases (two
 // barriers per tile).  `scr`: kSortScratchBytes.  Returns 1 if the result
 // is in w1, 0 if in w0.
+template <int U>
 __device__ int radix_sort8(uint64_t* w0, uint64_t* w1, uint32_t n, uint32_t lo, uint32_t hi,
                            uint32_t* scr) {
   uint32_t* hist = scr;               // [8][256]
@@ -1333,12 +1337,12 @@ __device__ int radix_sort8(uint64_t* w0, uint64_t* w1, uint32_t n, uint32_t lo, 
   const uint32_t np = (hi - lo + 7) / 8;
   for (uint32_t i = t; i < np * 256; i += nt) hist[i] = 0;
   __syncthreads();
-  for (uint32_t i0 = t; i0 < n; i0 += 4 * nt) {  // 4 words per thread in flight
-    uint64_t x[4];
+  for (uint32_t i0 = t; i0 < n; i0 += U * nt) {  // U words per thread in flight
+    uint64_t x[U];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) x[u] = i0 + u * nt < n ? w0[i0 + u * nt] : 0ull;
+    for (int u = 0; u < U; ++u) x[u] = i0 + u * nt < n ? w0[i0 + u * nt] : 0ull;
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < U; ++u)
       if (i0 + u * nt < n)
         for (uint32_t p = 0; p < np; ++p)
           atomicAdd(&hist[p * 256 + (uint32_t)((x[u] >> (lo + 8 * p)) & 255u)], 1u);
@@ -1427,16 +1431,17 @@ __device__ int radix_sort8(uint64_t* w0, uint64_t* w1, uint32_t n, uint32_t lo, 
 // Smallest coordinate per axis with the sequential `if (v < o) o = v`
 // semantics starting from point 0 (App. C voxel origin): NaN at point 0
 // poisons the axis; later NaNs never win; equal values keep the first.
+template <int U>
 __device__ void seq_min3(const float* d, uint32_t n, Smem& S, float* lo) {
   float l3[3] = {INFINITY, INFINITY, INFINITY};
-  for (uint32_t i0 = threadIdx.x; i0 < n; i0 += 4 * blockDim.x) {  // all axes, 4 points in flight
-    float v[4][3];
+  for (uint32_t i0 = threadIdx.x; i0 < n; i0 += U * blockDim.x) {  // all axes, U points in flight
+    float v[U][3];
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < U; ++u)
 #pragma unroll
       for (int k = 0; k < 3; ++k) v[u][k] = i0 + u * blockDim.x < n ? d[3 * (i0 + u * blockDim.x) + k] : INFINITY;
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < U; ++u)
 #pragma unroll
       for (int k = 0; k < 3; ++k) l3[k] = fminf(l3[k], v[u][k]);
   }
@@ -1462,6 +1467,7 @@ __device__ void seq_min3(const float* d, uint32_t n, Smem& S, float* lo) {
 // key = kx | ky<<21 | kz<<42, stable order by key, per voxel the count and
 // the mean of every float field = (float)(sum in point order (double) / count);
 // extra gathered fields take the voxel's first point.  Output ascending key.
+template <int U>
 __device__ int32_t op_voxel(const WaveArgs& a, Cloud& c, Smem& S, const OpDesc& op) {
   const uint32_t n = c.n[a.role_data];
   if (!(op.voxel > 0.0f)) return kOutOfBounds;
@@ -1474,22 +1480,22 @@ __device__ int32_t op_voxel(const WaveArgs& a, Cloud& c, Smem& S, const OpDesc& 
   if (op.has_origin) {
     o[0] = op.origin[0]; o[1] = op.origin[1]; o[2] = op.origin[2];
   } else {
-    seq_min3(d, n, S, o);
+    seq_min3<U>(d, n, S, o);
   }
   uint32_t* idx = reinterpret_cast<uint32_t*>(c.ix[0]);
   uint32_t* idx2 = reinterpret_cast<uint32_t*>(c.ix[1]);
   // pass 1: range check and per-axis extent (no stores)
   uint32_t bad = 0, mx[3] = {0, 0, 0};
-  for (uint32_t i0 = threadIdx.x; i0 < n; i0 += 4 * blockDim.x) {  // 4 points in flight
-    float v[4][3];
+  for (uint32_t i0 = threadIdx.x; i0 < n; i0 += U * blockDim.x) {  // U points in flight
+    float v[U][3];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < U; ++u) {
       const uint32_t i = i0 + u * blockDim.x;
 #pragma unroll
       for (int ax = 0; ax < 3; ++ax) v[u][ax] = i < n ? d[3 * i + ax] : o[ax];
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < U; ++u)
 #pragma unroll
       for (int ax = 0; ax < 3; ++ax) {
         const float q = floorf(__fdiv_rn(__fsub_rn(v[u][ax], o[ax]), op.voxel));
@@ -1511,16 +1517,16 @@ __device__ int32_t op_voxel(const WaveArgs& a, Cloud& c, Smem& S, const OpDesc& 
   const uint64_t* K = nullptr;  // 64-bit path: sorted keys
   const uint32_t* P = nullptr;  //              sorted original indices
   const uint64_t* W = nullptr;  // packed path: sorted (key << ib | index)
-  for (uint32_t i0 = threadIdx.x; i0 < n; i0 += 4 * blockDim.x) {  // 4 points in flight
-    float v[4][3];
+  for (uint32_t i0 = threadIdx.x; i0 < n; i0 += U * blockDim.x) {  // U points in flight
+    float v[U][3];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < U; ++u) {
       const uint32_t i = i0 + u * blockDim.x;
 #pragma unroll
       for (int ax = 0; ax < 3; ++ax) v[u][ax] = i < n ? d[3 * i + ax] : o[ax];
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < U; ++u) {
       const uint32_t i = i0 + u * blockDim.x;
       if (i >= n) break;
       uint64_t kk[3];
@@ -1537,7 +1543,7 @@ __device__ int32_t op_voxel(const WaveArgs& a, Cloud& c, Smem& S, const OpDesc& 
   }
   __syncthreads();
   if (packed) {
-    const int r = radix_sort8(c.key[0], c.key[1], n, ib, ib + kb, c.sort_buf);
+    const int r = radix_sort8<U>(c.key[0], c.key[1], n, ib, ib + kb, c.sort_buf);
     W = c.key[r];
   } else {
     const int r = radix_sort(c.key[0], idx, c.key[1], idx2, n, kb, S);
@@ -1604,8 +1610,10 @@ __device__ int32_t op_voxel(const WaveArgs& a, Cloud& c, Smem& S, const OpDesc& 
 // Applies the op chain (Pipeline map worker, pipeline.cpp:474-480): seed per
 // op = mix_seed(base, epoch, index, op id), or `fixed_seed` for the
 // single-op cloud-set API.  fail_op = 1-based failing transform.
+// (force-inlined: an outlined call would need the address of the kernel's
+// WaveArgs parameter, and ptxas would copy all ~3 KB of it to local memory)
 template <int MinBlocks>
-__device__ int32_t run_chain(const WaveArgs& a, Cloud& c, Smem& S, uint64_t epoch, uint64_t index,
+__device__ __forceinline__ int32_t run_chain(const WaveArgs& a, Cloud& c, Smem& S, uint64_t epoch, uint64_t index,
                              const uint64_t* fixed_seed, int32_t& fail_op, int op_begin, int op_end) {
   int32_t status = kOk;
   const int fd = a.role_data;
@@ -1629,7 +1637,7 @@ __device__ int32_t run_chain(const WaveArgs& a, Cloud& c, Smem& S, uint64_t epoc
         case kDownsample: status = op_downsample(a, c, S, op, seed); break;
         case kFps: status = op_fps<MinBlocks>(a, c, S, op); break;
         case kRangeCrop: status = op_range_crop(a, c, S, op); break;
-        case kVoxel: status = op_voxel(a, c, S, op); break;
+        case kVoxel: status = op_voxel<MinBlocks == 1 ? 4 : 1>(a, c, S, op); break;
         default: status = kUnknownOp; break;
       }
     }
@@ -1654,7 +1662,7 @@ __device__ __forceinline__ uint64_t field_bytes(const WaveArgs& a, int f) {
 
 // Tracked fields and the synthesized "count" field into the sample's batch
 // slots (leader CTA).
-__device__ void write_tracked(const WaveArgs& a, const Cloud& c, uint32_t s, int32_t& status) {
+__device__ __forceinline__ void write_tracked(const WaveArgs& a, const Cloud& c, uint32_t s, int32_t& status) {
   for (int f = 0; f < a.n_bytes_fields && status == kOk; ++f) {
     const int of = a.bytes_out[f];
     if (!((a.tracked_mask >> f) & 1u) || of < 0) continue;
@@ -1693,7 +1701,7 @@ __device__ __forceinline__ void copy16(uint8_t* dst, const uint8_t* src, uint64_
 
 // Chain split: the cloud after the prefix ops, to / from the hand-off slot
 // [header: status, present, n[8], elem[8], has_counts, n_counts | fields | counts].
-__device__ void handoff_store(const WaveArgs& a, const Cloud& c, uint8_t* hb) {
+__device__ __forceinline__ void handoff_store(const WaveArgs& a, const Cloud& c, uint8_t* hb) {
   for (int f = 0; f < a.n_bytes_fields; ++f)
     if (((a.tracked_mask >> f) & 1u) && ((c.present >> f) & 1u))
       copy16(hb + a.handoff_off[f], c.cur[f], (uint64_t)c.n[f] * c.elem[f]);
@@ -1711,7 +1719,7 @@ __device__ void handoff_store(const WaveArgs& a, const Cloud& c, uint8_t* hb) {
   }
 }
 
-__device__ void handoff_load(const WaveArgs& a, Cloud& c, Smem& S, const uint8_t* hb) {
+__device__ __forceinline__ void handoff_load(const WaveArgs& a, Cloud& c, Smem& S, const uint8_t* hb) {
   const uint32_t* h = reinterpret_cast<const uint32_t*>(hb);
   if (threadIdx.x == 0) {
     S.cl = S.proto;
@@ -1847,7 +1855,7 @@ __global__ void __launch_bounds__(512, MinBlocks) k_cloud(WaveArgs a) {
             status = kOutOfBounds;
             break;
           }
-          decode_bytes(c.cur[f], blob + foff[f], flen[f], delta, S);
+          decode_bytes<MinBlocks == 1 ? 4 : 1>(c.cur[f], blob + foff[f], flen[f], delta, S);
           uint32_t e;
           if (f == a.role_data || f == a.role_normal || f == a.role_color) {
             e = 12;
@@ -1868,7 +1876,8 @@ __global__ void __launch_bounds__(512, MinBlocks) k_cloud(WaveArgs a) {
             break;
           }
           if (leader) {
-            decode_bytes(a.out[of] + (uint64_t)s * a.out_stride[of], blob + foff[f], flen[f], delta, S);
+            decode_bytes<MinBlocks == 1 ? 4 : 1>(a.out[of] + (uint64_t)s * a.out_stride[of], blob + foff[f],
+                                                 flen[f], delta, S);
             if (threadIdx.x == 0) a.out_len[(uint64_t)of * a.n_samples + s] = flen[f];
           }
         }
