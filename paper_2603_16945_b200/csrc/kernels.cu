@@ -1855,7 +1855,7 @@ __global__ void __launch_bounds__(512, MinBlocks) k_cloud(WaveArgs a) {
             status = kOutOfBounds;
             break;
           }
-          decode_bytes<MinBlocks == 1 ? 4 : 1>(c.cur[f], blob + foff[f], flen[f], delta, S);
+          decode_bytes<1>(c.cur[f], blob + foff[f], flen[f], delta, S);
           uint32_t e;
           if (f == a.role_data || f == a.role_normal || f == a.role_color) {
             e = 12;
@@ -1876,7 +1876,7 @@ __global__ void __launch_bounds__(512, MinBlocks) k_cloud(WaveArgs a) {
             break;
           }
           if (leader) {
-            decode_bytes<MinBlocks == 1 ? 4 : 1>(a.out[of] + (uint64_t)s * a.out_stride[of], blob + foff[f],
+            decode_bytes<1>(a.out[of] + (uint64_t)s * a.out_stride[of], blob + foff[f],
                                                  flen[f], delta, S);
             if (threadIdx.x == 0) a.out_len[(uint64_t)of * a.n_samples + s] = flen[f];
           }
