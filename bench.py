@@ -287,21 +287,30 @@ def main():
         barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        d2h_async = P.lib().pcp_memcpy_d2h_async
         with Clocks(local) as ck:
             e0.record()
             nb = 0
-            for b in p:
+            # the bare C-ABI loop (pcp_pipeline_next_batch), as a C++ GpuPipeline
+            # would run it: no per-batch Python objects
+            while True:
+                b = p.next_batch_raw()
+                if b is None:
+                    break
                 nb += 1
                 if d2h:
                     # every field of every batch into pinned host memory, async on
-                    # the batch's serve stream (a ring of host buffers per field);
+                    # the pipeline's serve stream (a ring of host buffers per field);
                     # the closing device synchronize waits for the last copies
-                    for name, (kind, ptr, nbytes, offs, uni) in b.fields.items():
-                        key = (name, nb % 64)
-                        if key not in pinned or pinned[key].numel() < nbytes:
+                    for k in range(b.n_fields):
+                        f = b.fields[k]
+                        nbytes = f.nbytes
+                        key = (k, nb % 64)
+                        buf = pinned.get(key)
+                        if buf is None or buf.numel() < nbytes:
                             cls = 1 << max(12, (max(nbytes, 1) - 1).bit_length())
-                            pinned[key] = torch.empty(cls, dtype=torch.uint8, pin_memory=True)
-                        P.lib().pcp_memcpy_d2h_async(pinned[key].data_ptr(), ptr, nbytes, b.stream)
+                            buf = pinned[key] = torch.empty(cls, dtype=torch.uint8, pin_memory=True)
+                        d2h_async(buf.data_ptr(), f.d_ptr, nbytes, p.stream)
                         d2h_bytes += nbytes
             torch.cuda.synchronize()
             e1.record()

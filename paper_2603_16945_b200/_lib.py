@@ -217,6 +217,16 @@ class Pipeline:
             return None
         return DeviceBatch(b, self.stream)
 
+    def next_batch_raw(self):
+        """The bare pcp_pipeline_next_batch call (what a C++ GpuPipeline makes):
+        returns the library's batch struct — reused, valid until the next call —
+        or None at the end.  For throughput loops that need no Python objects."""
+        if not hasattr(self, "_raw"):
+            self._raw, self._eos = _Batch(), C.c_int()
+            self._next = lib().pcp_pipeline_next_batch
+        _check(self._next(self._h, C.byref(self._raw), C.byref(self._eos)))
+        return None if self._eos.value else self._raw
+
     def __iter__(self):
         while True:
             b = self.next_batch()
