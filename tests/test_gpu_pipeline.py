@@ -221,3 +221,57 @@ def test_async_d2h_matches_sync(pcp, tmp_path, slots):
         for name in wb:
             buf, nbytes, _ = gb[name]
             assert np.array_equal(buf.numpy()[:nbytes], wb[name][0].view(np.uint8)), name
+
+
+def _adversarial_blob(rng, n):
+    """Bytes that drive the LZ4 decoder through its corner cases: runs of one
+    byte and short-period patterns (self-overlapping matches, offsets 1..8),
+    random stretches (literals, some > 64 KB -> long 255-continued lengths),
+    repeats of earlier content up to ~60 KB back, and dense small-label
+    regions (chains of offset-4 matches)."""
+    out, size = [], 0
+    while size < n:
+        kind = rng.integers(0, 6)
+        if kind == 0:
+            piece = np.full(int(rng.integers(4, 3000)), rng.integers(0, 256), np.uint8)
+        elif kind == 1:
+            per = int(rng.integers(2, 9))
+            piece = np.tile(rng.integers(0, 256, per, dtype=np.uint8), int(rng.integers(2, 600)))
+        elif kind == 2:
+            piece = rng.integers(0, 256, int(rng.integers(1, 70000 if rng.random() < 0.15 else 2000)),
+                                 dtype=np.uint8)
+        elif kind == 3 and out:
+            prev = np.concatenate(out)
+            back = int(rng.integers(1, min(len(prev), 60000) + 1))
+            ln = int(rng.integers(4, 5000))
+            piece = np.resize(prev[len(prev) - back:], ln)
+        else:
+            labels = rng.integers(0, 4, int(rng.integers(16, 800))).astype(np.int32)
+            piece = np.repeat(labels, rng.integers(1, 40, len(labels))).view(np.uint8)
+        out.append(piece.astype(np.uint8))
+        size += len(piece)
+    return np.concatenate(out)[:n]
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3, 4, 5, 6])
+def test_lz4_adversarial_pages_through_pipeline(pcp, ref, tmp_path, seed):
+    """Pipeline decode (k_page_decode + k_page_matches: skim with skipped
+    windows, pointer-jumping match groups, slow path) of adversarial LZ4 pages
+    is byte-exact against the reference reader."""
+    rng = np.random.default_rng(seed)
+    schema = {"fields": {"blob": {"type": "bytes"}, "id": {"type": "int32"}}}
+    samples = [{"blob": _adversarial_blob(rng, int(rng.integers(20000, 300000))),
+                "id": np.array([i], np.int32)} for i in range(24)]
+    primary = pcp.write_dataset(tmp_path, "ds", schema, samples, group_size=6)  # compressible: LZ4 pages
+    got = []
+    for b in pcp.Pipeline(primary, {"base_seed": 1, "drop_remainder": False, "ops": [
+            {"id": 0, "kind": "source", "num_workers": 1, "queue_capacity": 8},
+            {"id": 1, "kind": "batch", "batch_size": 4, "num_workers": 1, "queue_capacity": 8},
+            {"id": 2, "kind": "sink", "num_workers": 1, "queue_capacity": 8}]}):
+        host = b.to_host()
+        arr, offs = host["blob"]
+        for k in range(b.n_samples):
+            got.append(bytes(arr.view(np.uint8)[offs[k]:offs[k + 1]]))
+    assert len(got) == len(samples)
+    for i, s in enumerate(samples):
+        assert got[i] == bytes(s["blob"]), i
