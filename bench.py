@@ -405,6 +405,10 @@ def main():
                                          for o in synth.CHAINS[CHAIN_OF[args.config]]] + ["writes"])
             tot_c = max(1, sum(oc))
             line["op_cycle_share"] = {n: round(c / tot_c, 4) for n, c in zip(names, oc)}
+            if "voxel_phase_cycles" in st1:
+                vp = st1["voxel_phase_cycles"]
+                line["voxel_phase_share"] = dict(zip(["origin+extent", "keys", "sort", "segments", "means"],
+                                                     [round(v / tot_c, 4) for v in vp]))
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

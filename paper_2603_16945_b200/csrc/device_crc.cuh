@@ -67,21 +67,34 @@ __device__ inline uint32_t bytes(const uint32_t* tab, const uint8_t* p, uint64_t
   return c ^ 0xFFFFFFFFu;
 }
 
-// Same over 4-byte words read from an aligned smem copy starting at byte
-// `mis` (0..3) — used for staged blobs.  Falls back to bytes for the edges.
+// Same over aligned 4-byte words (bytes up to the first word boundary and
+// after the last one one at a time).  Words are loaded kBatch at a time
+// ahead of the table chain, so a chunk in global memory exposes the load
+// latency once per batch instead of once per word.
+constexpr int kBatch = 16;
+
+__device__ __forceinline__ uint32_t word_step(const uint32_t* tab, uint32_t c, uint32_t w) {
+  c ^= w;
+  c = tab[c & 0xFF] ^ (c >> 8);
+  c = tab[c & 0xFF] ^ (c >> 8);
+  c = tab[c & 0xFF] ^ (c >> 8);
+  return tab[c & 0xFF] ^ (c >> 8);
+}
+
 __device__ inline uint32_t bytes_words(const uint32_t* tab, const uint8_t* p, uint64_t n) {
   uint32_t c = 0xFFFFFFFFu;
   uint64_t i = 0;
   const uint64_t head = (4 - ((uintptr_t)p & 3)) & 3;
   for (; i < head && i < n; ++i) c = tab[(c ^ p[i]) & 0xFF] ^ (c >> 8);
-  for (; i + 4 <= n; i += 4) {
-    uint32_t w = *reinterpret_cast<const uint32_t*>(p + i);
-    c ^= w;
-    c = tab[c & 0xFF] ^ (c >> 8);
-    c = tab[c & 0xFF] ^ (c >> 8);
-    c = tab[c & 0xFF] ^ (c >> 8);
-    c = tab[c & 0xFF] ^ (c >> 8);
+  for (; i + 4 * kBatch <= n; i += 4 * kBatch) {
+    const uint32_t* wp = reinterpret_cast<const uint32_t*>(p + i);
+    uint32_t v[kBatch];
+#pragma unroll
+    for (int b = 0; b < kBatch; ++b) v[b] = wp[b];
+#pragma unroll
+    for (int b = 0; b < kBatch; ++b) c = word_step(tab, c, v[b]);
   }
+  for (; i + 4 <= n; i += 4) c = word_step(tab, c, *reinterpret_cast<const uint32_t*>(p + i));
   for (; i < n; ++i) c = tab[(c ^ p[i]) & 0xFF] ^ (c >> 8);
   return c ^ 0xFFFFFFFFu;
 }

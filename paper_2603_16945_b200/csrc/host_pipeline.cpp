@@ -1260,6 +1260,7 @@ struct Pipeline {
       std::vector<unsigned long long> oc(kMaxOps + 2);
       CK(cudaDeviceSynchronize());
       CK(cudaMemcpy(oc.data(), d_op_cycles.p, oc.size() * 8, cudaMemcpyDeviceToHost));
+      j["voxel_phase_cycles"] = std::vector<unsigned long long>(oc.begin() + 10, oc.begin() + 15);
       oc.resize(proto.n_ops + 2);
       j["op_cycles"] = oc;
     }

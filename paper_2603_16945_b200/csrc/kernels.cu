@@ -1186,7 +1186,7 @@ __device__ int32_t op_range_crop(const WaveArgs& a, Cloud& c, Smem& S, const OpD
 // arbitrarily aligned source into a 16-B aligned destination.
 // U: 16-B chunks per thread in flight (4 in the 128-register build; 1 with
 // 64 registers, where deeper unrolling spills to local memory)
-template <int U>
+template <int U, int DU>
 __device__ void decode_bytes(uint8_t* dst, const uint8_t* src, uint64_t len, bool delta,
                              Smem& S) {
   const uint32_t t = threadIdx.x, nt = blockDim.x, lane = t & 31, w = t >> 5, nw = nt >> 5;
@@ -1228,30 +1228,99 @@ __device__ void decode_bytes(uint8_t* dst, const uint8_t* src, uint64_t len, boo
     __syncthreads();
     return;
   }
+  // XOR-delta: out[i] = XOR of in[0..i] over the (possibly unaligned) 4-byte
+  // words of src.  Words are read as 16-B quads of the aligned word stream A
+  // (the funnel shift's extra word comes from the next lane), one quad per
+  // lane per row, DU rows in flight per warp.  Two passes over contiguous warp
+  // segments of quads: (1) XOR-reduce, one prefix over the warp totals;
+  // (2) lane-local scan of the quad, warp scan of the lane totals, row
+  // carries chained from row totals.  Up to 3 head words (before the first
+  // 16-B boundary of A) and 3 tail words are done by thread 0.
   const uint64_t nwords = len >> 2;  // len % 4 == 0 for delta columns
   uint32_t* d32 = reinterpret_cast<uint32_t*>(dst);
-  const uint64_t seg = ((nwords + nw - 1) / nw + 31) & ~uint64_t(31);
-  const uint64_t s0 = min((uint64_t)w * seg, nwords), s1 = min(s0 + seg, nwords);
-  uint32_t carry = 0;
-  for (uint64_t base = s0; base < s1; base += 32) {
-    const uint64_t i = base + lane;
-    uint32_t v = i < s1 ? dev::ld_u32_unaligned(src + 4 * i) : 0u;
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
-      if ((int)lane >= o) v ^= y;
+  const uintptr_t sa = reinterpret_cast<uintptr_t>(src);
+  const uint32_t sh = (uint32_t)(sa & 3u) * 8u;
+  const uint32_t* A = reinterpret_cast<const uint32_t*>(sa & ~uintptr_t(3));
+  const uint64_t h0 = ((16u - (reinterpret_cast<uintptr_t>(A) & 15u)) & 15u) >> 2;
+  const uint64_t h = h0 < nwords ? h0 : nwords;
+  const uint64_t nq = (nwords - h) >> 2;
+  const uint64_t tail0 = h + 4 * nq;
+  const uint64_t segq = ((nq + nw - 1) / nw + 31) & ~uint64_t(31);
+  const uint64_t q0 = min((uint64_t)w * segq, nq), q1 = min(q0 + segq, nq);
+  auto word = [&](uint64_t i) -> uint32_t { return sh ? __funnelshift_r(A[i], A[i + 1], sh) : A[i]; };
+  // the 4 words of quad qi (lane-valid `ok`); every lane of the warp calls it
+  auto quad = [&](uint64_t qi, bool ok, uint32_t (&o)[4]) {
+    const uint4 q = ok ? *reinterpret_cast<const uint4*>(A + h + 4 * qi) : make_uint4(0u, 0u, 0u, 0u);
+    uint32_t nx = __shfl_down_sync(0xffffffffu, q.x, 1);
+    const bool next_ok = lane < 31 && qi + 1 < q1;
+    if (ok && !next_ok && sh) nx = A[h + 4 * qi + 4];
+    o[0] = __funnelshift_r(q.x, q.y, sh);
+    o[1] = __funnelshift_r(q.y, q.z, sh);
+    o[2] = __funnelshift_r(q.z, q.w, sh);
+    o[3] = __funnelshift_r(q.w, nx, sh);
+  };
+  uint32_t x = 0;
+  for (uint64_t base = q0; base < q1; base += 32 * DU) {
+    uint32_t v[DU][4];
+#pragma unroll
+    for (int u = 0; u < DU; ++u) {
+      const uint64_t qi = base + 32 * u + lane;
+      quad(qi, qi < q1, v[u]);
     }
-    v ^= carry;
-    if (i < s1) d32[i] = v;
-    carry = __shfl_sync(0xffffffffu, v, 31);
+#pragma unroll
+    for (int u = 0; u < DU; ++u) x ^= v[u][0] ^ v[u][1] ^ v[u][2] ^ v[u][3];
   }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) x ^= __shfl_xor_sync(0xffffffffu, x, o);
   uint32_t* red = reinterpret_cast<uint32_t*>(S.red);
+  __syncthreads();  // S.red may still be read by a previous user
+  if (lane == 0) red[w] = x;
+  if (t == 0) {
+    uint32_t hx = 0;
+    for (uint64_t i = 0; i < h; ++i) hx ^= word(i);
+    red[nw] = hx;
+  }
   __syncthreads();
-  if (lane == 0) red[w] = carry;
-  __syncthreads();
-  uint32_t cin = 0;
-  for (uint32_t k = 0; k < w; ++k) cin ^= red[k];
-  if (cin)
-    for (uint64_t i = s0 + lane; i < s1; i += 32) d32[i] ^= cin;
+  uint32_t carry = red[nw];
+  for (uint32_t k = 0; k < w; ++k) carry ^= red[k];
+  for (uint64_t base = q0; base < q1; base += 32 * DU) {
+    uint32_t v[DU][4];
+#pragma unroll
+    for (int u = 0; u < DU; ++u) {
+      const uint64_t qi = base + 32 * u + lane;
+      quad(qi, qi < q1, v[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < DU; ++u) {
+      v[u][1] ^= v[u][0];
+      v[u][2] ^= v[u][1];
+      v[u][3] ^= v[u][2];
+      uint32_t incl = v[u][3];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if ((int)lane >= o) incl ^= y;
+      }
+      const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+      const uint32_t pre = incl ^ v[u][3] ^ carry;
+      const uint64_t qi = base + 32 * u + lane;
+      if (qi < q1) {
+        uint32_t* d = d32 + h + 4 * qi;
+        d[0] = v[u][0] ^ pre;
+        d[1] = v[u][1] ^ pre;
+        d[2] = v[u][2] ^ pre;
+        d[3] = v[u][3] ^ pre;
+      }
+      carry ^= tot;
+    }
+  }
+  if (t == 0) {
+    uint32_t c0 = 0;
+    for (uint64_t i = 0; i < h; ++i) d32[i] = c0 ^= word(i);
+    c0 = red[nw];
+    for (uint32_t k = 0; k < nw; ++k) c0 ^= red[k];
+    for (uint64_t i = tail0; i < nwords; ++i) d32[i] = c0 ^= word(i);
+  }
   __syncthreads();
 }
 
@@ -1321,104 +1390,92 @@ __device__ int radix_sort(uint64_t* k0, uint32_t* v0, uint64_t* k1, uint32_t* v1
 
 // Stable LSD radix sort of 64-bit words on bits [lo, hi), 8-bit digits
 // (voxel keys packed above the point index, so the words carry their own
-// payload).  One read computes every pass's digit histogram; each pass then
-// reads and writes the words once: tiles of blockDim words are ranked stably
-// with __match_any_sync inside a warp and per-warp digit counts turned into
-// exclusive prefixes in place, against double-buffered bucket bases (two
-// barriers per tile).  `scr`: kSortScratchBytes.  Returns 1 if the result
-// is in w1, 0 if in w0.
+// payload), warp-partitioned: warp w owns the contiguous chunk
+// [w*per, (w+1)*per).  Per pass: (a) every warp counts its chunk's digits,
+// (b) one exclusive prefix over (digit, warp) gives each warp its bases,
+// (c) every warp scatters its chunk in order (__match_any_sync ranks against
+// its own counter row) — three block barriers per pass instead of two per
+// tile; chunks are contiguous and ordered by warp, so the sort is stable.
+// U words per lane are loaded ahead.  `scr`: kSortScratchBytes.  Returns 1
+// if the result is in w1, 0 if in w0.
 template <int U>
 __device__ int radix_sort8(uint64_t* w0, uint64_t* w1, uint32_t n, uint32_t lo, uint32_t hi,
                            uint32_t* scr) {
-  uint32_t* hist = scr;               // [8][256]
-  uint32_t* wcnt = scr + 8 * 256;     // [16][256]
-  uint32_t* base = wcnt + 16 * 256;   // [2][256]
+  uint32_t* dsum = scr;             // [32] per-warp scan partials
+  uint32_t* wcnt = scr + 8 * 256;   // [16][256]: counts, then bases
   const uint32_t t = threadIdx.x, nt = blockDim.x, lane = t & 31, w = t >> 5, nw = nt >> 5;
+  const uint32_t lt = (1u << lane) - 1u;
   const uint32_t np = (hi - lo + 7) / 8;
-  for (uint32_t i = t; i < np * 256; i += nt) hist[i] = 0;
-  __syncthreads();
-  for (uint32_t i0 = t; i0 < n; i0 += U * nt) {  // U words per thread in flight
-    uint64_t x[U];
+  const uint32_t per = ((n + nw - 1) / nw + 31) & ~31u;
+  const uint32_t c0 = min(w * per, n), c1 = min(c0 + per, n);
+  uint64_t* src = w0;
+  uint64_t* dst = w1;
+  for (uint32_t p = 0; p < np; ++p) {
+    const uint32_t sh = lo + 8 * p;
+    uint32_t* row = wcnt + w * 256;
+    for (uint32_t k = lane; k < 256; k += 32) row[k] = 0;
+    __syncwarp();
+    // (a) digit counts of this warp's chunk
+    for (uint32_t i0 = c0; i0 < c1; i0 += 32 * U) {
+      uint64_t x[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) x[u] = i0 + u * nt < n ? w0[i0 + u * nt] : 0ull;
+      for (int u = 0; u < U; ++u) {
+        const uint32_t i = i0 + 32 * u + lane;
+        x[u] = i < c1 ? src[i] : 0ull;
+      }
 #pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (i0 + u * nt < n)
-        for (uint32_t p = 0; p < np; ++p)
-          atomicAdd(&hist[p * 256 + (uint32_t)((x[u] >> (lo + 8 * p)) & 255u)], 1u);
-  }
-  __syncthreads();
-  if (w < np) {  // exclusive scan of pass w's histogram: 8 bins per lane
-    uint32_t* h = hist + w * 256;
-    uint32_t v[8], sum = 0;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      v[k] = h[lane * 8 + k];
-      sum += v[k];
+      for (int u = 0; u < U; ++u) {
+        const bool valid = i0 + 32 * u + lane < c1;
+        const uint32_t d = valid ? (uint32_t)((x[u] >> sh) & 255u) : 256u;
+        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        if (valid && (peers & lt) == 0) row[d] += __popc(peers);
+        __syncwarp();
+      }
     }
-    uint32_t x = sum;
+    __syncthreads();
+    // (b) bases in (digit, warp) order
+    uint32_t tot = 0;
+    if (t < 256)
+      for (uint32_t q = 0; q < nw; ++q) tot += wcnt[q * 256 + t];
+    uint32_t x = tot;
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
       if ((int)lane >= o) x += y;
     }
-    uint32_t acc = x - sum;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      h[lane * 8 + k] = acc;
-      acc += v[k];
-    }
-  }
-  __syncthreads();
-  uint64_t* src = w0;
-  uint64_t* dst = w1;
-  const uint32_t lt = (1u << lane) - 1u;
-  for (uint32_t p = 0; p < np; ++p) {
-    const uint32_t sh = lo + 8 * p;
-    for (uint32_t d = t; d < 256; d += nt) base[d] = hist[p * 256 + d];
-    uint32_t cb = 0;
+    if (t < 256 && lane == 31) dsum[w] = x;
     __syncthreads();
-    // tiles of 4 x blockDim words; warp w owns the contiguous 128 words
-    // [t0 + 128w, t0 + 128w + 128), ranked in four 32-word sub-tiles with a
-    // running per-warp digit count, so the tile order (warp, sub-tile, lane)
-    // is element order and the sort stays stable
-    const uint32_t tile = 4 * nt;
-    for (uint32_t t0 = 0; t0 < n; t0 += tile) {
-      for (uint32_t k = lane; k < 256; k += 32) wcnt[w * 256 + k] = 0;
-      __syncwarp();
-      uint64_t x[4];
-      uint32_t d[4], lr[4];
+    if (t < 256) {
+      uint32_t acc = x - tot;
+      for (uint32_t k = 0; k < w; ++k) acc += dsum[k];
+      for (uint32_t q = 0; q < nw; ++q) {
+        const uint32_t c = wcnt[q * 256 + t];
+        wcnt[q * 256 + t] = acc;
+        acc += c;
+      }
+    }
+    __syncthreads();
+    // (c) scatter this warp's chunk in order
+    for (uint32_t i0 = c0; i0 < c1; i0 += 32 * U) {
+      uint64_t x2[U];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const uint32_t i = t0 + 128 * w + 32 * u + lane;
-        x[u] = i < n ? src[i] : 0ull;
+      for (int u = 0; u < U; ++u) {
+        const uint32_t i = i0 + 32 * u + lane;
+        x2[u] = i < c1 ? src[i] : 0ull;
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const uint32_t i = t0 + 128 * w + 32 * u + lane;
-        const bool valid = i < n;
-        d[u] = valid ? (uint32_t)((x[u] >> sh) & 255u) : 256u;
-        const uint32_t peers = __match_any_sync(0xffffffffu, d[u]);
+      for (int u = 0; u < U; ++u) {
+        const bool valid = i0 + 32 * u + lane < c1;
+        const uint32_t d = valid ? (uint32_t)((x2[u] >> sh) & 255u) : 256u;
+        const uint32_t peers = __match_any_sync(0xffffffffu, d);
         const uint32_t rank = __popc(peers & lt);
-        lr[u] = (valid ? wcnt[w * 256 + d[u]] : 0u) + rank;
+        const uint32_t pos = valid ? row[d] + rank : 0u;
         __syncwarp();
-        if (valid && rank == 0) wcnt[w * 256 + d[u]] += __popc(peers);
-        __syncwarp();
-      }
-      __syncthreads();
-      for (uint32_t dd = t; dd < 256; dd += nt) {  // per digit: warps' exclusive prefix
-        uint32_t acc = 0;
-        for (uint32_t q = 0; q < nw; ++q) {
-          const uint32_t c = wcnt[q * 256 + dd];
-          wcnt[q * 256 + dd] = acc;
-          acc += c;
+        if (valid) {
+          dst[pos] = x2[u];
+          if (rank == 0) row[d] += __popc(peers);
         }
-        base[(cb ^ 1u) * 256 + dd] = base[cb * 256 + dd] + acc;
+        __syncwarp();
       }
-      __syncthreads();
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (d[u] < 256u) dst[base[cb * 256 + d[u]] + wcnt[w * 256 + d[u]] + lr[u]] = x[u];
-      cb ^= 1u;
     }
     __syncthreads();
     uint64_t* tmp = src;
@@ -1476,6 +1533,14 @@ __device__ int32_t op_voxel(const WaveArgs& a, Cloud& c, Smem& S, const OpDesc& 
   const int32_t st = check_move(a, c, mm);
   if (st) return st;
   const float* d = F(c, a.role_data);
+  long long vt = (a.op_cycles && threadIdx.x == 0) ? clock64() : 0;
+  auto vmark = [&](int slot) {  // PCP_OP_TIMING: voxel phases in op_cycles[10..15]
+    if (a.op_cycles && threadIdx.x == 0) {
+      const long long t1 = clock64();
+      atomicAdd(a.op_cycles + 10 + slot, (unsigned long long)(t1 - vt));
+      vt = t1;
+    }
+  };
   float o[3];
   if (op.has_origin) {
     o[0] = op.origin[0]; o[1] = op.origin[1]; o[2] = op.origin[2];
@@ -1505,6 +1570,7 @@ __device__ int32_t op_voxel(const WaveArgs& a, Cloud& c, Smem& S, const OpDesc& 
   }
   bad = dev::block_reduce(bad, dev::OpOr{}, 0u, S.red);
   if (bad) return kOutOfBounds;
+  vmark(0);  // origin + extent pass
   uint32_t bx[3];
   for (int ax = 0; ax < 3; ++ax) {
     const uint32_t m = dev::block_reduce(mx[ax], dev::OpMax{}, 0u, S.red);
@@ -1542,6 +1608,7 @@ __device__ int32_t op_voxel(const WaveArgs& a, Cloud& c, Smem& S, const OpDesc& 
     }
   }
   __syncthreads();
+  vmark(1);  // key pass
   if (packed) {
     const int r = radix_sort8<U>(c.key[0], c.key[1], n, ib, ib + kb, c.sort_buf);
     W = c.key[r];
@@ -1553,18 +1620,77 @@ __device__ int32_t op_voxel(const WaveArgs& a, Cloud& c, Smem& S, const OpDesc& 
   const uint64_t imask = ib ? ((1ull << ib) - 1) : 0ull;
   auto key_at = [&](uint32_t k) -> uint64_t { return packed ? W[k] >> ib : K[k]; };
   auto pt_at = [&](uint32_t k) -> uint32_t { return packed ? (uint32_t)(W[k] & imask) : P[k]; };
+  vmark(2);  // sort
+  // voxel starts (key changes), warp-partitioned: each warp counts the starts
+  // in its contiguous chunk, one prefix over the warp totals, then each warp
+  // writes its starts in order (two barriers instead of a block scan per tile)
   uint32_t* seg = reinterpret_cast<uint32_t*>(c.ix[2]);
-  uint32_t base = 0;
-  for (uint32_t t0 = 0; t0 < n; t0 += blockDim.x) {
-    const uint32_t i = t0 + threadIdx.x;
-    const bool f = i < n && (i == 0 || key_at(i) != key_at(i - 1));
-    uint32_t tot;
-    const uint32_t rk = dev::block_scan_excl(f ? 1u : 0u, &tot, S.red);
-    if (f) seg[base + rk] = i;
-    base += tot;
+  uint32_t V = 0;
+  {
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const uint32_t per = ((n + nw - 1) / nw + 31) & ~31u;
+    const uint32_t c0 = min(w * per, n), c1 = min(c0 + per, n);
+    auto starts = [&](uint32_t i0, uint32_t (&bal)[U]) {
+      bool f[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t i = i0 + 32 * u + lane;
+        f[u] = i < c1 && (i == 0 || key_at(i) != key_at(i - 1));
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) bal[u] = __ballot_sync(0xffffffffu, f[u]);
+    };
+    uint32_t cnt = 0;
+    for (uint32_t i0 = c0; i0 < c1; i0 += 32 * U) {
+      uint32_t bal[U];
+      starts(i0, bal);
+#pragma unroll
+      for (int u = 0; u < U; ++u) cnt += __popc(bal[u]);
+    }
+    uint32_t* wt = reinterpret_cast<uint32_t*>(S.red);
+    __syncthreads();
+    if (lane == 0) wt[w] = cnt;
+    __syncthreads();
+    uint32_t run = 0;
+    for (uint32_t k = 0; k < nw; ++k) {
+      if (k < w) run += wt[k];
+      V += wt[k];
+    }
+    const uint32_t lt = (1u << lane) - 1u;
+    for (uint32_t i0 = c0; i0 < c1; i0 += 32 * U) {
+      uint32_t bal[U];
+      starts(i0, bal);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if ((bal[u] >> lane) & 1u) seg[run + __popc(bal[u] & lt)] = i0 + 32 * u + lane;
+        run += __popc(bal[u]);
+      }
+    }
+    __syncthreads();
+  }
+  vmark(3);  // segments
+  // 1) gather every moved field into sorted order (alt), one point per thread:
+  //    independent loads, many in flight (the per-voxel loop below would
+  //    otherwise chain index load -> data load -> add per point)
+  for (uint32_t k = threadIdx.x; k < n; k += blockDim.x) {
+    const uint64_t p = pt_at(k);
+    for (int f = 0; f < a.n_bytes_fields; ++f) {
+      if (!((mm >> f) & 1u)) continue;
+      const uint32_t es = c.elem[f];
+      if ((es & 3u) == 0) {
+        const uint32_t w = es >> 2;
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(c.cur[f]) + p * w;
+        uint32_t* dst = reinterpret_cast<uint32_t*>(c.alt[f]) + (uint64_t)k * w;
+        for (uint32_t q = 0; q < w; ++q) dst[q] = src[q];
+      } else {
+        for (uint32_t b = 0; b < es; ++b) c.alt[f][(uint64_t)k * es + b] = c.cur[f][p * es + b];
+      }
+    }
   }
   __syncthreads();
-  const uint32_t V = base;
+  // 2) per voxel: sequential double sums over its contiguous run -- the sort
+  //    is stable, so run order = original point order (grid_subsample's
+  //    accumulation order) -- written back into cur (dead after the gather)
   for (uint32_t v = threadIdx.x; v < V; v += blockDim.x) {
     const uint32_t s0 = seg[v], s1 = v + 1 < V ? seg[v + 1] : n;
     const double cnt = (double)(s1 - s0);
@@ -1574,30 +1700,38 @@ __device__ int32_t op_voxel(const WaveArgs& a, Cloud& c, Smem& S, const OpDesc& 
                        f == a.role_intensity;
       if (avg) {
         const uint32_t comps = c.elem[f] / 4;
-        const float* src = reinterpret_cast<const float*>(c.cur[f]);
-        float* dst = reinterpret_cast<float*>(c.alt[f]);
-        for (uint32_t q = 0; q < comps; ++q) {
-          double acc = 0.0;
-          for (uint32_t k = s0; k < s1; ++k) acc = __dadd_rn(acc, (double)src[(uint64_t)pt_at(k) * comps + q]);
-          dst[(uint64_t)v * comps + q] = __double2float_rn(__ddiv_rn(acc, cnt));
+        const float* src = reinterpret_cast<const float*>(c.alt[f]);
+        float* dst = reinterpret_cast<float*>(c.cur[f]);
+        if (comps <= 4) {
+          double acc[4] = {0.0, 0.0, 0.0, 0.0};
+          for (uint32_t k = s0; k < s1; ++k) {
+            const float* e = src + (uint64_t)k * comps;
+#pragma unroll
+            for (uint32_t q = 0; q < 4; ++q)
+              if (q < comps) acc[q] = __dadd_rn(acc[q], (double)e[q]);
+          }
+#pragma unroll
+          for (uint32_t q = 0; q < 4; ++q)
+            if (q < comps) dst[(uint64_t)v * comps + q] = __double2float_rn(__ddiv_rn(acc[q], cnt));
+        } else {
+          for (uint32_t q = 0; q < comps; ++q) {
+            double acc = 0.0;
+            for (uint32_t k = s0; k < s1; ++k) acc = __dadd_rn(acc, (double)src[(uint64_t)k * comps + q]);
+            dst[(uint64_t)v * comps + q] = __double2float_rn(__ddiv_rn(acc, cnt));
+          }
         }
       } else {
         const uint32_t es = c.elem[f];
-        const uint64_t p0 = pt_at(s0);
-        for (uint32_t b = 0; b < es; ++b) c.alt[f][(uint64_t)v * es + b] = c.cur[f][p0 * es + b];
+        for (uint32_t b = 0; b < es; ++b) c.cur[f][(uint64_t)v * es + b] = c.alt[f][(uint64_t)s0 * es + b];
       }
     }
     if (c.counts) c.counts[v] = (int32_t)(s1 - s0);
   }
   __syncthreads();
+  vmark(4);  // means
   if (threadIdx.x == 0) {
-    for (int f = 0; f < a.n_bytes_fields; ++f) {
-      if (!((mm >> f) & 1u)) continue;
-      uint8_t* tmp = c.cur[f];
-      c.cur[f] = c.alt[f];
-      c.alt[f] = tmp;
-      c.n[f] = V;
-    }
+    for (int f = 0; f < a.n_bytes_fields; ++f)
+      if ((mm >> f) & 1u) c.n[f] = V;
     if (op.counts) {
       c.has_counts = 1;
       c.n_counts = V;
@@ -1855,7 +1989,7 @@ __global__ void __launch_bounds__(512, MinBlocks) k_cloud(WaveArgs a) {
             status = kOutOfBounds;
             break;
           }
-          decode_bytes<1>(c.cur[f], blob + foff[f], flen[f], delta, S);
+          decode_bytes<1, MinBlocks == 1 ? 8 : 4>(c.cur[f], blob + foff[f], flen[f], delta, S);
           uint32_t e;
           if (f == a.role_data || f == a.role_normal || f == a.role_color) {
             e = 12;
@@ -1876,7 +2010,7 @@ __global__ void __launch_bounds__(512, MinBlocks) k_cloud(WaveArgs a) {
             break;
           }
           if (leader) {
-            decode_bytes<1>(a.out[of] + (uint64_t)s * a.out_stride[of], blob + foff[f],
+            decode_bytes<1, MinBlocks == 1 ? 8 : 4>(a.out[of] + (uint64_t)s * a.out_stride[of], blob + foff[f],
                                                  flen[f], delta, S);
             if (threadIdx.x == 0) a.out_len[(uint64_t)of * a.n_samples + s] = flen[f];
           }
