@@ -11,7 +11,8 @@ A step = one pass of the hot path (page CRC + decode, record parse, the
 config's op chain, batch assembly) over this rank's shard of the synthetic
 dataset (record-sharded by slice, no collective on the data path).
 `value`: pages resident in HBM before the timed region.  `e2e`: pages in
-pinned host memory, per-wave H2D and per-batch D2H of every field inside the
+pinned host memory, per-wave H2D of the pages and every batch delivered in
+pinned host memory (host_batches: one D2H per field per wave) inside the
 timed region, through the C ABI (pcp_pipeline_* ).  Inputs per step exceed
 the 126 MB L2, so no flush is needed between steps.
 """
@@ -219,6 +220,7 @@ def main():
     ap.add_argument("--clouds-per-gpu", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-no-d2h", action="store_true", help="diagnostics: e2e without the batch reads")
     ap.add_argument("--cpu-sample", type=int, default=0, help="clouds per CPU step")
     ap.add_argument("--batch", type=int, default=0, help="override the config's batch size (diagnostics)")
     args = ap.parse_args()
@@ -278,16 +280,17 @@ def main():
     g = graph_for(args.config, cfg)
     points_per_step = 0
 
-    pinned = {}  # (field, ring slot) -> pinned host buffer, power-of-two size classes
 
     def timed(resident, steps, d2h):
-        p = P.Pipeline(primary, g, ids=ids, device=local, epochs=steps, resident=resident)
+        # d2h: host_batches -- every batch delivered in pinned host memory, as the
+        # reference's Pipeline::next_batch returns host Batches (one D2H per field
+        # per wave inside the library, the host waits for it before serving)
+        p = P.Pipeline(primary, g, ids=ids, device=local, epochs=steps, resident=resident,
+                       host_batches=d2h)
         st0 = p.stats()
-        d2h_bytes = 0
         barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        d2h_async = P.lib().pcp_memcpy_d2h_async
         with Clocks(local) as ck:
             e0.record()
             nb = 0
@@ -298,27 +301,13 @@ def main():
                 if b is None:
                     break
                 nb += 1
-                if d2h:
-                    # every field of every batch into pinned host memory, async on
-                    # the pipeline's serve stream (a ring of host buffers per field);
-                    # the closing device synchronize waits for the last copies
-                    for k in range(b.n_fields):
-                        f = b.fields[k]
-                        nbytes = f.nbytes
-                        key = (k, nb % 64)
-                        buf = pinned.get(key)
-                        if buf is None or buf.numel() < nbytes:
-                            cls = 1 << max(12, (max(nbytes, 1) - 1).bit_length())
-                            buf = pinned[key] = torch.empty(cls, dtype=torch.uint8, pin_memory=True)
-                        d2h_async(buf.data_ptr(), f.d_ptr, nbytes, p.stream)
-                        d2h_bytes += nbytes
             torch.cuda.synchronize()
             e1.record()
             e1.synchronize()
         ms = e0.elapsed_time(e1)
         st1 = p.stats()
         p.close()
-        return ms, st0, st1, nb, d2h_bytes, ck.summary()
+        return ms, st0, st1, nb, st1["d2h_bytes"] - st0["d2h_bytes"], ck.summary()
 
     # warm-up (W steps), then K timed steps on a fresh pipeline
     timed(True, args.warmup, False)
@@ -365,11 +354,20 @@ def main():
         roof["traffic_over_alg"] = dram / alg_per_launch
     e2e = None
     if not args.no_e2e:
-        timed(False, 1, True)  # untimed: allocate the pinned host buffers
-        ems, est0, est1, enb, d2h, _ = timed(False, args.steps, True)
+        timed(False, 1, True)  # untimed: fills the library's pinned-buffer pool
+        ems, est0, est1, enb, d2h, _ = timed(False, args.steps, not args.e2e_no_d2h)
         te = torch.tensor([ems], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        if os.environ.get("PCP_BENCH_DEBUG"):
+            print("e2e stats:", {k: est1[k] - est0[k] for k in ("cloud_kernel_ms", "decode_kernel_ms", "waves",
+                                                               "h2d_bytes", "host_launch_ms", "host_wait_ms")}, "ms", ems,
+                  "| resident:", {k: st1[k] - st0[k] for k in ("cloud_kernel_ms", "decode_kernel_ms", "waves",
+                                                              "host_launch_ms", "host_wait_ms")},
+                  "ms", ms, file=sys.stderr)
+            for row in est1.get("timeline", []):
+                print("wave h2d %.2f-%.2f decode %.2f-%.2f cloud %.2f-%.2f done %.2f host %.2f" % tuple(row),
+                      file=sys.stderr)
         e_clouds = est1["clouds"] - est0["clouds"]
         tc = torch.tensor([e_clouds], dtype=torch.float64, device="cuda")
         if world > 1:
@@ -377,9 +375,9 @@ def main():
         e2e = {"value": float(tc.item()) / (float(te.item()) / 1e3), "unit": "clouds/s",
                "h2d_bytes_per_step": (est1["h2d_bytes"] - est0["h2d_bytes"]) // args.steps,
                "d2h_bytes_per_step": d2h // args.steps,
-               "path": "pcp_pipeline_open(resident=false) + pcp_pipeline_next_batch + "
-                       "pcp_memcpy_d2h_async of every batch field into pinned host memory "
-                       "(device-synchronized before the clock stops)"}
+               "path": "pcp_pipeline_open(resident=false, host_batches=true) + "
+                       "pcp_pipeline_next_batch: pages H2D from pinned host memory each wave, "
+                       "every batch field delivered in pinned host memory (pcp_field.h_ptr)"}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         ids_cpu = np.arange(min(cpu_sample, len(idx)), dtype=np.uint64)

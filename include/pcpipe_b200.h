@@ -155,7 +155,11 @@ int pcp_write_dataset(const char* out_dir, const char* stem, const char* schema_
  * source → maps → batch on `device`.  entry_ids (optional) is the list of
  * index entries this pipeline walks — e.g. one GPU's shard; index i of the
  * walk is the seed index, like Item.index (pipeline.cpp:447-448).
- * Options: JSON {"epochs": n, "resident": true|false, "wave_batches": k}. */
+ * Options: JSON {"epochs": n, "resident": true|false, "wave_batches": k,
+ * "slots": s, "host_batches": true|false}.  host_batches delivers every batch
+ * in pinned host memory (pcp_field.h_ptr), like the reference's host Batch:
+ * once a wave's kernels finish, its fields are copied with one D2H per field
+ * (one per sample for ragged fields). */
 typedef struct pcp_pipeline pcp_pipeline;
 
 int pcp_pipeline_open(const char* primary_path, const char* graph_json,
@@ -170,6 +174,9 @@ typedef struct {
   uint64_t nbytes;           /* total bytes */
   const uint64_t* h_offsets; /* host [n_samples+1] byte offsets per sample */
   int32_t uniform;           /* 1 when every sample has the same length */
+  const uint8_t* h_ptr;      /* option host_batches: the field in pinned host
+                                memory (else NULL); d_ptr is then NULL for a
+                                ragged field */
 } pcp_field;
 
 typedef struct {

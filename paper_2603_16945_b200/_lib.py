@@ -47,7 +47,7 @@ class PcError(RuntimeError):
 class _Field(C.Structure):
     _fields_ = [("name", C.c_char * 48), ("kind", C.c_int32), ("d_ptr", C.c_void_p),
                 ("nbytes", C.c_uint64), ("h_offsets", C.POINTER(C.c_uint64)),
-                ("uniform", C.c_int32)]
+                ("uniform", C.c_int32), ("h_ptr", C.c_void_p)]
 
 
 class _Batch(C.Structure):
@@ -190,11 +190,11 @@ class Pipeline:
 
     def __init__(self, primary, graph, ids=None, device: int = 0, epochs: int = 1,
                  resident: bool = True, wave_batches: int = 0, force_serial_fy: bool = False,
-                 slots: int | None = None):
+                 slots: int | None = None, host_batches: bool = False):
         L = lib()
         g = graph if isinstance(graph, str) else json.dumps(graph)
         o = {"epochs": epochs, "resident": resident, "wave_batches": wave_batches,
-             "force_serial_fy": force_serial_fy}
+             "force_serial_fy": force_serial_fy, "host_batches": host_batches}
         if slots is not None:
             o["slots"] = slots
         opts = json.dumps(o)
@@ -226,6 +226,25 @@ class Pipeline:
             self._next = lib().pcp_pipeline_next_batch
         _check(self._next(self._h, C.byref(self._raw), C.byref(self._eos)))
         return None if self._eos.value else self._raw
+
+    def next_host_batch(self) -> dict | None:
+        """host_batches pipelines: the next batch as ``{name: (array, offsets)}``
+        copied out of the library's pinned wave buffer (the layout of
+        ``DeviceBatch.to_host``), or None at the end."""
+        b = self.next_batch_raw()
+        if b is None:
+            return None
+        out = {}
+        for i in range(b.n_fields):
+            f = b.fields[i]
+            if not f.h_ptr and f.nbytes:
+                raise PcError(1, "pipeline was not opened with host_batches")
+            kind = f.kind
+            raw = np.ctypeslib.as_array(C.cast(f.h_ptr, C.POINTER(C.c_uint8)), shape=(f.nbytes,)).copy() \
+                if f.nbytes else np.empty(0, np.uint8)
+            offs = np.ctypeslib.as_array(f.h_offsets, shape=(b.n_samples + 1,)).copy()
+            out[f.name.decode()] = (raw.view(_DTYPE_OF_KIND.get(kind, np.uint8)) if kind != 5 else raw, offs)
+        return out
 
     def __iter__(self):
         while True:

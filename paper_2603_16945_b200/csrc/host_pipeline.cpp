@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -105,6 +106,55 @@ struct HostBuf {  // pinned
     want = std::max<size_t>(want, 256);
     CK(cudaMallocHost(&p, want));
     n = want;
+  }
+  template <typename T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+// Process-wide pool of pinned host blocks (power-of-two sizes): a pipeline
+// reopened on the same process (e.g. a new epoch range) reuses the blocks
+// instead of paying cudaMallocHost again.
+struct PinnedPool {
+  std::mutex mu;
+  std::multimap<size_t, void*> free_blocks;
+  static PinnedPool& get() {
+    static PinnedPool* p = new PinnedPool;  // never destroyed: blocks outlive atexit order
+    return *p;
+  }
+  void* take(size_t want, size_t* got) {
+    size_t cls = 4096;
+    while (cls < want) cls <<= 1;
+    {
+      std::lock_guard<std::mutex> l(mu);
+      auto it = free_blocks.lower_bound(cls);
+      if (it != free_blocks.end() && it->first <= 2 * cls) {
+        void* q = it->second;
+        *got = it->first;
+        free_blocks.erase(it);
+        return q;
+      }
+    }
+    void* q = nullptr;
+    CK(cudaMallocHost(&q, cls));
+    *got = cls;
+    return q;
+  }
+  void give(void* q, size_t n) {
+    std::lock_guard<std::mutex> l(mu);
+    free_blocks.emplace(n, q);
+  }
+};
+
+struct PooledHostBuf {
+  void* p = nullptr;
+  size_t n = 0;
+  ~PooledHostBuf() {
+    if (p) PinnedPool::get().give(p, n);
+  }
+  void ensure(size_t want) {
+    if (want <= n) return;
+    if (p) PinnedPool::get().give(p, n);
+    p = PinnedPool::get().take(want, &n);
   }
   template <typename T>
   T* as() const { return static_cast<T*>(p); }
@@ -394,6 +444,7 @@ struct Wave {
   bool launched = false;
   cudaStream_t stream = nullptr;  // one stream per slot: consecutive waves overlap
   cudaEvent_t done = nullptr, k0 = nullptr, k1 = nullptr, d0 = nullptr, d1 = nullptr;
+  cudaEvent_t h0 = nullptr, h1 = nullptr;  // staging copies (timeline diagnostics)
   cudaEvent_t served = nullptr;  // serve stream passed this wave's last batch (user copies enqueued)
   uint64_t decode_alg_bytes = 0;  // payload + raw bytes of the pages k_page_decode handles
   DevBuf gscratch;                // k_cloud global slab (smem_mode 0), per slot
@@ -410,6 +461,11 @@ struct Wave {
   uint64_t* h_len = nullptr;
   uint64_t in_payload_bytes = 0, in_points = 0;
   std::vector<std::vector<uint64_t>> offsets;  // per field, for the served batch
+  // host_batches: the whole wave's batch fields in pinned host memory
+  PooledHostBuf h_out;
+  std::vector<uint64_t> h_base;                 // per field: offset in h_out
+  std::vector<std::vector<uint64_t>> woff;      // per field: n+1 sample offsets
+  cudaEvent_t host_ready = nullptr;
 };
 
 }  // namespace
@@ -422,6 +478,7 @@ struct Pipeline {
   std::vector<Entry> index, walk;
   bool resident = true;
   uint32_t wave_batches = 0;
+  bool host_batches = false;  // deliver batches in pinned host memory (one D2H per field per wave)
   uint32_t n_slots = 4;  // wave slots (streams): n_slots - 1 waves in flight while one is served
   bool slots_set = false;
   uint64_t epochs = 1;
@@ -463,7 +520,13 @@ struct Pipeline {
   uint64_t clouds = 0, points_in = 0, payload_bytes = 0, batches = 0;
   uint64_t h2d_bytes = 0, launches = 0, alg_bytes = 0;
   double kernel_ms = 0, cloud_kernel_ms = 0, decode_kernel_ms = 0;
+  double host_launch_ms = 0, host_wait_ms = 0;  // host-side wall time (diagnostics)
+  bool timeline_on = false;
+  cudaEvent_t t_open = nullptr;
+  std::chrono::steady_clock::time_point host_open;
+  std::vector<std::vector<double>> timeline;
   uint64_t decode_alg_bytes = 0;
+  uint64_t d2h_bytes = 0;  // host_batches: batch bytes copied to host
   uint32_t waves_done = 0;
 
   ~Pipeline() {
@@ -474,7 +537,12 @@ struct Pipeline {
       if (w.k1) cudaEventDestroy(w.k1);
       if (w.d0) cudaEventDestroy(w.d0);
       if (w.d1) cudaEventDestroy(w.d1);
+      if (w.h0) cudaEventDestroy(w.h0);
+      if (w.h1) cudaEventDestroy(w.h1);
       if (w.served) cudaEventDestroy(w.served);
+      if (w.host_ready) cudaEventDestroy(w.host_ready);
+      if (t_open) cudaEventDestroy(t_open);
+      t_open = nullptr;
     }
     if (stream) cudaStreamDestroy(stream);
     if (serve_stream) cudaStreamDestroy(serve_stream);
@@ -491,6 +559,7 @@ struct Pipeline {
       epochs = o.value("epochs", uint64_t{1});
       resident = o.value("resident", true);
       wave_batches = o.value("wave_batches", 0u);
+      host_batches = o.value("host_batches", false);
       if (o.contains("slots")) {
         n_slots = std::max(2u, std::min(8u, o.value("slots", n_slots)));
         slots_set = true;
@@ -540,8 +609,19 @@ struct Pipeline {
       CK(cudaEventCreate(&w.k1));
       CK(cudaEventCreate(&w.d0));
       CK(cudaEventCreate(&w.d1));
+      CK(cudaEventCreate(&w.h0));
+      CK(cudaEventCreate(&w.h1));
       CK(cudaEventCreateWithFlags(&w.served, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&w.host_ready, cudaEventDisableTiming));
       CK(cudaEventRecord(w.served, serve_stream));
+    }
+    if (const char* e = std::getenv("PCP_TIMELINE")) timeline_on = std::atoi(e) != 0;
+    if (timeline_on) {
+      CK(cudaDeviceSynchronize());
+      CK(cudaEventCreate(&t_open));
+      CK(cudaEventRecord(t_open, serve_stream));
+      CK(cudaEventSynchronize(t_open));
+      host_open = std::chrono::steady_clock::now();
     }
   }
 
@@ -1012,8 +1092,11 @@ struct Pipeline {
       out_total += align16(outs[f].stride * w.n) + 64;
     }
     w.outs.ensure(out_total);
+    // host_batches: size the pinned wave buffer up front (exact for fixed-size
+    // fields; ragged ones grow it on demand past 1 GiB)
+    if (host_batches) w.h_out.ensure(std::min<uint64_t>(out_total + 64, 1ull << 30));
     if (proto.split_at) w.handoff.ensure(proto.handoff_stride * w.n);
-    w.h_res.ensure(3 * align16(w.n * 4) + outs.size() * w.n * 8);
+    w.h_res.ensure(total - o_sst + 16);
     {
       uint64_t need = 0;
       for (size_t q = 0; q < outs.size(); ++q) need += align16(outs[q].stride * B) + 64;
@@ -1032,6 +1115,7 @@ struct Pipeline {
     uint8_t* dt = w.tables.as<uint8_t>();
     // staged input bytes
     const uint8_t* bytes = d_store.as<uint8_t>();
+    CK(cudaEventRecord(w.h0, w.stream));
     if (!resident) {
       uint64_t d_at = 64;
       for (const auto& r : runs) {
@@ -1043,6 +1127,7 @@ struct Pipeline {
       for (const auto& r : runs) h2d_bytes += r.second;
     }
     CK(cudaMemcpyAsync(dt, ht, up_bytes, cudaMemcpyHostToDevice, w.stream));
+    CK(cudaEventRecord(w.h1, w.stream));
     CK(cudaMemsetAsync(dt + o_acc, 0, o_len - o_acc, w.stream));
     // ---- args ----------------------------------------------------------------
     a.bytes = bytes;
@@ -1095,10 +1180,12 @@ struct Pipeline {
     w.h_op = reinterpret_cast<int32_t*>(hr + align16(w.n * 4));
     w.h_where = reinterpret_cast<int32_t*>(hr + 2 * align16(w.n * 4));
     w.h_len = reinterpret_cast<uint64_t*>(hr + 3 * align16(w.n * 4));
-    CK(cudaMemcpyAsync(w.h_status, dt + o_sst, w.n * 4, cudaMemcpyDeviceToHost, w.stream));
-    CK(cudaMemcpyAsync(w.h_op, dt + o_sop, w.n * 4, cudaMemcpyDeviceToHost, w.stream));
-    CK(cudaMemcpyAsync(w.h_where, dt + o_swh, w.n * 4, cudaMemcpyDeviceToHost, w.stream));
-    CK(cudaMemcpyAsync(w.h_len, dt + o_len, outs.size() * w.n * 8, cudaMemcpyDeviceToHost, w.stream));
+    // one contiguous region: the host layout mirrors o_sst..total
+    static_assert(sizeof(int32_t) == 4, "");
+    uint8_t* hr_dev = nullptr;
+    CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&hr_dev), hr, 0));
+    CK(launch_store_host(dt + o_sst, hr_dev, total - o_sst, w.stream));
+    ++launches;
     CK(cudaEventRecord(w.done, w.stream));
     w.launched = true;
   }
@@ -1120,28 +1207,105 @@ struct Pipeline {
     return "op " + std::to_string(node) + ": " + errc_name(st) + ": " + what;
   }
 
+  // host_batches: once a wave's kernels are done, its batch fields go to
+  // pinned host memory on the serve stream -- one D2H per field when every
+  // sample fills its slot (the slots are then contiguous), one per sample for
+  // ragged fields -- and the wave's first batch waits for them.
+  void stage_host(Wave& w) {
+    const uint64_t n = w.n;
+    w.woff.assign(outs.size(), std::vector<uint64_t>(n + 1, 0));
+    w.h_base.assign(outs.size(), 0);
+    std::vector<uint8_t> dense(outs.size(), 1);
+    uint64_t total = 0;
+    for (size_t f = 0; f < outs.size(); ++f) {
+      auto& off = w.woff[f];
+      for (uint64_t k = 0; k < n; ++k) {
+        const uint64_t L = w.h_len[f * n + k];
+        off[k + 1] = off[k] + L;
+        if (L != outs[f].stride) dense[f] = 0;
+      }
+      w.h_base[f] = total;
+      total = align16(total + off[n]) + 64;
+    }
+    w.h_out.ensure(total + 64);
+    uint8_t* ho = w.h_out.as<uint8_t>();
+    for (size_t f = 0; f < outs.size(); ++f) {
+      const uint8_t* src = w.outs.as<uint8_t>() + w.out_base[f];
+      uint8_t* dst = ho + w.h_base[f];
+      const auto& off = w.woff[f];
+      if (dense[f]) {
+        if (off[n]) CK(cudaMemcpyAsync(dst, src, off[n], cudaMemcpyDeviceToHost, serve_stream));
+      } else {
+        for (uint64_t k = 0; k < n; ++k)
+          if (off[k + 1] > off[k])
+            CK(cudaMemcpyAsync(dst + off[k], src + k * outs[f].stride, off[k + 1] - off[k],
+                               cudaMemcpyDeviceToHost, serve_stream));
+      }
+      d2h_bytes += off[n];
+    }
+    CK(cudaEventRecord(w.host_ready, serve_stream));
+    CK(cudaEventSynchronize(w.host_ready));
+  }
+
   // ---- iteration -------------------------------------------------------------
   int next_batch(pcp_batch* out, int* eos) {
     *eos = 0;
     if (failed) fail(fail_code, fail_msg);
     if (cur < 0 || served >= slots[cur].n_batches) {
-      if (cur >= 0) ++waves_done;
       const int ns = (int)slots.size();
+      using clk = std::chrono::steady_clock;
+      auto ms_since = [](clk::time_point t0) {
+        return std::chrono::duration<double, std::milli>(clk::now() - t0).count();
+      };
+      if (cur >= 0) {
+        // every batch of the served wave was handed out: its slot is free once
+        // the copies the user enqueued on the serve stream are done (the next
+        // wave in it waits on this event on the device)
+        ++waves_done;
+        CK(cudaEventRecord(slots[cur].served, serve_stream));
+        slots[cur].launched = false;
+      }
       const int nxt = cur < 0 ? 0 : (cur + 1) % ns;
       Wave& wn = slots[nxt];
       if (!wn.launched) {
         if (next_plan >= plan.size()) {
           *eos = 1;
+          cur = -1;  // repeated calls stay at end of stream
           return kOk;
         }
+        const auto t0 = clk::now();
         launch(wn, next_plan++);
+        host_launch_ms += ms_since(t0);
       }
+      // keep every slot busy while waiting: waves go to slots in ring order
+      // on per-slot streams, so up to `slots` waves overlap (copies, LZ4
+      // chains and k_cloud of different waves)
+      for (int d = 1; d < ns && next_plan < plan.size(); ++d) {
+        Wave& wp = slots[(nxt + d) % ns];
+        if (!wp.launched) {
+          const auto t0 = clk::now();
+          launch(wp, next_plan++);
+          host_launch_ms += ms_since(t0);
+        }
+      }
+      const auto tw = clk::now();
       CK(cudaEventSynchronize(wn.done));
+      host_wait_ms += ms_since(tw);
       float ms = 0;
       CK(cudaEventElapsedTime(&ms, wn.k0, wn.k1));
       cloud_kernel_ms += ms;
       CK(cudaEventElapsedTime(&ms, wn.d0, wn.d1));
       decode_kernel_ms += ms;
+      if (timeline_on) {  // PCP_TIMELINE=1: per-wave event times (ms from open)
+        std::vector<double> row;
+        for (cudaEvent_t e : {wn.h0, wn.h1, wn.d0, wn.d1, wn.k0, wn.k1, wn.done}) {
+          float t = 0;
+          CK(cudaEventElapsedTime(&t, t_open, e));
+          row.push_back(t);
+        }
+        row.push_back(std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - host_open).count());
+        timeline.push_back(row);
+      }
       decode_alg_bytes += wn.decode_alg_bytes;
       if (lz4_timing && wn.n_todo) {
         std::vector<long long> tm(wn.n_todo * 16);
@@ -1154,10 +1318,6 @@ struct Pipeline {
               lz4_phase_cycles[ph] = std::max(lz4_phase_cycles[ph], c);
             }
       }
-      if (cur >= 0) {
-        CK(cudaEventRecord(slots[cur].served, serve_stream));
-        slots[cur].launched = false;
-      }
       cur = nxt;
       served = 0;
       clouds += wn.n;
@@ -1166,11 +1326,11 @@ struct Pipeline {
       alg_bytes += wn.in_payload_bytes;
       points_in += wn.in_points;
       payload_bytes += wn.in_payload_bytes;
-      // keep slots-1 waves in flight ahead of the one being served (waves go
-      // to slots in ring order on per-slot streams, so they overlap)
-      for (int d = 1; d < ns && next_plan < plan.size(); ++d) {
-        Wave& wp = slots[(cur + d) % ns];
-        if (!wp.launched) launch(wp, next_plan++);
+      if (host_batches) {
+        // a failed wave is reported below, before any copy of its batches
+        bool ok = true;
+        for (uint64_t s = 0; s < wn.n && ok; ++s) ok = wn.h_status[s] == kOk;
+        if (ok) stage_host(wn);
       }
     }
     Wave& w = slots[cur];
@@ -1210,8 +1370,11 @@ struct Pipeline {
       pf.nbytes = off[nb];
       pf.h_offsets = off.data();
       uint8_t* slot0 = w.outs.as<uint8_t>() + w.out_base[f] + s0 * outs[f].stride;
+      if (host_batches) pf.h_ptr = w.h_out.as<uint8_t>() + w.h_base[f] + w.woff[f][s0];
       if (dense) {
         pf.d_ptr = slot0;
+      } else if (host_batches) {
+        pf.d_ptr = nullptr;  // ragged field: host copy only
       } else {
         // pack the batch's slots into CSR (one small kernel, synchronous)
         const uint64_t meta = 2 * (nb + 1) * 8;
@@ -1247,6 +1410,10 @@ struct Pipeline {
            {"decode_kernel_ms", decode_kernel_ms},
            {"decode_kernel_alg_bytes", decode_alg_bytes},
            {"h2d_bytes", h2d_bytes},
+           {"d2h_bytes", d2h_bytes},
+           {"host_launch_ms", host_launch_ms},
+           {"host_wait_ms", host_wait_ms},
+           {"timeline", timeline},
            {"launches", launches},
            {"grid", grid},
            {"threads", threads},

@@ -2451,6 +2451,23 @@ cudaError_t launch_compact(const uint8_t* src, uint64_t stride, const uint64_t* 
   return cudaGetLastError();
 }
 
+// Wave results (status / op / where / lengths) stored straight into mapped
+// pinned host memory by the SMs: posted PCIe writes, so the small result
+// read-back never queues in the copy engine behind (or ahead of) the bulk
+// batch copies of other waves.  n is a multiple of 16, both ends 16-B aligned.
+__global__ void k_store_host(const uint4* __restrict__ src, uint4* __restrict__ dst, uint64_t n16) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n16; i += (uint64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
+cudaError_t launch_store_host(const uint8_t* src, uint8_t* dst_mapped, uint64_t n, cudaStream_t st) {
+  const uint64_t n16 = (n + 15) / 16;
+  if (!n16) return cudaSuccess;
+  const uint32_t blocks = (uint32_t)std::min<uint64_t>(148, (n16 + 255) / 256);
+  k_store_host<<<blocks, 256, 0, st>>>(reinterpret_cast<const uint4*>(src), reinterpret_cast<uint4*>(dst_mapped), n16);
+  return cudaGetLastError();
+}
+
 cudaError_t occupancy_cloud(int* n, int threads, size_t smem, int min_blocks) {
   return min_blocks == 2 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(n, k_cloud<2>, threads, smem)
                          : cudaOccupancyMaxActiveBlocksPerMultiprocessor(n, k_cloud<1>, threads, smem);

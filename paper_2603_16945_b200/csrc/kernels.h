@@ -39,6 +39,8 @@ cudaError_t occupancy_cloud(int* n, int threads, size_t smem, int min_blocks);
 // Max co-resident clusters of `cluster` CTAs (k_cloud<1>, or k_apply_set).
 cudaError_t occupancy_cloud_clusters(int* n, int threads, size_t smem, uint32_t cluster, bool apply);
 cudaError_t set_apply_smem(size_t bytes);
+// n bytes (rounded up to 16) from device memory into mapped pinned host memory.
+cudaError_t launch_store_host(const uint8_t* src, uint8_t* dst_mapped, uint64_t n, cudaStream_t st);
 cudaError_t launch_compact(const uint8_t* src, uint64_t stride, const uint64_t* d_off,
                            const uint64_t* d_len, uint32_t n, uint8_t* dst, cudaStream_t st);
 

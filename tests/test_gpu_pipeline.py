@@ -223,6 +223,40 @@ def test_async_d2h_matches_sync(pcp, tmp_path, slots):
             assert np.array_equal(buf.numpy()[:nbytes], wb[name][0].view(np.uint8)), name
 
 
+@pytest.mark.parametrize("kind,resident", [("shapenet", True), ("shapenet", False),
+                                           ("kitti", True), ("kitti", False)])
+def test_host_batches_match_device_batches(pcp, tmp_path, kind, resident):
+    """host_batches (one D2H per field per wave into pinned host memory;
+    per-sample copies for ragged fields, e.g. voxel outputs) serves the same
+    bytes and offsets as the device batches, across slot reuse."""
+    from paper_2603_16945_b200 import synth
+    if kind == "shapenet":
+        primary = _ds(pcp, tmp_path, "shapenet", 96, group=8, n_points=700)
+        g = synth.graph(synth.CHAINS["shapenet_part"], batch_size=4)
+    else:
+        primary = _ds(pcp, tmp_path, "kitti", 24, group=4, lo=3000, hi=5000)
+        g = synth.graph(synth.CHAINS["kitti"], batch_size=2)
+    want = [b.to_host() for b in pcp.Pipeline(primary, g, wave_batches=2, slots=2, epochs=2)]
+    p = pcp.Pipeline(primary, g, wave_batches=2, slots=2, epochs=2, resident=resident, host_batches=True)
+    got = []
+    while True:
+        b = p.next_host_batch()
+        if b is None:
+            break
+        got.append(b)
+    st = p.stats()
+    p.close()
+    assert len(got) == len(want)
+    total = 0
+    for gb, wb in zip(got, want):
+        assert gb.keys() == wb.keys()
+        for name in wb:
+            assert np.array_equal(gb[name][1], wb[name][1]), name
+            assert np.array_equal(gb[name][0].view(np.uint8), wb[name][0].view(np.uint8)), name
+            total += wb[name][0].nbytes
+    assert st["d2h_bytes"] == total
+
+
 def _adversarial_blob(rng, n):
     """Bytes that drive the LZ4 decoder through its corner cases: runs of one
     byte and short-period patterns (self-overlapping matches, offsets 1..8),
