@@ -1672,18 +1672,56 @@ __device__ int32_t op_voxel(const WaveArgs& a, Cloud& c, Smem& S, const OpDesc& 
   // 1) gather every moved field into sorted order (alt), one point per thread:
   //    independent loads, many in flight (the per-voxel loop below would
   //    otherwise chain index load -> data load -> add per point)
-  for (uint32_t k = threadIdx.x; k < n; k += blockDim.x) {
-    const uint64_t p = pt_at(k);
-    for (int f = 0; f < a.n_bytes_fields; ++f) {
-      if (!((mm >> f) & 1u)) continue;
-      const uint32_t es = c.elem[f];
-      if ((es & 3u) == 0) {
-        const uint32_t w = es >> 2;
-        const uint32_t* src = reinterpret_cast<const uint32_t*>(c.cur[f]) + p * w;
-        uint32_t* dst = reinterpret_cast<uint32_t*>(c.alt[f]) + (uint64_t)k * w;
-        for (uint32_t q = 0; q < w; ++q) dst[q] = src[q];
-      } else {
-        for (uint32_t b = 0; b < es; ++b) c.alt[f][(uint64_t)k * es + b] = c.cur[f][p * es + b];
+  //    (4 points per thread per round for 4- and 12-byte points)
+  for (int f = 0; f < a.n_bytes_fields; ++f) {
+    if (!((mm >> f) & 1u)) continue;
+    const uint32_t es = c.elem[f];
+    if (es == 12 || es == 4) {
+      const uint32_t w = es >> 2;
+      const uint32_t* src = reinterpret_cast<const uint32_t*>(c.cur[f]);
+      uint32_t* dst = reinterpret_cast<uint32_t*>(c.alt[f]);
+      for (uint32_t k0 = threadIdx.x; k0 < n; k0 += 4 * blockDim.x) {
+        uint64_t p[4];
+        uint32_t v[4][3];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t k = k0 + u * blockDim.x;
+          p[u] = k < n ? pt_at(k) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t k = k0 + u * blockDim.x;
+          if (k < n) {
+            v[u][0] = src[p[u] * w];
+            if (w == 3) {
+              v[u][1] = src[p[u] * 3 + 1];
+              v[u][2] = src[p[u] * 3 + 2];
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t k = k0 + u * blockDim.x;
+          if (k < n) {
+            dst[(uint64_t)k * w] = v[u][0];
+            if (w == 3) {
+              dst[(uint64_t)k * 3 + 1] = v[u][1];
+              dst[(uint64_t)k * 3 + 2] = v[u][2];
+            }
+          }
+        }
+      }
+    } else {
+      for (uint32_t k = threadIdx.x; k < n; k += blockDim.x) {
+        const uint64_t p = pt_at(k);
+        if ((es & 3u) == 0) {
+          const uint32_t w = es >> 2;
+          const uint32_t* src = reinterpret_cast<const uint32_t*>(c.cur[f]) + p * w;
+          uint32_t* dst = reinterpret_cast<uint32_t*>(c.alt[f]) + (uint64_t)k * w;
+          for (uint32_t q = 0; q < w; ++q) dst[q] = src[q];
+        } else {
+          for (uint32_t b = 0; b < es; ++b) c.alt[f][(uint64_t)k * es + b] = c.cur[f][p * es + b];
+        }
       }
     }
   }
