@@ -378,6 +378,23 @@ def main():
                "path": "pcp_pipeline_open(resident=false, host_batches=true) + "
                        "pcp_pipeline_next_batch: pages H2D from pinned host memory each wave, "
                        "every batch field delivered in pinned host memory (pcp_field.h_ptr)"}
+        # the e2e bound: page bytes over PCIe against a plain pinned H2D copy
+        # measured now on this box (256 MiB x 4)
+        h2d_total = est1["h2d_bytes"] - est0["h2d_bytes"]
+        hb = torch.empty(256 << 20, dtype=torch.uint8, pin_memory=True)
+        db = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+        db.copy_(hb, non_blocking=True)
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record()
+        for _ in range(4):
+            db.copy_(hb, non_blocking=True)
+        c1.record()
+        c1.synchronize()
+        peak_h2d = 4 * (256 << 20) / (c0.elapsed_time(c1) / 1e3) / 1e9
+        del hb, db
+        e2e["pcie"] = {"h2d_gbs": h2d_total / (ems / 1e3) / 1e9, "h2d_peak_gbs": peak_h2d,
+                       "frac": h2d_total / (ems / 1e3) / 1e9 / peak_h2d,
+                       "d2h_gbs": d2h / (ems / 1e3) / 1e9}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         ids_cpu = np.arange(min(cpu_sample, len(idx)), dtype=np.uint64)
