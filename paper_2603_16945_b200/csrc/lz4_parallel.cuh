@@ -39,8 +39,8 @@ constexpr uint32_t kRing = 16384;      // shared-memory output window (bytes)
 constexpr uint32_t kStageTail = 128;   // staged bytes past a window for its last tokens
 constexpr uint32_t kStageBytes = kChunk + kStageTail + 32;  // + 16-B alignment slack (TMA)
 // ctl[0..72) control; jump tables d|d2 [2][kChunk] u32; stage buffers; d4
-// tables [2][kChunk] u16; window token positions [2][kChunk] u16
-constexpr uint32_t kSmemWords = 72 + 2 * kChunk + (2 * kStageBytes) / 4 + kChunk + kChunk;
+// tables [2][kChunk] u16; walker step records [2][kChunk] u32
+constexpr uint32_t kSmemWords = 72 + 2 * kChunk + (2 * kStageBytes) / 4 + kChunk + 2 * kChunk;
 constexpr uint32_t kRingChunk = 4096;  // refill granule
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 constexpr uint32_t kDoubleSpan = 2048;  // group output span resolved by pointer jumping
@@ -311,16 +311,23 @@ __device__ inline int32_t decode_prefix(const uint8_t* __restrict__ src, uint32_
     uint8_t* wb = reinterpret_cast<uint8_t*>(ctl + 72 + 2 * kChunk);  // 2 x kStageBytes bytes
     // four-token jumps d4 = d2(p) + d2(p + d2(p)) (u16, 0 = none): [2][kChunk]
     uint16_t* j4 = reinterpret_cast<uint16_t*>(ctl + 72 + 2 * kChunk + (2 * kStageBytes) / 4);
-    // window-relative token positions [2][kChunk] (u16): the walker writes
-    // window w's, the fill warps copy them to sc.tokpos (coalesced) after the
-    // next barrier — a lone thread's global stores would bound the walk
-    uint16_t* tw = j4 + 2 * kChunk;
+    // walker step records [2][kChunk] (u32): lp | code << 11 | k << 13 per
+    // step of 1 (code 0), 2 (1) or 4 (2) tokens starting at window offset lp,
+    // k = the step's first token within the window.  The fill warps expand
+    // them from the window's jump table into sc.tokpos after the next
+    // barrier: one shared store per step keeps the lone walker's MIO queue
+    // short (it used to store every position and load the fourth token's hop)
+    uint32_t* tw = reinterpret_cast<uint32_t*>(j4 + 2 * kChunk);
     uint64_t* sbar = reinterpret_cast<uint64_t*>(ctl + 64);     // stage barriers (ctl[64..67])
     const uintptr_t sbase = reinterpret_cast<uintptr_t>(src);
     // window w's bytes [c0, min(c0 + kChunk + kStageTail, n)) as the 16-B
     // aligned superset; readers index buf0 + ((src + c0) & 15)
+    // ctl[56 + b] = window staged in buffer b (~0u: none), ctl[58 + b] = stagings
+    // issued into buffer b (its mbarrier's phase parity is (count - 1) & 1)
     auto stage_async = [&](uint32_t w) {  // one thread
       const uint32_t b = w & 1u;
+      ctl[56 + b] = w;
+      ctl[58 + b] += 1;
       const uint32_t e = min(w * kChunk + kChunk + kStageTail, n);
       const uintptr_t g0 = (sbase + w * kChunk) & ~uintptr_t(15);
       const uintptr_t g1 = (sbase + e + 15) & ~uintptr_t(15);
@@ -393,6 +400,29 @@ __device__ inline int32_t decode_prefix(const uint8_t* __restrict__ src, uint32_
         t4[lp] = (uint16_t)r;
       }
     };
+    // window w's step records -> token positions in sc.tokpos[base ..)
+    // (reads window w's jump table, still intact: it is refilled for window
+    // w+2 only after the caller's barrier)
+    const uint32_t cap_seq = (uint32_t)match_capacity(n);
+    auto expand = [&](uint32_t w, uint32_t cnt, uint32_t base, uint32_t tid, uint32_t nthr) {
+      const uint32_t* tab = jt + (w & 1u) * kChunk;
+      const uint32_t* rec = tw + (w & 1u) * kChunk;
+      const uint32_t c0 = w * kChunk;
+      for (uint32_t i = tid; i < cnt; i += nthr) {
+        const uint32_t e = rec[i];
+        const uint32_t lp = e & 0x7FFu, code = (e >> 11) & 3u, o = base + (e >> 13);
+        if (o < cap_seq) sc.tokpos[o] = c0 + lp;
+        if (code) {
+          const uint32_t x = tab[lp];
+          if (o + 1 < cap_seq) sc.tokpos[o + 1] = c0 + lp + (x & 0xFFFFu);
+          if (code == 2) {
+            const uint32_t b = x >> 16;
+            if (o + 2 < cap_seq) sc.tokpos[o + 2] = c0 + lp + b;
+            if (o + 3 < cap_seq) sc.tokpos[o + 3] = c0 + lp + b + (tab[lp + b] & 0xFFFFu);
+          }
+        }
+      }
+    };
     if (t == 0) {
       dev::mbar_init(&sbar[0], 1);
       dev::mbar_init(&sbar[1], 1);
@@ -400,6 +430,8 @@ __device__ inline int32_t decode_prefix(const uint8_t* __restrict__ src, uint32_
     }
     __syncthreads();
     if (t == 0) {
+      ctl[58] = ctl[59] = 0;
+      ctl[57] = ~0u;
       stage_async(0);
       if (nch > 1) stage_async(1);
       ctl[54] = 0;  // walker position at the start of window w: ctl[54 + (w & 1)]
@@ -412,74 +444,77 @@ __device__ inline int32_t decode_prefix(const uint8_t* __restrict__ src, uint32_
     fill4(0, jt, j4, t, nt);
     __syncthreads();
     long long a_walk = 0, a_fill = 0;  // PCP_LZ4_TIMING
-    uint32_t pos = 0;  // walker state (thread 0)
+    // the walker is lane 0 of the LAST warp: the SMSP arbiter issues the
+    // highest warp id first, and the walker's serial chain is the skim's
+    // critical path; warps 0 .. nw-2 fill tables
+    const uint32_t wk = nt - 32;  // walker thread; fill threads are t < wk
+    uint32_t pos = 0;  // walker state
     uint32_t err = 0, done = 0, nseq = 0;
-    const uint32_t cap_seq = (uint32_t)match_capacity(n);
     for (uint32_t w = 0; w < nch; ++w) {
-      if (t >= 32) {
-        const long long f0 = (tm && t == 32) ? clock64() : 0;
+      if (t < wk) {
+        const long long f0 = (tm && t == 0) ? clock64() : 0;
         if (w > 0) {  // window w-1's token positions -> global
-          const uint32_t pb = (w - 1) & 1u, cnt = ctl[50 + pb], base = ctl[52 + pb];
-          const uint32_t c0p = (w - 1) * kChunk;
-          for (uint32_t i = t - 32; i < cnt; i += nt - 32)
-            if (base + i < cap_seq) sc.tokpos[base + i] = c0p + tw[pb * kChunk + i];
+          const uint32_t pb = (w - 1) & 1u;
+          expand(w - 1, ctl[50 + pb], ctl[52 + pb], t, wk);
+          named_sync_fill(wk);  // its jump table is refilled (window w+1) below
         }
         // window w's buffer was last read by fill(w) before the previous
         // barrier: refill it with window w+2 (async), then fill window w+1
-        if (t == 32 && w + 2 < nch) {
-          dev::fence_proxy_async();
-          stage_async(w + 2);
-        }
         // a window the walker has already passed (inside a long literal, or
-        // after the last sequence) is never read: skip its tables
-        // (uniform across the fill warps: the walker publishes the next
-        // window's start position in the other parity slot)
-        const bool need = ctl[54 + (w & 1u)] < (w + 2) * kChunk;
-        if (w + 1 < nch) dev::mbar_wait(&sbar[(w + 1) & 1u], ((w + 1) >> 1) & 1u);
+        // after the last sequence) is never read: skip its tables, and do not
+        // even stage it when that is known an iteration ahead (a C2 page is
+        // two-thirds such windows; staging them put one TMA latency per
+        // window on the critical path).  Uniform across the fill warps: the
+        // walker publishes the next window's start position in the other
+        // parity slot, and the stager records what each buffer holds.
+        const uint32_t wpos = ctl[54 + (w & 1u)];
+        if (t == 0) {
+          if (w + 2 < nch && wpos < (w + 3) * kChunk) {
+            dev::fence_proxy_async();
+            stage_async(w + 2);
+          } else {
+            ctl[56 + (w & 1u)] = ~0u;
+          }
+        }
+        const bool need = wpos < (w + 2) * kChunk;
+        const uint32_t b1 = (w + 1) & 1u;
+        if (w + 1 < nch && ctl[56 + b1] == w + 1) dev::mbar_wait(&sbar[b1], (ctl[58 + b1] - 1) & 1u);
         if (w + 1 < nch && need) {
           uint32_t* tb = jt + ((w + 1) & 1u) * kChunk;
-          fill(w + 1, tb, t - 32, nt - 32);
-          named_sync_fill(nt - 32);
-          fill2(w + 1, tb, t - 32, nt - 32);
-          named_sync_fill(nt - 32);
-          fill4(w + 1, tb, j4 + ((w + 1) & 1u) * kChunk, t - 32, nt - 32);
+          fill(w + 1, tb, t, wk);
+          named_sync_fill(wk);
+          fill2(w + 1, tb, t, wk);
+          named_sync_fill(wk);
+          fill4(w + 1, tb, j4 + ((w + 1) & 1u) * kChunk, t, wk);
         }
-        if (tm && t == 32) a_fill += clock64() - f0;
-      } else if (t == 0) {
+        if (tm && t == 0) a_fill += clock64() - f0;
+      } else if (t == wk) {
         const long long w0 = tm ? clock64() : 0;
         const uint32_t* tab = jt + (w & 1u) * kChunk;
         const uint16_t* t4 = j4 + (w & 1u) * kChunk;
         const uint32_t c0 = w * kChunk, len = min(c0 + kChunk, n) - c0;
-        uint16_t* tr = tw + (w & 1u) * kChunk;
-        uint32_t k = 0;  // tokens of this window (all start inside it)
+        uint32_t* tr = tw + (w & 1u) * kChunk;
+        uint32_t k = 0, r = 0;  // tokens / step records of this window (all start inside it)
         if (!done && pos < c0 + len) {
           uint32_t lp = pos - c0;
           while (true) {
-            // hot loop: one dependent LDS per one, two or four tokens
-            uint32_t x = tab[lp];
+            // hot loop: one round of two independent LDS (d|d2 and d4 at
+            // lp) per one, two or four tokens, branch-free step selection
+            uint32_t x = tab[lp], f = t4[lp];  // f: four-token jump (0: none)
             while ((x & 0xFFFFu) != 0xFFFFu) {
               const uint32_t a = x & 0xFFFFu, b = x >> 16;
-              const uint32_t f = t4[lp];  // four-token jump (0: none)
-              if (f) {  // tokens lp, lp+a, lp+b, lp+b+d(lp+b); next at lp+f
-                const uint32_t a2 = tab[lp + b] & 0xFFFFu;  // off the lp chain
-                tr[k] = (uint16_t)lp;
-                tr[k + 1] = (uint16_t)(lp + a);
-                tr[k + 2] = (uint16_t)(lp + b);
-                tr[k + 3] = (uint16_t)(lp + b + a2);
-                k += 4;
-                lp += f;
-              } else {
-                tr[k] = (uint16_t)lp;
-                if (b) tr[k + 1] = (uint16_t)(lp + a);
-                k += b ? 2u : 1u;
-                lp += b ? b : a;
-              }
+              const uint32_t code = f ? 2u : (b ? 1u : 0u);
+              tr[r++] = lp | (code << 11) | (k << 13);
+              k += 1u << code;
+              lp += f ? f : (b ? b : a);
               if (lp >= len) break;
               x = tab[lp];
+              f = t4[lp];
             }
             if (lp >= len) break;
             // entry 0xFFFF: parse this position exactly from global
-            tr[k++] = (uint16_t)lp;
+            tr[r++] = lp | (k << 13);
+            ++k;
             Seq sq;
             if (!parse_seq(src, n, c0 + lp, sq)) {
               err = done = 1;
@@ -494,7 +529,7 @@ __device__ inline int32_t decode_prefix(const uint8_t* __restrict__ src, uint32_
           }
           pos = done ? n : c0 + lp;
         }
-        ctl[50 + (w & 1u)] = k;
+        ctl[50 + (w & 1u)] = r;
         ctl[52 + (w & 1u)] = nseq;
         nseq += k;
         ctl[54 + ((w + 1) & 1u)] = pos;  // read by the fill warps in iteration w+1
@@ -503,13 +538,12 @@ __device__ inline int32_t decode_prefix(const uint8_t* __restrict__ src, uint32_
       __syncthreads();
     }
     {  // the last window's token positions -> global
-      const uint32_t pb = (nch - 1) & 1u, cnt = ctl[50 + pb], base = ctl[52 + pb];
-      for (uint32_t i = t; i < cnt; i += nt)
-        if (base + i < cap_seq) sc.tokpos[base + i] = (nch - 1) * kChunk + tw[pb * kChunk + i];
+      const uint32_t pb = (nch - 1) & 1u;
+      expand(nch - 1, ctl[50 + pb], ctl[52 + pb], t, nt);
     }
-    if (tm && t == 0) tm[8] = a_walk;
-    if (tm && t == 32) tm[9] = a_fill;
-    if (t == 0) {
+    if (tm && t == wk) tm[8] = a_walk;
+    if (tm && t == 0) tm[9] = a_fill;
+    if (t == wk) {
       ctl[0] = (err || !done) ? 1u : 0u;  // no last sequence → truncated stream
       ctl[1] = nseq;
       ctl[3] = nseq > cap_seq ? 1u : 0u;  // scratch too small: caller falls back
