@@ -224,20 +224,31 @@ __global__ void __launch_bounds__(kDecodeThreads, 1024 / kDecodeThreads) k_page_
 // Phase 4 of the LZ4 pages k_page_decode left pending: one warp per page
 // (the match chains are serial; a 32-thread CTA with a 16 KB ring lets ~13
 // pages per SM resolve at once instead of idling seven warps per page).
-__global__ void __launch_bounds__(32) k_page_matches(uint8_t* raw, const PageRef* pages,
+// Phase 4: warp 0 runs the match groups in order; warps 1-3 join every
+// pointer-jumping span (dense label regions: ~620 spans of <= 2 KB per C2
+// page, ~10 doubling rounds each), which a lone warp ran 64 bytes per lane
+// per round.
+constexpr uint32_t kMatchThreads = 128;
+__global__ void __launch_bounds__(kMatchThreads) k_page_matches(uint8_t* raw, const PageRef* pages,
                                                      const uint32_t* todo, const uint64_t* scratch_off,
                                                      uint8_t* scratch, uint32_t n_todo,
                                                      long long* timing) {
   __shared__ __align__(16) uint8_t ring[lz4p::kRing];
   __shared__ uint32_t pidx[lz4p::kDoubleSpan];
+  __shared__ uint32_t cmd[8];
   for (uint32_t w = blockIdx.x; w < n_todo; w += gridDim.x) {
     const PageRef pg = pages[todo[w]];
     if (!(pg.flags & kFlagOuterLz4)) continue;
     const lz4p::Scratch sc = lz4p::carve_scratch(scratch + scratch_off[w], pg.pay_len);
-    if (sc.hdr[1] != 1u) continue;
+    if (sc.hdr[1] != 1u) continue;  // uniform over the CTA
+    if (threadIdx.x >= 32) {
+      lz4p::matches_helper(sc, ring, pidx, cmd, blockDim.x);
+      continue;
+    }
     long long* tm = timing ? timing + 16 * (uint64_t)w + 8 : nullptr;  // [11] start, [12] end
     if (tm && threadIdx.x == 0) tm[3] = clock64();
-    lz4p::decode_matches(raw + pg.raw_dst, (uint32_t)pg.raw_len, sc, sc.hdr[0], ring, pidx, tm);
+    lz4p::decode_matches(raw + pg.raw_dst, (uint32_t)pg.raw_len, sc, sc.hdr[0], ring, pidx, tm,
+                         blockDim.x, cmd);
   }
 }
 
@@ -2402,7 +2413,7 @@ cudaError_t launch_page_decode(const uint8_t* bytes, uint8_t* raw, const PageRef
   (void)carve;
   k_page_decode<<<n_todo, kDecodeThreads, 0, st>>>(bytes, raw, pages, todo, scratch_off, scratch, n_todo,
                                         status, timing);
-  k_page_matches<<<n_todo, 32, 0, st>>>(raw, pages, todo, scratch_off, scratch, n_todo, timing);
+  k_page_matches<<<n_todo, kMatchThreads, 0, st>>>(raw, pages, todo, scratch_off, scratch, n_todo, timing);
   return cudaGetLastError();
 }
 

@@ -676,12 +676,109 @@ __device__ inline int32_t decode_prefix(const uint8_t* __restrict__ src, uint32_
   return kOk;
 }
 
-// Phase 4 of one page by ONE warp (lane = threadIdx.x & 31): the M matches
+// Named barrier 2 over the phase-4 warps; the OR of `v` over them.
+__device__ __forceinline__ void bar_jump(uint32_t nthreads) {
+  asm volatile("bar.sync 2, %0;" ::"r"(nthreads) : "memory");
+}
+__device__ __forceinline__ bool bar_jump_or(uint32_t nthreads, bool v) {
+  uint32_t r;
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\tsetp.ne.u32 p, %1, 0;\n\t"
+      "bar.red.or.pred q, 2, %2, p;\n\tselp.u32 %0, 1, 0, q;\n\t}"
+      : "=r"(r)
+      : "r"((uint32_t)v), "r"(nthreads)
+      : "memory");
+  return r != 0;
+}
+
+// Byte-level pointer jumping over the output span [g0, g0 + L) by threads
+// tid < nthr (nthr = 32: warp 0 alone; more: warp 0 + helper warps, synced
+// by named barrier 2): src(b) = b - off inside a match (the forward copy's
+// semantics, self-overlap included), b for literals; bytes below the span are
+// final in the ring.  Doubling until every pointer reaches a final byte takes
+// log2(chain depth) rounds instead of one dependency wave per link.  On entry
+// pidx holds the pointers; on exit the span's bytes are final in the ring.
+__device__ __forceinline__ void jump_rounds(uint8_t* ring, uint32_t* pidx, uint32_t g0, uint32_t L,
+                                            uint32_t tid, uint32_t nthr) {
+  for (int round = 0; round < 16; ++round) {  // depth <= L <= 2^11
+    bool ch = false;
+    for (uint32_t b0 = tid; b0 < L; b0 += 4 * nthr) {  // 4 bytes per thread in flight
+      uint32_t p[4], q[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t b = b0 + nthr * u;
+        p[u] = b < L ? pidx[b] : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) q[u] = (b0 + nthr * u < L && p[u] >= g0) ? pidx[p[u] - g0] : p[u];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (q[u] != p[u]) {
+          pidx[b0 + nthr * u] = q[u];
+          ch = true;
+        }
+    }
+    if (nthr > 32) {
+      if (!bar_jump_or(nthr, ch)) break;
+    } else {
+      __syncwarp();
+      if (!__any_sync(0xffffffffu, ch)) break;
+    }
+  }
+  // every final source is a literal of the span or a byte below it: those
+  // never change, so the gather has no read/write hazard
+  for (uint32_t b0 = tid; b0 < L; b0 += 4 * nthr) {
+    uint32_t p[4];
+    uint8_t v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) p[u] = b0 + nthr * u < L ? pidx[b0 + nthr * u] : g0 + b0 + nthr * u;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = p[u] != g0 + b0 + nthr * u ? ring[p[u] & (kRing - 1)] : 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (p[u] != g0 + b0 + nthr * u) ring[(g0 + b0 + nthr * u) & (kRing - 1)] = v[u];
+  }
+  if (nthr > 32) bar_jump(nthr);
+  else __syncwarp();
+}
+
+// Helper warps of phase 4 (threadIdx.x >= 32, nthr = all phase-4 threads):
+// wait for warp 0's span command (cmd[0] = 1, g0, L; 0 = page done), take a
+// share of the span init and of every jump round, in lockstep with warp 0's
+// barriers in decode_matches.
+// Match pointers of matches [q0, q0 + cnt) into pidx (span starting at g0),
+// one match per thread.
+__device__ __forceinline__ void span_pointers(const Scratch& sc, uint32_t* pidx, uint32_t g0, uint32_t q0,
+                                              uint32_t cnt, uint32_t tid, uint32_t nthr) {
+  for (uint32_t q = q0 + tid; q < q0 + cnt; q += nthr) {
+    const uint32_t mo = sc.m_mo[q], ml = sc.m_ml[q], a = mo - sc.m_off[q];
+    for (uint32_t j = 0; j < ml; ++j) pidx[mo - g0 + j] = a + j;
+  }
+}
+
+__device__ inline void matches_helper(const Scratch& sc, uint8_t* ring, uint32_t* pidx,
+                                      volatile uint32_t* cmd, uint32_t nthr) {
+  const uint32_t tid = threadIdx.x;
+  while (true) {
+    bar_jump(nthr);  // B1: command published
+    if (cmd[0] == 0) return;
+    const uint32_t g0 = cmd[1], L = cmd[2], q0 = cmd[3], cnt = cmd[4];
+    for (uint32_t b = tid; b < L; b += nthr) pidx[b] = g0 + b;
+    bar_jump(nthr);  // B2: span initialised
+    span_pointers(sc, pidx, g0, q0, cnt, tid, nthr);
+    bar_jump(nthr);  // B3: match pointers written
+    jump_rounds(ring, pidx, g0, L, tid, nthr);
+  }
+}
+
+// Phase 4 of one page by warp 0 (lane = threadIdx.x & 31): the M matches
 // recorded by decode_prefix, in order, through a shared-memory ring (`ring`:
-// kRing bytes).
+// kRing bytes).  With nthr > 32, warps 1.. run matches_helper and share the
+// pointer-jumping spans (cmd: 3 words of shared memory).
 __device__ inline void decode_matches(uint8_t* __restrict__ dst, uint32_t raw_len, Scratch sc,
                                       uint32_t M, uint8_t* ring, uint32_t* pidx,
-                                      long long* tm = nullptr) {
+                                      long long* tm = nullptr, uint32_t nthr = 32,
+                                      volatile uint32_t* cmd = nullptr) {
   const uint32_t t = threadIdx.x & 31u;
   {
 
@@ -737,47 +834,28 @@ __device__ inline void decode_matches(uint8_t* __restrict__ dst, uint32_t raw_le
     // Doubling until every pointer reaches a final byte takes log2(chain
     // depth) rounds instead of one dependency wave per link.  The caller
     // fills pidx with the matches' pointers after init_span.
-    auto init_span = [&](uint32_t g0, uint32_t L) {
-      for (uint32_t b = t; b < L; b += 32) pidx[b] = g0 + b;
-      __syncwarp();
-    };
-    auto jump_span = [&](uint32_t g0, uint32_t L) {
-      __syncwarp();
-      for (int round = 0; round < 16; ++round) {  // depth <= L <= 2^11
-        bool ch = false;
-        for (uint32_t b0 = t; b0 < L; b0 += 128) {  // 4 bytes per lane in flight
-          uint32_t p[4], q[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const uint32_t b = b0 + 32 * u;
-            p[u] = b < L ? pidx[b] : 0u;
-          }
-#pragma unroll
-          for (int u = 0; u < 4; ++u) q[u] = (b0 + 32 * u < L && p[u] >= g0) ? pidx[p[u] - g0] : p[u];
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (q[u] != p[u]) {
-              pidx[b0 + 32 * u] = q[u];
-              ch = true;
-            }
+    // span [g0, g0 + L) for pointer jumping (see jump_rounds): publish it to
+    // the helper warps, initialise pidx (all phase-4 threads)
+    // matches [q0, q0 + cnt) covering the span [g0, g0 + L): init pidx,
+    // write the match pointers, jump (all phase-4 threads)
+    auto span_jump = [&](uint32_t g0, uint32_t L, uint32_t q0, uint32_t cnt) {
+      if (nthr > 32) {
+        if (t == 0) {
+          cmd[1] = g0;
+          cmd[2] = L;
+          cmd[3] = q0;
+          cmd[4] = cnt;
+          cmd[0] = 1;
         }
-        __syncwarp();
-        if (!__any_sync(0xffffffffu, ch)) break;
+        bar_jump(nthr);  // B1
       }
-      // every final source is a literal of the span or a byte below it:
-      // those never change, so the gather has no read/write hazard
-      for (uint32_t b0 = t; b0 < L; b0 += 128) {
-        uint32_t p[4];
-        uint8_t v[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) p[u] = b0 + 32 * u < L ? pidx[b0 + 32 * u] : g0 + b0 + 32 * u;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) v[u] = p[u] != g0 + b0 + 32 * u ? ring[p[u] & (kRing - 1)] : 0;
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (p[u] != g0 + b0 + 32 * u) ring[(g0 + b0 + 32 * u) & (kRing - 1)] = v[u];
-      }
-      __syncwarp();
+      for (uint32_t b = t; b < L; b += nthr) pidx[b] = g0 + b;
+      if (nthr > 32) bar_jump(nthr);  // B2
+      else __syncwarp();
+      span_pointers(sc, pidx, g0, q0, cnt, t, nthr);
+      if (nthr > 32) bar_jump(nthr);  // B3
+      else __syncwarp();
+      jump_rounds(ring, pidx, g0, L, t, nthr);
     };
     uint32_t step = 32;
     for (uint32_t base = 0; base < M; base += step) {
@@ -809,13 +887,7 @@ __device__ inline void decode_matches(uint8_t* __restrict__ dst, uint32_t raw_le
           for (int k = 0; k < 8; ++k)
             if (32u * k + t < cntS) ok = ok && smo[k] - soff[k] >= lo && smo[k] + sml[k] <= hi;
           if (__all_sync(0xffffffffu, ok)) {
-            const uint32_t L = s_end - s_first;
-            init_span(s_first, L);
-#pragma unroll
-            for (int k = 0; k < 8; ++k)
-              if (32u * k + t < cntS)
-                for (uint32_t j = 0; j < sml[k]; ++j) pidx[smo[k] - s_first + j] = smo[k] - soff[k] + j;
-            jump_span(s_first, L);
+            span_jump(s_first, s_end - s_first, base, cntS);
             if (tm && t == 0) tm[7] += 1;
             step = cntS;
             continue;
@@ -836,10 +908,7 @@ __device__ inline void decode_matches(uint8_t* __restrict__ dst, uint32_t raw_le
         const bool src_ok = !act || (a >= lo && r_mo + r_ml <= hi);
         if (span_ok && __all_sync(0xffffffffu, src_ok) && pidx && g_end - g_first <= kDoubleSpan) {
           // dense group: pointer jumping (see jump_span)
-          init_span(g_first, g_end - g_first);
-          if (act)
-            for (uint32_t j = 0; j < r_ml; ++j) pidx[r_mo - g_first + j] = a + j;
-          jump_span(g_first, g_end - g_first);
+          span_jump(g_first, g_end - g_first, base, cnt);
           if (tm && t == 0) tm[7] += 1;
           continue;
         }
@@ -944,6 +1013,10 @@ __device__ inline void decode_matches(uint8_t* __restrict__ dst, uint32_t raw_le
     }
   }
   __syncwarp();
+  if (nthr > 32) {  // release the helper warps
+    if (t == 0) cmd[0] = 0;
+    bar_jump(nthr);  // B1
+  }
   if (tm && t == 0) tm[4] = clock64();
 }
 
