@@ -236,19 +236,20 @@ __global__ void __launch_bounds__(kMatchThreads) k_page_matches(uint8_t* raw, co
   __shared__ __align__(16) uint8_t ring[lz4p::kRing];
   __shared__ uint32_t pidx[lz4p::kDoubleSpan];
   __shared__ uint32_t cmd[8];
+  __shared__ uint32_t srec[3 * 256];  // a span's match records, staged by warp 0
   for (uint32_t w = blockIdx.x; w < n_todo; w += gridDim.x) {
     const PageRef pg = pages[todo[w]];
     if (!(pg.flags & kFlagOuterLz4)) continue;
     const lz4p::Scratch sc = lz4p::carve_scratch(scratch + scratch_off[w], pg.pay_len);
     if (sc.hdr[1] != 1u) continue;  // uniform over the CTA
     if (threadIdx.x >= 32) {
-      lz4p::matches_helper(sc, ring, pidx, cmd, blockDim.x);
+      lz4p::matches_helper(sc, ring, pidx, cmd, blockDim.x, srec);
       continue;
     }
     long long* tm = timing ? timing + 16 * (uint64_t)w + 8 : nullptr;  // [11] start, [12] end
     if (tm && threadIdx.x == 0) tm[3] = clock64();
     lz4p::decode_matches(raw + pg.raw_dst, (uint32_t)pg.raw_len, sc, sc.hdr[0], ring, pidx, tm,
-                         blockDim.x, cmd);
+                         blockDim.x, cmd, srec);
   }
 }
 

@@ -747,17 +747,21 @@ __device__ __forceinline__ void jump_rounds(uint8_t* ring, uint32_t* pidx, uint3
 // share of the span init and of every jump round, in lockstep with warp 0's
 // barriers in decode_matches.
 // Match pointers of matches [q0, q0 + cnt) into pidx (span starting at g0),
-// one match per thread.
-__device__ __forceinline__ void span_pointers(const Scratch& sc, uint32_t* pidx, uint32_t g0, uint32_t q0,
-                                              uint32_t cnt, uint32_t tid, uint32_t nthr) {
-  for (uint32_t q = q0 + tid; q < q0 + cnt; q += nthr) {
-    const uint32_t mo = sc.m_mo[q], ml = sc.m_ml[q], a = mo - sc.m_off[q];
+// one match per thread; records from shared memory (srec: mo[256], ml[256],
+// off[256], staged by warp 0) or, without it, from the scratch.
+__device__ __forceinline__ void span_pointers(const Scratch& sc, const uint32_t* srec, uint32_t* pidx,
+                                              uint32_t g0, uint32_t q0, uint32_t cnt, uint32_t tid,
+                                              uint32_t nthr) {
+  for (uint32_t i = tid; i < cnt; i += nthr) {
+    const uint32_t mo = srec ? srec[i] : sc.m_mo[q0 + i];
+    const uint32_t ml = srec ? srec[256 + i] : sc.m_ml[q0 + i];
+    const uint32_t a = mo - (srec ? srec[512 + i] : sc.m_off[q0 + i]);
     for (uint32_t j = 0; j < ml; ++j) pidx[mo - g0 + j] = a + j;
   }
 }
 
 __device__ inline void matches_helper(const Scratch& sc, uint8_t* ring, uint32_t* pidx,
-                                      volatile uint32_t* cmd, uint32_t nthr) {
+                                      volatile uint32_t* cmd, uint32_t nthr, const uint32_t* srec) {
   const uint32_t tid = threadIdx.x;
   while (true) {
     bar_jump(nthr);  // B1: command published
@@ -765,7 +769,7 @@ __device__ inline void matches_helper(const Scratch& sc, uint8_t* ring, uint32_t
     const uint32_t g0 = cmd[1], L = cmd[2], q0 = cmd[3], cnt = cmd[4];
     for (uint32_t b = tid; b < L; b += nthr) pidx[b] = g0 + b;
     bar_jump(nthr);  // B2: span initialised
-    span_pointers(sc, pidx, g0, q0, cnt, tid, nthr);
+    span_pointers(sc, srec, pidx, g0, q0, cnt, tid, nthr);
     bar_jump(nthr);  // B3: match pointers written
     jump_rounds(ring, pidx, g0, L, tid, nthr);
   }
@@ -778,11 +782,12 @@ __device__ inline void matches_helper(const Scratch& sc, uint8_t* ring, uint32_t
 __device__ inline void decode_matches(uint8_t* __restrict__ dst, uint32_t raw_len, Scratch sc,
                                       uint32_t M, uint8_t* ring, uint32_t* pidx,
                                       long long* tm = nullptr, uint32_t nthr = 32,
-                                      volatile uint32_t* cmd = nullptr) {
+                                      volatile uint32_t* cmd = nullptr, uint32_t* srec = nullptr) {
   const uint32_t t = threadIdx.x & 31u;
   {
 
-    uint32_t hi = 0, fl = 0;  // ring holds [hi - kRing, hi); global final below fl
+    uint32_t hi = 0, fl = 0;  // ring holds [max(hi - kRing, vlo), hi); global final below fl
+    uint32_t vlo = 0;         // start of the ring's valid bytes since the last skip
     auto move_chunk = [&](uint32_t from, uint32_t end, bool to_ring) {
       if (end - from == kRingChunk && ((uintptr_t)(dst + from) & 15u) == 0) {
         uint4* g4 = reinterpret_cast<uint4*>(dst + from);
@@ -802,10 +807,27 @@ __device__ inline void decode_matches(uint8_t* __restrict__ dst, uint32_t raw_le
         }
       }
     };
+    // chunks at or above hi and wholly below the chunk before g_first hold
+    // no match output (matches come in output order, and every earlier one
+    // landed below hi), so they are final in dst already -- phase 3 wrote the
+    // literals there.  Jump over them instead of streaming them through the
+    // ring (a C2 page's 24 KB float literals, 64 times) after writing the
+    // ring back.  Sources below the new window are read from dst.
+    auto skip_final = [&](uint32_t g_first) -> bool {
+      const uint32_t c = g_first & ~(kRingChunk - 1u);
+      if (c < hi + 2u * kRingChunk) return false;
+      while (fl < hi) {
+        const uint32_t end = min(fl + kRingChunk, hi);
+        move_chunk(fl, end, false);
+        fl = end;
+      }
+      fl = hi = vlo = c - kRingChunk;
+      return true;
+    };
     // flush final chunks below g_first, refill the ring up to g_end; false if
     // [g_first, g_end) cannot sit in the ring together with its sources
     auto ensure_ring = [&](uint32_t g_first, uint32_t g_end) -> bool {
-      bool moved = false;
+      bool moved = skip_final(g_first);
       while (fl + kRingChunk <= g_first && fl + kRingChunk <= hi) {
         move_chunk(fl, fl + kRingChunk, false);
         fl += kRingChunk;
@@ -838,7 +860,16 @@ __device__ inline void decode_matches(uint8_t* __restrict__ dst, uint32_t raw_le
     // the helper warps, initialise pidx (all phase-4 threads)
     // matches [q0, q0 + cnt) covering the span [g0, g0 + L): init pidx,
     // write the match pointers, jump (all phase-4 threads)
+    uint32_t smo[8], sml[8], soff[8];  // this iteration's records (lane t: base + 32k + t)
     auto span_jump = [&](uint32_t g0, uint32_t L, uint32_t q0, uint32_t cnt) {
+      if (srec) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          srec[32 * k + t] = smo[k];
+          srec[256 + 32 * k + t] = sml[k];
+          srec[512 + 32 * k + t] = soff[k];
+        }
+      }
       if (nthr > 32) {
         if (t == 0) {
           cmd[1] = g0;
@@ -852,26 +883,44 @@ __device__ inline void decode_matches(uint8_t* __restrict__ dst, uint32_t raw_le
       for (uint32_t b = t; b < L; b += nthr) pidx[b] = g0 + b;
       if (nthr > 32) bar_jump(nthr);  // B2
       else __syncwarp();
-      span_pointers(sc, pidx, g0, q0, cnt, t, nthr);
+      if (!srec) __syncwarp();
+      span_pointers(sc, srec, pidx, g0, q0, cnt, t, nthr);
       if (nthr > 32) bar_jump(nthr);  // B3
       else __syncwarp();
       jump_rounds(ring, pidx, g0, L, t, nthr);
     };
     uint32_t step = 32;
+    // the next 256 records, loaded an iteration ahead on the guess that this
+    // iteration is a full super-group (the usual case in label regions)
+    uint32_t pmo[8], pml[8], poff[8], pbase = ~0u;
+    auto load_recs = [&](uint32_t b, uint32_t (&mo)[8], uint32_t (&ml)[8], uint32_t (&of)[8]) {
+      const uint32_t c = min(256u, M - b);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t q = b + 32 * k + t;
+        const bool v = q < b + c;
+        mo[k] = v ? sc.m_mo[q] : 0u;
+        ml[k] = v ? sc.m_ml[q] : 0u;
+        of[k] = v ? sc.m_off[q] : 1u;
+      }
+    };
     for (uint32_t base = 0; base < M; base += step) {
       step = 32;
       // ---- super-group: up to 8 x 32 consecutive matches in one jump pass
       // when their output span is <= kDoubleSpan (dense label regions)
-      uint32_t smo[8], sml[8], soff[8];
       const uint32_t cntS = min(256u, M - base);
+      if (pbase == base) {
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const uint32_t q = base + 32 * k + t;
-        const bool v = q < base + cntS;
-        smo[k] = v ? sc.m_mo[q] : 0u;
-        sml[k] = v ? sc.m_ml[q] : 0u;
-        soff[k] = v ? sc.m_off[q] : 1u;
+        for (int k = 0; k < 8; ++k) {
+          smo[k] = pmo[k];
+          sml[k] = pml[k];
+          soff[k] = poff[k];
+        }
+      } else {
+        load_recs(base, smo, sml, soff);
       }
+      pbase = base + cntS;
+      if (pbase < M) load_recs(pbase, pmo, pml, poff);
       if (pidx && cntS > 32) {
         const uint32_t lastk = (cntS - 1) >> 5, lastl = (cntS - 1) & 31u;
         uint32_t e_last = 0;
@@ -881,7 +930,7 @@ __device__ inline void decode_matches(uint8_t* __restrict__ dst, uint32_t raw_le
         const uint32_t s_end = __shfl_sync(0xffffffffu, e_last, lastl);
         const uint32_t s_first = __shfl_sync(0xffffffffu, smo[0], 0);
         if (s_end - s_first <= kDoubleSpan && ensure_ring(s_first, s_end)) {
-          const uint32_t lo = hi > kRing ? hi - kRing : 0u;
+          const uint32_t lo = max(hi > kRing ? hi - kRing : 0u, vlo);
           bool ok = true;
 #pragma unroll
           for (int k = 0; k < 8; ++k)
@@ -901,7 +950,7 @@ __device__ inline void decode_matches(uint8_t* __restrict__ dst, uint32_t raw_le
         const uint32_t g_end = __shfl_sync(0xffffffffu, r_mo + r_ml, cnt - 1);
         const uint32_t g_first = __shfl_sync(0xffffffffu, r_mo, 0);
         const bool span_ok = ensure_ring(g_first, g_end);
-        const uint32_t lo = hi > kRing ? hi - kRing : 0u;
+        const uint32_t lo = max(hi > kRing ? hi - kRing : 0u, vlo);
         const bool act = t < cnt;
         const uint32_t a = r_mo - r_off;
         // every lane's source must be in the ring for the fast path
@@ -956,7 +1005,7 @@ __device__ inline void decode_matches(uint8_t* __restrict__ dst, uint32_t raw_le
         const uint32_t ml = __shfl_sync(0xffffffffu, r_ml, j);
         const uint32_t off = __shfl_sync(0xffffffffu, r_off, j);
         const uint32_t a = mo - off;
-        if (ml <= 32 && mo + ml <= hi && fl + kRingChunk > mo && a + kRing >= hi) {
+        if (ml <= 32 && mo + ml <= hi && fl + kRingChunk > mo && a + kRing >= hi && a >= vlo) {
           // fast path: no ring traffic, one pass, source inside the ring
           uint32_t r = t - off * __float2uint_rz(__fdividef((float)t + 0.5f, (float)off));
           r = off >= ml ? t : r;
@@ -965,7 +1014,7 @@ __device__ inline void decode_matches(uint8_t* __restrict__ dst, uint32_t raw_le
           __syncwarp();
           continue;
         }
-        bool moved = false;
+        bool moved = skip_final(mo);
         while (fl + kRingChunk <= mo && fl + kRingChunk <= hi) {  // final: write back
           move_chunk(fl, fl + kRingChunk, false);
           fl += kRingChunk;
@@ -984,7 +1033,7 @@ __device__ inline void decode_matches(uint8_t* __restrict__ dst, uint32_t raw_le
           moved = true;
         }
         if (moved) __syncwarp();
-        const uint32_t lo = hi > kRing ? hi - kRing : 0u;
+        const uint32_t lo = max(hi > kRing ? hi - kRing : 0u, vlo);
         if (ml <= 32 && a >= lo) {  // common case: one pass, source in the ring
           if (t < ml) {
             uint32_t r = t;
