@@ -541,9 +541,8 @@ struct Pipeline {
       if (w.h1) cudaEventDestroy(w.h1);
       if (w.served) cudaEventDestroy(w.served);
       if (w.host_ready) cudaEventDestroy(w.host_ready);
-      if (t_open) cudaEventDestroy(t_open);
-      t_open = nullptr;
     }
+    if (t_open) cudaEventDestroy(t_open);
     if (stream) cudaStreamDestroy(stream);
     if (serve_stream) cudaStreamDestroy(serve_stream);
   }
