@@ -581,6 +581,7 @@ struct Pipeline {
     CK(cudaStreamCreateWithFlags(&serve_stream, cudaStreamNonBlocking));
     load_store();
     plan_schema();
+    if (const char* e = std::getenv("PCP_WAVE_BATCHES")) wave_batches = (uint32_t)std::atoi(e);  // sweep switch
     plan_waves();
     upload_x2n(stream);
     std::vector<uint32_t> shift(kShiftEntries);
@@ -593,8 +594,10 @@ struct Pipeline {
       slots_set = true;
     }
     // default: 4 slots (3 waves in flight: the LZ4 match phase of one wave
-    // overlaps the decode / k_cloud of the others), fewer when the per-CTA
-    // global slabs of large-cloud chains would exceed ~48 GB
+    // overlaps the decode / k_cloud of the others); 5 when every cloud's
+    // buffers sit in shared memory (C2 +2%, measured: tools/sweep_slots.sh),
+    // fewer when the per-CTA global slabs of large-cloud chains would exceed ~48 GB
+    if (!slots_set && !proto.gscratch_per_cta) n_slots = 5;
     if (!slots_set && proto.gscratch_per_cta)
       while (n_slots > 2 && (uint64_t)n_slots * proto.gscratch_per_cta * std::max(grid, grid_pre) > (48ull << 30))
         --n_slots;

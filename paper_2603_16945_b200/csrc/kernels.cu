@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cfloat>
 #include <cstdint>
 
@@ -2414,7 +2415,12 @@ cudaError_t launch_page_decode(const uint8_t* bytes, uint8_t* raw, const PageRef
   (void)carve;
   k_page_decode<<<n_todo, kDecodeThreads, 0, st>>>(bytes, raw, pages, todo, scratch_off, scratch, n_todo,
                                         status, timing);
-  k_page_matches<<<n_todo, kMatchThreads, 0, st>>>(raw, pages, todo, scratch_off, scratch, n_todo, timing);
+  static const uint32_t match_threads = [] {  // PCP_MATCH_THREADS: sweep switch (32..kMatchThreads)
+    const char* e = std::getenv("PCP_MATCH_THREADS");
+    const int v = e ? std::atoi(e) : (int)kMatchThreads;
+    return (uint32_t)std::max(32, std::min((int)kMatchThreads, v / 32 * 32));
+  }();
+  k_page_matches<<<n_todo, match_threads, 0, st>>>(raw, pages, todo, scratch_off, scratch, n_todo, timing);
   return cudaGetLastError();
 }
 
