@@ -451,6 +451,7 @@ struct Wave {
   // device
   DevBuf bytes_stage, raw, tables, outs, compact, compact_meta, lz4_scratch, lz4_timing;
   DevBuf handoff;  // chain split: the clouds between the prefix and the cluster launch
+  DevBuf mt_pre;   // pre-seeded MT19937-64 states [n][n_rng][312] (k_seed_states)
   uint32_t n_todo = 0;
   HostBuf h_tables, h_res, h_compact_meta;
   std::vector<uint64_t> out_base;  // per output field: offset in outs
@@ -486,6 +487,7 @@ struct Pipeline {
   bool lz4_timing = std::getenv("PCP_LZ4_TIMING") != nullptr;
   bool op_timing = std::getenv("PCP_OP_TIMING") != nullptr;  // per-op SM cycles (diagnostics)
   bool no_fused_crc = std::getenv("PCP_NO_FUSED_CRC") != nullptr;  // experiment switch
+  bool no_preseed = std::getenv("PCP_NO_PRESEED") != nullptr;  // experiment switch: seed MT in k_cloud
   DevBuf d_op_cycles;
   std::vector<double> lz4_phase_cycles = std::vector<double>(4, 0.0);
   cudaStream_t stream = nullptr;        // wave compute (copies + kernels)
@@ -691,6 +693,14 @@ struct Pipeline {
     // ops
     a.n_ops = (int32_t)g.maps.size();
     a.base_seed = g.base_seed;
+    // RNG ops get a pre-seeded MT state per sample (k_seed_states)
+    a.n_rng = 0;
+    for (size_t k = 0; k < g.maps.size(); ++k) {
+      const int kd = g.maps[k].kind;
+      const bool rng_op = kd == kTranslate || kd == kJitter || kd == kRotate || kd == kRandomScale ||
+                          kd == kFlipYz || kd == kColorAugment || kd == kRandomCrop || kd == kDownsample;
+      a.rng_slot[k] = rng_op && !no_preseed ? (int8_t)a.n_rng++ : (int8_t)-1;
+    }
     uint32_t gather_all = 0;
     uint64_t max_target = 0;
     for (size_t k = 0; k < g.maps.size(); ++k) {
@@ -1098,6 +1108,7 @@ struct Pipeline {
     // fields; ragged ones grow it on demand past 1 GiB)
     if (host_batches) w.h_out.ensure(std::min<uint64_t>(out_total + 64, 1ull << 30));
     if (proto.split_at) w.handoff.ensure(proto.handoff_stride * w.n);
+    if (proto.n_rng) w.mt_pre.ensure(w.n * proto.n_rng * 312 * 8);
     w.h_res.ensure(total - o_sst + 16);
     {
       uint64_t need = 0;
@@ -1151,6 +1162,7 @@ struct Pipeline {
     a.shift_tab = d_shift.as<uint32_t>();
     a.gscratch = proto.gscratch_per_cta ? w.gscratch.as<uint8_t>() : nullptr;
     a.handoff = proto.split_at ? w.handoff.as<uint8_t>() : nullptr;
+    a.mt_pre = proto.n_rng ? w.mt_pre.as<uint64_t>() : nullptr;
     for (size_t f = 0; f < outs.size(); ++f) {
       a.out[f] = w.outs.as<uint8_t>() + w.out_base[f];
       a.out_stride[f] = outs[f].stride;
@@ -1173,7 +1185,7 @@ struct Pipeline {
     w.decode_alg_bytes = 0;
     for (uint32_t pi : todo) w.decode_alg_bytes += pages[pi].pay_len + pages[pi].raw_len;
     CK(launch_wave(a, grid, grid_pre, threads, smem, w.stream, w.k0, w.k1));
-    launches += (wins.empty() ? 0 : 1) + (todo.empty() ? 0 : 2) + (ng ? 1 : 0) + 1 + 1 + 1;
+    launches += (wins.empty() ? 0 : 1) + (todo.empty() ? 0 : 2) + (ng ? 1 : 0) + (proto.n_rng ? 1 : 0) + 1 + 1 + 1;
     h2d_bytes += up_bytes;
     // ---- results back to pinned host -------------------------------------------
 

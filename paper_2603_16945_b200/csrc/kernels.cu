@@ -336,6 +336,13 @@ constexpr int kRed = 64;  // reduction scratch words (8 B)
 
 
 
+// An op's seed (mix_seed, transforms.cpp:82-96) and, when k_seed_states ran,
+// its pre-seeded MT19937-64 state in global memory.
+struct Seed {
+  uint64_t v;
+  const uint64_t* pre;
+};
+
 struct Cloud {
   uint8_t* cur[kMaxBytesFields];
   uint8_t* alt[kMaxBytesFields];
@@ -513,13 +520,22 @@ __device__ void fy_resolve(Cloud& c, Smem& S, uint32_t N, uint32_t T) {
   __syncthreads();
 }
 
+// MT19937-64 seeding (std::mt19937_64(seed), transforms.cpp:114): a copy of
+// the state k_seed_states seeded for this (sample, op) when there is one,
+// else thread 0's serial 311-step recurrence.  Callers sync afterwards.
+__device__ __forceinline__ void seed_mt(Smem& S, Seed seed) {
+  if (seed.pre) {
+    for (uint32_t i = threadIdx.x; i < (uint32_t)rng::kN; i += blockDim.x) S.mt[i] = seed.pre[i];
+  } else if (threadIdx.x == 0) {
+    rng::seed_state(S.mt, seed.v);
+  }
+}
+
 // Draw index vector for downsample; returns false if a Lemire rejection
 // (probability ~range/2^64) needs the serial path.
-__device__ bool downsample_draws(Cloud& c, Smem& S, uint64_t seed, uint32_t N, uint32_t T) {
-  if (threadIdx.x == 0) {
-    rng::seed_state(S.mt, seed);
-    S.flag = 0;
-  }
+__device__ bool downsample_draws(Cloud& c, Smem& S, Seed seed, uint32_t N, uint32_t T) {
+  seed_mt(S, seed);
+  if (threadIdx.x == 0) S.flag = 0;
   __syncthreads();
   int32_t* J = c.ix[0];
   const bool fy = N >= T;
@@ -628,15 +644,22 @@ __device__ int32_t op_normalize(const WaveArgs& a, Cloud& c, Smem& S) {
 }
 
 // Broadcast the first k (<= 8) engine outputs to S.u32s/f32s via thread 0.
-__device__ void first_draws(Smem& S, uint64_t seed, int k, uint64_t* out) {
+__device__ void first_draws(Smem& S, Seed seed, int k, uint64_t* out) {
   __shared__ uint64_t o[8];
-  if (threadIdx.x == 0) rng::first_outputs(seed, k, o, S.mt);
+  if (threadIdx.x == 0) {
+    if (seed.pre) {  // words 0..kM+k of the pre-seeded state (k_seed_states)
+      for (int i = 0; i < k; ++i)
+        o[i] = rng::temper(rng::twist_word(seed.pre[i], seed.pre[i + 1], seed.pre[i + rng::kM]));
+    } else {
+      rng::first_outputs(seed.v, k, o, S.mt);
+    }
+  }
   __syncthreads();
   for (int i = 0; i < k; ++i) out[i] = o[i];
   __syncthreads();
 }
 
-__device__ int32_t op_translate(const WaveArgs& a, Cloud& c, Smem& S, uint64_t seed) {
+__device__ int32_t op_translate(const WaveArgs& a, Cloud& c, Smem& S, Seed seed) {
   uint64_t u[3];
   first_draws(S, seed, 3, u);
   const float t[3] = {rng::uniform_real(u[0], -0.2f, 0.2f), rng::uniform_real(u[1], -0.2f, 0.2f),
@@ -648,7 +671,7 @@ __device__ int32_t op_translate(const WaveArgs& a, Cloud& c, Smem& S, uint64_t s
   return kOk;
 }
 
-__device__ int32_t op_scale(const WaveArgs& a, Cloud& c, Smem& S, uint64_t seed) {
+__device__ int32_t op_scale(const WaveArgs& a, Cloud& c, Smem& S, Seed seed) {
   uint64_t u[1];
   first_draws(S, seed, 1, u);
   const float s = rng::uniform_real(u[0], 0.8f, 1.25f);
@@ -659,7 +682,7 @@ __device__ int32_t op_scale(const WaveArgs& a, Cloud& c, Smem& S, uint64_t seed)
   return kOk;
 }
 
-__device__ int32_t op_flip(const WaveArgs& a, Cloud& c, Smem& S, uint64_t seed) {
+__device__ int32_t op_flip(const WaveArgs& a, Cloud& c, Smem& S, Seed seed) {
   uint64_t u[1];
   first_draws(S, seed, 1, u);
   if (rng::uniform_real(u[0], 0.0f, 1.0f) < 0.5f) {
@@ -683,7 +706,7 @@ __device__ void rotate_field(float* v, uint32_t n, float cs, float sn) {
 }
 
 __device__ int32_t op_rotate(const WaveArgs& a, Cloud& c, Smem& S, const OpDesc& op,
-                             uint64_t seed) {
+                             Seed seed) {
   float theta = op.theta;
   if (!op.has_theta) {
     uint64_t u[1];
@@ -705,10 +728,10 @@ __device__ __forceinline__ float clampf(float v, float lo, float hi) {
 // jitter (transforms.cpp:159-168): normals n_0, n_1, ... from the polar
 // method; accepted attempt j yields n_2j = y*mult (returned) and
 // n_2j+1 = x*mult (saved).  Attempts are scanned 156 per twist.
-__device__ int32_t op_jitter(const WaveArgs& a, Cloud& c, Smem& S, uint64_t seed) {
+__device__ int32_t op_jitter(const WaveArgs& a, Cloud& c, Smem& S, Seed seed) {
   float* d = F(c, a.role_data);
   const uint32_t need = 3 * c.n[a.role_data];
-  if (threadIdx.x == 0) rng::seed_state(S.mt, seed);
+  seed_mt(S, seed);
   __syncthreads();
   uint32_t done = 0;  // normals produced
   while (done < need) {
@@ -740,11 +763,11 @@ __device__ int32_t op_jitter(const WaveArgs& a, Cloud& c, Smem& S, uint64_t seed
   return kOk;
 }
 
-__device__ int32_t op_color(const WaveArgs& a, Cloud& c, Smem& S, uint64_t seed) {
+__device__ int32_t op_color(const WaveArgs& a, Cloud& c, Smem& S, Seed seed) {
   if (!has(c, a.role_color) || c.n[a.role_color] == 0) return kMissingField;
   float* col = F(c, a.role_color);
   const uint32_t need = 3 * c.n[a.role_color];
-  if (threadIdx.x == 0) rng::seed_state(S.mt, seed);
+  seed_mt(S, seed);
   __syncthreads();
   for (uint32_t blk = 0; blk * rng::kN < need; ++blk) {
     rng::twist_block(S.mt);
@@ -777,7 +800,7 @@ __device__ uint32_t compact(Cloud& c, Smem& S, uint32_t n, Pred keep) {
 }
 
 // random_crop (transforms.cpp:220-271).
-__device__ int32_t op_random_crop(const WaveArgs& a, Cloud& c, Smem& S, uint64_t seed) {
+__device__ int32_t op_random_crop(const WaveArgs& a, Cloud& c, Smem& S, Seed seed) {
   const float* d = F(c, a.role_data);
   const uint32_t n = c.n[a.role_data];
   // bbox: sequential std::min/std::max from pts[0]: equal values keep the
@@ -875,7 +898,7 @@ __device__ int32_t op_random_crop(const WaveArgs& a, Cloud& c, Smem& S, uint64_t
 }
 
 __device__ int32_t op_downsample(const WaveArgs& a, Cloud& c, Smem& S, const OpDesc& op,
-                                 uint64_t seed) {
+                                 Seed seed) {
   if (op.num_points <= 0) return kOutOfBounds;
   const uint32_t T = (uint32_t)op.num_points;
   const uint32_t N = c.n[a.role_data];
@@ -887,7 +910,7 @@ __device__ int32_t op_downsample(const WaveArgs& a, Cloud& c, Smem& S, const OpD
   if (fast) {
     if (N >= T) fy_resolve(c, S, N, T);
   } else {
-    downsample_serial(c, S, seed, N, T);
+    downsample_serial(c, S, seed.v, N, T);
   }
   gather_mask_fields(a, c, mm, c.ix[0], T);
   return kOk;
@@ -1798,15 +1821,17 @@ __device__ int32_t op_voxel(const WaveArgs& a, Cloud& c, Smem& S, const OpDesc& 
 // (force-inlined: an outlined call would need the address of the kernel's
 // WaveArgs parameter, and ptxas would copy all ~3 KB of it to local memory)
 template <int MinBlocks>
-__device__ __forceinline__ int32_t run_chain(const WaveArgs& a, Cloud& c, Smem& S, uint64_t epoch, uint64_t index,
+__device__ __forceinline__ int32_t run_chain(const WaveArgs& a, Cloud& c, Smem& S, uint32_t sample, uint64_t epoch, uint64_t index,
                              const uint64_t* fixed_seed, int32_t& fail_op, int op_begin, int op_end) {
   int32_t status = kOk;
   const int fd = a.role_data;
   long long t0 = (a.op_cycles && threadIdx.x == 0) ? clock64() : 0;
   for (int k = op_begin; status == kOk && k < op_end; ++k) {
     const OpDesc& op = a.ops[k];
-    const uint64_t seed =
-        fixed_seed ? *fixed_seed : rng::mix_seed(a.base_seed, epoch, index, op.seed_op_id);
+    const Seed seed{fixed_seed ? *fixed_seed : rng::mix_seed(a.base_seed, epoch, index, op.seed_op_id),
+                    (a.mt_pre && !fixed_seed && a.rng_slot[k] >= 0)
+                        ? a.mt_pre + ((uint64_t)sample * a.n_rng + a.rng_slot[k]) * rng::kN
+                        : nullptr};
     if (c.n[fd] == 0) {
       status = kEmptyCloud;
     } else {
@@ -1959,7 +1984,7 @@ __global__ void __launch_bounds__(512, MinBlocks) k_cloud(WaveArgs a) {
       if (reinterpret_cast<const uint32_t*>(hb)[0] != (uint32_t)kOk) continue;  // uniform
       handoff_load(a, c, S, hb);
       int32_t fail_op = 0;
-      int32_t status = run_chain<MinBlocks>(a, c, S, sw.epoch, sw.index, nullptr, fail_op, a.op_begin, a.op_end);
+      int32_t status = run_chain<MinBlocks>(a, c, S, s, sw.epoch, sw.index, nullptr, fail_op, a.op_begin, a.op_end);
       if (status == kOk && leader) write_tracked(a, c, s, status);
       if (threadIdx.x == 0 && leader) {
         a.sample_status[s] = status;
@@ -2082,7 +2107,7 @@ __global__ void __launch_bounds__(512, MinBlocks) k_cloud(WaveArgs a) {
       if (status == kOk && a.role_color >= 0 && flen[a.role_color] % 12) status = kMissingField;
       if (status != kOk) fail_op = 1;
       if (status == kOk)
-        status = run_chain<MinBlocks>(a, c, S, sw.epoch, sw.index, nullptr, fail_op, a.op_begin, a.op_end);
+        status = run_chain<MinBlocks>(a, c, S, s, sw.epoch, sw.index, nullptr, fail_op, a.op_begin, a.op_end);
     }
 
     // ---- chain split, first launch: hand the cloud to the cluster launch ---
@@ -2201,7 +2226,7 @@ __global__ void __launch_bounds__(512, 1) k_apply_set(WaveArgs a) {
     }
     __syncthreads();
     if (status == kOk && n == 0) status = kEmptyCloud;
-    if (status == kOk) status = run_chain<1>(a, c, S, 0, 0, a.set_seeds + s, fail_op, 0, a.n_ops);
+    if (status == kOk) status = run_chain<1>(a, c, S, s, 0, 0, a.set_seeds + s, fail_op, 0, a.n_ops);
     if (status == kOk && leader) {
       for (int f = 0; f < a.n_bytes_fields && status == kOk; ++f) {
         if (!((a.tracked_mask >> f) & 1u) || !a.set_out[f]) continue;
@@ -2444,9 +2469,33 @@ cudaError_t launch_clustered(K kern, const WaveArgs& a, int grid, int threads, s
 }
 }  // namespace
 
+// MT19937-64 seeding for every (sample, RNG op) of the wave, one thread
+// each: the 311-step serial recurrence (std::mt19937_64::seed) leaves
+// k_cloud's critical path, where thread 0 ran it while the CTA waited (~8 K
+// cycles per downsample and ~4 K per first_draws op).  Op order: rng_slot.
+__global__ void __launch_bounds__(64) k_seed_states(WaveArgs a) {
+  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (uint64_t)a.n_samples * a.n_rng) return;
+  const uint32_t s = (uint32_t)(t / a.n_rng), j = (uint32_t)(t % a.n_rng);
+  int k = 0;
+  while (k < a.n_ops && a.rng_slot[k] != (int8_t)j) ++k;
+  const SampleWork sw = a.samples[s];
+  uint64_t x = rng::mix_seed(a.base_seed, sw.epoch, sw.index, a.ops[k].seed_op_id);
+  uint64_t* out = a.mt_pre + t * rng::kN;
+  out[0] = x;
+  for (uint32_t i = 1; i < (uint32_t)rng::kN; ++i) {
+    x = rng::seed_step(x, i);
+    out[i] = x;
+  }
+}
+
 cudaError_t launch_wave(const WaveArgs& a, int grid, int grid_pre, int threads, size_t smem,
                         cudaStream_t st, cudaEvent_t k0, cudaEvent_t k1) {
   if (a.n_groups) k_scalar_parse<<<(a.n_groups + 127) / 128, 128, 0, st>>>(a);
+  if (a.mt_pre && a.n_samples && a.n_rng) {
+    const uint64_t n = (uint64_t)a.n_samples * a.n_rng;
+    k_seed_states<<<(uint32_t)((n + 63) / 64), 64, 0, st>>>(a);
+  }
   if (k0) cudaEventRecord(k0, st);
   if (a.n_samples) {
     if (a.fps_cluster > 1 && a.split_at > 0) {

@@ -160,6 +160,12 @@ struct WaveArgs {
   int32_t n_ops;
   OpDesc ops[kMaxOps];
   uint64_t base_seed;
+  // MT19937-64 states seeded ahead of k_cloud by k_seed_states, one per
+  // (sample, RNG op): [n_samples][n_rng][312] words; rng_slot[k] = op k's
+  // index among the RNG ops or -1.  mt_pre = nullptr: ops seed in k_cloud.
+  uint64_t* mt_pre;
+  int32_t n_rng;
+  int8_t rng_slot[kMaxOps];
   // outputs: per output field, a slot of out_stride[f] bytes per sample
   int32_t n_out;
   uint8_t* out[kMaxFields];

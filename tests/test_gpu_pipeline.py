@@ -117,6 +117,20 @@ def test_serial_fisher_yates_path(pcp, ref, orc, tmp_path):
     assert_batches_equal(_run(pcp, primary, g, force_serial_fy=True), want)
 
 
+def test_preseeded_states_match_in_kernel_seeding(pcp, ref, orc, tmp_path, monkeypatch):
+    """k_seed_states (MT19937-64 seeded per sample and RNG op ahead of k_cloud)
+    against the in-kernel serial seeding (PCP_NO_PRESEED) and the reference,
+    over every RNG op kind in one chain."""
+    from paper_2603_16945_b200 import synth
+    primary = _ds(pcp, tmp_path, "scannet", 6, group=2, lo=3000, hi=9000)
+    g = synth.graph(["color_augment", "translate", "flip_yz", "random_scale", "random_crop",
+                     ("downsample", {"num_points": 2048}), "rotate", "jitter"], batch_size=2)
+    pre = _run(pcp, primary, g)
+    monkeypatch.setenv("PCP_NO_PRESEED", "1")
+    assert_batches_equal(_run(pcp, primary, g), pre)
+    assert_batches_equal(pre, expected_run(ref, orc, primary, g), float_fields=tolerant_fields(g))
+
+
 def test_corrupt_payload_is_worker_panic(pcp, tmp_path):
     """A flipped payload byte → CRC mismatch → WorkerPanic at that batch."""
     from paper_2603_16945_b200 import synth
