@@ -8,7 +8,7 @@
 set -u
 TAG=${1:-round1}
 OUT=gpurun_out
-B=$(git rev-parse --short HEAD 2>/dev/null || cat .build_id 2>/dev/null || echo unknown)
+B=$(cat .build_id 2>/dev/null || git rev-parse --short HEAD 2>/dev/null || echo unknown)
 mkdir -p $OUT
 nproc > $OUT/${TAG}_nproc.txt
 python bench.py > $OUT/${TAG}_default.json 2> $OUT/${TAG}_default.err
