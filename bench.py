@@ -3,9 +3,13 @@
 point clouds/s and Mpoints/s per GPU and for N GPUs, next to the reference CPU
 pipeline, with the HBM-roofline fraction of the dominant kernel).
 
-  python bench.py [--gpus N --steps K --warmup W] [--config shapenet_part]
+  python bench.py [--gpus N --steps K --warmup W] [--config s3dis] [--quantized]
   torchrun --nproc-per-node N bench.py --gpus N ...   (one process per GPU)
   python bench.py --impl reference ...                (the reference CPU arm)
+
+Default workload (N=1 headline): C3 S3DIS-shaped rooms — BASELINE.json's
+metric names no config, so the line is quoted on the largest single-GPU
+configuration; the other four configs are under --config.
 
 A step = one pass of the hot path (page CRC + decode, record parse, the
 config's op chain, batch assembly) over this rank's shard of the synthetic
@@ -13,8 +17,12 @@ dataset (record-sharded by slice, no collective on the data path).
 `value`: pages resident in HBM before the timed region.  `e2e`: pages in
 pinned host memory, per-wave H2D of the pages and every batch delivered in
 pinned host memory (host_batches: one D2H per field per wave) inside the
-timed region, through the C ABI (pcp_pipeline_* ).  Inputs per step exceed
+timed region, through the C ABI (pcp_pipeline_*).  Inputs per step exceed
 the 126 MB L2, so no flush is needed between steps.
+`roofline`: per-kernel times from a separate serial pass (option "serial":
+one wave in flight, CUDA events around each kernel on the wave's stream), so
+every kernel's time is its own and the kernel times sum to at most the
+serial step time.
 """
 from __future__ import annotations
 
@@ -34,19 +42,19 @@ import numpy as np  # noqa: E402
 
 # workload per config: generator, points, clouds per GPU, group size, batch
 CONFIGS = {
-    "shapenet_part": dict(gen="shapenet", kw={"n_points": 2048}, clouds=16384, group=64, batch=32,
+    "shapenet_part": dict(gen="shapenet", kw={"n_points": 2048}, clouds=16384, group=64, batch=32, cpu_sample=4096,
                           points=2048, desc="ShapeNet-part-shaped 2048-pt clouds + per-point seg "
                           "labels: normalize, downsample 1024 (+seg), random_scale, shuffle; B 32"),
-    "modelnet40": dict(gen="modelnet", kw={"n_points": 10000}, clouds=2048, group=32, batch=32,
+    "modelnet40": dict(gen="modelnet", kw={"n_points": 10000}, clouds=2048, group=32, batch=32, cpu_sample=256,
                        points=10000, desc="ModelNet40-shaped 10k-pt clouds + normals: normalize, "
                        "FPS 1024, rotate, jitter; B 32"),
-    "kitti": dict(gen="kitti", kw={}, clouds=512, group=16, batch=4, points=120000,
+    "kitti": dict(gen="kitti", kw={}, clouds=512, group=16, batch=4, points=120000, cpu_sample=64,
                   desc="KITTI-shaped ~120k-pt XYZI frames: range crop, voxel 0.05 m (+counts), "
                   "rotate, flip_yz; B 4 (CSR batches)"),
-    "s3dis": dict(gen="s3dis", kw={"mean_points": 1_000_000}, clouds=256, group=1, batch=4,
+    "s3dis": dict(gen="s3dis", kw={"mean_points": 1_000_000}, clouds=256, group=1, batch=4, cpu_sample=32,
                   points=1_000_000, desc="S3DIS-shaped ~1M-pt XYZRGB rooms: grid 0.04 m, "
                   "random_crop, downsample 4096; B 4"),
-    "scannet": dict(gen="scannet", kw={}, clouds=192, group=4, batch=4, points=275000,
+    "scannet": dict(gen="scannet", kw={}, clouds=192, group=4, batch=4, points=275000, cpu_sample=16,
                     desc="ScanNet-shaped 50k-500k-pt XYZRGB scenes: grid 0.02 m, downsample "
                     "40000, FPS 20000; B 4"),
 }
@@ -54,6 +62,28 @@ CHAIN_OF = {k: k for k in CONFIGS}
 REF_OPS = {"normalize", "translate", "jitter", "rotate", "random_scale", "flip_yz",
            "color_augment", "random_crop", "downsample"}
 SLICES = 8
+DEFAULT_CONFIG = "s3dis"
+
+
+def load_synth():
+    """paper_2603_16945_b200/synth.py (pure numpy) loaded by path, so the
+    reference arm never imports the package (nor maps its CUDA library)."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "pcp_synth", os.path.join(ROOT, "paper_2603_16945_b200", "synth.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def gen_samples(cfg, n, quantized, first=0, chunk=2048):
+    synth = load_synth()
+    gen = getattr(synth, cfg["gen"])
+    schema, samples = None, []
+    for f in range(first, first + n, chunk):
+        schema, s = gen(min(chunk, first + n - f), quantized=quantized, first=f, **cfg["kw"])
+        samples += s
+    return schema, samples
 
 
 def env():
@@ -63,23 +93,27 @@ def env():
 
 def dataset(cfg_name, cfg, world, quantized, rank, barrier):
     """Rank 0 writes the synthetic dataset (clouds_per_gpu x world clouds,
-    8 slices) to local disk; every rank then opens it."""
-    from paper_2603_16945_b200 import synth, write_dataset
+    8 slices) to local disk with the library's writer (byte-identical to the
+    reference's write_dataset, tests/test_host.py); every rank then opens it."""
+    from paper_2603_16945_b200 import write_dataset
     d = f"/tmp/pcp_bench_{cfg_name}_{'q' if quantized else 'raw'}_{cfg['clouds']}x{world}"
     primary = os.path.join(d, "ds.pcrecord")
     if rank == 0:
-        n = cfg["clouds"] * world
-        gen = getattr(synth, cfg["gen"])
-        chunk = 2048
-        schema, samples = None, []
-        for first in range(0, n, chunk):
-            schema, s = gen(min(chunk, n - first), quantized=quantized, first=first, **cfg["kw"])
-            samples += s
+        schema, samples = gen_samples(cfg, cfg["clouds"] * world, quantized)
         write_dataset(d, "ds", schema, samples, slice_count=SLICES, group_size=cfg["group"],
                       n_threads=min(32, os.cpu_count() or 1))
         del samples
     barrier()
     return primary
+
+
+def reference_dataset(cfg_name, cfg, quantized, n):
+    """The reference arm's input: n clouds of the same workload written by the
+    REFERENCE writer (oracle/_ref write_dataset, format.cpp:499-610)."""
+    from oracle.ffi import Ref
+    d = f"/tmp/pcp_refarm_{cfg_name}_{'q' if quantized else 'raw'}_{n}"
+    schema, samples = gen_samples(cfg, n, quantized)
+    return Ref().write_dataset(d, "ds", schema, samples, slice_count=SLICES, group_size=cfg["group"])
 
 
 class Clocks:
@@ -163,50 +197,88 @@ def ncu_traffic(workload, kernel):
 
 
 def graph_for(cfg_name, cfg, workers=1):
-    from paper_2603_16945_b200 import synth
+    synth = load_synth()
     return synth.graph(synth.CHAINS[CHAIN_OF[cfg_name]], batch_size=cfg["batch"], base_seed=42,
                        workers=workers)
 
 
-def cpu_reference(primary, graph, sample_ids, steps, warmup):
-    """CPU baseline on a bounded sample of the same dataset.
+APPC_OPS = {"fps", "voxel", "grid_subsample", "range_crop"}
 
-    Graphs made only of reference ops run in the reference Pipeline
-    (oracle/_ref: unmodified reference sources) with all host threads,
-    run_benchmark-style timing (bench.cpp:43-96) -> kind "reference".
-    Graphs with App. C ops (fps / voxel / grid / range crop — absent from the
-    reference) run reference read_sample + reference ops + the C restatement
-    for the rest, one thread -> kind "port"."""
-    from oracle.ffi import Orc, Ref
+
+def cpu_reference(primary, graph, sample_ids, steps, warmup):
+    """The reference CPU pipeline on a bounded sample of the same workload,
+    with all host threads, run_benchmark timing (bench.cpp:43-96: items over
+    the cost time, warm-up batch excluded from the clock).
+
+    Chains of reference ops run in the reference Pipeline (oracle/_ref: the
+    unmodified reference sources) -> kind "reference".  Chains with App. C
+    ops (fps / voxel / grid / range crop: absent from the reference) run the
+    same reference Pipeline, whose SourceFn applies the chain up to the last
+    App. C op after read_sample (App. C ops in the C restatement, reference
+    ops in the reference apply_map) on every host thread, the remaining
+    reference ops in its map workers -> kind "port".  Returns
+    (clouds/s median, cores, kind, description)."""
+    from oracle.ffi import Ref
     ref = Ref()
     ncpu = os.cpu_count() or 1
     g = json.loads(json.dumps(graph))
-    steps_ops = [(o["map"], o.get("params", {}), o["id"]) for o in g["ops"] if o["kind"] == "map"]
-    if all(k in REF_OPS for k, _, _ in steps_ops):
-        for o in g["ops"]:
-            if o["kind"] == "source":
-                o["num_workers"] = min(4, ncpu)
-            elif o["kind"] == "map":
-                o["num_workers"] = ncpu
-        vals = []
-        for i in range(warmup + steps):
-            r = ref.bench_pipeline(primary, g, repeats=1, ids=sample_ids)
-            if i >= warmup:
-                vals.append(r["items"] / r["cost_time_s"])
-        return statistics.median(vals), ncpu, "reference"
-    orc = Orc()
+    maps = [o for o in g["ops"] if o["kind"] == "map"]
+    last_c = max([i for i, o in enumerate(maps) if o["map"] in APPC_OPS], default=-1)
+    src = g["ops"][0]
+    for o in maps:
+        o["num_workers"] = ncpu
+    if last_c < 0:
+        src["num_workers"] = min(4, ncpu)
+        run = lambda: ref.bench_pipeline(primary, g, repeats=1, ids=sample_ids)
+        kind, how = "reference", f"reference Pipeline (oracle/_ref), {min(4, ncpu)} source + {ncpu} map workers"
+    else:
+        src["num_workers"] = ncpu
+        prefix = [{"map": o["map"], "params": o.get("params", {}), "op_id": o["id"]} for o in maps[:last_c + 1]]
+        g2 = dict(g, ops=[src] + maps[last_c + 1:] + [o for o in g["ops"] if o["kind"] in ("batch", "sink")])
+        run = lambda: ref.bench_composed(primary, g2, prefix, repeats=1, ids=sample_ids)
+        kind = "port"
+        how = (f"reference Pipeline (oracle/_ref) with {ncpu} source workers whose SourceFn runs "
+               f"read_sample + {'/'.join(p['map'] for p in prefix)} (App. C ops in the C restatement, "
+               f"reference ops in reference apply_map)"
+               + (f", then {ncpu} map workers for {'/'.join(o['map'] for o in maps[last_c + 1:])}"
+                  if maps[last_c + 1:] else ""))
     vals = []
     for i in range(warmup + steps):
-        t0 = time.perf_counter()
-        for k, smp in enumerate(ref.read_samples(primary, sample_ids)):
-            for kind, params, op_id in steps_ops:
-                seed = ref.mix_seed(g.get("base_seed", 0), 0, k, op_id)
-                impl = ref if kind in REF_OPS and "gather" not in params else orc
-                smp = impl.apply_map(kind, params, smp, seed)
-        dt = time.perf_counter() - t0
+        r = run()
         if i >= warmup:
-            vals.append(len(sample_ids) / dt)
-    return statistics.median(vals), 1, "port"
+            vals.append(r["items"] / r["cost_time_s"])
+    return statistics.median(vals), ncpu, kind, how
+
+
+def kernel_pass(P, primary, g, ids, local, steps):
+    """Per-kernel device time without overlap: a fresh pipeline with option
+    "serial" (one wave in flight), CUDA events around every kernel on the
+    wave's stream.  Returns ({kernel: {ms_per_step, alg_bytes_per_step}},
+    serial ms per step)."""
+    import torch
+    p = P.Pipeline(primary, g, ids=ids, device=local, epochs=steps, resident=True, serial=True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    while p.next_batch_raw() is not None:
+        pass
+    torch.cuda.synchronize()
+    e1.record()
+    e1.synchronize()
+    st = p.stats()
+    p.close()
+    out = {}
+    names = {"k_crc_windows": "crc", "k_page_decode+k_page_matches": "decode", "k_cloud": "cloud",
+             "k_wave_offsets+k_compact_wave": "csr"}
+    for k, key in names.items():
+        ms = st[f"{key}_kernel_ms"]
+        by = st[f"{key}_kernel_alg_bytes"]
+        if ms > 0:
+            out[k] = {"ms_per_step": ms / steps, "alg_bytes_per_step": by / steps}
+    for k, v in st.get("kernels", {}).items():  # further timed kernels (name -> ms, alg bytes)
+        if v["ms"] > 0:
+            out[k] = {"ms_per_step": v["ms"] / steps, "alg_bytes_per_step": v["alg_bytes"] / steps}
+    return out, e0.elapsed_time(e1) / steps, st
 
 
 def main():
@@ -215,11 +287,12 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="shapenet_part", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
     ap.add_argument("--quantized", action="store_true", help="LZ4 page variant")
     ap.add_argument("--clouds-per-gpu", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-kernel-pass", action="store_true")
     ap.add_argument("--e2e-no-d2h", action="store_true", help="diagnostics: e2e without the batch reads")
     ap.add_argument("--cpu-sample", type=int, default=0, help="clouds per CPU step")
     ap.add_argument("--batch", type=int, default=0, help="override the config's batch size (diagnostics)")
@@ -230,37 +303,42 @@ def main():
     if args.clouds_per_gpu:
         cfg["clouds"] = args.clouds_per_gpu
     rank, world, local = env()
-    variant = "quantized (LZ4 pages)" if args.quantized else "raw float (stored-raw pages)"
-    config = {"workload": args.config, "desc": cfg["desc"], "variant": variant,
+    coords = "1 mm-quantised coordinates" if args.quantized else "raw float32 coordinates"
+    config = {"workload": args.config, "desc": cfg["desc"], "variant": coords,
               "clouds_per_gpu_per_step": cfg["clouds"], "points_per_cloud": cfg["points"],
               "batch": cfg["batch"], "group_size": cfg["group"], "slices": SLICES,
               "parallelism": f"record-sharded by slice, {world} independent pipelines",
               "l2": "inputs per step > 126 MB L2 (no flush needed)"}
     metric = "point clouds/sec (PcRecord -> training batch)"
-    cpu_sample = args.cpu_sample or {"shapenet_part": 4096, "modelnet40": 64, "kitti": 16,
-                                     "s3dis": 2, "scannet": 2}[args.config]
+    cpu_sample = args.cpu_sample or cfg["cpu_sample"]
 
     if args.impl == "reference":
         if rank != 0:
             return
-        primary = dataset(args.config, cfg, 1, args.quantized, 0, lambda: None)
+        # input written by the reference's own writer; the reference arm maps
+        # no library of this repo
+        primary = reference_dataset(args.config, cfg, args.quantized, cpu_sample)
         g = graph_for(args.config, cfg)
-        from paper_2603_16945_b200 import shard
-        idx = shard.read_index(primary)
-        ids = np.arange(min(cpu_sample, len(idx)), dtype=np.uint64)
-        v, ncpu, kind = cpu_reference(primary, g, ids, args.steps, args.warmup)
+        v, ncpu, kind, how = cpu_reference(primary, g, None, args.steps, args.warmup)
+        config["clouds_per_gpu_per_step"] = cpu_sample
         line = {"metric": metric, "value": v, "unit": "clouds/s", "impl": "reference",
                 "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-                "data": "synthetic", "config": config,
+                "data": "synthetic (seeded generators, paper_2603_16945_b200/synth.py; pages written by "
+                        "the reference write_dataset)", "config": config,
                 "mpoints_per_sec": v * cfg["points"] / 1e6,
                 "cpu_baseline": {"value": v, "unit": "clouds/s", "cores": ncpu, "kind": kind,
-                                 "sample": f"{len(ids)} clouds per step (first entries); "
-                                           f"{'reference Pipeline, ' + str(ncpu) + ' map workers' if kind == 'reference' else 'reference reads/ops + C restatement for App. C ops, 1 thread'}"},
+                                 "sample": f"{cpu_sample} clouds of the workload per step; {how}"},
                 "e2e": {"value": v, "unit": "clouds/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
         if args.config == "shapenet_part":
             line["note"] = "reference downsample ignores the 'gather' extension (seg stays unmoved)"
+        try:  # the reference arm must map no library of this repo
+            with open("/proc/self/maps") as f:
+                mapped = sorted({ln.split()[-1] for ln in f if ln.rstrip().endswith(".so")})
+            line["mapped_repo_libraries"] = [m for m in mapped if m.startswith(ROOT) and "/oracle/" not in m]
+        except OSError:
+            pass
         print(json.dumps(line), flush=True)
         return
 
@@ -278,8 +356,6 @@ def main():
     idx = shard.read_index(primary)
     ids = shard.slice_shard(idx, world, rank)
     g = graph_for(args.config, cfg)
-    points_per_step = 0
-
 
     def timed(resident, steps, d2h):
         # d2h: host_batches -- every batch delivered in pinned host memory, as the
@@ -323,35 +399,39 @@ def main():
         dist.all_reduce(tot)
     clouds_all, points_all = float(tot[0]), float(tot[1])
     value = clouds_all / (ms_max / 1e3)
-    # roofline of the dominant kernel, measured live with CUDA events on the
-    # wave streams (k_cloud and k_page_decode are both timed per wave)
-    peak, peak_kind = peaks()
-    waves = max(1, st1["waves"] - st0["waves"])
-    kern = {}
-    for name, ms_key, by_key in (("k_cloud", "cloud_kernel_ms", "cloud_kernel_alg_bytes"),
-                                 ("k_page_decode", "decode_kernel_ms", "decode_kernel_alg_bytes")):
-        kms = st1[ms_key] - st0[ms_key]
-        kby = st1[by_key] - st0[by_key]
-        kern[name] = {"ms_per_step": kms / args.steps, "alg_bytes_per_step": kby / args.steps,
-                      "achieved_gbs": kby / (kms / 1e3) / 1e9 if kms > 0 else 0.0,
-                      "share_of_step": kms / ms if ms else None}
-    dom = max(kern, key=lambda k: kern[k]["ms_per_step"])
-    # the decode events bracket k_page_decode + k_page_matches (phase 4)
-    dram, cap_clouds = ncu_traffic(args.config, "k_page_decode+k_page_matches" if dom == "k_page_decode" else dom)
-    alg_per_launch = kern[dom]["alg_bytes_per_step"] * args.steps / waves
-    if dram is not None and cap_clouds:  # capture wave -> this run's wave (per-cloud traffic)
-        dram = dram / cap_clouds * (clouds_rank / waves)
-    achieved = kern[dom]["achieved_gbs"]
-    roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "peak_kind": peak_kind, "traffic": dram,
-            "alg_bytes_per_launch": kern[dom]["alg_bytes_per_step"] * args.steps / waves,
-            "kernels": kern}
-    if dom == "k_page_decode":
-        roof["kernel"] = "k_page_decode + k_page_matches"
-        roof["note"] = ("latency-bound: one serial LZ4 token/match chain per page "
-                        "(DESIGN.md 4.2); HBM fraction reported for completeness")
-    if dram is not None and alg_per_launch:
-        roof["traffic_over_alg"] = dram / alg_per_launch
+    pages = {"block_pages_lz4": st1.get("block_pages_lz4"), "block_pages_stored_raw": st1.get("block_pages_stored_raw")}
+    config["variant"] += (f"; block pages: {pages['block_pages_lz4']} LZ4, "
+                          f"{pages['block_pages_stored_raw']} stored-raw")
+
+    roof = None
+    if not args.no_kernel_pass:
+        # roofline of the dominant kernel: per-kernel device time from the
+        # serial pass (no overlap between waves), algorithmic bytes per kernel
+        # over that time, against the burst HBM peak
+        peak, peak_kind = peaks()
+        ksteps = max(1, min(args.steps, 3))
+        kern, serial_ms, sst = kernel_pass(P, primary, g, ids, local, ksteps)
+        for k, v in kern.items():
+            v["achieved_gbs"] = v["alg_bytes_per_step"] / (v["ms_per_step"] / 1e3) / 1e9
+            v["share_of_serial_step"] = v["ms_per_step"] / serial_ms
+        dom = max(kern, key=lambda k: kern[k]["ms_per_step"])
+        waves = max(1, sst["waves"]) / ksteps  # waves per step
+        alg_per_launch = kern[dom]["alg_bytes_per_step"] / waves
+        dram, cap_clouds = ncu_traffic(args.config + ("_q" if args.quantized else ""), dom)
+        if dram is not None and cap_clouds:  # capture wave -> this run's wave (per-cloud traffic)
+            dram = dram / cap_clouds * (clouds_rank / args.steps / waves)
+        roof = {"bound": "hbm", "kernel": dom, "achieved": kern[dom]["achieved_gbs"], "peak": peak,
+                "unit": "GB/s", "frac": kern[dom]["achieved_gbs"] / peak,
+                "peak_kind": f"{peak_kind} burst copy bandwidth (kernel timed alone)",
+                "traffic": dram, "alg_bytes_per_launch": alg_per_launch,
+                "serial_ms_per_step": serial_ms, "kernels": kern,
+                "timing": "serial pass (option serial: one wave in flight), CUDA events around each "
+                          "kernel on the wave stream; kernel ms per step sum to <= serial_ms_per_step"}
+        if dram is not None and alg_per_launch:
+            roof["traffic_over_alg"] = dram / alg_per_launch
+        if dom == "k_page_decode+k_page_matches":
+            roof["note"] = ("latency-bound: one serial LZ4 token/match chain per page "
+                            "(DESIGN.md 4.2); HBM fraction reported for completeness")
     e2e = None
     if not args.no_e2e:
         timed(False, 1, True)  # untimed: fills the library's pinned-buffer pool
@@ -398,11 +478,9 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         ids_cpu = np.arange(min(cpu_sample, len(idx)), dtype=np.uint64)
-        v, ncpu, kind = cpu_reference(primary, g, ids_cpu, 1, 0)
+        v, ncpu, kind, how = cpu_reference(primary, g, ids_cpu, 1, 0)
         cpu = {"value": v, "unit": "clouds/s", "cores": ncpu, "kind": kind,
-               "sample": f"{len(ids_cpu)} clouds of the same dataset; "
-                         + (f"reference Pipeline (oracle/_ref), {ncpu} map workers" if kind == "reference"
-                            else "reference reads/ops + C restatement for App. C ops, 1 thread")}
+               "sample": f"{len(ids_cpu)} clouds of the same dataset; {how}"}
     if rank == 0:
         line = {"metric": metric, "value": value, "unit": "clouds/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
@@ -415,7 +493,7 @@ def main():
                 "batches_per_step": nb / args.steps}
         if "op_cycles" in st1:  # PCP_OP_TIMING=1 diagnostics: share of k_cloud CTA time
             oc = st1["op_cycles"]
-            from paper_2603_16945_b200 import synth
+            synth = load_synth()
             names = (["stage+decode"] + [o if isinstance(o, str) else o[0]
                                          for o in synth.CHAINS[CHAIN_OF[args.config]]] + ["writes"])
             tot_c = max(1, sum(oc))

@@ -188,8 +188,14 @@ typedef struct {
 } pcp_batch;
 
 /* Next batch in dataset order (Pipeline::next_batch); *end_of_stream = 1
- * and PCP_OK once the final epoch drained.  The views stay valid until the
- * pipeline has moved two waves further. */
+ * and PCP_OK once the final epoch drained.
+ * View lifetime: every pointer in *out (d_ptr, h_ptr, h_offsets) is valid
+ * until the NEXT pcp_pipeline_next_batch / pcp_pipeline_close call on this
+ * handle.  Device reads of d_ptr must be enqueued on pcp_pipeline_stream()
+ * before that call: the slot is refilled only after the work already queued
+ * on that stream (the reference returns Batch by value; copy what you keep).
+ * Variable-length fields (crop / voxel outputs, strings) are CSR: d_ptr is
+ * contiguous over the batch's samples with h_offsets[k] byte offsets. */
 int pcp_pipeline_next_batch(pcp_pipeline* p, pcp_batch* out, int* end_of_stream);
 /* Stream on which the returned batch views are ready (use it for D2H of the
  * batch; waves are computed on an internal stream). cudaStream_t as void*. */

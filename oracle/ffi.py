@@ -149,6 +149,9 @@ class Ref:
         L.ref_bench_pipeline.argtypes = [C.c_char_p, C.c_char_p, C.c_uint32, u64p, C.c_size_t,
                                          C.POINTER(C.c_double), C.POINTER(C.c_uint64),
                                          C.POINTER(C.c_uint64), C.POINTER(C.c_double)]
+        L.ref_bench_composed.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_uint32, u64p,
+                                         C.c_size_t, C.POINTER(C.c_double), C.POINTER(C.c_uint64),
+                                         C.POINTER(C.c_uint64), C.POINTER(C.c_double)]
         L.ref_free.argtypes = [C.c_void_p]
 
     def _check(self, st):
@@ -257,6 +260,23 @@ class Ref:
             p, n = arr.ctypes.data_as(C.POINTER(C.c_uint64)), len(arr)
         t, items, batches, cpu = C.c_double(), C.c_uint64(), C.c_uint64(), C.c_double()
         self._check(self.L.ref_bench_pipeline(str(primary).encode(), g.encode(), repeats, p, n,
+                                              C.byref(t), C.byref(items), C.byref(batches),
+                                              C.byref(cpu)))
+        return {"cost_time_s": t.value, "items": items.value, "batches": batches.value,
+                "avg_cpu_percent": cpu.value}
+
+
+    def bench_composed(self, primary, graph: dict, prefix: list, repeats=1, ids=None) -> dict:
+        """run_benchmark over the reference Pipeline whose SourceFn applies
+        ``prefix`` ([{"map", "params", "op_id"}], App. C ops via the C
+        restatement, reference ops via the reference apply_map) after
+        read_sample; ``graph`` carries the reference-op suffix."""
+        arr = np.ascontiguousarray(ids if ids is not None else [], dtype=np.uint64)
+        p = arr.ctypes.data_as(C.POINTER(C.c_uint64)) if ids is not None else None
+        t, items, batches, cpu = C.c_double(), C.c_uint64(), C.c_uint64(), C.c_double()
+        self._check(self.L.ref_bench_composed(str(primary).encode(), json.dumps(graph).encode(),
+                                              json.dumps(prefix).encode(), repeats, p,
+                                              len(arr) if ids is not None else 0,
                                               C.byref(t), C.byref(items), C.byref(batches),
                                               C.byref(cpu)))
         return {"cost_time_s": t.value, "items": items.value, "batches": batches.value,

@@ -19,6 +19,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <algorithm>
+#include <map>
 #include <vector>
 
 #include "pcpipe/bench.hpp"
@@ -29,6 +31,7 @@
 #include "pcpipe/metadata.hpp"
 #include "pcpipe/pipeline.hpp"
 #include "pcpipe/transforms.hpp"
+#include "pcpipe_oracle.h"
 
 using namespace pcpipe;
 
@@ -343,6 +346,189 @@ int ref_bench_pipeline(const char* primary, const char* graph_json,
     PipelineGraph g = PipelineGraph::from_json(json::parse(graph_json));
     SourceFn src = [rd, idx](std::uint64_t, std::uint64_t i) {
       return rd->read_sample(idx->sample_meta_list[i]);
+    };
+    BenchReport rep = run_benchmark(g, src, idx->size(), repeats, 50);
+    *cost_time_s = rep.cost_time_s;
+    *items = rep.items;
+    *batches = rep.batches;
+    *avg_cpu_percent = rep.avg_cpu_percent;
+  });
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// CPU baseline for chains with App. C ops (fps / voxel / grid_subsample /
+// range_crop and the "gather" extension), which the reference lacks.  The
+// reference Pipeline runs as shipped; its SourceFn (pipeline.cpp:442-462,
+// source workers = all host threads) reads the sample with the reference
+// reader and applies the chain's prefix up to the last non-reference step:
+// reference ops through the reference apply_map, App. C ops through the C
+// restatement (pcpipe_oracle.c, compiled into this library), each seeded with
+// the reference mix_seed(base, epoch, index, op_id).  The remaining
+// reference-op suffix runs in the Pipeline's own map workers.
+namespace {
+
+struct Step {
+  std::string map;
+  json params;
+  std::uint64_t op_id;
+};
+
+bool is_ref_op(const Step& st) {
+  static const char* k[] = {"normalize", "translate", "jitter", "rotate", "random_scale",
+                            "flip_yz", "color_augment", "random_crop", "downsample"};
+  if (st.params.is_object() && st.params.contains("gather")) return false;
+  for (const char* n : k)
+    if (st.map == n) return true;
+  return false;
+}
+
+Blob& blob_of(Sample& s, const std::string& name) { return std::get<Blob>(s.values.at(name)); }
+bool has_blob(const Sample& s, const std::string& name) {
+  auto it = s.values.find(name);
+  return it != s.values.end() && std::holds_alternative<Blob>(it->second);
+}
+
+// Orc.apply_map (oracle/ffi.py) in C++: Sample <-> orc_cloud.
+Sample orc_apply(const Step& st, Sample s, std::uint64_t seed) {
+  static const std::map<std::string, int> kinds = {
+      {"normalize", ORC_NORMALIZE}, {"translate", ORC_TRANSLATE}, {"jitter", ORC_JITTER},
+      {"rotate", ORC_ROTATE}, {"random_scale", ORC_RANDOM_SCALE}, {"flip_yz", ORC_FLIP_YZ},
+      {"color_augment", ORC_COLOR_AUGMENT}, {"random_crop", ORC_RANDOM_CROP},
+      {"downsample", ORC_DOWNSAMPLE}, {"fps", ORC_FPS}, {"voxel", ORC_VOXEL},
+      {"grid_subsample", ORC_VOXEL}, {"range_crop", ORC_RANGE_CROP}};
+  const auto kit = kinds.find(st.map);
+  if (kit == kinds.end()) fail(Errc::kUnknownOp, "unknown map '" + st.map + "'");
+  const json p = st.params.is_object() ? st.params : json::object();
+  std::vector<std::string> gather;
+  if (p.contains("gather"))
+    for (const auto& g : p["gather"]) gather.push_back(g.get<std::string>());
+  if (!has_blob(s, "data")) fail(Errc::kMissingField, "sample has no 'data' coordinates");
+  const char* p3[3] = {"data", "normal", "color"};
+  bool present[3] = {false, false, false};
+  std::size_t len3[3] = {0, 0, 0};
+  for (int k = 0; k < 3; ++k) {
+    if (!has_blob(s, p3[k])) continue;
+    const Blob& b = blob_of(s, p3[k]);
+    if (k > 0 && b.empty()) continue;
+    if (b.size() % 12) fail(Errc::kMissingField, std::string(p3[k]) + " is not an Nx3 float32 blob");
+    present[k] = true;
+    len3[k] = b.size() / 12;
+  }
+  const std::size_t n = len3[0];
+  if (n == 0) fail(Errc::kEmptyCloud, "zero points");
+  const std::int64_t tgt = p.value("num_points", std::int64_t{0});
+  std::size_t cap = std::max<std::size_t>({n, (std::size_t)std::max<std::int64_t>(tgt, 0), len3[1], len3[2], 1});
+  std::vector<float> buf3[3];
+  orc_cloud cl{};
+  float** dst3[3] = {&cl.data, &cl.normal, &cl.color};
+  for (int k = 0; k < 3; ++k) {
+    if (!present[k]) continue;
+    buf3[k].assign(cap * 3, 0.0f);
+    const Blob& b = blob_of(s, p3[k]);
+    std::memcpy(buf3[k].data(), b.data(), b.size());
+    *dst3[k] = buf3[k].data();
+  }
+  cl.n = n;
+  cl.n_normal = present[1] ? len3[1] : 0;
+  cl.n_color = present[2] ? len3[2] : 0;
+  std::vector<float> bi;
+  if (has_blob(s, "intensity") && !blob_of(s, "intensity").empty()) {
+    const Blob& b = blob_of(s, "intensity");
+    const std::size_t ni = b.size() / 4;
+    bi.assign(std::max(cap, ni), 0.0f);
+    std::memcpy(bi.data(), b.data(), ni * 4);
+    cl.intensity = bi.data();
+    cl.n_intensity = ni;
+  }
+  std::vector<std::string> extra;
+  for (const auto& g : gather)
+    if (g != "intensity" && s.values.count(g)) extra.push_back(g);
+  if (extra.size() > ORC_MAX_EXTRA) extra.resize(ORC_MAX_EXTRA);
+  std::vector<std::vector<std::uint8_t>> eb(extra.size());
+  for (std::size_t e = 0; e < extra.size(); ++e) {
+    const Blob& b = blob_of(s, extra[e]);
+    const std::size_t es = std::max<std::size_t>(1, b.size() / n);
+    eb[e].assign(cap * es, 0);
+    std::memcpy(eb[e].data(), b.data(), std::min(b.size(), eb[e].size()));
+    cl.extra[e] = eb[e].data();
+    cl.extra_elem[e] = es;
+    cl.n_extra[e] = b.size() / es;
+  }
+  std::vector<std::int32_t> counts;
+  const bool want_counts = (st.map == "voxel" || st.map == "grid_subsample") &&
+                           p.value("counts", st.map == "voxel");
+  if (want_counts) {
+    counts.assign(cap, 0);
+    cl.counts = counts.data();
+  }
+  cl.cap = cap;
+  orc_params op{};
+  if (p.contains("theta")) {
+    op.has_theta = 1;
+    op.theta = p["theta"].get<float>();
+  }
+  op.num_points = tgt;
+  op.gather_intensity = std::find(gather.begin(), gather.end(), "intensity") != gather.end();
+  op.gather_extra = !extra.empty();
+  op.voxel_size = p.value("voxel_size", 0.0f);
+  if (p.contains("origin")) {
+    op.has_origin = 1;
+    for (int k = 0; k < 3; ++k) op.origin[k] = p["origin"][k].get<float>();
+  }
+  if (p.contains("lo"))
+    for (int k = 0; k < 3; ++k) op.lo[k] = p["lo"][k].get<float>();
+  if (p.contains("hi"))
+    for (int k = 0; k < 3; ++k) op.hi[k] = p["hi"][k].get<float>();
+  const int st_code = orc_apply_map(kit->second, &op, &cl, seed);
+  if (st_code) fail(static_cast<Errc>(st_code - 1), "apply_map(" + st.map + ") restatement");
+  auto put_blob = [&](const char* name, const void* src, std::size_t nbytes) {
+    const auto* b = static_cast<const std::uint8_t*>(src);
+    s.values[name] = Blob(b, b + nbytes);
+  };
+  put_blob("data", buf3[0].data(), cl.n * 12);
+  if (present[1]) put_blob("normal", buf3[1].data(), cl.n_normal * 12);
+  if (present[2]) put_blob("color", buf3[2].data(), cl.n_color * 12);
+  if (cl.intensity) put_blob("intensity", bi.data(), cl.n_intensity * 4);
+  for (std::size_t e = 0; e < extra.size(); ++e)
+    put_blob(extra[e].c_str(), eb[e].data(), cl.n_extra[e] * cl.extra_elem[e]);
+  if (want_counts) put_blob("count", counts.data(), cl.n_counts * 4);
+  return s;
+}
+
+}  // namespace
+
+extern "C" {
+
+// prefix_json: [{"map":..., "params":{...}, "op_id":k}, ...] applied in the
+// SourceFn; graph_json holds the reference-op suffix (map nodes) to run in
+// the Pipeline.  source_workers = threads for the SourceFn.
+int ref_bench_composed(const char* primary, const char* graph_json, const char* prefix_json,
+                       std::uint32_t repeats, const std::uint64_t* ids, std::size_t n_ids,
+                       double* cost_time_s, std::uint64_t* items, std::uint64_t* batches,
+                       double* avg_cpu_percent) {
+  return guarded([&] {
+    auto rd = std::make_shared<DatasetReader>(primary);
+    auto idx = std::make_shared<IndexTable>(
+        select_entries(build_index({rd->header()}), ids, n_ids));
+    const json gj = json::parse(graph_json);
+    PipelineGraph g = PipelineGraph::from_json(gj);
+    const std::uint64_t base = gj.value("base_seed", std::uint64_t{0});
+    auto steps = std::make_shared<std::vector<Step>>();
+    for (const auto& o : json::parse(prefix_json))
+      steps->push_back({o.at("map").get<std::string>(), o.value("params", json::object()),
+                        o.at("op_id").get<std::uint64_t>()});
+    SourceFn src = [rd, idx, steps, base](std::uint64_t epoch, std::uint64_t i) {
+      Sample s = rd->read_sample(idx->sample_meta_list[i]);
+      for (const auto& st : *steps) {
+        const std::uint64_t seed = mix_seed(base, epoch, i, st.op_id);
+        if (is_ref_op(st))
+          s = apply_map(map_kind_from_name(st.map), st.params, std::move(s), seed);
+        else
+          s = orc_apply(st, std::move(s), seed);
+      }
+      return s;
     };
     BenchReport rep = run_benchmark(g, src, idx->size(), repeats, 50);
     *cost_time_s = rep.cost_time_s;

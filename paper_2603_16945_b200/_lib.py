@@ -190,11 +190,11 @@ class Pipeline:
 
     def __init__(self, primary, graph, ids=None, device: int = 0, epochs: int = 1,
                  resident: bool = True, wave_batches: int = 0, force_serial_fy: bool = False,
-                 slots: int | None = None, host_batches: bool = False):
+                 slots: int | None = None, host_batches: bool = False, **options):
         L = lib()
         g = graph if isinstance(graph, str) else json.dumps(graph)
         o = {"epochs": epochs, "resident": resident, "wave_batches": wave_batches,
-             "force_serial_fy": force_serial_fy, "host_batches": host_batches}
+             "force_serial_fy": force_serial_fy, "host_batches": host_batches, **options}
         if slots is not None:
             o["slots"] = slots
         opts = json.dumps(o)

@@ -434,6 +434,7 @@ struct OutField {
   int32_t kind;        // value kind of the batch field
   int32_t schema_idx;  // schema field, or -1 for synthesized fields
   uint64_t stride;     // slot bytes per sample
+  bool varlen;         // bytes / string: per-sample lengths may differ (CSR)
 };
 
 struct Wave {
@@ -444,28 +445,32 @@ struct Wave {
   bool launched = false;
   cudaStream_t stream = nullptr;  // one stream per slot: consecutive waves overlap
   cudaEvent_t done = nullptr, k0 = nullptr, k1 = nullptr, d0 = nullptr, d1 = nullptr;
+  cudaEvent_t c0 = nullptr, c1 = nullptr, s0 = nullptr, s1 = nullptr;  // CRC windows, wave CSR
+  uint64_t crc_alg_bytes = 0;     // payload bytes k_crc_windows reads
   cudaEvent_t h0 = nullptr, h1 = nullptr;  // staging copies (timeline diagnostics)
   cudaEvent_t served = nullptr;  // serve stream passed this wave's last batch (user copies enqueued)
   uint64_t decode_alg_bytes = 0;  // payload + raw bytes of the pages k_page_decode handles
   DevBuf gscratch;                // k_cloud global slab (smem_mode 0), per slot
   // device
-  DevBuf bytes_stage, raw, tables, outs, compact, compact_meta, lz4_scratch, lz4_timing;
+  DevBuf bytes_stage, raw, tables, outs, compact, lz4_scratch, lz4_timing;
   DevBuf handoff;  // chain split: the clouds between the prefix and the cluster launch
   DevBuf mt_pre;   // pre-seeded MT19937-64 states [n][n_rng][312] (k_seed_states)
   uint32_t n_todo = 0;
-  HostBuf h_tables, h_res, h_compact_meta;
-  std::vector<uint64_t> out_base;  // per output field: offset in outs
+  HostBuf h_tables, h_res;
+  std::vector<uint64_t> out_base;  // per output field: offset in outs (and in compact)
   // results (pinned, filled by D2H)
   int32_t* h_status = nullptr;
   int32_t* h_op = nullptr;
   int32_t* h_where = nullptr;
   uint64_t* h_len = nullptr;
+  uint64_t* h_woff = nullptr;   // [n_var][n+1] sample byte offsets of varlen fields (k_wave_offsets)
+  uint32_t* h_dense = nullptr;  // [n_out] every sample fills its slot
+  uint64_t staged = 0;          // host_batches: samples [0, staged) are in h_out
   uint64_t in_payload_bytes = 0, in_points = 0;
   std::vector<std::vector<uint64_t>> offsets;  // per field, for the served batch
   // host_batches: the whole wave's batch fields in pinned host memory
   PooledHostBuf h_out;
   std::vector<uint64_t> h_base;                 // per field: offset in h_out
-  std::vector<std::vector<uint64_t>> woff;      // per field: n+1 sample offsets
   cudaEvent_t host_ready = nullptr;
 };
 
@@ -501,9 +506,12 @@ struct Pipeline {
   // page heads: [group] -> scalar, block
   std::vector<PageHead> scalar_head, block_head;
   bool block_tiles_payload_ok = true;
+  uint64_t block_pages_lz4 = 0;
   // schema / outputs
   std::vector<int32_t> bytes_fields;  // schema index per bytes field
   std::vector<OutField> outs;
+  std::vector<int32_t> var_index;  // batch field -> varlen slot (or -1)
+  uint32_t n_var = 0;
   WaveArgs proto{};
   int threads = 512, grid = 0, grid_pre = 0;
   size_t smem = 0;
@@ -521,7 +529,9 @@ struct Pipeline {
   // stats
   uint64_t clouds = 0, points_in = 0, payload_bytes = 0, batches = 0;
   uint64_t h2d_bytes = 0, launches = 0, alg_bytes = 0;
-  double kernel_ms = 0, cloud_kernel_ms = 0, decode_kernel_ms = 0;
+  double kernel_ms = 0, cloud_kernel_ms = 0, decode_kernel_ms = 0, crc_kernel_ms = 0, csr_kernel_ms = 0;
+  uint64_t crc_alg_bytes = 0, csr_alg_bytes = 0;
+  bool serial = false;  // option "serial": one wave in flight (non-overlapped kernel timing)
   double host_launch_ms = 0, host_wait_ms = 0;  // host-side wall time (diagnostics)
   bool timeline_on = false;
   cudaEvent_t t_open = nullptr;
@@ -540,6 +550,8 @@ struct Pipeline {
       if (w.d0) cudaEventDestroy(w.d0);
       if (w.d1) cudaEventDestroy(w.d1);
       if (w.h0) cudaEventDestroy(w.h0);
+      for (cudaEvent_t e : {w.c0, w.c1, w.s0, w.s1})
+        if (e) cudaEventDestroy(e);
       if (w.h1) cudaEventDestroy(w.h1);
       if (w.served) cudaEventDestroy(w.served);
       if (w.host_ready) cudaEventDestroy(w.host_ready);
@@ -566,6 +578,7 @@ struct Pipeline {
         slots_set = true;
       }
       force_serial_fy = o.value("force_serial_fy", false);
+      serial = o.value("serial", false);
     }
     h = read_header(primary);
     dir = fs::path(primary).parent_path().string();
@@ -614,6 +627,7 @@ struct Pipeline {
       CK(cudaEventCreate(&w.d0));
       CK(cudaEventCreate(&w.d1));
       CK(cudaEventCreate(&w.h0));
+      for (cudaEvent_t* e : {&w.c0, &w.c1, &w.s0, &w.s1}) CK(cudaEventCreate(e));
       CK(cudaEventCreate(&w.h1));
       CK(cudaEventCreateWithFlags(&w.served, cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&w.host_ready, cudaEventDisableTiming));
@@ -655,6 +669,7 @@ struct Pipeline {
       const uint64_t avail_b = data[gr.slice].size() - std::min<uint64_t>(gr.block_off, data[gr.slice].size());
       scalar_head[gi] = parse_page_head(base + gr.scalar_off, std::min(avail_s, gr.scalar_len));
       block_head[gi] = parse_page_head(base + gr.block_off, std::min(avail_b, gr.block_len));
+      if (block_head[gi].flags & kFlagOuterLz4) ++block_pages_lz4;
     }
     if (resident) {
       d_store.ensure(store_bytes);
@@ -810,6 +825,7 @@ struct Pipeline {
         o.stride = es * h.schema[f].elems();
       }
       o.stride = std::max<uint64_t>(o.stride, 4);
+      o.varlen = h.schema[f].kind == kBytes || h.schema[f].kind == kString;
       a.fields[f].out_index = (int32_t)outs.size();
       outs.push_back(o);
     }
@@ -821,6 +837,7 @@ struct Pipeline {
       o.kind = kBytes;
       o.schema_idx = -1;
       o.stride = align4(cap * 4);
+      o.varlen = true;
       size_t pos = 0;
       while (pos < outs.size() && outs[pos].name < o.name) ++pos;
       outs.insert(outs.begin() + pos, o);
@@ -832,6 +849,10 @@ struct Pipeline {
     }
     if (outs.size() > (size_t)PCP_MAX_BATCH_FIELDS) fail(kOutOfBounds, "too many batch fields");
     a.n_out = (int32_t)outs.size();
+    var_index.assign(outs.size(), -1);
+    n_var = 0;
+    for (size_t f = 0; f < outs.size(); ++f)
+      if (outs[f].varlen) var_index[f] = (int32_t)n_var++;
     // per-CTA buffer plan for k_cloud (sizes from the op chain, shared
     // memory by priority, the rest in a per-CTA global slab)
     bool any_stored_raw = false;
@@ -1089,7 +1110,9 @@ struct Pipeline {
     const uint64_t o_sop = o_sst + sz(w.n * 4);
     const uint64_t o_swh = o_sop + sz(w.n * 4);
     const uint64_t o_len = o_swh + sz(w.n * 4);
-    const uint64_t total = o_len + sz(outs.size() * w.n * 8);
+    const uint64_t o_woff = o_len + sz(outs.size() * w.n * 8);
+    const uint64_t o_dense = o_woff + sz((uint64_t)n_var * (w.n + 1) * 8);
+    const uint64_t total = o_dense + sz(outs.size() * 4);
     // size every buffer first (a dry run stops here: open() pre-sizes the
     // slots for the largest planned wave so no cudaMalloc lands mid-run)
     w.h_tables.ensure(up_bytes);
@@ -1104,19 +1127,13 @@ struct Pipeline {
       out_total += align16(outs[f].stride * w.n) + 64;
     }
     w.outs.ensure(out_total);
+    if (n_var) w.compact.ensure(out_total);
     // host_batches: size the pinned wave buffer up front (exact for fixed-size
     // fields; ragged ones grow it on demand past 1 GiB)
     if (host_batches) w.h_out.ensure(std::min<uint64_t>(out_total + 64, 1ull << 30));
     if (proto.split_at) w.handoff.ensure(proto.handoff_stride * w.n);
     if (proto.n_rng) w.mt_pre.ensure(w.n * proto.n_rng * 312 * 8);
     w.h_res.ensure(total - o_sst + 16);
-    {
-      uint64_t need = 0;
-      for (size_t q = 0; q < outs.size(); ++q) need += align16(outs[q].stride * B) + 64;
-      w.compact.ensure(need);
-      w.compact_meta.ensure(2 * (uint64_t)(B + 1) * 8 * outs.size());
-      w.h_compact_meta.ensure(2 * (uint64_t)(B + 1) * 8 * outs.size());
-    }
     if (dry) return;
     uint8_t* ht = w.h_tables.as<uint8_t>();
     std::memcpy(ht + o_pages, pages.data(), pages.size() * sizeof(PageRef));
@@ -1168,8 +1185,12 @@ struct Pipeline {
       a.out_stride[f] = outs[f].stride;
     }
     // ---- kernels ---------------------------------------------------------------
+    CK(cudaEventRecord(w.c0, w.stream));
     CK(launch_crc_windows(bytes, reinterpret_cast<const CrcWindow*>(dt + o_wins),
                           (uint32_t)wins.size(), d_shift.as<uint32_t>(), a.page_crc_acc, sms, w.stream));
+    CK(cudaEventRecord(w.c1, w.stream));
+    w.crc_alg_bytes = 0;
+    for (const auto& cw : wins) w.crc_alg_bytes += cw.len;
     long long* tm = nullptr;
     if (lz4_timing) {  // PCP_LZ4_TIMING=1: per-page phase clocks (diagnostics)
       w.lz4_timing.ensure(todo.size() * 128);
@@ -1186,6 +1207,25 @@ struct Pipeline {
     for (uint32_t pi : todo) w.decode_alg_bytes += pages[pi].pay_len + pages[pi].raw_len;
     CK(launch_wave(a, grid, grid_pre, threads, smem, w.stream, w.k0, w.k1));
     launches += (wins.empty() ? 0 : 1) + (todo.empty() ? 0 : 2) + (ng ? 1 : 0) + (proto.n_rng ? 1 : 0) + 1 + 1 + 1;
+    // ---- per-wave CSR of the variable-length fields (device side) ------------
+    {
+      WaveCsr c{};
+      c.n_out = (uint32_t)outs.size();
+      c.n_var = n_var;
+      for (size_t f = 0; f < outs.size(); ++f) {
+        c.stride[f] = outs[f].stride;
+        c.var_index[f] = var_index[f];
+        if (var_index[f] >= 0) c.var_field[var_index[f]] = (int32_t)f;
+        c.outs[f] = w.outs.as<uint8_t>() + w.out_base[f];
+        c.compact[f] = n_var ? w.compact.as<uint8_t>() + w.out_base[f] : nullptr;
+      }
+      c.woff = reinterpret_cast<uint64_t*>(dt + o_woff);
+      c.dense = reinterpret_cast<uint32_t*>(dt + o_dense);
+      CK(cudaEventRecord(w.s0, w.stream));
+      CK(launch_wave_csr(a.out_len, c, (uint32_t)w.n, sms, w.stream));
+      CK(cudaEventRecord(w.s1, w.stream));
+      launches += 1 + (n_var ? 1 : 0);
+    }
     h2d_bytes += up_bytes;
     // ---- results back to pinned host -------------------------------------------
 
@@ -1193,7 +1233,10 @@ struct Pipeline {
     w.h_status = reinterpret_cast<int32_t*>(hr);
     w.h_op = reinterpret_cast<int32_t*>(hr + align16(w.n * 4));
     w.h_where = reinterpret_cast<int32_t*>(hr + 2 * align16(w.n * 4));
-    w.h_len = reinterpret_cast<uint64_t*>(hr + 3 * align16(w.n * 4));
+    w.h_len = reinterpret_cast<uint64_t*>(hr + (o_len - o_sst));
+    w.h_woff = reinterpret_cast<uint64_t*>(hr + (o_woff - o_sst));
+    w.h_dense = reinterpret_cast<uint32_t*>(hr + (o_dense - o_sst));
+    w.staged = 0;
     // one contiguous region: the host layout mirrors o_sst..total
     static_assert(sizeof(int32_t) == 4, "");
     uint8_t* hr_dev = nullptr;
@@ -1222,43 +1265,39 @@ struct Pipeline {
   }
 
   // host_batches: once a wave's kernels are done, its batch fields go to
-  // pinned host memory on the serve stream -- one D2H per field when every
-  // sample fills its slot (the slots are then contiguous), one per sample for
-  // ragged fields -- and the wave's first batch waits for them.
-  void stage_host(Wave& w) {
-    const uint64_t n = w.n;
-    w.woff.assign(outs.size(), std::vector<uint64_t>(n + 1, 0));
+  // pinned host memory on the serve stream: one D2H per field per wave (dense
+  // fields from their contiguous slots, variable-length fields from the
+  // wave's device CSR).  Only samples [0, lim) are copied: the batches before
+  // a wave's first failing batch are served intact, the failing one raises.
+  void stage_host(Wave& w, uint64_t lim) {
     w.h_base.assign(outs.size(), 0);
-    std::vector<uint8_t> dense(outs.size(), 1);
     uint64_t total = 0;
+    std::vector<uint64_t> bytes(outs.size(), 0);
     for (size_t f = 0; f < outs.size(); ++f) {
-      auto& off = w.woff[f];
-      for (uint64_t k = 0; k < n; ++k) {
-        const uint64_t L = w.h_len[f * n + k];
-        off[k + 1] = off[k] + L;
-        if (L != outs[f].stride) dense[f] = 0;
-      }
+      bytes[f] = field_offset(w, f, lim);
       w.h_base[f] = total;
-      total = align16(total + off[n]) + 64;
+      total = align16(total + bytes[f]) + 64;
     }
     w.h_out.ensure(total + 64);
     uint8_t* ho = w.h_out.as<uint8_t>();
     for (size_t f = 0; f < outs.size(); ++f) {
-      const uint8_t* src = w.outs.as<uint8_t>() + w.out_base[f];
-      uint8_t* dst = ho + w.h_base[f];
-      const auto& off = w.woff[f];
-      if (dense[f]) {
-        if (off[n]) CK(cudaMemcpyAsync(dst, src, off[n], cudaMemcpyDeviceToHost, serve_stream));
-      } else {
-        for (uint64_t k = 0; k < n; ++k)
-          if (off[k + 1] > off[k])
-            CK(cudaMemcpyAsync(dst + off[k], src + k * outs[f].stride, off[k + 1] - off[k],
-                               cudaMemcpyDeviceToHost, serve_stream));
-      }
-      d2h_bytes += off[n];
+      if (bytes[f]) CK(cudaMemcpyAsync(ho + w.h_base[f], field_base(w, f), bytes[f], cudaMemcpyDeviceToHost,
+                                       serve_stream));
+      d2h_bytes += bytes[f];
     }
     CK(cudaEventRecord(w.host_ready, serve_stream));
     CK(cudaEventSynchronize(w.host_ready));
+    w.staged = lim;
+  }
+
+  // Batch field layout of a finished wave: dense fields (every sample fills
+  // its slot) are their slots; variable-length ones live in the wave's CSR.
+  bool field_dense(const Wave& w, size_t f) const { return !outs[f].varlen || w.h_dense[f] != 0; }
+  uint64_t field_offset(const Wave& w, size_t f, uint64_t s) const {
+    return field_dense(w, f) ? s * outs[f].stride : w.h_woff[(uint64_t)var_index[f] * (w.n + 1) + s];
+  }
+  const uint8_t* field_base(const Wave& w, size_t f) const {
+    return (field_dense(w, f) ? w.outs.as<uint8_t>() : w.compact.as<uint8_t>()) + w.out_base[f];
   }
 
   // ---- iteration -------------------------------------------------------------
@@ -1293,8 +1332,8 @@ struct Pipeline {
       }
       // keep every slot busy while waiting: waves go to slots in ring order
       // on per-slot streams, so up to `slots` waves overlap (copies, LZ4
-      // chains and k_cloud of different waves)
-      for (int d = 1; d < ns && next_plan < plan.size(); ++d) {
+      // chains and k_cloud of different waves).  "serial": one wave at a time.
+      for (int d = 1; d < ns && next_plan < plan.size() && !serial; ++d) {
         Wave& wp = slots[(nxt + d) % ns];
         if (!wp.launched) {
           const auto t0 = clk::now();
@@ -1310,6 +1349,13 @@ struct Pipeline {
       cloud_kernel_ms += ms;
       CK(cudaEventElapsedTime(&ms, wn.d0, wn.d1));
       decode_kernel_ms += ms;
+      CK(cudaEventElapsedTime(&ms, wn.c0, wn.c1));
+      crc_kernel_ms += ms;
+      crc_alg_bytes += wn.crc_alg_bytes;
+      CK(cudaEventElapsedTime(&ms, wn.s0, wn.s1));
+      csr_kernel_ms += ms;
+      for (size_t f = 0; f < outs.size(); ++f)  // bytes moved by k_compact_wave (read + write)
+        if (!field_dense(wn, f)) csr_alg_bytes += 2 * field_offset(wn, f, wn.n);
       if (timeline_on) {  // PCP_TIMELINE=1: per-wave event times (ms from open)
         std::vector<double> row;
         for (cudaEvent_t e : {wn.h0, wn.h1, wn.d0, wn.d1, wn.k0, wn.k1, wn.done}) {
@@ -1341,10 +1387,14 @@ struct Pipeline {
       points_in += wn.in_points;
       payload_bytes += wn.in_payload_bytes;
       if (host_batches) {
-        // a failed wave is reported below, before any copy of its batches
-        bool ok = true;
-        for (uint64_t s = 0; s < wn.n && ok; ++s) ok = wn.h_status[s] == kOk;
-        if (ok) stage_host(wn);
+        uint64_t first_bad = wn.n;
+        for (uint64_t s = 0; s < wn.n; ++s)
+          if (wn.h_status[s] != kOk) {
+            first_bad = s;
+            break;
+          }
+        const uint64_t B64 = g.batch_size;
+        stage_host(wn, first_bad == wn.n ? wn.n : first_bad / B64 * B64);
       }
     }
     Wave& w = slots[cur];
@@ -1371,42 +1421,17 @@ struct Pipeline {
       std::snprintf(pf.name, sizeof(pf.name), "%s", outs[f].name.c_str());
       pf.kind = outs[f].kind;
       auto& off = w.offsets[f];
-      bool dense = true;
-      for (uint32_t k = 0; k < nb; ++k) {
-        const uint64_t L = w.h_len[f * w.n + s0 + k];
-        off[k + 1] = off[k] + L;
-        if (L != outs[f].stride) dense = false;
-      }
+      const uint64_t b0 = field_offset(w, f, s0);
       bool uniform = true;
-      for (uint32_t k = 1; k < nb; ++k)
+      for (uint32_t k = 0; k < nb; ++k) {
+        off[k + 1] = field_offset(w, f, s0 + k + 1) - b0;
         if (w.h_len[f * w.n + s0 + k] != w.h_len[f * w.n + s0]) uniform = false;
+      }
       pf.uniform = uniform ? 1 : 0;
       pf.nbytes = off[nb];
       pf.h_offsets = off.data();
-      uint8_t* slot0 = w.outs.as<uint8_t>() + w.out_base[f] + s0 * outs[f].stride;
-      if (host_batches) pf.h_ptr = w.h_out.as<uint8_t>() + w.h_base[f] + w.woff[f][s0];
-      if (dense) {
-        pf.d_ptr = slot0;
-      } else if (host_batches) {
-        pf.d_ptr = nullptr;  // ragged field: host copy only
-      } else {
-        // pack the batch's slots into CSR (one small kernel, synchronous)
-        const uint64_t meta = 2 * (nb + 1) * 8;
-        uint64_t* hm = w.h_compact_meta.as<uint64_t>() + 2 * (uint64_t)(B + 1) * f;
-        uint64_t* dm = w.compact_meta.as<uint64_t>() + 2 * (uint64_t)(B + 1) * f;
-        for (uint32_t k = 0; k < nb; ++k) {
-          hm[k] = off[k];
-          hm[nb + 1 + k] = off[k + 1] - off[k];
-        }
-        CK(cudaMemcpyAsync(dm, hm, meta, cudaMemcpyHostToDevice, serve_stream));
-        uint64_t base = 0;
-        for (size_t q = 0; q < f; ++q) base += align16(outs[q].stride * B) + 64;
-        uint8_t* dst = w.compact.as<uint8_t>() + base;
-        CK(launch_compact(slot0, outs[f].stride, dm, dm + nb + 1, nb, dst, serve_stream));
-        ++launches;
-        CK(cudaStreamSynchronize(serve_stream));
-        pf.d_ptr = dst;
-      }
+      pf.d_ptr = const_cast<uint8_t*>(field_base(w, f)) + b0;
+      if (host_batches) pf.h_ptr = w.h_out.as<uint8_t>() + w.h_base[f] + b0;
     }
     ++served;
     ++batches;
@@ -1423,6 +1448,13 @@ struct Pipeline {
            {"cloud_kernel_alg_bytes", alg_bytes},
            {"decode_kernel_ms", decode_kernel_ms},
            {"decode_kernel_alg_bytes", decode_alg_bytes},
+           {"crc_kernel_ms", crc_kernel_ms},
+           {"crc_kernel_alg_bytes", crc_alg_bytes},
+           {"csr_kernel_ms", csr_kernel_ms},
+           {"csr_kernel_alg_bytes", csr_alg_bytes},
+           {"serial", serial},
+           {"block_pages_lz4", block_pages_lz4},
+           {"block_pages_stored_raw", block_head.size() - block_pages_lz4},
            {"h2d_bytes", h2d_bytes},
            {"d2h_bytes", d2h_bytes},
            {"host_launch_ms", host_launch_ms},

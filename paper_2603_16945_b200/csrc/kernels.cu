@@ -2526,33 +2526,98 @@ cudaError_t launch_wave(const WaveArgs& a, int grid, int grid_pre, int threads, 
   return cudaGetLastError();
 }
 
-// Ragged batch → CSR: sample i's len[i] bytes from slot i to dst + off[i].
-// blockIdx.y = sample, blockIdx.x strides its bytes; 4-byte words when the
-// slot stride and the CSR offset allow (every float/int32 field does).
-__global__ void k_compact(const uint8_t* src, uint64_t stride, const uint64_t* off,
-                          const uint64_t* len, uint32_t n, uint8_t* dst) {
-  const uint32_t i = blockIdx.y;
-  if (i >= n) return;
-  const uint8_t* s = src + (uint64_t)i * stride;
-  uint8_t* d = dst + off[i];
-  const uint64_t L = len[i];
-  const uint64_t step = (uint64_t)gridDim.x * blockDim.x;
-  const uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if ((((uintptr_t)s | (uintptr_t)d) & 3u) == 0) {
-    const uint32_t* s4 = reinterpret_cast<const uint32_t*>(s);
-    uint32_t* d4 = reinterpret_cast<uint32_t*>(d);
-    for (uint64_t k = t0; k < L / 4; k += step) d4[k] = s4[k];
-    for (uint64_t k = (L & ~3ull) + t0; k < L; k += step) d[k] = s[k];
-  } else {
-    for (uint64_t k = t0; k < L; k += step) d[k] = s[k];
+// Per-wave CSR of the variable-length batch fields (Batch::stacked order,
+// pipeline.cpp:170-200).  k_wave_offsets: one CTA per batch field scans the
+// wave's out_len into sample byte offsets (varlen fields) and flags fields
+// whose samples all fill their slot exactly ("dense": the slots are then
+// already contiguous and stay in place).  k_compact_wave: every (varlen
+// field, sample) pair of a non-dense field copies its bytes from its slot to
+// compact + offset.  Two launches per wave replace a compaction launch and a
+// stream sync per batch per field.
+__global__ void __launch_bounds__(1024) k_wave_offsets(const uint64_t* __restrict__ out_len, WaveCsr c,
+                                                       uint32_t n) {
+  const uint32_t f = blockIdx.x;
+  __shared__ uint64_t warp_sum[32];
+  __shared__ uint64_t carry;
+  __shared__ int all_dense;
+  if (threadIdx.x == 0) {
+    carry = 0;
+    all_dense = 1;
+  }
+  __syncthreads();
+  const int vi = c.var_index[f];
+  uint64_t* woff = vi >= 0 ? c.woff + (uint64_t)vi * (n + 1) : nullptr;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  bool dense = true;
+  for (uint32_t base = 0; base < n; base += blockDim.x) {
+    const uint32_t s = base + threadIdx.x;
+    const uint64_t L = s < n ? out_len[(uint64_t)f * n + s] : 0;
+    if (s < n && L != c.stride[f]) dense = false;
+    if (!woff) continue;
+    uint64_t v = L;  // inclusive warp scan
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint64_t y = __shfl_up_sync(0xffffffffu, v, d);
+      if (lane >= (uint32_t)d) v += y;
+    }
+    if (lane == 31) warp_sum[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+      uint64_t w = lane < (blockDim.x >> 5) ? warp_sum[lane] : 0;
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xffffffffu, w, d);
+        if (lane >= (uint32_t)d) w += y;
+      }
+      warp_sum[lane] = w;  // inclusive over warps
+    }
+    __syncthreads();
+    const uint64_t excl = carry + (warp ? warp_sum[warp - 1] : 0) + v - L;
+    if (s < n) woff[s] = excl;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = excl + L;
+    __syncthreads();
+  }
+  if (!dense) atomicAnd(&all_dense, 0);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    c.dense[f] = (uint32_t)all_dense;
+    if (woff) woff[n] = carry;
   }
 }
 
-cudaError_t launch_compact(const uint8_t* src, uint64_t stride, const uint64_t* d_off,
-                           const uint64_t* d_len, uint32_t n, uint8_t* dst, cudaStream_t st) {
-  if (!n) return cudaSuccess;
-  const uint32_t bx = (uint32_t)std::min<uint64_t>(64, (stride / 4 + 255) / 256 + 1);
-  k_compact<<<dim3(bx, n), 256, 0, st>>>(src, stride, d_off, d_len, n, dst);
+__global__ void k_compact_wave(const uint64_t* __restrict__ out_len, WaveCsr c, uint32_t n) {
+  const uint64_t items = (uint64_t)c.n_var * n;
+  for (uint64_t it = blockIdx.x; it < items; it += gridDim.x) {
+    const uint32_t vi = (uint32_t)(it / n), s = (uint32_t)(it % n);
+    const int f = c.var_field[vi];
+    if (c.dense[f]) continue;  // uniform per CTA
+    const uint64_t L = out_len[(uint64_t)f * n + s];
+    const uint8_t* src = c.outs[f] + (uint64_t)s * c.stride[f];
+    uint8_t* dst = c.compact[f] + c.woff[(uint64_t)vi * (n + 1) + s];
+    if ((((uintptr_t)src | (uintptr_t)dst) & 15u) == 0) {
+      const uint4* s16 = reinterpret_cast<const uint4*>(src);
+      uint4* d16 = reinterpret_cast<uint4*>(dst);
+      for (uint64_t k = threadIdx.x; k < L / 16; k += blockDim.x) d16[k] = s16[k];
+      for (uint64_t k = (L & ~15ull) + threadIdx.x; k < L; k += blockDim.x) dst[k] = src[k];
+    } else if ((((uintptr_t)src | (uintptr_t)dst) & 3u) == 0) {
+      const uint32_t* s4 = reinterpret_cast<const uint32_t*>(src);
+      uint32_t* d4 = reinterpret_cast<uint32_t*>(dst);
+      for (uint64_t k = threadIdx.x; k < L / 4; k += blockDim.x) d4[k] = s4[k];
+      for (uint64_t k = (L & ~3ull) + threadIdx.x; k < L; k += blockDim.x) dst[k] = src[k];
+    } else {
+      for (uint64_t k = threadIdx.x; k < L; k += blockDim.x) dst[k] = src[k];
+    }
+  }
+}
+
+cudaError_t launch_wave_csr(const uint64_t* out_len, const WaveCsr& c, uint32_t n, int sms,
+                            cudaStream_t st) {
+  if (!n || !c.n_out) return cudaSuccess;
+  k_wave_offsets<<<c.n_out, 1024, 0, st>>>(out_len, c, n);
+  if (c.n_var) {
+    const uint64_t items = (uint64_t)c.n_var * n;
+    const uint32_t grid = (uint32_t)std::min<uint64_t>(items, (uint64_t)sms * 8);
+    k_compact_wave<<<grid, 256, 0, st>>>(out_len, c, n);
+  }
   return cudaGetLastError();
 }
 

@@ -41,8 +41,19 @@ cudaError_t occupancy_cloud_clusters(int* n, int threads, size_t smem, uint32_t 
 cudaError_t set_apply_smem(size_t bytes);
 // n bytes (rounded up to 16) from device memory into mapped pinned host memory.
 cudaError_t launch_store_host(const uint8_t* src, uint8_t* dst_mapped, uint64_t n, cudaStream_t st);
-cudaError_t launch_compact(const uint8_t* src, uint64_t stride, const uint64_t* d_off,
-                           const uint64_t* d_len, uint32_t n, uint8_t* dst, cudaStream_t st);
+// Per-wave CSR of variable-length batch fields (k_wave_offsets + k_compact_wave).
+struct WaveCsr {
+  uint32_t n_out, n_var;
+  uint64_t stride[16];
+  int32_t var_index[16];  // batch field -> varlen slot, or -1
+  int32_t var_field[16];  // varlen slot -> batch field
+  const uint8_t* outs[16];
+  uint8_t* compact[16];
+  uint64_t* woff;  // [n_var][n+1]
+  uint32_t* dense; // [n_out]
+};
+cudaError_t launch_wave_csr(const uint64_t* out_len, const WaveCsr& c, uint32_t n, int sms,
+                            cudaStream_t st);
 
 cudaError_t launch_apply_set(const WaveArgs& a, int grid, int threads, size_t smem,
                              cudaStream_t st);

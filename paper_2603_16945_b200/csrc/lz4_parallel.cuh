@@ -2,28 +2,29 @@
 // writes one block per page, lz4_block.cpp:33-110), output byte-identical to
 // lz4::decompress (lz4_block.cpp:113-156) with the same error verdicts.
 //
-// The token chain of an LZ4 block is serial; on the reference's pages it is
-// ~1 sequence per 20 B (avg literal 16 B, match 5 B).  We
-// parallelise it in four phases, all inside one CTA:
+// The token chain of an LZ4 block is serial; on the reference's quantised
+// pages it is ~1 sequence per 8 B (avg literal ~4 B, match ~4 B; SURVEY.md
+// App. A).  Speculative parsing from chunk starts was measured and rejected
+// (most chunks never re-synchronise).  The decoder instead:
 //
-//  1. speculative parse: the payload is cut into CH-byte chunks; thread k
-//     parses chunk k as if a token started at its first byte, marking every
-//     token position it visits in a per-chunk bitmap.  LZ4 token chains are
-//     self-synchronising: a chain started at a wrong byte soon lands on a
-//     true token position and from then on IS the true chain.
-//  2. stitch: thread k re-walks chunk k from the assumed entry (the previous
-//     chunk's speculative exit) until it hits a marked position (converged),
-//     verifying the exit; thread 0 then chains the true entries, re-walking
-//     only chunks whose assumption failed (rare).
-//  3. true parse per chunk from its verified entry: count, scan, then parse
-//     again copying literals and emitting match records (all reference
-//     bounds checks, in the reference's order, with the global output
-//     position now known).
-//  4. matches: resolved in stream order by one warp through a shared-memory
-//     ring of the output (match-to-match dependency chains are thousands
-//     deep on real pages, so this part is inherently sequential).
-//     Overlapping copies use dst[mo+i] = dst[mo-off + i % off], the closed
-//     form of the byte-wise copy.
+//  1-2. skim (k_page_decode): 2 KB windows of the payload are staged in
+//     shared memory by cp.async.bulk (TMA, one mbarrier per buffer) a window
+//     ahead.  Warps 1-7 fill window w+1's jump table d(p) = distance to the
+//     next token if one started at p (plus two- and four-token jumps) while
+//     one lane of the last warp walks window w with one round of two
+//     independent shared loads per one, two or four tokens, storing a u32
+//     step record per step; the fill warps expand the records into global
+//     token positions.  Windows inside long literals are skipped.
+//  3. all sequences in parallel: block scans give output positions; literals
+//     are copied in 16-B aligned output chunks; match records are emitted
+//     with every reference bounds check (all violations are kCorruptPage, so
+//     verdicts do not depend on order).
+//  4. matches (k_page_matches): resolved in stream order through a 16 KB
+//     shared-memory ring of the output.  Runs of matches whose output span
+//     fits 2 KB are resolved by pointer jumping (every byte points at its
+//     source, doubling until it reaches a final byte, then one gather); the
+//     rest go one match per lane in dependency waves.  Overlapping copies use
+//     dst[mo+i] = dst[mo-off + i % off], the closed form of the byte-wise copy.
 #pragma once
 
 #include <cstdint>
