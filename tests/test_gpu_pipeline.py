@@ -323,3 +323,29 @@ def test_lz4_adversarial_pages_through_pipeline(pcp, ref, tmp_path, seed):
     assert len(got) == len(samples)
     for i, s in enumerate(samples):
         assert got[i] == bytes(s["blob"]), i
+
+
+@pytest.mark.parametrize("resident", [True, False])
+def test_corrupt_payload_host_batches_serves_intact_batches(pcp, tmp_path, resident):
+    """host_batches: the batches of a wave before its failing batch are served
+    intact from pinned host memory (first wave of the slot, so no stale
+    buffers exist), then the failing batch raises WorkerPanic."""
+    from paper_2603_16945_b200 import synth
+    primary = _ds(pcp, tmp_path, "shapenet", 32, group=8, n_points=256)
+    g = synth.graph(["normalize"], batch_size=8)
+    want = [b.to_host() for b in pcp.Pipeline(primary, g)][:3]
+    with open(primary, "rb") as f:
+        blob = bytearray(f.read())
+    blob[-100] ^= 0x10  # inside the last group's block payload
+    with open(primary, "wb") as f:
+        f.write(blob)
+    p = pcp.Pipeline(primary, g, host_batches=True, resident=resident)
+    for k in range(3):
+        got = p.next_host_batch()
+        assert got is not None
+        for name in want[k]:
+            assert np.array_equal(got[name][0].view(np.uint8), want[k][name][0].view(np.uint8)), (k, name)
+    with pytest.raises(pcp.PcError) as ei:
+        p.next_host_batch()
+    assert ei.value.errc == "WorkerPanic" and "ChecksumMismatch" in str(ei.value)
+    p.close()
