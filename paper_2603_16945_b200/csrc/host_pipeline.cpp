@@ -1158,7 +1158,7 @@ struct Pipeline {
     }
     CK(cudaMemcpyAsync(dt, ht, up_bytes, cudaMemcpyHostToDevice, w.stream));
     CK(cudaEventRecord(w.h1, w.stream));
-    CK(cudaMemsetAsync(dt + o_acc, 0, o_len - o_acc, w.stream));
+    CK(cudaMemsetAsync(dt + o_acc, 0, o_woff - o_acc, w.stream));  // incl. out_len: failed samples write none
     // ---- args ----------------------------------------------------------------
     a.bytes = bytes;
     a.raw = w.raw.as<uint8_t>();
