@@ -31,6 +31,7 @@
 #include "host_format.h"
 #include "json.hpp"
 #include "kernels.h"
+#include "voxel_wave.h"
 
 namespace pcp {
 
@@ -447,13 +448,17 @@ struct Wave {
   cudaEvent_t done = nullptr, k0 = nullptr, k1 = nullptr, d0 = nullptr, d1 = nullptr;
   cudaEvent_t c0 = nullptr, c1 = nullptr, s0 = nullptr, s1 = nullptr;  // CRC windows, wave CSR
   uint64_t crc_alg_bytes = 0;     // payload bytes k_crc_windows reads
+  uint64_t vx_alg_bytes = 0;      // decoded tracked-field bytes the vx stage reads
   cudaEvent_t h0 = nullptr, h1 = nullptr;  // staging copies (timeline diagnostics)
   cudaEvent_t served = nullptr;  // serve stream passed this wave's last batch (user copies enqueued)
   uint64_t decode_alg_bytes = 0;  // payload + raw bytes of the pages k_page_decode handles
   DevBuf gscratch;                // k_cloud global slab (smem_mode 0), per slot
   // device
   DevBuf bytes_stage, raw, tables, outs, compact, lz4_scratch, lz4_timing;
-  DevBuf handoff;  // chain split: the clouds between the prefix and the cluster launch
+  DevBuf handoff;  // chain split: the clouds between launches (decoded clouds A for the vx stage)
+  DevBuf handoff_b;  // vx stage output (voxelized clouds B)
+  DevBuf vx_cl, vx_tiles, vx_cnt, vx_w0, vx_w1;  // vx stage scratch
+  cudaEvent_t v0 = nullptr, v1 = nullptr;        // vx stage
   DevBuf mt_pre;   // pre-seeded MT19937-64 states [n][n_rng][312] (k_seed_states)
   uint32_t n_todo = 0;
   HostBuf h_tables, h_res;
@@ -532,6 +537,13 @@ struct Pipeline {
   double kernel_ms = 0, cloud_kernel_ms = 0, decode_kernel_ms = 0, crc_kernel_ms = 0, csr_kernel_ms = 0;
   uint64_t crc_alg_bytes = 0, csr_alg_bytes = 0;
   bool serial = false;  // option "serial": one wave in flight (non-overlapped kernel timing)
+  // multi-CTA voxel stage (voxel_wave.cu) for large clouds whose chain starts
+  // with [range_crop,] voxel; option "vx": false keeps it in k_cloud
+  bool vx_allowed = true, vx_on = false;
+  uint64_t vx_min_points = 32768;
+  VxArgs vx_proto{};
+  double vx_kernel_ms = 0;
+  uint64_t vx_alg_bytes = 0;
   double host_launch_ms = 0, host_wait_ms = 0;  // host-side wall time (diagnostics)
   bool timeline_on = false;
   cudaEvent_t t_open = nullptr;
@@ -550,7 +562,7 @@ struct Pipeline {
       if (w.d0) cudaEventDestroy(w.d0);
       if (w.d1) cudaEventDestroy(w.d1);
       if (w.h0) cudaEventDestroy(w.h0);
-      for (cudaEvent_t e : {w.c0, w.c1, w.s0, w.s1})
+      for (cudaEvent_t e : {w.c0, w.c1, w.s0, w.s1, w.v0, w.v1})
         if (e) cudaEventDestroy(e);
       if (w.h1) cudaEventDestroy(w.h1);
       if (w.served) cudaEventDestroy(w.served);
@@ -579,6 +591,8 @@ struct Pipeline {
       }
       force_serial_fy = o.value("force_serial_fy", false);
       serial = o.value("serial", false);
+      vx_allowed = o.value("vx", true);
+      vx_min_points = o.value("vx_min_points", vx_min_points);
     }
     h = read_header(primary);
     dir = fs::path(primary).parent_path().string();
@@ -598,6 +612,12 @@ struct Pipeline {
     plan_schema();
     if (const char* e = std::getenv("PCP_WAVE_BATCHES")) wave_batches = (uint32_t)std::atoi(e);  // sweep switch
     plan_waves();
+    if (vx_on) {  // k_cloud launches around the vx stage: one CTA per cloud of a wave at most
+      uint64_t mx = 1;
+      for (uint64_t n : plan_n) mx = std::max(mx, n);
+      if (proto.fps_cluster <= 1) grid = (int)std::min<uint64_t>(grid, mx);
+      grid_pre = (int)std::min<uint64_t>(std::max(grid_pre, 1), mx);
+    }
     upload_x2n(stream);
     std::vector<uint32_t> shift(kShiftEntries);
     build_shift_table(shift.data());
@@ -627,7 +647,7 @@ struct Pipeline {
       CK(cudaEventCreate(&w.d0));
       CK(cudaEventCreate(&w.d1));
       CK(cudaEventCreate(&w.h0));
-      for (cudaEvent_t* e : {&w.c0, &w.c1, &w.s0, &w.s1}) CK(cudaEventCreate(e));
+      for (cudaEvent_t* e : {&w.c0, &w.c1, &w.s0, &w.s1, &w.v0, &w.v1}) CK(cudaEventCreate(e));
       CK(cudaEventCreate(&w.h1));
       CK(cudaEventCreateWithFlags(&w.served, cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&w.host_ready, cudaEventDisableTiming));
@@ -864,20 +884,22 @@ struct Pipeline {
     a.op_begin = 0;
     a.op_end = a.n_ops;
     a.split_at = 0;
+    a.vx_first = a.vx_last = -1;
     if (a.fps_cluster > 1) {  // run the ops before the first FPS one CTA per cloud
       int f = 0;
       while (f < a.n_ops && a.ops[f].kind != kFps) ++f;
-      if (f > 0 && f < a.n_ops) {
-        a.split_at = f;
-        uint64_t at = 128;  // header: status, present, n[8], elem[8], has_counts, n_counts
-        for (int k = 0; k < kMaxBytesFields; ++k) {
-          a.handoff_off[k] = at;
-          if ((a.tracked_mask >> k) & 1u) at = align16(at + (uint64_t)a.cap_points * a.field_cap[k]);
-        }
-        a.handoff_off[kMaxBytesFields] = at;
-        if (a.voxel_scratch) at = align16(at + 4ull * a.cap_points);
-        a.handoff_stride = at;
+      if (f > 0 && f < a.n_ops) a.split_at = f;
+    }
+    plan_vx(a);
+    if (a.split_at || vx_on) {  // hand-off slot layout (fields sized like the per-CTA buffers)
+      uint64_t at = 128;  // header: status, present, n[8], elem[8], has_counts, n_counts
+      for (int k = 0; k < kMaxBytesFields; ++k) {
+        a.handoff_off[k] = at;
+        if ((a.tracked_mask >> k) & 1u) at = align16(at + (uint64_t)a.cap_points * a.field_cap[k] + 16);
       }
+      a.handoff_off[kMaxBytesFields] = at;
+      if (a.voxel_scratch) at = align16(at + 4ull * a.cap_points + 16);
+      a.handoff_stride = at;
     }
     if (op_timing) {
       d_op_cycles.ensure((kMaxOps + 2) * 8);
@@ -909,6 +931,48 @@ struct Pipeline {
     a.force_serial_fy = force_serial_fy ? 1 : 0;
   }
 
+  // The multi-CTA voxel stage takes the chain's leading [range_crop,] voxel
+  // when clouds are large and the ops move exactly the tracked fields (so the
+  // voxelized hand-off holds the whole cloud).
+  void plan_vx(WaveArgs& a) {
+    vx_on = false;
+    if (!vx_allowed || a.n_ops == 0 || a.role_data < 0 || a.cap_points < vx_min_points) return;
+    int first = 0, last = -1;
+    if (a.ops[0].kind == kVoxel) last = 0;
+    else if (a.ops[0].kind == kRangeCrop && a.n_ops > 1 && a.ops[1].kind == kVoxel) last = 1;
+    if (last < 0) return;
+    if (a.split_at && a.split_at <= last) return;
+    const OpDesc& vo = a.ops[last];
+    uint32_t mm = vo.gather_mask;
+    for (int r : {a.role_data, a.role_normal, a.role_color, a.role_intensity})
+      if (r >= 0) mm |= 1u << r;
+    if (mm != a.tracked_mask) return;
+    if (last == 1 && a.ops[0].gather_mask != vo.gather_mask) return;
+    vx_on = true;
+    a.vx_first = first;
+    a.vx_last = last;
+    VxArgs& v = vx_proto;
+    std::memset(&v, 0, sizeof(v));
+    v.n_bytes_fields = a.n_bytes_fields;
+    v.role_data = a.role_data;
+    v.role_normal = a.role_normal;
+    v.role_color = a.role_color;
+    v.role_intensity = a.role_intensity;
+    v.mm = mm;
+    v.has_crop = last == 1;
+    for (int k = 0; k < 3; ++k) {
+      v.lo[k] = a.ops[0].lo[k];
+      v.hi[k] = a.ops[0].hi[k];
+      v.origin[k] = vo.origin[k];
+    }
+    v.voxel = vo.voxel;
+    v.has_origin = vo.has_origin;
+    v.counts = vo.counts;
+    v.vx_first = first;
+    v.vx_last = last;
+    v.max_passes = kVxMaxPasses;
+  }
+
 
   void plan_waves() {
     const uint64_t n = walk.size();
@@ -920,7 +984,10 @@ struct Pipeline {
       // whose serial LZ4 chain runs concurrently
       uint64_t gmax = 1;
       for (const auto& gr : h.groups) gmax = std::max<uint64_t>(gmax, gr.sample_count);
-      const uint64_t want = std::max<uint64_t>(8192, 2ull * sms * gmax);
+      uint64_t want = std::max<uint64_t>(8192, 2ull * sms * gmax);
+      // multi-CTA voxel chains: ~64 M input points per wave, so the per-wave
+      // hand-off slots and sort words of several waves in flight stay modest
+      if (vx_on) want = std::max<uint64_t>(B, (64ull << 20) / std::max<uint64_t>(1, proto.cap_points));
       wb = (uint32_t)std::max<uint64_t>(1, (want + B - 1) / B);
     }
     const uint64_t W = (uint64_t)wb * B;
@@ -1131,7 +1198,18 @@ struct Pipeline {
     // host_batches: size the pinned wave buffer up front (exact for fixed-size
     // fields; ragged ones grow it on demand past 1 GiB)
     if (host_batches) w.h_out.ensure(std::min<uint64_t>(out_total + 64, 1ull << 30));
-    if (proto.split_at) w.handoff.ensure(proto.handoff_stride * w.n);
+    if (proto.split_at || vx_on) w.handoff.ensure(proto.handoff_stride * w.n);
+    uint64_t vx_tiles_bound = 0;
+    if (vx_on) {
+      const uint64_t T = voxel_wave_tile_points();
+      vx_tiles_bound = w.n * ((proto.cap_points + T - 1) / T);
+      w.handoff_b.ensure(proto.handoff_stride * w.n);
+      w.vx_cl.ensure(sizeof(VxCloud) * w.n);
+      w.vx_tiles.ensure(16 + 3 * 4 * vx_tiles_bound);
+      w.vx_cnt.ensure(1024 * vx_tiles_bound);
+      w.vx_w0.ensure(8ull * proto.cap_points * w.n);
+      w.vx_w1.ensure(8ull * proto.cap_points * w.n);
+    }
     if (proto.n_rng) w.mt_pre.ensure(w.n * proto.n_rng * 312 * 8);
     w.h_res.ensure(total - o_sst + 16);
     if (dry) return;
@@ -1178,7 +1256,29 @@ struct Pipeline {
     a.out_len = reinterpret_cast<uint64_t*>(dt + o_len);
     a.shift_tab = d_shift.as<uint32_t>();
     a.gscratch = proto.gscratch_per_cta ? w.gscratch.as<uint8_t>() : nullptr;
-    a.handoff = proto.split_at ? w.handoff.as<uint8_t>() : nullptr;
+    a.handoff_in = a.handoff_out = a.handoff_fallback = nullptr;
+    a.vx_state = nullptr;
+    VxArgs vx = vx_proto;
+    if (vx_on) {
+      vx.n_samples = (uint32_t)w.n;
+      vx.A = w.handoff.as<uint8_t>();
+      vx.B = w.handoff_b.as<uint8_t>();
+      vx.stride = proto.handoff_stride;
+      for (int k = 0; k <= kMaxBytesFields; ++k) vx.off[k] = proto.handoff_off[k];
+      vx.cl = w.vx_cl.as<VxCloud>();
+      vx.total_tiles = w.vx_tiles.as<uint32_t>();
+      vx.tile_cloud = vx.total_tiles + 4;
+      vx.tile_kept = vx.tile_cloud + vx_tiles_bound;
+      vx.tile_kofs = vx.tile_kept + vx_tiles_bound;
+      vx.cnt = w.vx_cnt.as<uint32_t>();
+      vx.w0 = w.vx_w0.as<uint64_t>();
+      vx.w1 = w.vx_w1.as<uint64_t>();
+      vx.sample_status = a.sample_status;
+      vx.sample_op = a.sample_op;
+      vx.sample_where = a.sample_where;
+      a.vx_state = vx.cl;
+      a.handoff_fallback = vx.A;
+    }
     a.mt_pre = proto.n_rng ? w.mt_pre.as<uint64_t>() : nullptr;
     for (size_t f = 0; f < outs.size(); ++f) {
       a.out[f] = w.outs.as<uint8_t>() + w.out_base[f];
@@ -1205,8 +1305,16 @@ struct Pipeline {
     w.n_todo = (uint32_t)todo.size();
     w.decode_alg_bytes = 0;
     for (uint32_t pi : todo) w.decode_alg_bytes += pages[pi].pay_len + pages[pi].raw_len;
-    CK(launch_wave(a, grid, grid_pre, threads, smem, w.stream, w.k0, w.k1));
-    launches += (wins.empty() ? 0 : 1) + (todo.empty() ? 0 : 2) + (ng ? 1 : 0) + (proto.n_rng ? 1 : 0) + 1 + 1 + 1;
+    CK(launch_wave(a, grid, grid_pre, threads, smem, w.stream, w.k0, w.k1, vx_on ? &vx : nullptr,
+                   (uint32_t)vx_tiles_bound, sms, w.v0, w.v1, w.handoff.as<uint8_t>()));
+    launches += (wins.empty() ? 0 : 1) + (todo.empty() ? 0 : 2) + (ng ? 1 : 0) + (proto.n_rng ? 1 : 0) + 1 + 1 + 1 +
+                (vx_on ? 2 + 7 + 3 * kVxMaxPasses : 0) + (proto.split_at ? 1 : 0);
+    if (vx_on) {
+      uint64_t per_pt = 0;
+      for (int f = 0; f < proto.n_bytes_fields; ++f)
+        if ((proto.tracked_mask >> f) & 1u) per_pt += proto.field_cap[f];
+      w.vx_alg_bytes = w.in_points * per_pt;
+    }
     // ---- per-wave CSR of the variable-length fields (device side) ------------
     {
       WaveCsr c{};
@@ -1347,6 +1455,12 @@ struct Pipeline {
       float ms = 0;
       CK(cudaEventElapsedTime(&ms, wn.k0, wn.k1));
       cloud_kernel_ms += ms;
+      if (vx_on) {  // the vx stage runs between the k_cloud launches
+        CK(cudaEventElapsedTime(&ms, wn.v0, wn.v1));
+        cloud_kernel_ms -= ms;
+        vx_kernel_ms += ms;
+        vx_alg_bytes += wn.vx_alg_bytes;
+      }
       CK(cudaEventElapsedTime(&ms, wn.d0, wn.d1));
       decode_kernel_ms += ms;
       CK(cudaEventElapsedTime(&ms, wn.c0, wn.c1));
@@ -1451,6 +1565,8 @@ struct Pipeline {
            {"crc_kernel_ms", crc_kernel_ms},
            {"crc_kernel_alg_bytes", crc_alg_bytes},
            {"csr_kernel_ms", csr_kernel_ms},
+           {"vx", vx_on},
+           {"kernels", json{{"k_vx_*(voxel stage)", json{{"ms", vx_kernel_ms}, {"alg_bytes", vx_alg_bytes}}}}},
            {"csr_kernel_alg_bytes", csr_alg_bytes},
            {"serial", serial},
            {"block_pages_lz4", block_pages_lz4},

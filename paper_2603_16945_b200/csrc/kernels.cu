@@ -26,6 +26,7 @@
 #include "device_util.cuh"
 #include "lz4_parallel.cuh"
 #include "kernels.h"
+#include "voxel_wave.h"
 #include "pcp_internal.h"
 
 namespace pcp {
@@ -1913,10 +1914,11 @@ __device__ __forceinline__ void copy16(uint8_t* dst, const uint8_t* src, uint64_
 // [header: status, present, n[8], elem[8], has_counts, n_counts | fields | counts].
 __device__ __forceinline__ void handoff_store(const WaveArgs& a, const Cloud& c, uint8_t* hb) {
   for (int f = 0; f < a.n_bytes_fields; ++f)
-    if (((a.tracked_mask >> f) & 1u) && ((c.present >> f) & 1u))
+    if (((a.tracked_mask >> f) & 1u) && ((c.present >> f) & 1u) && c.cur[f] != hb + a.handoff_off[f])
       copy16(hb + a.handoff_off[f], c.cur[f], (uint64_t)c.n[f] * c.elem[f]);
-  if (c.has_counts) copy16(hb + a.handoff_off[kMaxBytesFields], reinterpret_cast<const uint8_t*>(c.counts),
-                           (uint64_t)c.n_counts * 4);
+  if (c.has_counts && reinterpret_cast<uint8_t*>(c.counts) != hb + a.handoff_off[kMaxBytesFields])
+    copy16(hb + a.handoff_off[kMaxBytesFields], reinterpret_cast<const uint8_t*>(c.counts),
+           (uint64_t)c.n_counts * 4);
   if (threadIdx.x == 0) {
     uint32_t* h = reinterpret_cast<uint32_t*>(hb);
     h[1] = c.present;
@@ -1929,7 +1931,9 @@ __device__ __forceinline__ void handoff_store(const WaveArgs& a, const Cloud& c,
   }
 }
 
-__device__ __forceinline__ void handoff_load(const WaveArgs& a, Cloud& c, Smem& S, const uint8_t* hb) {
+// in_place: the cloud's current buffers ARE the hand-off slot (one CTA per
+// cloud owns it; ops write alt buffers / in place as usual), no copy.
+__device__ __forceinline__ void handoff_load(const WaveArgs& a, Cloud& c, Smem& S, uint8_t* hb, bool in_place) {
   const uint32_t* h = reinterpret_cast<const uint32_t*>(hb);
   if (threadIdx.x == 0) {
     S.cl = S.proto;
@@ -1937,11 +1941,14 @@ __device__ __forceinline__ void handoff_load(const WaveArgs& a, Cloud& c, Smem& 
     for (int f = 0; f < kMaxBytesFields; ++f) {
       S.cl.n[f] = h[2 + f];
       S.cl.elem[f] = h[10 + f];
+      if (in_place && ((a.tracked_mask >> f) & 1u)) S.cl.cur[f] = hb + a.handoff_off[f];
     }
     S.cl.has_counts = (int32_t)h[18];
     S.cl.n_counts = h[19];
+    if (in_place && a.voxel_scratch) S.cl.counts = reinterpret_cast<int32_t*>(hb + a.handoff_off[kMaxBytesFields]);
   }
   __syncthreads();
+  if (in_place) return;
   for (int f = 0; f < a.n_bytes_fields; ++f)
     if (((a.tracked_mask >> f) & 1u) && ((c.present >> f) & 1u))
       copy16(c.cur[f], hb + a.handoff_off[f], (uint64_t)c.n[f] * c.elem[f]);
@@ -1977,20 +1984,30 @@ __global__ void __launch_bounds__(512, MinBlocks) k_cloud(WaveArgs a) {
   uint32_t phase = 0;
   for (uint32_t s = blockIdx.x / CL; s < a.n_samples; s += gridDim.x / CL) {
     const SampleWork sw = a.samples[s];
-    if (a.handoff_mode == 2) {
-      // chain split, second launch: the cloud after the prefix ops; a failed
-      // prefix already wrote the (final) status
-      const uint8_t* hb = a.handoff + (uint64_t)s * a.handoff_stride;
+    if (a.handoff_in) {
+      // chain split, a later launch: the cloud after the earlier ops; a failed
+      // earlier stage already wrote the (final) status.  Multi-CTA voxel
+      // clouds whose keys did not fit the packed sort (vx fallback) take
+      // their decoded input and run the voxel ops here instead.
+      uint8_t* hb = a.handoff_in + (uint64_t)s * a.handoff_stride;
+      int op0 = a.op_begin;
+      if (a.vx_state && a.vx_state[s].fallback) {
+        hb = a.handoff_fallback + (uint64_t)s * a.handoff_stride;
+        op0 = a.vx_first;
+      }
       if (reinterpret_cast<const uint32_t*>(hb)[0] != (uint32_t)kOk) continue;  // uniform
-      handoff_load(a, c, S, hb);
+      handoff_load(a, c, S, hb, CL == 1);
       int32_t fail_op = 0;
-      int32_t status = run_chain<MinBlocks>(a, c, S, s, sw.epoch, sw.index, nullptr, fail_op, a.op_begin, a.op_end);
-      if (status == kOk && leader) write_tracked(a, c, s, status);
-      if (threadIdx.x == 0 && leader) {
+      int32_t status = run_chain<MinBlocks>(a, c, S, s, sw.epoch, sw.index, nullptr, fail_op, op0, a.op_end);
+      uint8_t* ho = a.handoff_out ? a.handoff_out + (uint64_t)s * a.handoff_stride : nullptr;
+      if (ho && status == kOk) handoff_store(a, c, ho);
+      if (status == kOk && leader && !ho) write_tracked(a, c, s, status);
+      if (threadIdx.x == 0 && leader && (!ho || status != kOk)) {
         a.sample_status[s] = status;
         a.sample_op[s] = status == kOk ? -1 : fail_op;
         a.sample_where[s] = 0;
       }
+      if (ho && threadIdx.x == 0) reinterpret_cast<uint32_t*>(ho)[0] = (uint32_t)status;
       __syncthreads();
       continue;
     }
@@ -2002,6 +2019,7 @@ __global__ void __launch_bounds__(512, MinBlocks) k_cloud(WaveArgs a) {
     const bool range_ok = sw.blob_end <= pg.raw_len && sw.blob_start <= sw.blob_end;
     uint64_t* flen = S.flen;
     uint64_t* foff = S.foff;
+    uint8_t* hb = a.handoff_out ? a.handoff_out + (uint64_t)s * a.handoff_stride : nullptr;
     if (threadIdx.x == 0) {
       int32_t st0 = rec.status;
       if (st0 == kOk && !range_ok) st0 = kRangeOutOfBounds;
@@ -2018,6 +2036,9 @@ __global__ void __launch_bounds__(512, MinBlocks) k_cloud(WaveArgs a) {
       S.pre_status = st0;
       S.cl = S.proto;
       S.cl.present = 0;
+      if (hb && a.op_begin == a.op_end)  // decode-only launch: straight into the hand-off slot
+        for (int f = 0; f < kMaxBytesFields; ++f)
+          if ((a.tracked_mask >> f) & 1u) S.cl.cur[f] = hb + a.handoff_off[f];
     }
     __syncthreads();
     int32_t status = S.pre_status;
@@ -2110,13 +2131,12 @@ __global__ void __launch_bounds__(512, MinBlocks) k_cloud(WaveArgs a) {
         status = run_chain<MinBlocks>(a, c, S, s, sw.epoch, sw.index, nullptr, fail_op, a.op_begin, a.op_end);
     }
 
-    // ---- chain split, first launch: hand the cloud to the cluster launch ---
-    uint8_t* hb = a.handoff_mode == 1 ? a.handoff + (uint64_t)s * a.handoff_stride : nullptr;
+    // ---- chain split, first launch: hand the cloud to the next launch -----
     if (hb && status == kOk) handoff_store(a, c, hb);
     // ---- write tracked fields + scalar values into the batch slot --------
     const long long tc2 = (a.op_cycles && threadIdx.x == 0) ? clock64() : 0;
     if (status == kOk && leader) {
-      if (a.handoff_mode != 1) write_tracked(a, c, s, status);
+      if (!hb) write_tracked(a, c, s, status);
       uint32_t vo = rec.vals_off;
       for (int f = 0; f < a.n_fields && status == kOk; ++f) {
         const FieldDesc fdsc = a.fields[f];
@@ -2490,34 +2510,77 @@ __global__ void __launch_bounds__(64) k_seed_states(WaveArgs a) {
 }
 
 cudaError_t launch_wave(const WaveArgs& a, int grid, int grid_pre, int threads, size_t smem,
-                        cudaStream_t st, cudaEvent_t k0, cudaEvent_t k1) {
+                        cudaStream_t st, cudaEvent_t k0, cudaEvent_t k1, const VxArgs* vx,
+                        uint32_t vx_tiles, int sms, cudaEvent_t v0, cudaEvent_t v1, uint8_t* handoff_a) {
   if (a.n_groups) k_scalar_parse<<<(a.n_groups + 127) / 128, 128, 0, st>>>(a);
   if (a.mt_pre && a.n_samples && a.n_rng) {
     const uint64_t n = (uint64_t)a.n_samples * a.n_rng;
     k_seed_states<<<(uint32_t)((n + 63) / 64), 64, 0, st>>>(a);
   }
   if (k0) cudaEventRecord(k0, st);
+  auto one_cta_per_cloud = [&](const WaveArgs& x, int g) {
+    if (x.min_blocks == 2) k_cloud<2><<<g, threads, smem, st>>>(x);
+    else k_cloud<1><<<g, threads, smem, st>>>(x);
+  };
   if (a.n_samples) {
-    if (a.fps_cluster > 1 && a.split_at > 0) {
+    if (vx) {
+      // decode-only launch into the hand-off slots A, the multi-CTA voxel
+      // stage A -> B, then the rest of the chain from B (and, with a cluster
+      // FPS split, from A again after the ops before the FPS)
+      const int g1 = a.fps_cluster > 1 ? grid_pre : grid;
+      WaveArgs l1 = a;
+      l1.fps_cluster = 1;
+      l1.op_begin = 0;
+      l1.op_end = a.vx_first;
+      l1.handoff_in = nullptr;
+      l1.handoff_out = handoff_a;
+      l1.vx_state = nullptr;
+      one_cta_per_cloud(l1, g1);
+      if (v0) cudaEventRecord(v0, st);
+      cudaError_t e = launch_voxel_wave(*vx, vx_tiles, sms, st);
+      if (e != cudaSuccess) return e;
+      if (v1) cudaEventRecord(v1, st);
+      const int stop = a.split_at ? a.split_at : a.n_ops;
+      const bool l2_runs = !a.split_at || a.vx_last + 1 < stop;
+      if (l2_runs) {
+        WaveArgs l2 = a;
+        l2.fps_cluster = 1;
+        l2.op_begin = a.vx_last + 1;
+        l2.op_end = stop;
+        l2.handoff_in = vx->B;
+        l2.handoff_out = a.split_at ? handoff_a : nullptr;
+        one_cta_per_cloud(l2, g1);
+      }
+      if (a.split_at) {
+        WaveArgs l3 = a;
+        l3.op_begin = a.split_at;
+        l3.op_end = a.n_ops;
+        l3.handoff_in = l2_runs ? handoff_a : vx->B;
+        l3.handoff_out = nullptr;
+        if (l2_runs) l3.vx_state = nullptr;
+        e = launch_clustered(k_cloud<1>, l3, grid, threads, smem, st);
+        if (e != cudaSuccess) return e;
+      }
+    } else if (a.fps_cluster > 1 && a.split_at > 0) {
       // chain split: ops [0, split_at) one CTA per cloud, then the cluster
       WaveArgs pre = a, post = a;
       pre.fps_cluster = 1;
       pre.op_begin = 0;
       pre.op_end = a.split_at;
-      pre.handoff_mode = 1;
+      pre.handoff_in = nullptr;
+      pre.handoff_out = handoff_a;
       post.op_begin = a.split_at;
       post.op_end = a.n_ops;
-      post.handoff_mode = 2;
+      post.handoff_in = handoff_a;
+      post.handoff_out = nullptr;
       k_cloud<1><<<grid_pre, threads, smem, st>>>(pre);
       const cudaError_t e = launch_clustered(k_cloud<1>, post, grid, threads, smem, st);
       if (e != cudaSuccess) return e;
     } else if (a.fps_cluster > 1) {
       const cudaError_t e = launch_clustered(k_cloud<1>, a, grid, threads, smem, st);
       if (e != cudaSuccess) return e;
-    } else if (a.min_blocks == 2) {
-      k_cloud<2><<<grid, threads, smem, st>>>(a);
     } else {
-      k_cloud<1><<<grid, threads, smem, st>>>(a);
+      one_cta_per_cloud(a, grid);
     }
   }
   if (k1) cudaEventRecord(k1, st);

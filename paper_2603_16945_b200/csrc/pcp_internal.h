@@ -132,6 +132,28 @@ struct FieldDesc {
   int32_t out_index;    // output slot (std::map name order)
 };
 
+// Per-cloud state of the multi-CTA voxel stage (voxel_wave.cu).
+struct VxCloud {
+  uint32_t n;          // input points (data)
+  uint32_t n_tiles;    // tiles of the input / of the sorted words
+  uint32_t tile0;      // first global tile of this cloud
+  uint32_t kept;       // points surviving the range crop (all when none)
+  uint64_t word0;      // first sort word of this cloud
+  int32_t status;      // Errc+1 of the vx ops (0 OK)
+  int32_t fail_op;     // 1-based failing op
+  uint32_t fallback;   // 1: keys too wide for the packed sort -> k_cloud runs the ops
+  uint32_t active;     // 1: the vx kernels process this cloud
+  uint32_t mn[3], mx[3];  // ordered-float min / max per axis over kept points
+  uint32_t nan;        // a kept point has a NaN coordinate
+  float o[3];          // voxel origin
+  uint32_t q0[3];      // smallest key per axis (subtracted: order-preserving)
+  uint32_t bx[3];      // key bits per axis
+  uint32_t kb, ib;     // key bits, point-index bits (word = key << ib | index)
+  uint32_t passes;     // 8-bit radix passes
+  uint32_t V;          // voxels
+  uint32_t hist[8][256];  // digit histogram per pass (whole cloud)
+};
+
 // Everything a wave launch needs (passed by value to the kernels).
 struct WaveArgs {
   const uint8_t* bytes;     // device byte store (slice data areas)
@@ -199,10 +221,21 @@ struct WaveArgs {
   // through a per-sample buffer; split_at = 0: no split
   int32_t split_at;
   int32_t op_begin, op_end;       // this launch's op range
-  int32_t handoff_mode;           // 0 none, 1 write the cloud after op_end, 2 read it before op_begin
-  uint8_t* handoff;               // [n_samples][handoff_stride]
+  // hand-off slots [n_samples][handoff_stride]: handoff_in = read the cloud
+  // before op_begin (instead of decoding its page), handoff_out = write it
+  // after op_end (instead of the batch slots); null = not used
+  uint8_t* handoff_in;
+  uint8_t* handoff_out;
   uint64_t handoff_stride;
   uint64_t handoff_off[kMaxBytesFields + 1];  // per tracked field, [kMaxBytesFields] = counts
+  // multi-CTA voxel stage (voxel_wave.cu) for large clouds: ops
+  // [vx_first, vx_last] ([range_crop,] voxel) run across the GPU between the
+  // decode-only launch and the rest of the chain; vx_first = -1: none.
+  // Clouds flagged `fallback` (keys too wide for the packed sort) run those
+  // ops in k_cloud from their decoded slot (handoff_fallback).
+  int32_t vx_first, vx_last;
+  const VxCloud* vx_state;  // [n_samples]
+  uint8_t* handoff_fallback;
   // cloud-set mode (pcp_apply_map): clouds come from CSR arrays instead of
   // pages; bytes-field slots 0..7 = data, normal, color, intensity, extra0..3
   int32_t set_mode;

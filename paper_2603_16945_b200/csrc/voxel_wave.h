@@ -1,0 +1,55 @@
+// voxel_wave.h — multi-CTA voxel / grid subsample stage (voxel_wave.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "pcp_internal.h"
+
+namespace pcp {
+
+constexpr uint32_t kVxMaxPasses = 6;  // 8-bit digits: keys up to 48 bits (wider: k_cloud fallback)
+
+// Arguments of the stage (by value).  A = decoded clouds (hand-off slots of
+// the decode-only k_cloud launch), B = voxelized clouds (hand-off slots the
+// rest of the chain reads); both [n_samples][stride] with the k_cloud
+// hand-off header and field offsets `off`.
+struct VxArgs {
+  uint32_t n_samples;
+  uint8_t* A;
+  uint8_t* B;
+  uint64_t stride;
+  uint64_t off[kMaxBytesFields + 1];
+  int32_t n_bytes_fields;
+  int32_t role_data, role_normal, role_color, role_intensity;
+  uint32_t mm;          // fields the ops move (roles + gathered extras)
+  int32_t has_crop;     // leading range_crop (vx_first) before the voxel op (vx_last)
+  float lo[3], hi[3];
+  float voxel;
+  int32_t has_origin;
+  float origin[3];
+  int32_t counts;       // emit per-voxel counts
+  int32_t vx_first, vx_last;
+  uint32_t max_passes;  // radix passes launched (kernels skip passes a cloud does not need)
+  // scratch
+  VxCloud* cl;          // [n_samples]
+  uint32_t* total_tiles;
+  uint32_t* tile_cloud;  // [tiles]
+  uint32_t* tile_kept;   // [tiles] kept points, later voxel starts
+  uint32_t* tile_kofs;   // [tiles] compaction offsets, later voxel offsets
+  uint32_t* cnt;         // [tiles][256]
+  uint64_t* w0;          // [points] sort words (ping)
+  uint64_t* w1;          // (pong)
+  // statuses of failing clouds (the rest report from the last k_cloud launch)
+  int32_t* sample_status;
+  int32_t* sample_op;
+  int32_t* sample_where;
+};
+
+// tiles_bound: an upper bound of the wave's tiles (sum over samples of
+// ceil(points / voxel_wave_tile_points())).
+cudaError_t launch_voxel_wave(const VxArgs& v, uint32_t tiles_bound, int sms, cudaStream_t st);
+uint32_t voxel_wave_tile_points();
+
+}  // namespace pcp
