@@ -1106,7 +1106,9 @@ struct Pipeline {
       }
       // fused CRC only when this wave's samples tile the stored-raw payload
       // exactly once
-      bool fused = !(bh.flags & kFlagOuterLz4) && bh.pay_len == bh.raw_len && !no_fused_crc;
+      // (not with the vx stage: one CTA would CRC a whole multi-MB blob; the
+      // windowed kernel spreads it over the GPU)
+      bool fused = !(bh.flags & kFlagOuterLz4) && bh.pay_len == bh.raw_len && !no_fused_crc && !vx_on;
       uint64_t at = 0;
       for (uint32_t r = 0; fused && r < gr.sample_count; ++r) {
         if (hits[i][r] != 1 || gr.blob_ranges[r][0] != at) fused = false;

@@ -2525,8 +2525,8 @@ cudaError_t launch_wave(const WaveArgs& a, int grid, int grid_pre, int threads, 
   if (a.n_samples) {
     if (vx) {
       // decode-only launch into the hand-off slots A, the multi-CTA voxel
-      // stage A -> B, then the rest of the chain from B (and, with a cluster
-      // FPS split, from A again after the ops before the FPS)
+      // stage (A voxelized in place, B scratch), then the rest of the chain
+      // from A (with a cluster FPS split: the ops before the FPS write A back)
       const int g1 = a.fps_cluster > 1 ? grid_pre : grid;
       WaveArgs l1 = a;
       l1.fps_cluster = 1;
@@ -2547,7 +2547,7 @@ cudaError_t launch_wave(const WaveArgs& a, int grid, int grid_pre, int threads, 
         l2.fps_cluster = 1;
         l2.op_begin = a.vx_last + 1;
         l2.op_end = stop;
-        l2.handoff_in = vx->B;
+        l2.handoff_in = handoff_a;
         l2.handoff_out = a.split_at ? handoff_a : nullptr;
         one_cta_per_cloud(l2, g1);
       }
@@ -2555,7 +2555,7 @@ cudaError_t launch_wave(const WaveArgs& a, int grid, int grid_pre, int threads, 
         WaveArgs l3 = a;
         l3.op_begin = a.split_at;
         l3.op_end = a.n_ops;
-        l3.handoff_in = l2_runs ? handoff_a : vx->B;
+        l3.handoff_in = handoff_a;
         l3.handoff_out = nullptr;
         if (l2_runs) l3.vx_state = nullptr;
         e = launch_clustered(k_cloud<1>, l3, grid, threads, smem, st);

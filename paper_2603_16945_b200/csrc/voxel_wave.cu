@@ -19,10 +19,11 @@
 //             upsweep (tile digit counts) / colscan (per digit, over tiles)
 //             / downsweep (stable in-tile ranks, scatter)
 //   segs      per tile: voxel starts (key changes) counted, scanned per cloud
+//   gather    payload of the moved fields into sorted order (A -> B)
 //   means     one thread per voxel: count, sequential double sums over its
 //             run in point order (the sort is stable) = bit-exact App. C
-//             means, first point of gathered extra fields
-//   finish    per cloud: the hand-off header the rest of the chain reads
+//             means, first point of gathered extra fields (B -> A)
+//   finish    per cloud: the hand-off header (A) the rest of the chain reads
 //
 // The words carry the point index, so (key, index) order is the App. C
 // order (ascending key, original order inside a voxel) and the means sum in
@@ -543,8 +544,77 @@ __global__ void __launch_bounds__(kThreads) k_vx_segscan(VxArgs v) {
   if (threadIdx.x == 0) c.V = carry;
 }
 
+// Payload of every moved field into sorted order: B[f][k] = A[f][index(k)]
+// (one sorted position per thread per round: coalesced word reads and
+// stores, independent random loads -- many in flight).
+__global__ void __launch_bounds__(kThreads) k_vx_gather(VxArgs v) {
+  const uint32_t total = *v.total_tiles;
+  for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
+    uint32_t s, j, nw;
+    if (!sort_tile(v, t, -1, s, j, nw)) continue;  // uniform
+    const VxCloud& c = v.cl[s];
+    const uint64_t* W = sorted(v, c) + (uint64_t)j * kTile;
+    const uint8_t* A = slot(v, v.A, s);
+    uint8_t* B = v.B + (uint64_t)s * v.stride;
+    const uint32_t* ha = hdr(v, v.A, s);
+    const uint32_t moved = v.mm & ha[1];
+    const uint64_t imask = c.ib ? ((1ull << c.ib) - 1) : 0ull;
+    uint32_t idx[kItems];
+#pragma unroll
+    for (uint32_t r = 0; r < kItems; ++r) {
+      const uint32_t i = r * kThreads + threadIdx.x;
+      idx[r] = i < nw ? (uint32_t)(W[i] & imask) : 0u;
+    }
+    const uint64_t k0 = (uint64_t)j * kTile;
+    for (int f = 0; f < v.n_bytes_fields; ++f) {
+      if (!((moved >> f) & 1u)) continue;
+      const uint32_t es = ha[10 + f];
+      if (es == 12) {
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(A + v.off[f]);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(B + v.off[f]);
+        uint32_t x[kItems][3];
+#pragma unroll
+        for (uint32_t r = 0; r < kItems; ++r)
+          if (r * kThreads + threadIdx.x < nw)
+#pragma unroll
+            for (int q = 0; q < 3; ++q) x[r][q] = src[3ull * idx[r] + q];
+#pragma unroll
+        for (uint32_t r = 0; r < kItems; ++r) {
+          const uint32_t i = r * kThreads + threadIdx.x;
+          if (i < nw)
+#pragma unroll
+            for (int q = 0; q < 3; ++q) dst[3 * (k0 + i) + q] = x[r][q];
+        }
+      } else if (es == 4) {
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(A + v.off[f]);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(B + v.off[f]);
+        uint32_t x[kItems];
+#pragma unroll
+        for (uint32_t r = 0; r < kItems; ++r)
+          if (r * kThreads + threadIdx.x < nw) x[r] = src[idx[r]];
+#pragma unroll
+        for (uint32_t r = 0; r < kItems; ++r) {
+          const uint32_t i = r * kThreads + threadIdx.x;
+          if (i < nw) dst[k0 + i] = x[r];
+        }
+      } else {
+        const uint8_t* src = A + v.off[f];
+        uint8_t* dst = B + v.off[f];
+        for (uint32_t r = 0; r < kItems; ++r) {
+          const uint32_t i = r * kThreads + threadIdx.x;
+          if (i < nw)
+            for (uint32_t b = 0; b < es; ++b) dst[(k0 + i) * es + b] = src[(uint64_t)idx[r] * es + b];
+        }
+      }
+    }
+  }
+}
+
 // One thread per voxel start (thread-contiguous items, so the block scan
-// numbers the tile's starts in order).
+// numbers the tile's starts in order): count and sequential double sums over
+// the voxel's contiguous sorted run in B (point order inside the voxel),
+// means / first point written to A at the voxel index (A's payload is dead
+// after k_vx_gather; the voxelized cloud lives in A from here on).
 __global__ void __launch_bounds__(kThreads) k_vx_means(VxArgs v) {
   __shared__ uint32_t sh[kWarps + 1];
   const uint32_t total = *v.total_tiles;
@@ -556,18 +626,22 @@ __global__ void __launch_bounds__(kThreads) k_vx_means(VxArgs v) {
     const uint32_t base = j * kTile + threadIdx.x * kItems;
     const uint32_t end = j * kTile + nw;
     uint32_t starts = 0;
+    uint64_t prev = base ? W[base - 1] >> c.ib : ~0ull;
 #pragma unroll
     for (uint32_t r = 0; r < kItems; ++r) {
       const uint32_t i = base + r;
-      if (i < end && (i == 0 || (W[i] >> c.ib) != (W[i - 1] >> c.ib))) starts |= 1u << r;
+      if (i < end) {
+        const uint64_t key = W[i] >> c.ib;
+        if (i == 0 || key != prev) starts |= 1u << r;
+        prev = key;
+      }
     }
     uint32_t tot;
     uint32_t vid = v.tile_kofs[t] + block_excl_scan(__popc(starts), sh, &tot);
-    const uint8_t* A = slot(v, v.A, s);
-    uint8_t* B = v.B + (uint64_t)s * v.stride;
+    uint8_t* A = v.A + (uint64_t)s * v.stride;
+    const uint8_t* B = v.B + (uint64_t)s * v.stride;
     const uint32_t* ha = hdr(v, v.A, s);
     const uint32_t moved = v.mm & ha[1];
-    const uint64_t imask = c.ib ? ((1ull << c.ib) - 1) : 0ull;
     while (starts) {
       const uint32_t r = __ffs(starts) - 1;
       starts &= starts - 1;
@@ -576,29 +650,36 @@ __global__ void __launch_bounds__(kThreads) k_vx_means(VxArgs v) {
       uint32_t k1 = k0 + 1;
       while (k1 < c.kept && (W[k1] >> c.ib) == key) ++k1;
       const double cnt = (double)(k1 - k0);
-      const uint32_t first = (uint32_t)(W[k0] & imask);
       for (int f = 0; f < v.n_bytes_fields; ++f) {
         if (!((moved >> f) & 1u)) continue;
         const bool avg = f == v.role_data || f == v.role_normal || f == v.role_color || f == v.role_intensity;
         const uint32_t es = ha[10 + f];
         if (avg) {
           const uint32_t comps = es / 4;  // 3 or 1
-          const float* src = reinterpret_cast<const float*>(A + v.off[f]);
-          float* dst = reinterpret_cast<float*>(B + v.off[f]);
-          double acc[3] = {0.0, 0.0, 0.0};
-          for (uint32_t k = k0; k < k1; ++k) {
-            const uint64_t p = W[k] & imask;
-            for (uint32_t q = 0; q < comps && q < 3; ++q) acc[q] = __dadd_rn(acc[q], (double)src[p * comps + q]);
+          const float* src = reinterpret_cast<const float*>(B + v.off[f]);
+          float* dst = reinterpret_cast<float*>(A + v.off[f]);
+          if (comps == 3) {
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+            for (uint32_t k = k0; k < k1; ++k) {
+              a0 = __dadd_rn(a0, (double)src[3ull * k]);
+              a1 = __dadd_rn(a1, (double)src[3ull * k + 1]);
+              a2 = __dadd_rn(a2, (double)src[3ull * k + 2]);
+            }
+            dst[3ull * vid] = __double2float_rn(__ddiv_rn(a0, cnt));
+            dst[3ull * vid + 1] = __double2float_rn(__ddiv_rn(a1, cnt));
+            dst[3ull * vid + 2] = __double2float_rn(__ddiv_rn(a2, cnt));
+          } else {
+            double a0 = 0.0;
+            for (uint32_t k = k0; k < k1; ++k) a0 = __dadd_rn(a0, (double)src[k]);
+            dst[vid] = __double2float_rn(__ddiv_rn(a0, cnt));
           }
-          for (uint32_t q = 0; q < comps && q < 3; ++q)
-            dst[(uint64_t)vid * comps + q] = __double2float_rn(__ddiv_rn(acc[q], cnt));
-        } else {  // gathered extra field: the voxel's first point
-          const uint8_t* src = A + v.off[f] + (uint64_t)first * es;
-          uint8_t* dst = B + v.off[f] + (uint64_t)vid * es;
+        } else {  // gathered extra field: the voxel's first point (smallest index)
+          const uint8_t* src = B + v.off[f] + (uint64_t)k0 * es;
+          uint8_t* dst = A + v.off[f] + (uint64_t)vid * es;
           for (uint32_t b = 0; b < es; ++b) dst[b] = src[b];
         }
       }
-      if (v.counts) reinterpret_cast<int32_t*>(B + v.off[kMaxBytesFields])[vid] = (int32_t)(k1 - k0);
+      if (v.counts) reinterpret_cast<int32_t*>(A + v.off[kMaxBytesFields])[vid] = (int32_t)(k1 - k0);
       ++vid;
     }
     __syncthreads();
@@ -610,31 +691,21 @@ __global__ void k_vx_finish(VxArgs v) {
   const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= v.n_samples) return;
   const VxCloud& c = v.cl[s];
-  const uint32_t* ha = hdr(v, v.A, s);
-  uint32_t* hb = reinterpret_cast<uint32_t*>(v.B + (uint64_t)s * v.stride);
-  if (ha[0] != (uint32_t)kOk) {  // the decode launch failed: it wrote the status
-    hb[0] = ha[0];
-    return;
-  }
-  if (c.fallback) {
-    hb[0] = kOk;
-    return;
-  }
+  uint32_t* h = reinterpret_cast<uint32_t*>(v.A + (uint64_t)s * v.stride);
+  // decode launch failed (it wrote the status) or fallback (A keeps the
+  // decoded cloud; k_cloud runs the voxel ops): header unchanged
+  if (h[0] != (uint32_t)kOk || c.fallback) return;
   if (c.status != kOk) {
-    hb[0] = (uint32_t)c.status;
+    h[0] = (uint32_t)c.status;
     v.sample_status[s] = c.status;
     v.sample_op[s] = c.fail_op;
     v.sample_where[s] = 0;
     return;
   }
-  hb[1] = ha[1];
-  for (int f = 0; f < kMaxBytesFields; ++f) {
-    hb[2 + f] = (((v.mm & ha[1]) >> f) & 1u) ? c.V : ha[2 + f];
-    hb[10 + f] = ha[10 + f];
-  }
-  hb[18] = v.counts ? 1u : 0u;
-  hb[19] = v.counts ? c.V : 0u;
-  hb[0] = kOk;
+  for (int f = 0; f < kMaxBytesFields; ++f)
+    if (((v.mm & h[1]) >> f) & 1u) h[2 + f] = c.V;
+  h[18] = v.counts ? 1u : 0u;
+  h[19] = v.counts ? c.V : 0u;
 }
 
 }  // namespace
@@ -654,6 +725,7 @@ cudaError_t launch_voxel_wave(const VxArgs& v, uint32_t tiles_bound, int sms, cu
   }
   k_vx_segcount<<<grid, kThreads, 0, st>>>(v);
   k_vx_segscan<<<v.n_samples, kThreads, 0, st>>>(v);
+  k_vx_gather<<<grid, kThreads, 0, st>>>(v);
   k_vx_means<<<grid, kThreads, 0, st>>>(v);
   k_vx_finish<<<(v.n_samples + 127) / 128, 128, 0, st>>>(v);
   return cudaGetLastError();

@@ -12,9 +12,10 @@ namespace pcp {
 constexpr uint32_t kVxMaxPasses = 6;  // 8-bit digits: keys up to 48 bits (wider: k_cloud fallback)
 
 // Arguments of the stage (by value).  A = decoded clouds (hand-off slots of
-// the decode-only k_cloud launch), B = voxelized clouds (hand-off slots the
-// rest of the chain reads); both [n_samples][stride] with the k_cloud
-// hand-off header and field offsets `off`.
+// the decode-only k_cloud launch), voxelized in place by the stage (the rest
+// of the chain reads A); B = scratch slots of the same layout (the sorted
+// payload); both [n_samples][stride] with the k_cloud hand-off header and
+// field offsets `off`.
 struct VxArgs {
   uint32_t n_samples;
   uint8_t* A;
