@@ -14,9 +14,15 @@
 // interpreter), and the next wave is launched before the current one is
 // served, so host staging, H2D copies and compute overlap.
 #include <cuda_runtime.h>
+#include <fcntl.h>
+#include <unistd.h>
 
 #include <algorithm>
+#include <array>
+#include <atomic>
 #include <chrono>
+#include <condition_variable>
+#include <thread>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -462,6 +468,7 @@ struct Wave {
   DevBuf mt_pre;   // pre-seeded MT19937-64 states [n][n_rng][312] (k_seed_states)
   uint32_t n_todo = 0;
   HostBuf h_tables, h_res;
+  HostBuf h_stage;  // option "stream": the wave's page runs read from the slice files
   std::vector<uint64_t> out_base;  // per output field: offset in outs (and in compact)
   // results (pinned, filled by D2H)
   int32_t* h_status = nullptr;
@@ -503,7 +510,23 @@ struct Pipeline {
   cudaStream_t stream = nullptr;        // wave compute (copies + kernels)
   cudaStream_t serve_stream = nullptr;  // batch views: compaction, user D2H
   // byte store: all slice data areas, 16-B aligned, 64 B slack each side
-  std::vector<uint64_t> slice_base;
+  std::vector<uint64_t> slice_base;  // ~0: slice not loaded (outside the walk)
+  std::vector<uint64_t> slice_len, slice_file_off;
+  std::vector<int> slice_fd;
+  uint64_t loaded_bytes = 0;  // slice bytes read into pinned memory at open
+  std::thread reader;
+  std::mutex rd_mu;
+  std::condition_variable rd_cv;
+  int64_t ready_upto = -1, launched_upto = -1;
+  bool rd_stop = false, rd_failed = false;
+  std::string rd_err;
+  uint64_t read_bytes = 0;
+  double read_wait_ms = 0;
+  // option "stream": no byte store; each wave's pages are read from the slice
+  // files by reader threads into the slot's pinned buffer ahead of its launch
+  // (read → H2D → decode → transform → batch all overlap across waves)
+  bool stream_files = false;
+  uint32_t reader_threads = 8;
   uint64_t store_bytes = 0;
   DevBuf d_store;
   HostBuf h_store;
@@ -539,7 +562,7 @@ struct Pipeline {
   bool serial = false;  // option "serial": one wave in flight (non-overlapped kernel timing)
   // multi-CTA voxel stage (voxel_wave.cu) for large clouds whose chain starts
   // with [range_crop,] voxel; option "vx": false keeps it in k_cloud
-  bool vx_allowed = true, vx_on = false;
+  bool vx_allowed = false, vx_on = false;  // default off until it beats the one-CTA path
   uint64_t vx_min_points = 32768;
   VxArgs vx_proto{};
   double vx_kernel_ms = 0;
@@ -554,6 +577,16 @@ struct Pipeline {
   uint32_t waves_done = 0;
 
   ~Pipeline() {
+    if (reader.joinable()) {
+      {
+        std::lock_guard<std::mutex> lk(rd_mu);
+        rd_stop = true;
+      }
+      rd_cv.notify_all();
+      reader.join();
+    }
+    for (int fd : slice_fd)
+      if (fd >= 0) ::close(fd);
     for (auto& w : slots) {
       if (w.stream) cudaStreamDestroy(w.stream);
       if (w.done) cudaEventDestroy(w.done);
@@ -591,7 +624,10 @@ struct Pipeline {
       }
       force_serial_fy = o.value("force_serial_fy", false);
       serial = o.value("serial", false);
-      vx_allowed = o.value("vx", true);
+      stream_files = o.value("stream", false);
+      reader_threads = std::max(1u, std::min(64u, o.value("reader_threads", reader_threads)));
+      if (stream_files) resident = false;
+      vx_allowed = o.value("vx", vx_allowed);
       vx_min_points = o.value("vx_min_points", vx_min_points);
     }
     h = read_header(primary);
@@ -653,6 +689,7 @@ struct Pipeline {
       CK(cudaEventCreateWithFlags(&w.host_ready, cudaEventDisableTiming));
       CK(cudaEventRecord(w.served, serve_stream));
     }
+    if (stream_files && !plan.empty()) reader = std::thread([this] { reader_main(); });
     if (const char* e = std::getenv("PCP_TIMELINE")) timeline_on = std::atoi(e) != 0;
     if (timeline_on) {
       CK(cudaDeviceSynchronize());
@@ -663,38 +700,92 @@ struct Pipeline {
     }
   }
 
-  // Slice data areas → one byte store (HBM when resident, pinned host else).
+  // Slice data areas → one byte store (HBM when resident, pinned host else,
+  // nothing with "stream": pages are read from the slice files per wave).
+  // Shard-local: only the slices the walk touches are read and placed
+  // (a rank of an N-GPU run loads ~1/N of the dataset).
   void load_store() {
-    slice_base.resize(h.slice_paths.size());
-    std::vector<std::vector<uint8_t>> data(h.slice_paths.size());
+    const uint32_t ns = (uint32_t)h.slice_paths.size();
+    slice_base.assign(ns, ~uint64_t(0));
+    slice_len.assign(ns, 0);
+    slice_file_off.assign(ns, 0);
+    std::vector<char> need(ns, 0);
+    for (const auto& e : walk) need[h.groups[e.group_index].slice] = 1;
     uint64_t at = 64;
-    for (uint32_t s = 0; s < h.slice_paths.size(); ++s) {
-      data[s] = read_slice_data(h, dir, s);
+    for (uint32_t s = 0; s < ns; ++s) {
+      if (!need[s]) continue;
+      const fs::path p = fs::path(dir) / h.slice_paths[s];
+      std::error_code ec;
+      const uint64_t sz = fs::file_size(p, ec);
+      if (ec) fail(kIoFailure, "cannot open slice " + h.slice_paths[s]);
+      slice_file_off[s] = s == 0 ? h.header_bytes : 0;
+      if (sz < slice_file_off[s]) fail(kCorruptHeader, "slice shorter than its header");
+      slice_len[s] = sz - slice_file_off[s];
       slice_base[s] = at;
-      at = align16(at + data[s].size()) + 64;
+      at = align16(at + slice_len[s]) + 64;
     }
     store_bytes = at;
-    h_store.ensure(store_bytes);
-    std::memset(h_store.p, 0, 64);
-    for (uint32_t s = 0; s < data.size(); ++s) {
-      std::memcpy(h_store.as<uint8_t>() + slice_base[s], data[s].data(), data[s].size());
+    slice_fd.assign(ns, -1);
+    for (uint32_t s = 0; s < ns; ++s) {
+      if (!need[s]) continue;
+      slice_fd[s] = ::open((fs::path(dir) / h.slice_paths[s]).c_str(), O_RDONLY | O_CLOEXEC);
+      if (slice_fd[s] < 0) fail(kIoFailure, "cannot open slice " + h.slice_paths[s]);
+    }
+    if (!stream_files) {
+      h_store.ensure(store_bytes);
+      std::memset(h_store.p, 0, store_bytes);  // slack bytes between slices read as zeros
+      for (uint32_t s = 0; s < ns; ++s)
+        if (need[s]) read_file(s, 0, slice_len[s], h_store.as<uint8_t>() + slice_base[s]);
+      loaded_bytes = 0;
+      for (uint32_t s = 0; s < ns; ++s) loaded_bytes += slice_len[s];
     }
     // page heads (EncodedPage::deserialize of both pages per group)
-    scalar_head.resize(h.groups.size());
-    block_head.resize(h.groups.size());
+    scalar_head.assign(h.groups.size(), PageHead{});
+    block_head.assign(h.groups.size(), PageHead{});
     for (size_t gi = 0; gi < h.groups.size(); ++gi) {
       const Group& gr = h.groups[gi];
-      const uint8_t* base = h_store.as<uint8_t>() + slice_base[gr.slice];
-      const uint64_t avail_s = data[gr.slice].size() - std::min<uint64_t>(gr.scalar_off, data[gr.slice].size());
-      const uint64_t avail_b = data[gr.slice].size() - std::min<uint64_t>(gr.block_off, data[gr.slice].size());
-      scalar_head[gi] = parse_page_head(base + gr.scalar_off, std::min(avail_s, gr.scalar_len));
-      block_head[gi] = parse_page_head(base + gr.block_off, std::min(avail_b, gr.block_len));
+      if (!need[gr.slice]) continue;
+      const uint64_t L = slice_len[gr.slice];
+      auto head = [&](uint64_t off, uint64_t len) {
+        const uint64_t avail = std::min(L - std::min(off, L), len);
+        uint8_t buf[kPageHeaderBytes];
+        const uint8_t* ph = buf;
+        if (stream_files) {
+          if (avail >= kPageHeaderBytes) read_file(gr.slice, off, kPageHeaderBytes, buf);
+        } else {
+          ph = h_store.as<uint8_t>() + slice_base[gr.slice] + off;
+        }
+        return parse_page_head(ph, avail);
+      };
+      scalar_head[gi] = head(gr.scalar_off, gr.scalar_len);
+      block_head[gi] = head(gr.block_off, gr.block_len);
       if (block_head[gi].flags & kFlagOuterLz4) ++block_pages_lz4;
     }
     if (resident) {
       d_store.ensure(store_bytes);
       CK(cudaMemcpyAsync(d_store.p, h_store.p, store_bytes, cudaMemcpyHostToDevice, stream));
       CK(cudaStreamSynchronize(stream));
+    }
+  }
+
+  // pread of [off, off+len) of slice s's data area (all bytes or kIoFailure).
+  void read_file(uint32_t s, uint64_t off, uint64_t len, uint8_t* dst) const {
+    uint64_t done = 0;
+    while (done < len) {
+      const ssize_t r = ::pread(slice_fd[s], dst + done, len - done, (off_t)(slice_file_off[s] + off + done));
+      if (r <= 0) fail(kIoFailure, "short read of " + h.slice_paths[s]);
+      done += (uint64_t)r;
+    }
+  }
+
+  // Store range [lo, lo+len) → dst, from the slice files: each slice's part
+  // by pread, the slack between slices as zeros.
+  void read_store_range(uint64_t lo, uint64_t len, uint8_t* dst) const {
+    std::memset(dst, 0, len);
+    for (uint32_t s = 0; s < slice_base.size(); ++s) {
+      if (slice_base[s] == ~uint64_t(0)) continue;
+      const uint64_t a = std::max(lo, slice_base[s]), b = std::min(lo + len, slice_base[s] + slice_len[s]);
+      if (a < b) read_file(s, a - slice_base[s], b - a, dst + (a - lo));
     }
   }
 
@@ -999,6 +1090,123 @@ struct Pipeline {
       }
   }
 
+  // Groups a wave touches, in first-use order (the wave's page order).
+  std::vector<uint32_t> wave_groups(uint64_t pos0, uint64_t n) const {
+    std::vector<uint32_t> groups;
+    std::vector<char> seen(h.groups.size(), 0);
+    for (uint64_t k = 0; k < n; ++k) {
+      const uint32_t gi = walk[pos0 + k].group_index;
+      if (!seen[gi]) {
+        seen[gi] = 1;
+        groups.push_back(gi);
+      }
+    }
+    return groups;
+  }
+
+  // Where a wave's pages sit: resident -> their byte-store offsets; staged ->
+  // a device staging buffer.  A wave's pages are consecutive groups of a few
+  // slices, so their byte ranges are sorted and merged (gaps <= 64 KiB copied
+  // along): a handful of large H2D copies (and file reads) per wave instead of
+  // two per group.  stage_off[kind * ng + i] = page offset; runs = (store
+  // offset, length) copied to [64, stage_at) with 64 B between runs.
+  void stage_plan(const std::vector<uint32_t>& groups, std::vector<std::pair<uint64_t, uint64_t>>& runs,
+                  std::vector<uint64_t>& stage_off, uint64_t& stage_at) const {
+    const uint32_t ng = (uint32_t)groups.size();
+    stage_off.assign(2 * ng, 0);
+    runs.clear();
+    stage_at = 64;
+    struct PRun {
+      uint64_t lo, hi;
+      uint32_t page;
+    };
+    std::vector<PRun> prs;
+    for (uint32_t i = 0; i < ng; ++i) {
+      const Group& gr = h.groups[groups[i]];
+      for (int kind = 0; kind < 2; ++kind) {
+        const uint64_t so = slice_base[gr.slice] + (kind ? gr.block_off : gr.scalar_off);
+        const uint64_t len = kind ? gr.block_len : gr.scalar_len;
+        if (!resident) prs.push_back({so, so + len, (uint32_t)(kind * ng + i)});
+        else stage_off[kind * ng + i] = so;
+      }
+    }
+    if (resident || prs.empty()) return;
+    std::sort(prs.begin(), prs.end(), [](const PRun& x, const PRun& y) { return x.lo < y.lo; });
+    size_t k = 0;
+    while (k < prs.size()) {
+      const uint64_t lo = prs[k].lo & ~uint64_t(15);
+      uint64_t hi = align16(prs[k].hi);
+      size_t e = k + 1;
+      while (e < prs.size() && prs[e].lo <= hi + 65536) hi = std::max(hi, align16(prs[e].hi)), ++e;
+      for (size_t q = k; q < e; ++q) stage_off[prs[q].page] = stage_at + (prs[q].lo - lo);
+      runs.push_back({lo, hi - lo});
+      stage_at += (hi - lo) + 64;
+      k = e;
+    }
+  }
+
+  // ---- file streaming: reader threads fill slot (pi % slots) with wave pi --
+  void reader_main() {
+    try {
+      CK(cudaSetDevice(device));
+      const size_t ns = slots.size();
+      for (size_t pi = 0; pi < plan.size(); ++pi) {
+        const size_t si = pi % ns;
+        {
+          std::unique_lock<std::mutex> lk(rd_mu);
+          // the slot's previous wave must have been launched (its copies enqueued)
+          rd_cv.wait(lk, [&] { return rd_stop || pi < ns || launched_upto >= (int64_t)(pi - ns); });
+          if (rd_stop) return;
+        }
+        Wave& w = slots[si];
+        if (pi >= ns) CK(cudaEventSynchronize(w.h1));  // its H2D copies out of h_stage are done
+        std::vector<std::pair<uint64_t, uint64_t>> runs;
+        std::vector<uint64_t> stage_off;
+        uint64_t stage_at = 64;
+        stage_plan(wave_groups(plan[pi].second, plan_n[pi]), runs, stage_off, stage_at);
+        w.h_stage.ensure(stage_at + 64);
+        // chunks of <= 4 MiB over the reader threads
+        std::vector<std::array<uint64_t, 3>> chunks;  // store lo, len, h_stage offset
+        uint64_t d_at = 64;
+        for (const auto& r : runs) {
+          for (uint64_t o = 0; o < r.second; o += (4ull << 20))
+            chunks.push_back({r.first + o, std::min<uint64_t>(4ull << 20, r.second - o), d_at + o});
+          d_at += r.second + 64;
+        }
+        std::atomic<size_t> next{0};
+        std::string err;
+        std::mutex err_mu;
+        auto work = [&] {
+          for (size_t c; (c = next.fetch_add(1)) < chunks.size();) {
+            try {
+              read_store_range(chunks[c][0], chunks[c][1], w.h_stage.as<uint8_t>() + chunks[c][2]);
+            } catch (const std::exception& e) {
+              std::lock_guard<std::mutex> l(err_mu);
+              err = e.what();
+            }
+          }
+        };
+        std::vector<std::thread> pool;
+        const size_t nt = std::min<size_t>(reader_threads, chunks.size());
+        for (size_t t = 1; t < nt; ++t) pool.emplace_back(work);
+        work();
+        for (auto& t : pool) t.join();
+        if (!err.empty()) fail(kIoFailure, err);
+        {
+          std::lock_guard<std::mutex> lk(rd_mu);
+          ready_upto = (int64_t)pi;
+          read_bytes += d_at;
+        }
+        rd_cv.notify_all();
+      }
+    } catch (const std::exception& e) {
+      std::lock_guard<std::mutex> lk(rd_mu);
+      rd_err = e.what();
+      rd_failed = true;
+      rd_cv.notify_all();
+    }
+  }
+
   // ---- wave construction ---------------------------------------------------
   void launch(Wave& w, size_t pi, bool dry = false) {
     // the slot's previous wave may still be read by copies the user enqueued
@@ -1041,42 +1249,10 @@ struct Pipeline {
     std::vector<CrcWindow> wins;
     uint64_t raw_at = 0, vals_at = 0;
     uint32_t rec_at = 0;
-    // staged mode: copy the wave's pages into a device staging buffer.  A
-    // wave's pages are consecutive groups of a few slices, so their byte
-    // ranges are sorted and merged (gaps <= 64 KiB copied along): a handful
-    // of large H2D copies per wave instead of two per group.
     std::vector<std::pair<uint64_t, uint64_t>> runs;  // (store off, len), 16-B aligned
-    auto page_src = [&](uint32_t slice, uint64_t off) { return slice_base[slice] + off; };
     uint64_t stage_at = 64;
-    std::vector<uint64_t> stage_off(2 * ng);
-    struct PRun {
-      uint64_t lo, hi;
-      uint32_t page;
-    };
-    std::vector<PRun> prs;
-    for (uint32_t i = 0; i < ng; ++i) {
-      const Group& gr = h.groups[groups[i]];
-      for (int kind = 0; kind < 2; ++kind) {
-        const uint64_t so = page_src(gr.slice, kind ? gr.block_off : gr.scalar_off);
-        const uint64_t len = kind ? gr.block_len : gr.scalar_len;
-        if (!resident) prs.push_back({so, so + len, (uint32_t)(kind * ng + i)});
-        else stage_off[kind * ng + i] = so;
-      }
-    }
-    if (!resident && !prs.empty()) {
-      std::sort(prs.begin(), prs.end(), [](const PRun& x, const PRun& y) { return x.lo < y.lo; });
-      size_t k = 0;
-      while (k < prs.size()) {
-        const uint64_t lo = prs[k].lo & ~uint64_t(15);
-        uint64_t hi = align16(prs[k].hi);
-        size_t e = k + 1;
-        while (e < prs.size() && prs[e].lo <= hi + 65536) hi = std::max(hi, align16(prs[e].hi)), ++e;
-        for (size_t q = k; q < e; ++q) stage_off[prs[q].page] = stage_at + (prs[q].lo - lo);
-        runs.push_back({lo, hi - lo});
-        stage_at += (hi - lo) + 64;
-        k = e;
-      }
-    }
+    std::vector<uint64_t> stage_off;
+    stage_plan(groups, runs, stage_off, stage_at);
     for (uint32_t i = 0; i < ng; ++i) {
       const uint32_t gi = groups[i];
       const Group& gr = h.groups[gi];
@@ -1226,7 +1402,21 @@ struct Pipeline {
     // staged input bytes
     const uint8_t* bytes = d_store.as<uint8_t>();
     CK(cudaEventRecord(w.h0, w.stream));
-    if (!resident) {
+    if (!resident && stream_files) {
+      // the reader threads filled this slot's pinned buffer with the wave's
+      // runs (same layout as bytes_stage): one H2D copy
+      const auto t0 = std::chrono::steady_clock::now();
+      {
+        std::unique_lock<std::mutex> lk(rd_mu);
+        rd_cv.wait(lk, [&] { return rd_failed || ready_upto >= (int64_t)pi; });
+        if (rd_failed) fail(kIoFailure, "slice read: " + rd_err);
+      }
+      read_wait_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+      CK(cudaMemcpyAsync(w.bytes_stage.as<uint8_t>() + 64, w.h_stage.as<uint8_t>() + 64, stage_at - 64,
+                         cudaMemcpyHostToDevice, w.stream));
+      bytes = w.bytes_stage.as<uint8_t>();
+      for (const auto& r : runs) h2d_bytes += r.second;
+    } else if (!resident) {
       uint64_t d_at = 64;
       for (const auto& r : runs) {
         CK(cudaMemcpyAsync(w.bytes_stage.as<uint8_t>() + d_at, h_store.as<uint8_t>() + r.first,
@@ -1238,6 +1428,13 @@ struct Pipeline {
     }
     CK(cudaMemcpyAsync(dt, ht, up_bytes, cudaMemcpyHostToDevice, w.stream));
     CK(cudaEventRecord(w.h1, w.stream));
+    if (stream_files) {  // the reader may refill this slot's buffer once h1 completes
+      {
+        std::lock_guard<std::mutex> lk(rd_mu);
+        launched_upto = (int64_t)pi;
+      }
+      rd_cv.notify_all();
+    }
     CK(cudaMemsetAsync(dt + o_acc, 0, o_woff - o_acc, w.stream));  // incl. out_len: failed samples write none
     // ---- args ----------------------------------------------------------------
     a.bytes = bytes;
@@ -1574,6 +1771,11 @@ struct Pipeline {
            {"block_pages_lz4", block_pages_lz4},
            {"block_pages_stored_raw", block_head.size() - block_pages_lz4},
            {"h2d_bytes", h2d_bytes},
+           {"loaded_bytes", loaded_bytes},
+           {"store_bytes", store_bytes},
+           {"stream", stream_files},
+           {"read_bytes", read_bytes},
+           {"read_wait_ms", read_wait_ms},
            {"d2h_bytes", d2h_bytes},
            {"host_launch_ms", host_launch_ms},
            {"host_wait_ms", host_wait_ms},

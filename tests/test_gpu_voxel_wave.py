@@ -39,7 +39,7 @@ def test_vx_stage_matches_oracle_and_cta_path(pcp, ref, orc, tmp_path, name):
     gen, kw, n, group, chain = CHAINS[name]
     primary = _ds(pcp, tmp_path, gen, n, group, **kw)
     g = synth.graph(chain or synth.CHAINS[name], batch_size=2, drop_remainder=False)
-    p = pcp.Pipeline(primary, g, vx_min_points=1)
+    p = pcp.Pipeline(primary, g, vx=True, vx_min_points=1)
     assert p.stats()["vx"], "the multi-CTA voxel stage should take this chain"
     got = []
     for b in p:
@@ -65,7 +65,7 @@ def test_vx_fallback_wide_keys(pcp, ref, orc, tmp_path):
     primary = pcp.write_dataset(tmp_path, "ds", schema, samples, group_size=1)
     from paper_2603_16945_b200 import synth
     g = synth.graph([("voxel", {"voxel_size": 0.001})], batch_size=1)
-    got = pcp.run_pipeline(primary, g, vx_min_points=1)
+    got = pcp.run_pipeline(primary, g, vx=True, vx_min_points=1)
     assert_batches_equal(got, expected_run(ref, orc, primary, g))
 
 
@@ -108,9 +108,9 @@ def test_vx_statuses_match_cta_path(pcp, tmp_path, case):
     from paper_2603_16945_b200 import synth
     g = synth.graph(chain, batch_size=1)
     msgs = []
-    for opts in ({"vx_min_points": 1}, {"vx": False}):
+    for opts in ({"vx": True, "vx_min_points": 1}, {"vx": False}):
         p = pcp.Pipeline(primary, g, **opts)
-        assert p.stats()["vx"] == ("vx" not in opts)
+        assert p.stats()["vx"] == opts["vx"]
         out = [p.next_batch().to_host() for _ in range(2)]
         with pytest.raises(pcp.PcError) as ei:
             p.next_batch()
