@@ -156,15 +156,43 @@ int pcp_write_dataset(const char* out_dir, const char* stem, const char* schema_
  * index entries this pipeline walks — e.g. one GPU's shard; index i of the
  * walk is the seed index, like Item.index (pipeline.cpp:447-448).
  * Options: JSON {"epochs": n, "resident": true|false, "wave_batches": k,
- * "slots": s, "host_batches": true|false}.  host_batches delivers every batch
- * in pinned host memory (pcp_field.h_ptr), like the reference's host Batch:
- * once a wave's kernels finish, its fields are copied with one D2H per field
- * (one per sample for ragged fields). */
+ * "slots": s, "host_batches": true|false, "stream": true|false,
+ * "reader_threads": t, "serial": true|false, "vx": true|false}.
+ *   resident      pages of the walk's slices in HBM (read once at open);
+ *                 false: in pinned host memory, H2D per wave
+ *   stream        no copy at open: reader threads read each wave's pages from
+ *                 the slice files into the wave slot's pinned buffer ahead
+ *                 of its launch (datasets larger than host RAM / HBM)
+ *   host_batches  every batch also in pinned host memory (pcp_field.h_ptr),
+ *                 like the reference's host Batch: one D2H per field per wave
+ *   serial        one wave in flight (non-overlapped per-kernel timing)
+ *   vx            multi-CTA voxel stage for large clouds
+ * Only the slices the walk touches are read (shard-local loading). */
 typedef struct pcp_pipeline pcp_pipeline;
 
 int pcp_pipeline_open(const char* primary_path, const char* graph_json,
                       const uint64_t* entry_ids, uint64_t n_entries, int device,
                       const char* options_json, pcp_pipeline** out);
+
+/* Caller-supplied pages: the SourceFn analogue (Pipeline(graph, SourceFn,
+ * samples_per_epoch, opts), pipeline.hpp:157-160; the streaming SourceFn of
+ * stream_dataset, streaming.cpp:324-351, blocks until a sample's slice is
+ * staged).  The stage asks `read` for byte ranges of slice data areas (offset
+ * 0 = first byte after the primary slice's header; continuation slices from
+ * their first byte), from reader threads, ahead of each wave; `read` may block
+ * until the slice is present and returns 0 or an Errc+1 status (surfaced
+ * from next_batch).  `done` (optional) is called on the caller's thread once
+ * the pages of walk positions [first_index, first_index+count) of `epoch` are
+ * on the device (their host bytes may be evicted).  `header` = the primary
+ * slice's FileHeader bytes ("PCRC", version, JSON length, JSON), e.g. from a
+ * meta index.  Options as pcp_pipeline_open ("stream" is implied). */
+typedef int (*pcp_page_source_fn)(void* user, uint32_t slice, uint64_t offset, uint64_t length,
+                                  uint8_t* dst);
+typedef void (*pcp_wave_done_fn)(void* user, uint64_t epoch, uint64_t first_index, uint64_t count);
+int pcp_pipeline_open_source(const uint8_t* header, size_t header_len, const char* graph_json,
+                             const uint64_t* entry_ids, uint64_t n_entries, int device,
+                             const char* options_json, pcp_page_source_fn read,
+                             pcp_wave_done_fn done, void* user, pcp_pipeline** out);
 
 #define PCP_MAX_BATCH_FIELDS 16
 typedef struct {

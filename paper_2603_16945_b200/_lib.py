@@ -57,6 +57,10 @@ class _Batch(C.Structure):
 
 _lib = None
 
+# pcp_page_source_fn / pcp_wave_done_fn (include/pcpipe_b200.h)
+PAGE_SOURCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint32, C.c_uint64, C.c_uint64, C.POINTER(C.c_uint8))
+WAVE_DONE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64)
+
 
 def lib():
     """Load the CUDA library (built by ``make -C paper_2603_16945_b200``)."""
@@ -74,6 +78,9 @@ def lib():
                                         C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32]
         L.pcp_pipeline_open.argtypes = [C.c_char_p, C.c_char_p, C.POINTER(C.c_uint64), C.c_uint64,
                                         C.c_int, C.c_char_p, C.POINTER(C.c_void_p)]
+        L.pcp_pipeline_open_source.argtypes = [C.c_char_p, C.c_size_t, C.c_char_p, C.POINTER(C.c_uint64),
+                                               C.c_uint64, C.c_int, C.c_char_p, PAGE_SOURCE_FN, WAVE_DONE_FN,
+                                               C.c_void_p, C.POINTER(C.c_void_p)]
         L.pcp_pipeline_next_batch.argtypes = [C.c_void_p, C.POINTER(_Batch), C.POINTER(C.c_int)]
         L.pcp_pipeline_stream.restype = C.c_void_p
         L.pcp_pipeline_stream.argtypes = [C.c_void_p]
@@ -208,6 +215,42 @@ class Pipeline:
                                    C.byref(h)))
         self._h = h
         self.stream = L.pcp_pipeline_stream(h)
+
+    @classmethod
+    def from_source(cls, header: bytes, graph, read, done=None, ids=None, device: int = 0,
+                    epochs: int = 1, **options):
+        """Pipeline over caller-supplied pages (pcp_pipeline_open_source, the
+        SourceFn analogue): ``read(slice, offset, length) -> bytes`` may block
+        until the slice is present; ``done(epoch, first_index, count)`` is
+        called once those walk positions' pages are on the device."""
+        self = cls.__new__(cls)
+        L = lib()
+        g = graph if isinstance(graph, str) else json.dumps(graph)
+        opts = json.dumps({"epochs": epochs, **options})
+
+        def _read(_user, sl, off, n, dst):
+            try:
+                b = read(sl, off, n)
+                if len(b) != n:
+                    return K["IoFailure"]
+                C.memmove(dst, b, n)
+                return 0
+            except Exception:
+                return K["IoFailure"]
+
+        self._read_cb = PAGE_SOURCE_FN(_read)
+        self._done_cb = WAVE_DONE_FN(lambda _u, e, f, n: done(e, f, n)) if done else WAVE_DONE_FN()
+        h = C.c_void_p()
+        if ids is None:
+            p, n = None, 0
+        else:
+            self._ids = np.ascontiguousarray(ids, dtype=np.uint64)
+            p, n = self._ids.ctypes.data_as(C.POINTER(C.c_uint64)), len(self._ids)
+        _check(L.pcp_pipeline_open_source(header, len(header), g.encode(), p, n, device, opts.encode(),
+                                          self._read_cb, self._done_cb, None, C.byref(h)))
+        self._h = h
+        self.stream = L.pcp_pipeline_stream(h)
+        return self
 
     def next_batch(self) -> DeviceBatch | None:
         b = _Batch()

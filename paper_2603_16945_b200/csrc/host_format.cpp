@@ -130,19 +130,7 @@ std::vector<FieldSpec> schema_from_json(const std::string& text) {
 }
 
 // ---------------------------------------------------------------- read
-Header read_header(const std::string& primary) {
-  std::ifstream f(primary, std::ios::binary);
-  if (!f) fail(kIoFailure, "cannot open " + primary);
-  char magic[4];
-  if (!f.read(magic, 4)) fail(kCorruptHeader, "file too short");
-  if (std::memcmp(magic, "PCRC", 4) != 0) fail(kBadMagic, "not a .pcrecord file");
-  uint16_t version = 0;
-  if (!f.read(reinterpret_cast<char*>(&version), 2)) fail(kCorruptHeader, "file too short");
-  if (version != 1) fail(kUnsupportedVersion, "version " + std::to_string(version));
-  uint32_t len = 0;
-  if (!f.read(reinterpret_cast<char*>(&len), 4)) fail(kCorruptHeader, "file too short");
-  std::string buf(len, '\0');
-  if (!f.read(buf.data(), len)) fail(kCorruptHeader, "header truncated");
+Header parse_header_json(const std::string& buf) {
   json j = json::parse(buf, nullptr, false);
   if (j.is_discarded()) fail(kCorruptHeader, "header is not valid JSON");
   Header h;
@@ -181,6 +169,37 @@ Header read_header(const std::string& primary) {
       if (r[0] > r[1]) fail(kCorruptHeader, "blob range inverted");
   }
   h.header_bytes = header_byte_size(h);
+  return h;
+}
+
+// FileHeader bytes (magic, version, JSON length, JSON) already in memory:
+// parse + check_invariants (format.cpp:612-629,364-376); no slice-size checks.
+Header parse_header_bytes(const uint8_t* p, size_t n) {
+  if (n < 10) fail(kCorruptHeader, "file too short");
+  if (std::memcmp(p, "PCRC", 4) != 0) fail(kBadMagic, "not a .pcrecord file");
+  uint16_t version = 0;
+  std::memcpy(&version, p + 4, 2);
+  if (version != 1) fail(kUnsupportedVersion, "version " + std::to_string(version));
+  uint32_t len = 0;
+  std::memcpy(&len, p + 6, 4);
+  if (10ull + len > n) fail(kCorruptHeader, "header truncated");
+  return parse_header_json(std::string(reinterpret_cast<const char*>(p) + 10, len));
+}
+
+Header read_header(const std::string& primary) {
+  std::ifstream f(primary, std::ios::binary);
+  if (!f) fail(kIoFailure, "cannot open " + primary);
+  char magic[4];
+  if (!f.read(magic, 4)) fail(kCorruptHeader, "file too short");
+  if (std::memcmp(magic, "PCRC", 4) != 0) fail(kBadMagic, "not a .pcrecord file");
+  uint16_t version = 0;
+  if (!f.read(reinterpret_cast<char*>(&version), 2)) fail(kCorruptHeader, "file too short");
+  if (version != 1) fail(kUnsupportedVersion, "version " + std::to_string(version));
+  uint32_t len = 0;
+  if (!f.read(reinterpret_cast<char*>(&len), 4)) fail(kCorruptHeader, "file too short");
+  std::string buf(len, '\0');
+  if (!f.read(buf.data(), len)) fail(kCorruptHeader, "header truncated");
+  Header h = parse_header_json(buf);
   // slice sizes (:630-652)
   const fs::path dir = fs::path(primary).parent_path();
   uint64_t on_disk = 0;

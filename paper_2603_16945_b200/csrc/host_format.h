@@ -69,6 +69,9 @@ struct PageHead {  // the 21-byte EncodedPage prefix (format.cpp:276-299)
 // read_header (format.cpp:612-653): magic, version, JSON, invariants, slice
 // sizes.  Throws Fail with the reference's Errc.
 Header read_header(const std::string& primary);
+// The same from header bytes in memory (e.g. a streamed meta index), no
+// slice-size checks (the slices are not local yet).
+Header parse_header_bytes(const uint8_t* p, size_t n);
 // build_index (metadata.cpp:20-52) for one header.
 std::vector<Entry> build_index(const Header& h);
 // Reads one slice's data area (whole file; primary minus its header).

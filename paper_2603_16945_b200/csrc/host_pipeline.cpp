@@ -606,6 +606,12 @@ struct Pipeline {
     if (serve_stream) cudaStreamDestroy(serve_stream);
   }
 
+  // Caller-supplied pages (pcp_pipeline_open_source): the SourceFn analogue.
+  pcp_page_source_fn src_read = nullptr;
+  pcp_wave_done_fn src_done = nullptr;
+  void* src_user = nullptr;
+  const std::vector<uint8_t>* src_header = nullptr;
+
   void open(const std::string& primary, const std::string& graph_json, const uint64_t* ids,
             uint64_t n_ids, int dev, const std::string& options) {
     sms = require_device(dev);
@@ -630,8 +636,14 @@ struct Pipeline {
       vx_allowed = o.value("vx", vx_allowed);
       vx_min_points = o.value("vx_min_points", vx_min_points);
     }
-    h = read_header(primary);
-    dir = fs::path(primary).parent_path().string();
+    if (src_header) {  // pages come from the caller: header bytes only, no files
+      h = parse_header_bytes(src_header->data(), src_header->size());
+      stream_files = true;
+      resident = false;
+    } else {
+      h = read_header(primary);
+      dir = fs::path(primary).parent_path().string();
+    }
     index = build_index(h);
     if (ids) {
       for (uint64_t i = 0; i < n_ids; ++i) {
@@ -712,21 +724,28 @@ struct Pipeline {
     std::vector<char> need(ns, 0);
     for (const auto& e : walk) need[h.groups[e.group_index].slice] = 1;
     uint64_t at = 64;
+    std::vector<uint64_t> extent(ns, 0);  // page-covered part of each slice data area
+    for (const auto& gr : h.groups)
+      extent[gr.slice] = std::max({extent[gr.slice], gr.scalar_off + gr.scalar_len, gr.block_off + gr.block_len});
     for (uint32_t s = 0; s < ns; ++s) {
       if (!need[s]) continue;
-      const fs::path p = fs::path(dir) / h.slice_paths[s];
-      std::error_code ec;
-      const uint64_t sz = fs::file_size(p, ec);
-      if (ec) fail(kIoFailure, "cannot open slice " + h.slice_paths[s]);
-      slice_file_off[s] = s == 0 ? h.header_bytes : 0;
-      if (sz < slice_file_off[s]) fail(kCorruptHeader, "slice shorter than its header");
-      slice_len[s] = sz - slice_file_off[s];
+      if (src_read) {
+        slice_len[s] = extent[s];
+      } else {
+        const fs::path p = fs::path(dir) / h.slice_paths[s];
+        std::error_code ec;
+        const uint64_t sz = fs::file_size(p, ec);
+        if (ec) fail(kIoFailure, "cannot open slice " + h.slice_paths[s]);
+        slice_file_off[s] = s == 0 ? h.header_bytes : 0;
+        if (sz < slice_file_off[s]) fail(kCorruptHeader, "slice shorter than its header");
+        slice_len[s] = sz - slice_file_off[s];
+      }
       slice_base[s] = at;
       at = align16(at + slice_len[s]) + 64;
     }
     store_bytes = at;
     slice_fd.assign(ns, -1);
-    for (uint32_t s = 0; s < ns; ++s) {
+    for (uint32_t s = 0; s < ns && !src_read; ++s) {
       if (!need[s]) continue;
       slice_fd[s] = ::open((fs::path(dir) / h.slice_paths[s]).c_str(), O_RDONLY | O_CLOEXEC);
       if (slice_fd[s] < 0) fail(kIoFailure, "cannot open slice " + h.slice_paths[s]);
@@ -770,6 +789,11 @@ struct Pipeline {
 
   // pread of [off, off+len) of slice s's data area (all bytes or kIoFailure).
   void read_file(uint32_t s, uint64_t off, uint64_t len, uint8_t* dst) const {
+    if (src_read) {  // caller-supplied pages (may block until the slice is present)
+      const int st = src_read(src_user, s, off, len, dst);
+      if (st) fail(st, "page source failed for slice " + std::to_string(s));
+      return;
+    }
     uint64_t done = 0;
     while (done < len) {
       const ssize_t r = ::pread(slice_fd[s], dst + done, len - done, (off_t)(slice_file_off[s] + off + done));
@@ -1691,6 +1715,7 @@ struct Pipeline {
               lz4_phase_cycles[ph] = std::max(lz4_phase_cycles[ph], c);
             }
       }
+      if (src_done) src_done(src_user, wn.epoch, wn.pos0, wn.n);  // its pages are on the device
       cur = nxt;
       served = 0;
       clouds += wn.n;
@@ -2030,6 +2055,25 @@ int pcp_pipeline_open(const char* primary, const char* graph_json, const uint64_
   return guarded([&] {
     auto p = std::make_unique<pcp_pipeline>();
     p->impl.open(primary, graph_json, ids, n_ids, device, options ? options : "");
+    *out = p.release();
+  });
+}
+
+int pcp_pipeline_open_source(const uint8_t* header, size_t header_len, const char* graph_json,
+                             const uint64_t* ids, uint64_t n_ids, int device, const char* options,
+                             pcp_page_source_fn read, pcp_wave_done_fn done, void* user,
+                             pcp_pipeline** out) {
+  *out = nullptr;
+  return guarded([&] {
+    if (!header || !read) fail(kOutOfBounds, "header bytes and a page source are required");
+    auto p = std::make_unique<pcp_pipeline>();
+    const std::vector<uint8_t> hb(header, header + header_len);
+    p->impl.src_header = &hb;
+    p->impl.src_read = read;
+    p->impl.src_done = done;
+    p->impl.src_user = user;
+    p->impl.open("", graph_json, ids, n_ids, device, options ? options : "");
+    p->impl.src_header = nullptr;
     *out = p.release();
   });
 }

@@ -106,3 +106,54 @@ def test_stream_read_failure_is_io_failure(pcp, tmp_path):
             pass
     assert ei.value.errc == "IoFailure"
     p.close()
+
+
+def test_caller_supplied_pages_like_stream_dataset(pcp, ref, orc, tmp_path):
+    """pcp_pipeline_open_source driven like stream_dataset's SourceFn
+    (streaming.cpp:324-351): slices 'download' in the background, the page
+    source blocks until the requested slice is present, consumption is
+    reported per wave.  Output = the reference run over the same shard."""
+    import threading
+    import time
+    from paper_2603_16945_b200 import shard, synth
+    primary = _ds(pcp, tmp_path, "shapenet", 96, group=8, slices=4, n_points=600)
+    g = synth.graph(synth.CHAINS["shapenet_part"], batch_size=4)
+    with open(primary, "rb") as f:
+        head = f.read(10)
+        (jl,) = np.frombuffer(head[6:10], np.uint32)
+        header = head + f.read(int(jl))
+    d = os.path.dirname(primary)
+    names = sorted(f for f in os.listdir(d) if ".pcrecord" in f)
+    files = {}
+    for i, name in enumerate(["ds.pcrecord"] + [f"ds.pcrecord{k}" for k in range(1, len(names))]):
+        with open(os.path.join(d, name), "rb") as f:
+            files[i] = f.read()[len(header) if i == 0 else 0:]
+    present, cv = set(), threading.Condition()
+
+    def downloader():
+        for sl in (3, 1, 0, 2):
+            time.sleep(0.05)
+            with cv:
+                present.add(sl)
+                cv.notify_all()
+
+    def read(sl, off, n):
+        with cv:
+            cv.wait_for(lambda: sl in present, timeout=30)
+        return files[sl][off:off + n]
+
+    consumed = []
+    idx = shard.read_index(primary)
+    ids = shard.strided_shard(len(idx), 2, 1)  # the reference's padded strided rule
+    t = threading.Thread(target=downloader)
+    t.start()
+    p = pcp.Pipeline.from_source(header, g, read, lambda e, f, n: consumed.append((e, f, n)), ids=ids,
+                                 epochs=2, wave_batches=2, slots=2)
+    got = [{"epoch": b.epoch, "batch_index": b.batch_index, "samples": b.samples()} for b in p]
+    p.close()
+    t.join()
+    assert_batches_equal(got, expected_run(ref, orc, primary, g, ids=ids, epochs=2))
+    per_epoch = {}
+    for e, f, n in consumed:
+        per_epoch[e] = per_epoch.get(e, 0) + n
+    assert per_epoch == {0: len(ids) // 4 * 4, 1: len(ids) // 4 * 4}
