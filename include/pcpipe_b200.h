@@ -230,6 +230,18 @@ int pcp_pipeline_next_batch(pcp_pipeline* p, pcp_batch* out, int* end_of_stream)
 void* pcp_pipeline_stream(pcp_pipeline* p);
 /* Stats JSON (clouds, points, bytes, kernel ms …); caller must not free. */
 const char* pcp_pipeline_stats(pcp_pipeline* p);
+/* Pipeline::metrics (pipeline.hpp:140-149): MetricsSnapshot as JSON
+ * {uptime_seconds, ops:[{op_id, kind, num_workers, items, busy_seconds,
+ * out_queue_size, out_queue_capacity}], sink_polls, sink_empty_polls,
+ * sink_size, sink_capacity, batches_emitted, items_emitted} plus the GPU
+ * knobs (slots, wave_batches).  Valid until the next call; do not free. */
+const char* pcp_pipeline_metrics(pcp_pipeline* p);
+/* Pipeline::update_op_config (pipeline.hpp:168-170) for the device knobs:
+ * JSON {"slots": 2..8, "wave_batches": k >= 1}.  Applied at the next wave
+ * boundary after the waves in flight are served; batches, their order and
+ * their seeds do not change.  PCP_E_OUT_OF_BOUNDS for values out of range
+ * (or while streaming from files), PCP_E_UNKNOWN_OP for unknown knobs. */
+int pcp_pipeline_update_config(pcp_pipeline* p, const char* config_json);
 void pcp_pipeline_close(pcp_pipeline* p);
 
 /* ---- small device-memory helpers for hosts without a CUDA runtime ----- */

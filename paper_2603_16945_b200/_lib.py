@@ -87,6 +87,9 @@ def lib():
         L.pcp_pipeline_stats.restype = C.c_char_p
         L.pcp_pipeline_stats.argtypes = [C.c_void_p]
         L.pcp_pipeline_close.argtypes = [C.c_void_p]
+        L.pcp_pipeline_metrics.restype = C.c_char_p
+        L.pcp_pipeline_metrics.argtypes = [C.c_void_p]
+        L.pcp_pipeline_update_config.argtypes = [C.c_void_p, C.c_char_p]
         L.pcp_memcpy_d2h.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]
         L.pcp_memcpy_d2h_async.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]
         L.pcp_memcpy_h2d.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]

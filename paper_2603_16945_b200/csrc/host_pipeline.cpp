@@ -553,7 +553,12 @@ struct Pipeline {
   bool failed = false;
   int32_t fail_code = 0;
   std::string fail_msg;
-  std::string stats_json;
+  std::string stats_json, metrics_json;
+  json pending_cfg = json::object();
+  bool has_pending = false;
+  uint64_t reconfigs = 0, sink_polls = 0, sink_empty_polls = 0, items_emitted = 0;
+  uint32_t cur_wave_batches = 0;
+  std::chrono::steady_clock::time_point t_start = std::chrono::steady_clock::now();
   // stats
   uint64_t clouds = 0, points_in = 0, payload_bytes = 0, batches = 0;
   uint64_t h2d_bytes = 0, launches = 0, alg_bytes = 0;
@@ -576,6 +581,27 @@ struct Pipeline {
   uint64_t d2h_bytes = 0;  // host_batches: batch bytes copied to host
   uint32_t waves_done = 0;
 
+  void create_slot(Wave& w) {
+    CK(cudaStreamCreateWithFlags(&w.stream, cudaStreamNonBlocking));
+    for (size_t pi = 0; pi < plan.size() && plan[pi].first == plan[next_plan < plan.size() ? next_plan : 0].first;
+         ++pi)
+      if (pi >= next_plan) launch(w, pi, true);  // pre-size for the waves still to come
+    if (proto.gscratch_per_cta) w.gscratch.ensure(proto.gscratch_per_cta * std::max(grid, grid_pre));
+    for (cudaEvent_t* e : {&w.done, &w.k0, &w.k1, &w.d0, &w.d1, &w.h0, &w.h1, &w.c0, &w.c1, &w.s0, &w.s1, &w.v0, &w.v1})
+      CK(cudaEventCreate(e));
+    CK(cudaEventCreateWithFlags(&w.served, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&w.host_ready, cudaEventDisableTiming));
+    CK(cudaEventRecord(w.served, serve_stream));
+  }
+
+  static void destroy_slot(Wave& w) {
+    if (w.stream) cudaStreamDestroy(w.stream);
+    for (cudaEvent_t e : {w.done, w.k0, w.k1, w.d0, w.d1, w.h0, w.h1, w.c0, w.c1, w.s0, w.s1, w.v0, w.v1,
+                          w.served, w.host_ready})
+      if (e) cudaEventDestroy(e);
+    w.stream = nullptr;
+  }
+
   ~Pipeline() {
     if (reader.joinable()) {
       {
@@ -587,20 +613,7 @@ struct Pipeline {
     }
     for (int fd : slice_fd)
       if (fd >= 0) ::close(fd);
-    for (auto& w : slots) {
-      if (w.stream) cudaStreamDestroy(w.stream);
-      if (w.done) cudaEventDestroy(w.done);
-      if (w.k0) cudaEventDestroy(w.k0);
-      if (w.k1) cudaEventDestroy(w.k1);
-      if (w.d0) cudaEventDestroy(w.d0);
-      if (w.d1) cudaEventDestroy(w.d1);
-      if (w.h0) cudaEventDestroy(w.h0);
-      for (cudaEvent_t e : {w.c0, w.c1, w.s0, w.s1, w.v0, w.v1})
-        if (e) cudaEventDestroy(e);
-      if (w.h1) cudaEventDestroy(w.h1);
-      if (w.served) cudaEventDestroy(w.served);
-      if (w.host_ready) cudaEventDestroy(w.host_ready);
-    }
+    for (auto& w : slots) destroy_slot(w);
     if (t_open) cudaEventDestroy(t_open);
     if (stream) cudaStreamDestroy(stream);
     if (serve_stream) cudaStreamDestroy(serve_stream);
@@ -684,23 +697,10 @@ struct Pipeline {
     if (!slots_set && proto.gscratch_per_cta)
       while (n_slots > 2 && (uint64_t)n_slots * proto.gscratch_per_cta * std::max(grid, grid_pre) > (48ull << 30))
         --n_slots;
+    slots.reserve(8);  // reconfiguration resizes in place (Wave owns device buffers)
     slots.resize(n_slots);
-    for (auto& w : slots) {
-      CK(cudaStreamCreateWithFlags(&w.stream, cudaStreamNonBlocking));
-      for (size_t pi = 0; pi < plan.size() && plan[pi].first == 0; ++pi) launch(w, pi, true);
-      if (proto.gscratch_per_cta) w.gscratch.ensure(proto.gscratch_per_cta * std::max(grid, grid_pre));
-      CK(cudaEventCreate(&w.done));
-      CK(cudaEventCreate(&w.k0));
-      CK(cudaEventCreate(&w.k1));
-      CK(cudaEventCreate(&w.d0));
-      CK(cudaEventCreate(&w.d1));
-      CK(cudaEventCreate(&w.h0));
-      for (cudaEvent_t* e : {&w.c0, &w.c1, &w.s0, &w.s1, &w.v0, &w.v1}) CK(cudaEventCreate(e));
-      CK(cudaEventCreate(&w.h1));
-      CK(cudaEventCreateWithFlags(&w.served, cudaEventDisableTiming));
-      CK(cudaEventCreateWithFlags(&w.host_ready, cudaEventDisableTiming));
-      CK(cudaEventRecord(w.served, serve_stream));
-    }
+    for (auto& w : slots) create_slot(w);
+    t_start = std::chrono::steady_clock::now();
     if (stream_files && !plan.empty()) reader = std::thread([this] { reader_main(); });
     if (const char* e = std::getenv("PCP_TIMELINE")) timeline_on = std::atoi(e) != 0;
     if (timeline_on) {
@@ -1106,9 +1106,20 @@ struct Pipeline {
       wb = (uint32_t)std::max<uint64_t>(1, (want + B - 1) / B);
     }
     const uint64_t W = (uint64_t)wb * B;
+    cur_wave_batches = wb;
     const uint64_t usable = g.drop_remainder ? (n / B) * B : n;
-    for (uint64_t e = 0; e < epochs; ++e)
-      for (uint64_t p = 0; p < usable; p += W) {
+    // (re)plan from the end of the waves already launched (live
+    // reconfiguration keeps the walk, the seeds and the batch boundaries)
+    uint64_t e0 = 0, p0 = 0;
+    if (next_plan > 0) {
+      e0 = plan[next_plan - 1].first;
+      p0 = plan[next_plan - 1].second + plan_n[next_plan - 1];
+      if (p0 >= usable) ++e0, p0 = 0;
+    }
+    plan.resize(next_plan);
+    plan_n.resize(next_plan);
+    for (uint64_t e = e0; e < epochs; ++e)
+      for (uint64_t p = e == e0 ? p0 : 0; p < usable; p += W) {
         plan.push_back({e, p});
         plan_n.push_back(std::min<uint64_t>(W, usable - p));
       }
@@ -1634,6 +1645,7 @@ struct Pipeline {
   // ---- iteration -------------------------------------------------------------
   int next_batch(pcp_batch* out, int* eos) {
     *eos = 0;
+    ++sink_polls;
     if (failed) fail(fail_code, fail_msg);
     if (cur < 0 || served >= slots[cur].n_batches) {
       const int ns = (int)slots.size();
@@ -1649,7 +1661,15 @@ struct Pipeline {
         CK(cudaEventRecord(slots[cur].served, serve_stream));
         slots[cur].launched = false;
       }
-      const int nxt = cur < 0 ? 0 : (cur + 1) % ns;
+      int nxt = cur < 0 ? 0 : (cur + 1) % ns;
+      if (has_pending && !slots[nxt].launched) {
+        bool busy = false;
+        for (const auto& w : slots) busy |= w.launched;
+        if (!busy) {  // drained: apply (Pipeline::update_op_config, pipeline.cpp:691-732)
+          apply_config();
+          nxt = 0;
+        }
+      }
       Wave& wn = slots[nxt];
       if (!wn.launched) {
         if (next_plan >= plan.size()) {
@@ -1664,8 +1684,8 @@ struct Pipeline {
       // keep every slot busy while waiting: waves go to slots in ring order
       // on per-slot streams, so up to `slots` waves overlap (copies, LZ4
       // chains and k_cloud of different waves).  "serial": one wave at a time.
-      for (int d = 1; d < ns && next_plan < plan.size() && !serial; ++d) {
-        Wave& wp = slots[(nxt + d) % ns];
+      for (int d = 1; d < (int)slots.size() && next_plan < plan.size() && !serial && !has_pending; ++d) {
+        Wave& wp = slots[(nxt + d) % slots.size()];
         if (!wp.launched) {
           const auto t0 = clk::now();
           launch(wp, next_plan++);
@@ -1673,6 +1693,7 @@ struct Pipeline {
         }
       }
       const auto tw = clk::now();
+      if (cudaEventQuery(wn.done) == cudaErrorNotReady) ++sink_empty_polls;  // the consumer waits on the device
       CK(cudaEventSynchronize(wn.done));
       host_wait_ms += ms_since(tw);
       float ms = 0;
@@ -1773,7 +1794,93 @@ struct Pipeline {
     }
     ++served;
     ++batches;
+    items_emitted += nb;
     return kOk;
+  }
+
+  // ---- live reconfiguration (update_op_config) -----------------------------
+  // {"slots": s, "wave_batches": k}: applied at the next wave boundary once
+  // the waves in flight are served (content, order and seeds are independent
+  // of both knobs).  Not while streaming from files (the reader's plan).
+  void update_config(const std::string& text) {
+    json o = json::parse(text, nullptr, false);
+    if (o.is_discarded() || !o.is_object()) fail(kOutOfBounds, "config is not a JSON object");
+    for (auto it = o.begin(); it != o.end(); ++it)
+      if (it.key() != "slots" && it.key() != "wave_batches") fail(kUnknownOp, "knob '" + it.key() + "'");
+    if (o.contains("slots")) {
+      const int64_t v = o["slots"].get<int64_t>();
+      if (v < 2 || v > 8) fail(kOutOfBounds, "slots outside [2, 8]");
+    }
+    if (o.contains("wave_batches") && o["wave_batches"].get<int64_t>() < 1)
+      fail(kOutOfBounds, "wave_batches must be >= 1");
+    if (stream_files) fail(kOutOfBounds, "not reconfigurable while streaming pages from files");
+    for (auto it = o.begin(); it != o.end(); ++it) pending_cfg[it.key()] = it.value();
+    has_pending = true;
+  }
+
+  void apply_config() {
+    if (pending_cfg.contains("wave_batches")) {
+      wave_batches = pending_cfg["wave_batches"].get<uint32_t>();
+      plan_waves();
+    }
+    if (pending_cfg.contains("slots")) {
+      const size_t want = pending_cfg["slots"].get<size_t>();
+      CK(cudaStreamSynchronize(serve_stream));
+      while (slots.size() > want) {
+        destroy_slot(slots.back());
+        slots.pop_back();
+      }
+      const size_t have = slots.size();
+      slots.resize(want);
+      for (size_t k = have; k < want; ++k) create_slot(slots[k]);
+      n_slots = (uint32_t)want;
+    }
+    pending_cfg = json::object();
+    has_pending = false;
+    ++reconfigs;
+  }
+
+  // Pipeline::metrics (pipeline.hpp:140-149, pipeline.cpp:734-766) for the
+  // device stage: the map nodes run as one fused kernel stage per wave
+  // (busy = its device time), the source node is page CRC + decode, the sink
+  // is the served wave; an "empty poll" is a next_batch that had to wait for
+  // the device (the data-side signal of detect_bottleneck).
+  const char* metrics() {
+    const double up = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+    json ops = json::array();
+    ops.push_back({{"op_id", g.source_id}, {"kind", "source"},
+                   {"num_workers", stream_files ? reader_threads : 1u}, {"items", clouds},
+                   {"busy_seconds", (crc_kernel_ms + decode_kernel_ms) * 1e-3},
+                   {"out_queue_size", 0}, {"out_queue_capacity", 0}});
+    std::vector<uint32_t> map_nodes;
+    for (const auto& m : g.maps)
+      if (map_nodes.empty() || map_nodes.back() != m.node_id) map_nodes.push_back(m.node_id);
+    const uint64_t in_flight = [&] {
+      uint64_t k = 0;
+      for (const auto& w : slots) k += w.launched ? 1 : 0;
+      return k;
+    }();
+    for (uint32_t id : map_nodes)
+      ops.push_back({{"op_id", id}, {"kind", "map"}, {"num_workers", (uint64_t)slots.size()}, {"items", clouds},
+                     {"busy_seconds", (cloud_kernel_ms + vx_kernel_ms) * 1e-3 / map_nodes.size()},
+                     {"out_queue_size", in_flight}, {"out_queue_capacity", (uint64_t)slots.size()}});
+    const uint64_t ready = (cur >= 0 && served < slots[cur].n_batches) ? slots[cur].n_batches - served : 0;
+    ops.push_back({{"op_id", g.batch_id}, {"kind", "batch"}, {"num_workers", 1}, {"items", items_emitted},
+                   {"busy_seconds", csr_kernel_ms * 1e-3}, {"out_queue_size", ready},
+                   {"out_queue_capacity", (uint64_t)slots.size() * cur_wave_batches}});
+    json m{{"uptime_seconds", up},
+           {"ops", ops},
+           {"sink_polls", sink_polls},
+           {"sink_empty_polls", sink_empty_polls},
+           {"sink_size", ready},
+           {"sink_capacity", (uint64_t)slots.size() * cur_wave_batches},
+           {"batches_emitted", batches},
+           {"items_emitted", items_emitted},
+           {"slots", (uint64_t)slots.size()},
+           {"wave_batches", cur_wave_batches},
+           {"reconfigs", reconfigs}};
+    metrics_json = m.dump();
+    return metrics_json.c_str();
   }
 
   const char* stats() {
@@ -2085,6 +2192,12 @@ int pcp_pipeline_next_batch(pcp_pipeline* p, pcp_batch* out, int* eos) {
 void* pcp_pipeline_stream(pcp_pipeline* p) { return p->impl.serve_stream; }
 
 const char* pcp_pipeline_stats(pcp_pipeline* p) { return p->impl.stats(); }
+
+const char* pcp_pipeline_metrics(pcp_pipeline* p) { return p->impl.metrics(); }
+
+int pcp_pipeline_update_config(pcp_pipeline* p, const char* config_json) {
+  return guarded([&] { p->impl.update_config(config_json ? config_json : ""); });
+}
 
 void pcp_pipeline_close(pcp_pipeline* p) { delete p; }
 
