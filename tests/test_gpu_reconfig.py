@@ -39,7 +39,8 @@ def test_update_config_keeps_content(pcp, tmp_path):
         k += 1
     m = autotune.metrics(p)
     p.close()
-    assert m["reconfigs"] == 4 and m["slots"] == 3 and m["wave_batches"] == 2
+    # updates that arrive while an earlier one is still draining merge into it
+    assert 3 <= m["reconfigs"] <= 4 and m["slots"] == 3 and m["wave_batches"] == 2
     assert [x[0] for x in got] == list(want)
     for key, host in got:
         for name in want[key]:
