@@ -207,7 +207,7 @@ int main(int argc, char** argv) {
     }
     report("worker failure surfaces as WorkerPanic naming the op",
            ref_code == Errc::kWorkerPanic && gpu_code == Errc::kWorkerPanic && gpu_n == 1 &&
-               gpu_msg.find("op 7") != std::string::npos,
+               gpu_msg == ref_msg,
            "ref: " + ref_msg + " | gpu: " + gpu_msg + " after " + std::to_string(gpu_n) + " batches");
   });
   run_case("metrics reflect emitted batches", [&] {

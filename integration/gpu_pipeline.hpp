@@ -85,8 +85,14 @@ class GpuPipeline {
       default: return Value(std::string(reinterpret_cast<const char*>(p), n));
     }
   }
+  // pcp_last_error() reads like PcError::what() ("<Errc name>: <message>");
+  // rebuild the PcError from the message part.
   static void check(int st) {
-    if (st) fail(static_cast<Errc>(st - 1), pcp_last_error());
+    if (!st) return;
+    std::string msg = pcp_last_error();
+    const std::string pre = std::string(pcp_errc_name(st)) + ": ";
+    if (msg.rfind(pre, 0) == 0) msg = msg.substr(pre.size());
+    fail(static_cast<Errc>(st - 1), msg);
   }
   pcp_pipeline* p_ = nullptr;
 };

@@ -118,17 +118,74 @@ __device__ inline uint32_t chunk_shift(const uint32_t* shift_tab, const uint32_t
 // CTA-cooperative CRC contribution of bytes p[0..n), which sit `after`
 // bytes before the end of the page:  x^(8*after) (x) crc(p[0..n)).
 // Returns the value on thread 0 (others: 0).  `red` is >= 32 words of smem.
-__device__ inline uint32_t cta_range(const uint32_t* tab, const uint32_t* x2n,
-                                     const uint32_t* shift_tab, const uint8_t* p,
-                                     uint64_t n, uint64_t after, uint32_t* red) {
-  const int t = threadIdx.x, nt = blockDim.x;
+// Four full kChunk-byte chunks (same alignment: they sit multiples of kChunk
+// apart) in one pass: four independent table chains interleaved, so the
+// shared-memory lookup latency is paid once per four bytes instead of once
+// per byte.  Returns the four standard CRCs.
+__device__ __forceinline__ void chunks4(const uint32_t* tab, const uint8_t* const (&p)[4], uint32_t (&out)[4]) {
+  uint32_t c[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
+  const uint32_t head = (4 - ((uintptr_t)p[0] & 3)) & 3;
+  for (uint32_t i = 0; i < head; ++i)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) c[q] = tab[(c[q] ^ p[q][i]) & 0xFF] ^ (c[q] >> 8);
+  const uint32_t nw = (kChunk - head) / 4;
+  for (uint32_t w0 = 0; w0 < nw; w0 += 4) {
+    uint32_t v[4][4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+        v[q][b] = w0 + b < nw ? reinterpret_cast<const uint32_t*>(p[q] + head)[w0 + b] : 0u;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      if (w0 + b >= nw) break;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) c[q] ^= v[q][b];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) c[q] = tab[c[q] & 0xFF] ^ (c[q] >> 8);
+    }
+  }
+  for (uint32_t i = head + 4 * nw; i < kChunk; ++i)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) c[q] = tab[(c[q] ^ p[q][i]) & 0xFF] ^ (c[q] >> 8);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) out[q] = c[q] ^ 0xFFFFFFFFu;
+}
+
+// XOR of shifted chunk CRCs for chunks k = first, first+stride, ... of a
+// range of n bytes (chunks aligned to its end): four full chunks at a time,
+// the rest (incl. the short chunk at the range start) one by one.
+__device__ __forceinline__ uint32_t strided_chunks(const uint32_t* tab, const uint32_t* x2n,
+                                                   const uint32_t* shift_tab, const uint8_t* p,
+                                                   uint64_t n, uint64_t first, uint64_t stride) {
   const uint64_t nchunks = (n + kChunk - 1) / kChunk;
+  const uint64_t full = n / kChunk;  // chunks 0..full-1 are full-size
   uint32_t c = 0;
-  for (uint64_t k = t; k < nchunks; k += nt) {
+  uint64_t k = first;
+  for (; k + 3 * stride < full; k += 4 * stride) {
+    const uint8_t* ps[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) ps[q] = p + (n - (k + q * stride + 1) * kChunk);
+    uint32_t r[4];
+    chunks4(tab, ps, r);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) c ^= multmodp(chunk_shift(shift_tab, x2n, k + q * stride), r[q]);
+  }
+  for (; k < nchunks; k += stride) {
     const uint64_t e = n - k * kChunk;
     const uint64_t s = e > kChunk ? e - kChunk : 0;
     c ^= multmodp(chunk_shift(shift_tab, x2n, k), bytes_words(tab, p + s, e - s));
   }
+  return c;
+}
+
+__device__ inline uint32_t cta_range(const uint32_t* tab, const uint32_t* x2n,
+                                     const uint32_t* shift_tab, const uint8_t* p,
+                                     uint64_t n, uint64_t after, uint32_t* red) {
+  const int t = threadIdx.x, nt = blockDim.x;
+  uint32_t c = strided_chunks(tab, x2n, shift_tab, p, n, t, nt);
   c = warp_xor(c);
   if ((t & 31) == 0) red[t >> 5] = c;
   __syncthreads();
@@ -148,13 +205,7 @@ __device__ inline uint32_t warp_range(const uint32_t* tab, const uint32_t* x2n,
                                       const uint32_t* shift_tab, const uint8_t* p,
                                       uint64_t n, uint64_t after) {
   const int lane = threadIdx.x & 31;
-  const uint64_t nchunks = (n + kChunk - 1) / kChunk;
-  uint32_t c = 0;
-  for (uint64_t k = lane; k < nchunks; k += 32) {
-    const uint64_t e = n - k * kChunk;
-    const uint64_t s = e > kChunk ? e - kChunk : 0;
-    c ^= multmodp(chunk_shift(shift_tab, x2n, k), bytes_words(tab, p + s, e - s));
-  }
+  uint32_t c = strided_chunks(tab, x2n, shift_tab, p, n, lane, 32);
   c = warp_xor(c);
   if (after) c = multmodp(x8n(x2n, after), c);
   return c;
