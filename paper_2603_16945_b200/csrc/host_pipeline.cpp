@@ -464,6 +464,7 @@ struct Wave {
   DevBuf handoff;  // chain split: the clouds between launches (decoded clouds A for the vx stage)
   DevBuf handoff_b;  // vx stage output (voxelized clouds B)
   DevBuf vx_cl, vx_tiles, vx_cnt, vx_w0, vx_w1;  // vx stage scratch
+  DevBuf vx_bt, vx_bcnt, vx_boff, vx_items, vx_T;  // vx bucket mode
   cudaEvent_t v0 = nullptr, v1 = nullptr;        // vx stage
   DevBuf mt_pre;   // pre-seeded MT19937-64 states [n][n_rng][312] (k_seed_states)
   uint32_t n_todo = 0;
@@ -569,6 +570,7 @@ struct Pipeline {
   // with [range_crop,] voxel; option "vx": false keeps it in k_cloud
   bool vx_allowed = false, vx_on = false;  // default off until it beats the one-CTA path
   uint64_t vx_min_points = 32768;
+  bool vx_msd = true;  // option "vx_buckets": bucket mode of the vx stage
   VxArgs vx_proto{};
   double vx_kernel_ms = 0;
   uint64_t vx_alg_bytes = 0;
@@ -648,6 +650,7 @@ struct Pipeline {
       if (stream_files) resident = false;
       vx_allowed = o.value("vx", vx_allowed);
       vx_min_points = o.value("vx_min_points", vx_min_points);
+      vx_msd = o.value("vx_buckets", vx_msd);
     }
     if (src_header) {  // pages come from the caller: header bytes only, no files
       h = parse_header_bytes(src_header->data(), src_header->size());
@@ -1412,10 +1415,17 @@ struct Pipeline {
     // fields; ragged ones grow it on demand past 1 GiB)
     if (host_batches) w.h_out.ensure(std::min<uint64_t>(out_total + 64, 1ull << 30));
     if (proto.split_at || vx_on) w.handoff.ensure(proto.handoff_stride * w.n);
-    uint64_t vx_tiles_bound = 0;
+    uint64_t vx_tiles_bound = 0, vx_btiles_bound = 0, vx_max_items = 0;
     if (vx_on) {
       const uint64_t T = voxel_wave_tile_points();
       vx_tiles_bound = w.n * ((proto.cap_points + T - 1) / T);
+      vx_btiles_bound = w.n * ((proto.cap_points + kVxBTile - 1) / kVxBTile);
+      vx_max_items = proto.cap_points / (kVxItemCap / 2) + 2;
+      w.vx_bt.ensure(16 + 4 * vx_btiles_bound);
+      w.vx_bcnt.ensure(4ull * kVxBuckets * vx_btiles_bound);
+      w.vx_boff.ensure(4ull * (kVxBuckets + 1) * w.n);
+      w.vx_items.ensure(4ull * vx_max_items * w.n);
+      w.vx_T.ensure(proto.handoff_stride * w.n);
       w.handoff_b.ensure(proto.handoff_stride * w.n);
       w.vx_cl.ensure(sizeof(VxCloud) * w.n);
       w.vx_tiles.ensure(16 + 3 * 4 * vx_tiles_bound);
@@ -1507,6 +1517,14 @@ struct Pipeline {
       vx.cnt = w.vx_cnt.as<uint32_t>();
       vx.w0 = w.vx_w0.as<uint64_t>();
       vx.w1 = w.vx_w1.as<uint64_t>();
+      vx.total_btiles = w.vx_bt.as<uint32_t>();
+      vx.btile_cloud = vx.total_btiles + 4;
+      vx.bcnt = w.vx_bcnt.as<uint32_t>();
+      vx.boff = w.vx_boff.as<uint32_t>();
+      vx.item_v = w.vx_items.as<uint32_t>();
+      vx.max_items = (uint32_t)vx_max_items;
+      vx.T = w.vx_T.as<uint8_t>();
+      vx.msd_enabled = vx_msd ? 1 : 0;
       vx.sample_status = a.sample_status;
       vx.sample_op = a.sample_op;
       vx.sample_where = a.sample_where;
@@ -1540,9 +1558,9 @@ struct Pipeline {
     w.decode_alg_bytes = 0;
     for (uint32_t pi : todo) w.decode_alg_bytes += pages[pi].pay_len + pages[pi].raw_len;
     CK(launch_wave(a, grid, grid_pre, threads, smem, w.stream, w.k0, w.k1, vx_on ? &vx : nullptr,
-                   (uint32_t)vx_tiles_bound, sms, w.v0, w.v1, w.handoff.as<uint8_t>()));
+                   (uint32_t)vx_tiles_bound, (uint32_t)vx_btiles_bound, sms, w.v0, w.v1, w.handoff.as<uint8_t>()));
     launches += (wins.empty() ? 0 : 1) + (todo.empty() ? 0 : 2) + (ng ? 1 : 0) + (proto.n_rng ? 1 : 0) + 1 + 1 + 1 +
-                (vx_on ? 2 + 7 + 3 * kVxMaxPasses : 0) + (proto.split_at ? 1 : 0);
+                (vx_on ? 2 + 14 + 3 * kVxMaxPasses : 0) + (proto.split_at ? 1 : 0);
     if (vx_on) {
       uint64_t per_pt = 0;
       for (int f = 0; f < proto.n_bytes_fields; ++f)

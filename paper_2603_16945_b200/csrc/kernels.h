@@ -37,8 +37,8 @@ uint64_t lz4_scratch_bytes(uint64_t pay);  // per LZ4 page
 // launch into handoff_a and the rest of the chain.
 struct VxArgs;
 cudaError_t launch_wave(const WaveArgs& a, int grid, int grid_pre, int threads, size_t smem, cudaStream_t st,
-                        cudaEvent_t k0, cudaEvent_t k1, const VxArgs* vx, uint32_t vx_tiles, int sms,
-                        cudaEvent_t v0, cudaEvent_t v1, uint8_t* handoff_a);
+                        cudaEvent_t k0, cudaEvent_t k1, const VxArgs* vx, uint32_t vx_tiles,
+                        uint32_t vx_btiles, int sms, cudaEvent_t v0, cudaEvent_t v1, uint8_t* handoff_a);
 cudaError_t occupancy_cloud(int* n, int threads, size_t smem, int min_blocks);
 // Max co-resident clusters of `cluster` CTAs (k_cloud<1>, or k_apply_set).
 cudaError_t occupancy_cloud_clusters(int* n, int threads, size_t smem, uint32_t cluster, bool apply);

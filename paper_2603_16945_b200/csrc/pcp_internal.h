@@ -151,6 +151,14 @@ struct VxCloud {
   uint32_t kb, ib;     // key bits, point-index bits (word = key << ib | index)
   uint32_t passes;     // 8-bit radix passes
   uint32_t V;          // voxels
+  // bucket (MSD) mode: stable scatter by the top key bits into buckets,
+  // then every work item (whole buckets, <= kVxItemCap records) is sorted,
+  // segmented and reduced in shared memory
+  uint32_t msd;        // 1: bucket mode, 0: global LSD radix sort
+  uint32_t btile0, n_btiles;  // scatter tiles (kVxBTile points)
+  uint32_t bb, lowbits;       // bucket bits (<= 12), key bits below the bucket
+  uint32_t n_items;           // work items
+  uint32_t max_bucket;        // records in the largest bucket
   uint32_t hist[8][256];  // digit histogram per pass (whole cloud)
 };
 

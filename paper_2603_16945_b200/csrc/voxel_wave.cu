@@ -33,6 +33,7 @@
 #include <algorithm>
 #include <cstdint>
 
+#include "device_sort.cuh"
 #include "device_util.cuh"
 #include "voxel_wave.h"
 
@@ -105,10 +106,11 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t x, uint32_t* sh, ui
 // ---------------------------------------------------------------- prep
 __global__ void __launch_bounds__(1024) k_vx_prep(VxArgs v) {
   __shared__ uint32_t wsum[33];
-  __shared__ uint32_t carry_t;
+  __shared__ uint32_t carry_t, carry_b;
   __shared__ unsigned long long carry_w;
   if (threadIdx.x == 0) {
     carry_t = 0;
+    carry_b = 0;
     carry_w = 0;
   }
   __syncthreads();
@@ -171,19 +173,41 @@ __global__ void __launch_bounds__(1024) k_vx_prep(VxArgs v) {
     }
     __syncthreads();
     const uint64_t p0 = carry_w + wsum[w] + pi - n;
+    __syncthreads();
+    const uint32_t btiles = (n + kVxBTile - 1) / kVxBTile;
+    const uint32_t bi = warp_incl_scan(btiles);
+    if (lane == 31) wsum[w] = bi;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t acc = 0;
+      for (uint32_t k = 0; k < nw; ++k) {
+        const uint32_t c = wsum[k];
+        wsum[k] = acc;
+        acc += c;
+      }
+    }
+    __syncthreads();
+    const uint32_t bt0 = carry_b + wsum[w] + bi - btiles;
     if (s < v.n_samples) {
       v.cl[s].tile0 = t0;
       v.cl[s].word0 = p0;
+      v.cl[s].btile0 = bt0;
+      v.cl[s].n_btiles = btiles;
       for (uint32_t k = 0; k < tiles; ++k) v.tile_cloud[t0 + k] = s;
+      for (uint32_t k = 0; k < btiles; ++k) v.btile_cloud[bt0 + k] = s;
     }
     __syncthreads();
     if (threadIdx.x == blockDim.x - 1) {
       carry_t = t0 + tiles;
+      carry_b = bt0 + btiles;
       carry_w = p0 + n;
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) *v.total_tiles = carry_t;
+  if (threadIdx.x == 0) {
+    *v.total_tiles = carry_t;
+    *v.total_btiles = carry_b;
+  }
 }
 
 // ---------------------------------------------------------------- bounds
@@ -311,10 +335,8 @@ __global__ void __launch_bounds__(kThreads) k_vx_plan(VxArgs v) {
   c.kb = kb;
   c.ib = ib;
   c.passes = (kb + 7) / 8;
-  if (kb + ib > 64 || c.passes > kVxMaxPasses) {  // k_cloud's op_voxel handles it
-    c.fallback = 1;
-    c.active = 0;
-  }
+  c.bb = kb < 12 ? kb : 12;
+  c.lowbits = kb - c.bb;
 }
 
 // ---------------------------------------------------------------- keys
@@ -325,7 +347,7 @@ __global__ void __launch_bounds__(kThreads) k_vx_keys(VxArgs v) {
   for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
     const uint32_t s = v.tile_cloud[t];
     const VxCloud& c = v.cl[s];
-    if (!c.active) continue;  // uniform
+    if (!c.active || c.msd) continue;  // uniform (bucket-mode clouds skip the LSD path)
     for (uint32_t k = threadIdx.x; k < c.passes * 256; k += kThreads) (&hist[0][0])[k] = 0;
     const float* d = reinterpret_cast<const float*>(slot(v, v.A, s) + v.off[v.role_data]);
     const uint32_t i0 = (t - c.tile0) * kTile + threadIdx.x * kItems;  // thread-contiguous: order-preserving scan
@@ -372,7 +394,7 @@ __device__ __forceinline__ bool sort_tile(const VxArgs& v, uint32_t t, int pass,
                                           uint32_t& j, uint32_t& n_w) {
   s = v.tile_cloud[t];
   const VxCloud& c = v.cl[s];
-  if (!c.active || (pass >= 0 && (uint32_t)pass >= c.passes)) return false;
+  if (!c.active || c.msd || (pass >= 0 && (uint32_t)pass >= c.passes)) return false;
   j = t - c.tile0;
   const uint32_t w0 = j * kTile;
   if (w0 >= c.kept) return false;
@@ -412,7 +434,7 @@ __global__ void __launch_bounds__(kThreads) k_vx_upsweep(VxArgs v, uint32_t pass
 __global__ void __launch_bounds__(1024) k_vx_colscan(VxArgs v, uint32_t pass) {
   const uint32_t s = blockIdx.x;
   const VxCloud& c = v.cl[s];
-  if (!c.active || pass >= c.passes) return;
+  if (!c.active || c.msd || pass >= c.passes) return;
   const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t d = blockIdx.y * 32 + w;
   // digit base: cloud-wide count of smaller digits
@@ -527,7 +549,7 @@ __global__ void __launch_bounds__(kThreads) k_vx_segscan(VxArgs v) {
   __shared__ uint32_t carry;
   const uint32_t s = blockIdx.x;
   VxCloud& c = v.cl[s];
-  if (!c.active) return;
+  if (!c.active || c.msd) return;
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
   const uint32_t tiles = (c.kept + kTile - 1) / kTile;
@@ -686,6 +708,378 @@ __global__ void __launch_bounds__(kThreads) k_vx_means(VxArgs v) {
   }
 }
 
+// ---------------------------------------------------------------- bucket mode
+__device__ __forceinline__ uint64_t point_key(const VxArgs& v, const VxCloud& c, float x, float y, float z) {
+  const float p[3] = {x, y, z};
+  uint64_t key = 0;
+  uint32_t sh_bits = 0;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    key |= (uint64_t)((uint32_t)qkey(p[a], c.o[a], v.voxel) - c.q0[a]) << sh_bits;
+    sh_bits += c.bx[a];
+  }
+  return key;
+}
+
+// Per scatter tile (kVxBTile points): bucket histogram of the kept points.
+__global__ void __launch_bounds__(kThreads) k_vx_bhist(VxArgs v) {
+  __shared__ uint32_t h[kVxBuckets];
+  const uint32_t total = *v.total_btiles;
+  for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
+    const uint32_t s = v.btile_cloud[t];
+    const VxCloud& c = v.cl[s];
+    if (!c.active) continue;  // uniform
+    const uint32_t nb = 1u << c.bb;
+    for (uint32_t k = threadIdx.x; k < nb; k += kThreads) h[k] = 0;
+    __syncthreads();
+    const float* d = reinterpret_cast<const float*>(slot(v, v.A, s) + v.off[v.role_data]);
+    const uint32_t i0 = (t - c.btile0) * kVxBTile;
+    const uint32_t i1 = min(c.n, i0 + kVxBTile);
+    for (uint32_t i = i0 + threadIdx.x; i < i1; i += kThreads) {
+      const float x = d[3ull * i], y = d[3ull * i + 1], z = d[3ull * i + 2];
+      if (in_box(v, x, y, z)) atomicAdd(&h[point_key(v, c, x, y, z) >> c.lowbits], 1u);
+    }
+    __syncthreads();
+    uint32_t* out = v.bcnt + (uint64_t)t * kVxBuckets;
+    for (uint32_t k = threadIdx.x; k < nb; k += kThreads) out[k] = h[k];
+    __syncthreads();
+  }
+}
+
+// grid (n_samples, kVxBuckets / 32), warp per bucket: exclusive scan of the
+// bucket's tile counts over the cloud's scatter tiles; totals to boff.
+__global__ void __launch_bounds__(1024) k_vx_bcol(VxArgs v) {
+  const uint32_t s = blockIdx.x;
+  const VxCloud& c = v.cl[s];
+  if (!c.active) return;
+  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t b = blockIdx.y * 32 + w;
+  if (b >= (1u << c.bb)) return;
+  uint32_t carry = 0;
+  for (uint32_t j0 = 0; j0 < c.n_btiles; j0 += 32) {
+    const uint32_t j = j0 + lane;
+    uint32_t* p = v.bcnt + (uint64_t)(c.btile0 + j) * kVxBuckets + b;
+    const uint32_t x = j < c.n_btiles ? *p : 0;
+    const uint32_t inc = warp_incl_scan(x);
+    if (j < c.n_btiles) *p = carry + inc - x;
+    carry += __shfl_sync(0xffffffffu, inc, 31);
+  }
+  if (lane == 0) v.boff[(uint64_t)s * (kVxBuckets + 1) + b] = carry;
+}
+
+// Per cloud: bucket offsets (exclusive scan), the largest bucket, and the
+// mode: bucket mode when every work item fits shared memory and the item
+// sort word fits 64 bits, else the global LSD sort (whose packed word may in
+// turn not fit: then k_cloud's op_voxel runs the ops).
+__global__ void __launch_bounds__(1024) k_vx_bbase(VxArgs v) {
+  __shared__ uint32_t wsum[33];
+  __shared__ uint32_t wmax[32];
+  const uint32_t s = blockIdx.x;
+  VxCloud& c = v.cl[s];
+  if (!c.active) return;
+  const uint32_t nb = 1u << c.bb;
+  uint32_t* bo = v.boff + (uint64_t)s * (kVxBuckets + 1);
+  const uint32_t per = (nb + blockDim.x - 1) / blockDim.x;  // <= 4
+  uint32_t x[4] = {0, 0, 0, 0}, sum = 0, mx = 0;
+  for (uint32_t q = 0; q < per; ++q) {
+    const uint32_t b = threadIdx.x * per + q;
+    x[q] = b < nb ? bo[b] : 0;
+    sum += x[q];
+    mx = max(mx, x[q]);
+  }
+  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t inc = warp_incl_scan(sum);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 31) wsum[w] = inc;
+  if (lane == 0) wmax[w] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t acc = 0, m = 0;
+    for (uint32_t k = 0; k < blockDim.x / 32; ++k) {
+      const uint32_t cw = wsum[k];
+      wsum[k] = acc;
+      acc += cw;
+      m = max(m, wmax[k]);
+    }
+    wsum[32] = acc;
+    wmax[0] = m;
+  }
+  __syncthreads();
+  uint32_t run = wsum[w] + inc - sum;
+  for (uint32_t q = 0; q < per; ++q) {
+    const uint32_t b = threadIdx.x * per + q;
+    if (b < nb) bo[b] = run;
+    run += x[q];
+  }
+  if (threadIdx.x == 0) {
+    bo[nb] = wsum[32];  // == kept
+    c.max_bucket = wmax[0];
+    const bool fits = v.msd_enabled && c.max_bucket <= kVxItemCap / 2 && 13 + c.lowbits + c.bb <= 64;
+    c.msd = fits ? 1u : 0u;
+    c.n_items = fits ? c.kept / (kVxItemCap / 2) + 1 : 0;
+    if (!fits && (c.kb + c.ib > 64 || c.passes > kVxMaxPasses)) {  // k_cloud's op_voxel handles it
+      c.fallback = 1;
+      c.active = 0;
+    }
+  }
+}
+
+// Stable scatter of a tile's kept points into their buckets: the tile's
+// (bucket, position) words are sorted in shared memory (stable radix sort),
+// so each bucket's records are written as one contiguous run at
+// bucket offset + tile base, in point order.  Records: the key (w0) and the
+// payload of every moved field (B, same layout as A).
+__global__ void __launch_bounds__(kThreads) k_vx_bscatter(VxArgs v) {
+  extern __shared__ __align__(16) uint8_t dyn[];
+  uint64_t* sw0 = reinterpret_cast<uint64_t*>(dyn);
+  uint64_t* sw1 = sw0 + kVxBTile;
+  uint32_t* h = reinterpret_cast<uint32_t*>(sw1 + kVxBTile);  // [kVxBuckets + 1]
+  uint32_t* scr = h + kVxBuckets + 32;
+  __shared__ uint32_t sh[kWarps + 1];
+  const uint32_t total = *v.total_btiles;
+  for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
+    const uint32_t s = v.btile_cloud[t];
+    const VxCloud& c = v.cl[s];
+    if (!c.active || !c.msd) continue;  // uniform
+    const uint32_t nb = 1u << c.bb;
+    const float* d = reinterpret_cast<const float*>(slot(v, v.A, s) + v.off[v.role_data]);
+    const uint32_t i0 = (t - c.btile0) * kVxBTile;
+    const uint32_t m = min(c.n, i0 + kVxBTile) - i0;
+    (void)nb;
+    for (uint32_t k = threadIdx.x; k < kVxBuckets; k += kThreads) h[k] = 0;
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < m; j += kThreads) {
+      const uint32_t i = i0 + j;
+      const float x = d[3ull * i], y = d[3ull * i + 1], z = d[3ull * i + 2];
+      uint64_t b = kVxBuckets;  // dropped by the crop: sorts last
+      if (in_box(v, x, y, z)) {
+        b = point_key(v, c, x, y, z) >> c.lowbits;
+        atomicAdd(&h[b], 1u);
+      }
+      sw0[j] = (b << 13) | j;
+    }
+    __syncthreads();
+    // tile-local bucket starts (exclusive scan of h, 16 buckets per thread)
+    {
+      constexpr uint32_t per = kVxBuckets / kThreads;
+      uint32_t x[per], sum = 0;
+#pragma unroll
+      for (uint32_t q = 0; q < per; ++q) {
+        x[q] = h[threadIdx.x * per + q];
+        sum += x[q];
+      }
+      uint32_t tot;
+      uint32_t run = block_excl_scan(sum, sh, &tot);
+#pragma unroll
+      for (uint32_t q = 0; q < per; ++q) {
+        h[threadIdx.x * per + q] = run;
+        run += x[q];
+      }
+      if (threadIdx.x == 0) h[kVxBuckets] = tot;
+    }
+    const int r = radix_sort8<4>(sw0, sw1, m, 13, 26, scr);
+    const uint64_t* sorted_w = r ? sw1 : sw0;
+    __syncthreads();
+    const uint32_t kept = h[kVxBuckets];
+    const uint32_t* bo = v.boff + (uint64_t)s * (kVxBuckets + 1);
+    const uint32_t* tb = v.bcnt + (uint64_t)t * kVxBuckets;
+    const uint8_t* A = slot(v, v.A, s);
+    uint8_t* B = v.B + (uint64_t)s * v.stride;
+    const uint32_t* ha = hdr(v, v.A, s);
+    const uint32_t moved = v.mm & ha[1];
+    for (uint32_t j = threadIdx.x; j < kept; j += kThreads) {
+      const uint64_t wj = sorted_w[j];
+      const uint32_t b = (uint32_t)(wj >> 13), li = (uint32_t)(wj & 8191u);
+      const uint32_t pos = bo[b] + tb[b] + (j - h[b]);
+      const uint32_t i = i0 + li;
+      const float x = d[3ull * i], y = d[3ull * i + 1], z = d[3ull * i + 2];
+      v.w0[c.word0 + pos] = point_key(v, c, x, y, z);
+      for (int f = 0; f < v.n_bytes_fields; ++f) {
+        if (!((moved >> f) & 1u)) continue;
+        const uint32_t es = ha[10 + f];
+        if ((es & 3u) == 0) {
+          const uint32_t* src = reinterpret_cast<const uint32_t*>(A + v.off[f]) + (uint64_t)i * (es >> 2);
+          uint32_t* dst = reinterpret_cast<uint32_t*>(B + v.off[f]) + (uint64_t)pos * (es >> 2);
+          for (uint32_t q = 0; q < (es >> 2); ++q) dst[q] = src[q];
+        } else {
+          for (uint32_t q = 0; q < es; ++q) B[v.off[f] + (uint64_t)pos * es + q] = A[v.off[f] + (uint64_t)i * es + q];
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Work item w of a cloud: the buckets whose offset falls in
+// [w * half, (w + 1) * half), at most kVxItemCap records.
+__device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t* a, uint32_t n, uint32_t x) {
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (a[mid] < x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ void item_range(const VxArgs& v, const VxCloud& c, uint32_t s, uint32_t w,
+                                           uint32_t& b0, uint32_t& r0, uint32_t& r1) {
+  constexpr uint32_t half = kVxItemCap / 2;
+  const uint32_t nb = 1u << c.bb;
+  const uint32_t* bo = v.boff + (uint64_t)s * (kVxBuckets + 1);
+  b0 = lower_bound_u32(bo, nb, w * half);
+  const uint32_t b1 = lower_bound_u32(bo, nb, (w + 1) * half);
+  r0 = b0 < nb ? bo[b0] : c.kept;
+  r1 = b1 < nb ? bo[b1] : c.kept;
+}
+
+// grid (max_items, n_samples): sort the item's records by key in shared
+// memory (stable: ties keep point order), find the voxels, and reduce each
+// voxel's run sequentially in double (App. C means) into T at r0 + voxel.
+__global__ void __launch_bounds__(kThreads) k_vx_item(VxArgs v) {
+  extern __shared__ __align__(16) uint8_t dyn[];
+  uint64_t* sw0 = reinterpret_cast<uint64_t*>(dyn);
+  uint64_t* sw1 = sw0 + kVxItemCap;
+  uint32_t* scr = reinterpret_cast<uint32_t*>(sw1 + kVxItemCap);
+  __shared__ uint32_t sh[kWarps + 1];
+  __shared__ unsigned long long red[32];
+  const uint32_t s = blockIdx.y, w = blockIdx.x;
+  const VxCloud& c = v.cl[s];
+  if (!c.active || !c.msd || w >= c.n_items) return;
+  uint32_t b0, r0, r1;
+  item_range(v, c, s, w, b0, r0, r1);
+  const uint32_t m = r1 - r0;
+  uint32_t* iv = v.item_v + (uint64_t)s * v.max_items;
+  if (m == 0) {
+    if (threadIdx.x == 0) iv[w] = 0;
+    return;
+  }
+  const uint64_t kbase = (uint64_t)b0 << c.lowbits;
+  const uint64_t* K = v.w0 + c.word0 + r0;
+  unsigned long long kmax = 0;
+  for (uint32_t j = threadIdx.x; j < m; j += kThreads) {
+    const uint64_t rel = K[j] - kbase;
+    sw0[j] = (rel << 13) | j;
+    kmax = max(kmax, (unsigned long long)rel);
+  }
+  kmax = dev::block_reduce(kmax, dev::OpMax{}, 0ull, red);
+  const uint32_t relbits = kmax ? 64u - __clzll(kmax) : 0u;
+  const int r = relbits ? radix_sort8<4>(sw0, sw1, m, 13, 13 + relbits, scr) : 0;
+  const uint64_t* S = r ? sw1 : sw0;
+  uint32_t* seg = reinterpret_cast<uint32_t*>(r ? sw0 : sw1);  // the free buffer
+  __syncthreads();
+  // voxel starts, in order (thread-contiguous items for the block scan)
+  constexpr uint32_t per = kVxItemCap / kThreads;  // 32
+  uint32_t flags = 0;
+  const uint32_t j0 = threadIdx.x * per;
+  for (uint32_t q = 0; q < per; ++q) {
+    const uint32_t j = j0 + q;
+    if (j < m && (j == 0 || (S[j] >> 13) != (S[j - 1] >> 13))) flags |= 1u << q;
+  }
+  uint32_t V;
+  uint32_t vid = block_excl_scan(__popc(flags), sh, &V);
+  for (uint32_t q = 0; q < per; ++q)
+    if ((flags >> q) & 1u) seg[vid++] = j0 + q;
+  __syncthreads();
+  const uint8_t* B = v.B + (uint64_t)s * v.stride;
+  uint8_t* T = v.T + (uint64_t)s * v.stride;
+  const uint32_t* ha = hdr(v, v.A, s);
+  const uint32_t moved = v.mm & ha[1];
+  for (uint32_t vx = threadIdx.x; vx < V; vx += kThreads) {
+    const uint32_t s0 = seg[vx], s1 = vx + 1 < V ? seg[vx + 1] : m;
+    const double cnt = (double)(s1 - s0);
+    for (int f = 0; f < v.n_bytes_fields; ++f) {
+      if (!((moved >> f) & 1u)) continue;
+      const bool avg = f == v.role_data || f == v.role_normal || f == v.role_color || f == v.role_intensity;
+      const uint32_t es = ha[10 + f];
+      if (avg) {
+        const float* src = reinterpret_cast<const float*>(B + v.off[f]) + (uint64_t)r0 * (es / 4);
+        float* dst = reinterpret_cast<float*>(T + v.off[f]) + (uint64_t)(r0 + vx) * (es / 4);
+        if (es == 12) {
+          double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+          for (uint32_t k = s0; k < s1; ++k) {
+            const uint32_t p = (uint32_t)(S[k] & 8191u);
+            a0 = __dadd_rn(a0, (double)src[3 * p]);
+            a1 = __dadd_rn(a1, (double)src[3 * p + 1]);
+            a2 = __dadd_rn(a2, (double)src[3 * p + 2]);
+          }
+          dst[0] = __double2float_rn(__ddiv_rn(a0, cnt));
+          dst[1] = __double2float_rn(__ddiv_rn(a1, cnt));
+          dst[2] = __double2float_rn(__ddiv_rn(a2, cnt));
+        } else {
+          double a0 = 0.0;
+          for (uint32_t k = s0; k < s1; ++k) a0 = __dadd_rn(a0, (double)src[S[k] & 8191u]);
+          dst[0] = __double2float_rn(__ddiv_rn(a0, cnt));
+        }
+      } else {  // gathered extra field: the voxel's first point
+        const uint32_t p = (uint32_t)(S[s0] & 8191u);
+        const uint8_t* src = B + v.off[f] + (uint64_t)(r0 + p) * es;
+        uint8_t* dst = T + v.off[f] + (uint64_t)(r0 + vx) * es;
+        for (uint32_t q = 0; q < es; ++q) dst[q] = src[q];
+      }
+    }
+    if (v.counts) reinterpret_cast<int32_t*>(T + v.off[kMaxBytesFields])[r0 + vx] = (int32_t)(s1 - s0);
+  }
+  if (threadIdx.x == 0) iv[w] = V;
+}
+
+__global__ void __launch_bounds__(kThreads) k_vx_iscan(VxArgs v) {
+  __shared__ uint32_t sh[kWarps + 1];
+  __shared__ uint32_t carry;
+  const uint32_t s = blockIdx.x;
+  VxCloud& c = v.cl[s];
+  if (!c.active || !c.msd) return;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  uint32_t* iv = v.item_v + (uint64_t)s * v.max_items;
+  for (uint32_t j0 = 0; j0 < c.n_items; j0 += kThreads) {
+    const uint32_t j = j0 + threadIdx.x;
+    const uint32_t x = j < c.n_items ? iv[j] : 0;
+    uint32_t tot;
+    const uint32_t ex = block_excl_scan(x, sh, &tot);
+    if (j < c.n_items) iv[j] = carry + ex;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) c.V = carry;
+}
+
+// grid (max_items, n_samples): voxel results of item w from T[r0 ..] to A at
+// the item's voxel offset.
+__global__ void __launch_bounds__(kThreads) k_vx_compact(VxArgs v) {
+  const uint32_t s = blockIdx.y, w = blockIdx.x;
+  const VxCloud& c = v.cl[s];
+  if (!c.active || !c.msd || w >= c.n_items) return;
+  uint32_t b0, r0, r1;
+  item_range(v, c, s, w, b0, r0, r1);
+  const uint32_t* iv = v.item_v + (uint64_t)s * v.max_items;
+  const uint32_t vo = iv[w], vn = (w + 1 < c.n_items ? iv[w + 1] : c.V) - vo;
+  if (!vn) return;
+  const uint8_t* T = v.T + (uint64_t)s * v.stride;
+  uint8_t* A = v.A + (uint64_t)s * v.stride;
+  const uint32_t* ha = hdr(v, v.A, s);
+  const uint32_t moved = v.mm & ha[1];
+  for (int f = 0; f < v.n_bytes_fields; ++f) {
+    if (!((moved >> f) & 1u)) continue;
+    const uint32_t es = ha[10 + f];
+    if ((es & 3u) == 0) {
+      const uint32_t* src = reinterpret_cast<const uint32_t*>(T + v.off[f]) + (uint64_t)r0 * (es >> 2);
+      uint32_t* dst = reinterpret_cast<uint32_t*>(A + v.off[f]) + (uint64_t)vo * (es >> 2);
+      for (uint32_t k = threadIdx.x; k < vn * (es >> 2); k += kThreads) dst[k] = src[k];
+    } else {
+      for (uint32_t k = threadIdx.x; k < vn * es; k += kThreads)
+        A[v.off[f] + (uint64_t)vo * es + k] = T[v.off[f] + (uint64_t)r0 * es + k];
+    }
+  }
+  if (v.counts) {
+    const int32_t* src = reinterpret_cast<const int32_t*>(T + v.off[kMaxBytesFields]) + r0;
+    int32_t* dst = reinterpret_cast<int32_t*>(A + v.off[kMaxBytesFields]) + vo;
+    for (uint32_t k = threadIdx.x; k < vn; k += kThreads) dst[k] = src[k];
+  }
+}
+
 // ---------------------------------------------------------------- finish
 __global__ void k_vx_finish(VxArgs v) {
   const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
@@ -710,13 +1104,35 @@ __global__ void k_vx_finish(VxArgs v) {
 
 }  // namespace
 
-cudaError_t launch_voxel_wave(const VxArgs& v, uint32_t tiles_bound, int sms, cudaStream_t st) {
+constexpr size_t kBScatterSmem = 2 * 8 * kVxBTile + 4 * (kVxBuckets + 32) + kSortScratchBytes;
+constexpr size_t kItemSmem = 2 * 8 * kVxItemCap + kSortScratchBytes;
+
+size_t voxel_wave_item_smem() { return kItemSmem > kBScatterSmem ? kItemSmem : kBScatterSmem; }
+
+cudaError_t launch_voxel_wave(const VxArgs& v, uint32_t tiles_bound, uint32_t btiles_bound, int sms,
+                              cudaStream_t st) {
   if (!v.n_samples) return cudaSuccess;
+  static const bool attrs = [] {
+    cudaFuncSetAttribute(k_vx_bscatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBScatterSmem);
+    cudaFuncSetAttribute(k_vx_item, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kItemSmem);
+    return true;
+  }();
+  (void)attrs;
   cudaMemsetAsync(v.cl, 0, sizeof(VxCloud) * v.n_samples, st);
   k_vx_prep<<<1, 1024, 0, st>>>(v);
   const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(tiles_bound, (uint32_t)sms * 8));
+  const uint32_t bgrid = std::max<uint32_t>(1, std::min<uint32_t>(btiles_bound, (uint32_t)sms * 4));
   k_vx_bounds<<<grid, kThreads, 0, st>>>(v);
   k_vx_plan<<<v.n_samples, kThreads, 0, st>>>(v);
+  // bucket mode (decided per cloud by k_vx_bbase)
+  k_vx_bhist<<<bgrid, kThreads, 0, st>>>(v);
+  k_vx_bcol<<<dim3(v.n_samples, kVxBuckets / 32), 1024, 0, st>>>(v);
+  k_vx_bbase<<<v.n_samples, 1024, 0, st>>>(v);
+  k_vx_bscatter<<<std::min<uint32_t>(bgrid, (uint32_t)sms), kThreads, kBScatterSmem, st>>>(v);
+  k_vx_item<<<dim3(v.max_items, v.n_samples), kThreads, kItemSmem, st>>>(v);
+  k_vx_iscan<<<v.n_samples, kThreads, 0, st>>>(v);
+  k_vx_compact<<<dim3(v.max_items, v.n_samples), kThreads, 0, st>>>(v);
+  // global LSD mode (the other clouds)
   k_vx_keys<<<grid, kThreads, 0, st>>>(v);
   for (uint32_t p = 0; p < v.max_passes; ++p) {
     k_vx_upsweep<<<grid, kThreads, 0, st>>>(v, p);

@@ -10,6 +10,9 @@
 namespace pcp {
 
 constexpr uint32_t kVxMaxPasses = 6;  // 8-bit digits: keys up to 48 bits (wider: k_cloud fallback)
+constexpr uint32_t kVxBuckets = 4096;  // bucket mode: up to 12 top key bits
+constexpr uint32_t kVxBTile = 8192;    // bucket mode: points per scatter tile
+constexpr uint32_t kVxItemCap = 8192;  // bucket mode: records per work item (shared memory)
 
 // Arguments of the stage (by value).  A = decoded clouds (hand-off slots of
 // the decode-only k_cloud launch), voxelized in place by the stage (the rest
@@ -42,6 +45,15 @@ struct VxArgs {
   uint32_t* cnt;         // [tiles][256]
   uint64_t* w0;          // [points] sort words (ping)
   uint64_t* w1;          // (pong)
+  // bucket mode scratch
+  uint32_t* total_btiles;
+  uint32_t* btile_cloud;  // [btiles]
+  uint32_t* bcnt;         // [btiles][kVxBuckets]: tile counts -> tile write bases
+  uint32_t* boff;         // [n_samples][kVxBuckets + 1]: bucket offsets
+  uint32_t* item_v;       // [n_samples][max_items]: voxels per item -> voxel offsets
+  uint32_t max_items;
+  uint8_t* T;             // voxel results per item before compaction (slots like A)
+  int32_t msd_enabled;    // 0: every cloud takes the LSD path
   // statuses of failing clouds (the rest report from the last k_cloud launch)
   int32_t* sample_status;
   int32_t* sample_op;
@@ -50,7 +62,10 @@ struct VxArgs {
 
 // tiles_bound: an upper bound of the wave's tiles (sum over samples of
 // ceil(points / voxel_wave_tile_points())).
-cudaError_t launch_voxel_wave(const VxArgs& v, uint32_t tiles_bound, int sms, cudaStream_t st);
+cudaError_t launch_voxel_wave(const VxArgs& v, uint32_t tiles_bound, uint32_t btiles_bound, int sms,
+                              cudaStream_t st);
+// Dynamic shared memory of the bucket-mode item kernel (set once per device).
+size_t voxel_wave_item_smem();
 uint32_t voxel_wave_tile_points();
 
 }  // namespace pcp

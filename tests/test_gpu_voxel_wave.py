@@ -33,13 +33,14 @@ CHAINS = {
 }
 
 
+@pytest.mark.parametrize("buckets", [True, False], ids=["bucket_mode", "lsd_mode"])
 @pytest.mark.parametrize("name", list(CHAINS))
-def test_vx_stage_matches_oracle_and_cta_path(pcp, ref, orc, tmp_path, name):
+def test_vx_stage_matches_oracle_and_cta_path(pcp, ref, orc, tmp_path, name, buckets):
     from paper_2603_16945_b200 import synth
     gen, kw, n, group, chain = CHAINS[name]
     primary = _ds(pcp, tmp_path, gen, n, group, **kw)
     g = synth.graph(chain or synth.CHAINS[name], batch_size=2, drop_remainder=False)
-    p = pcp.Pipeline(primary, g, vx=True, vx_min_points=1)
+    p = pcp.Pipeline(primary, g, vx=True, vx_min_points=1, vx_buckets=buckets)
     assert p.stats()["vx"], "the multi-CTA voxel stage should take this chain"
     got = []
     for b in p:
@@ -49,6 +50,27 @@ def test_vx_stage_matches_oracle_and_cta_path(pcp, ref, orc, tmp_path, name):
     assert_batches_equal(got, want, float_fields=tolerant_fields(g))
     cta = pcp.run_pipeline(primary, g, vx=False)
     assert_batches_equal(got, cta)
+
+
+def test_vx_bucket_overflow_takes_lsd(pcp, ref, orc, tmp_path):
+    """Few wide voxels: buckets above the shared-memory item capacity send
+    the cloud to the global LSD sort; a mixed wave (one cloud of each kind)
+    is exact."""
+    rng = np.random.default_rng(11)
+    schema = {"fields": {"data": {"type": "bytes"}, "intensity": {"type": "bytes"},
+                         "label": {"type": "int32"}}}
+    samples = []
+    for i in range(4):
+        side = 1.0 if i % 2 == 0 else 40.0
+        p = rng.uniform(0, side, (40000, 3)).astype(np.float32)
+        samples.append({"data": p.reshape(-1).view(np.uint8),
+                        "intensity": rng.uniform(0, 1, 40000).astype(np.float32).view(np.uint8),
+                        "label": np.array([i], np.int32)})
+    primary = pcp.write_dataset(tmp_path, "ds", schema, samples, group_size=2)
+    from paper_2603_16945_b200 import synth
+    g = synth.graph([("voxel", {"voxel_size": 0.3}), "flip_yz"], batch_size=2)
+    got = pcp.run_pipeline(primary, g, vx=True, vx_min_points=1)
+    assert_batches_equal(got, expected_run(ref, orc, primary, g))
 
 
 def test_vx_fallback_wide_keys(pcp, ref, orc, tmp_path):
