@@ -632,6 +632,7 @@ struct Pipeline {
     sms = require_device(dev);
     device = dev;
     g = parse_graph(graph_json);
+    if (const char* e = std::getenv("PCP_VX")) vx_allowed = std::atoi(e) != 0;  // experiment switch
     if (!options.empty()) {
       json o = json::parse(options, nullptr, false);
       if (o.is_discarded()) fail(kOutOfBounds, "options are not valid JSON");

@@ -746,25 +746,29 @@ __global__ void __launch_bounds__(kThreads) k_vx_bhist(VxArgs v) {
   }
 }
 
-// grid (n_samples, kVxBuckets / 32), warp per bucket: exclusive scan of the
-// bucket's tile counts over the cloud's scatter tiles; totals to boff.
-__global__ void __launch_bounds__(1024) k_vx_bcol(VxArgs v) {
+// grid (n_samples, kVxBuckets / 256): thread per bucket (a warp reads 32
+// consecutive buckets of a tile row: coalesced), running exclusive sum down
+// the cloud's scatter tiles (8 rows loaded ahead); totals to boff.
+__global__ void __launch_bounds__(256) k_vx_bcol(VxArgs v) {
   const uint32_t s = blockIdx.x;
   const VxCloud& c = v.cl[s];
   if (!c.active) return;
-  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const uint32_t b = blockIdx.y * 32 + w;
+  const uint32_t b = blockIdx.y * 256 + threadIdx.x;
   if (b >= (1u << c.bb)) return;
+  uint32_t* col = v.bcnt + (uint64_t)c.btile0 * kVxBuckets + b;
   uint32_t carry = 0;
-  for (uint32_t j0 = 0; j0 < c.n_btiles; j0 += 32) {
-    const uint32_t j = j0 + lane;
-    uint32_t* p = v.bcnt + (uint64_t)(c.btile0 + j) * kVxBuckets + b;
-    const uint32_t x = j < c.n_btiles ? *p : 0;
-    const uint32_t inc = warp_incl_scan(x);
-    if (j < c.n_btiles) *p = carry + inc - x;
-    carry += __shfl_sync(0xffffffffu, inc, 31);
+  for (uint32_t j0 = 0; j0 < c.n_btiles; j0 += 8) {
+    uint32_t x[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) x[q] = j0 + q < c.n_btiles ? col[(uint64_t)(j0 + q) * kVxBuckets] : 0u;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (j0 + q < c.n_btiles) {
+        col[(uint64_t)(j0 + q) * kVxBuckets] = carry;
+        carry += x[q];
+      }
   }
-  if (lane == 0) v.boff[(uint64_t)s * (kVxBuckets + 1) + b] = carry;
+  v.boff[(uint64_t)s * (kVxBuckets + 1) + b] = carry;
 }
 
 // Per cloud: bucket offsets (exclusive scan), the largest bucket, and the
@@ -815,7 +819,8 @@ __global__ void __launch_bounds__(1024) k_vx_bbase(VxArgs v) {
   if (threadIdx.x == 0) {
     bo[nb] = wsum[32];  // == kept
     c.max_bucket = wmax[0];
-    const bool fits = v.msd_enabled && c.max_bucket <= kVxItemCap / 2 && 13 + c.lowbits + c.bb <= 64;
+    const uint32_t pb = c.kept > 1 ? 32u - __clz(c.kept - 1) : 1u;  // item position bits (worst case)
+    const bool fits = v.msd_enabled && (pb < 13 ? 13 : pb) + c.kb <= 64;
     c.msd = fits ? 1u : 0u;
     c.n_items = fits ? c.kept / (kVxItemCap / 2) + 1 : 0;
     if (!fits && (c.kb + c.ib > 64 || c.passes > kVxMaxPasses)) {  // k_cloud's op_voxel handles it
@@ -957,30 +962,34 @@ __global__ void __launch_bounds__(kThreads) k_vx_item(VxArgs v) {
   }
   const uint64_t kbase = (uint64_t)b0 << c.lowbits;
   const uint64_t* K = v.w0 + c.word0 + r0;
+  // an item above the shared-memory capacity (a dense bucket) sorts in
+  // global memory: its key range of w0 and w1 are the ping-pong buffers
+  const bool big = m > kVxItemCap;
+  const uint32_t pb = big ? 32u - __clz(m - 1) : 13u;  // position bits
+  uint64_t* a0 = big ? v.w1 + c.word0 + r0 : sw0;
+  uint64_t* a1 = big ? v.w0 + c.word0 + r0 : sw1;
   unsigned long long kmax = 0;
   for (uint32_t j = threadIdx.x; j < m; j += kThreads) {
     const uint64_t rel = K[j] - kbase;
-    sw0[j] = (rel << 13) | j;
+    a0[j] = (rel << pb) | j;
     kmax = max(kmax, (unsigned long long)rel);
   }
-  kmax = dev::block_reduce(kmax, dev::OpMax{}, 0ull, red);
+  kmax = dev::block_reduce(kmax, dev::OpMax{}, 0ull, red);  // (its barriers order the K reads before a1 writes)
   const uint32_t relbits = kmax ? 64u - __clzll(kmax) : 0u;
-  const int r = relbits ? radix_sort8<4>(sw0, sw1, m, 13, 13 + relbits, scr) : 0;
-  const uint64_t* S = r ? sw1 : sw0;
-  uint32_t* seg = reinterpret_cast<uint32_t*>(r ? sw0 : sw1);  // the free buffer
+  const int r = relbits ? radix_sort8<4>(a0, a1, m, pb, pb + relbits, scr) : 0;
+  const uint64_t* S = r ? a1 : a0;
+  uint32_t* seg = reinterpret_cast<uint32_t*>(r ? a0 : a1);  // the free buffer
+  const uint64_t pmask = (1ull << pb) - 1;
   __syncthreads();
-  // voxel starts, in order (thread-contiguous items for the block scan)
-  constexpr uint32_t per = kVxItemCap / kThreads;  // 32
-  uint32_t flags = 0;
-  const uint32_t j0 = threadIdx.x * per;
-  for (uint32_t q = 0; q < per; ++q) {
-    const uint32_t j = j0 + q;
-    if (j < m && (j == 0 || (S[j] >> 13) != (S[j - 1] >> 13))) flags |= 1u << q;
-  }
+  // voxel starts, numbered in order: thread-contiguous ranges, one block scan
+  const uint32_t per = (m + kThreads - 1) / kThreads;
+  const uint32_t ja = min(m, threadIdx.x * per), jb = min(m, ja + per);
+  uint32_t cnt = 0;
+  for (uint32_t j = ja; j < jb; ++j) cnt += (j == 0 || (S[j] >> pb) != (S[j - 1] >> pb)) ? 1u : 0u;
   uint32_t V;
-  uint32_t vid = block_excl_scan(__popc(flags), sh, &V);
-  for (uint32_t q = 0; q < per; ++q)
-    if ((flags >> q) & 1u) seg[vid++] = j0 + q;
+  uint32_t vid = block_excl_scan(cnt, sh, &V);
+  for (uint32_t j = ja; j < jb; ++j)
+    if (j == 0 || (S[j] >> pb) != (S[j - 1] >> pb)) seg[vid++] = j;
   __syncthreads();
   const uint8_t* B = v.B + (uint64_t)s * v.stride;
   uint8_t* T = v.T + (uint64_t)s * v.stride;
@@ -999,7 +1008,7 @@ __global__ void __launch_bounds__(kThreads) k_vx_item(VxArgs v) {
         if (es == 12) {
           double a0 = 0.0, a1 = 0.0, a2 = 0.0;
           for (uint32_t k = s0; k < s1; ++k) {
-            const uint32_t p = (uint32_t)(S[k] & 8191u);
+            const uint32_t p = (uint32_t)(S[k] & pmask);
             a0 = __dadd_rn(a0, (double)src[3 * p]);
             a1 = __dadd_rn(a1, (double)src[3 * p + 1]);
             a2 = __dadd_rn(a2, (double)src[3 * p + 2]);
@@ -1009,11 +1018,11 @@ __global__ void __launch_bounds__(kThreads) k_vx_item(VxArgs v) {
           dst[2] = __double2float_rn(__ddiv_rn(a2, cnt));
         } else {
           double a0 = 0.0;
-          for (uint32_t k = s0; k < s1; ++k) a0 = __dadd_rn(a0, (double)src[S[k] & 8191u]);
+          for (uint32_t k = s0; k < s1; ++k) a0 = __dadd_rn(a0, (double)src[S[k] & pmask]);
           dst[0] = __double2float_rn(__ddiv_rn(a0, cnt));
         }
       } else {  // gathered extra field: the voxel's first point
-        const uint32_t p = (uint32_t)(S[s0] & 8191u);
+        const uint32_t p = (uint32_t)(S[s0] & pmask);
         const uint8_t* src = B + v.off[f] + (uint64_t)(r0 + p) * es;
         uint8_t* dst = T + v.off[f] + (uint64_t)(r0 + vx) * es;
         for (uint32_t q = 0; q < es; ++q) dst[q] = src[q];
@@ -1126,7 +1135,7 @@ cudaError_t launch_voxel_wave(const VxArgs& v, uint32_t tiles_bound, uint32_t bt
   k_vx_plan<<<v.n_samples, kThreads, 0, st>>>(v);
   // bucket mode (decided per cloud by k_vx_bbase)
   k_vx_bhist<<<bgrid, kThreads, 0, st>>>(v);
-  k_vx_bcol<<<dim3(v.n_samples, kVxBuckets / 32), 1024, 0, st>>>(v);
+  k_vx_bcol<<<dim3(v.n_samples, kVxBuckets / 256), 256, 0, st>>>(v);
   k_vx_bbase<<<v.n_samples, 1024, 0, st>>>(v);
   k_vx_bscatter<<<std::min<uint32_t>(bgrid, (uint32_t)sms), kThreads, kBScatterSmem, st>>>(v);
   k_vx_item<<<dim3(v.max_items, v.n_samples), kThreads, kItemSmem, st>>>(v);
