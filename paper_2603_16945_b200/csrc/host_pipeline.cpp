@@ -1423,7 +1423,7 @@ struct Pipeline {
       vx_btiles_bound = w.n * ((proto.cap_points + kVxBTile - 1) / kVxBTile);
       vx_max_items = proto.cap_points / (kVxItemCap / 2) + 2;
       w.vx_bt.ensure(16 + 4 * vx_btiles_bound);
-      w.vx_bcnt.ensure(4ull * kVxBuckets * vx_btiles_bound);
+      w.vx_bcnt.ensure(4ull * kVxBuckets * w.n);
       w.vx_boff.ensure(4ull * (kVxBuckets + 1) * w.n);
       w.vx_items.ensure(4ull * vx_max_items * w.n);
       w.vx_T.ensure(proto.handoff_stride * w.n);
@@ -1520,7 +1520,8 @@ struct Pipeline {
       vx.w1 = w.vx_w1.as<uint64_t>();
       vx.total_btiles = w.vx_bt.as<uint32_t>();
       vx.btile_cloud = vx.total_btiles + 4;
-      vx.bcnt = w.vx_bcnt.as<uint32_t>();
+      vx.bcur = w.vx_bcnt.as<uint32_t>();
+      vx.any_lsd = vx.total_btiles + 1;
       vx.boff = w.vx_boff.as<uint32_t>();
       vx.item_v = w.vx_items.as<uint32_t>();
       vx.max_items = (uint32_t)vx_max_items;

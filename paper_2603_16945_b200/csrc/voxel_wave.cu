@@ -44,6 +44,7 @@ constexpr uint32_t kThreads = 256;
 constexpr uint32_t kItems = 8;
 constexpr uint32_t kTile = kThreads * kItems;  // points / words per tile
 constexpr uint32_t kWarps = kThreads / 32;
+constexpr uint32_t kBThreads = 512;  // bucket histogram / scatter
 
 __device__ __forceinline__ uint32_t ord_f(float x) {  // float order as unsigned order
   const uint32_t b = __float_as_uint(x);
@@ -341,6 +342,7 @@ __global__ void __launch_bounds__(kThreads) k_vx_plan(VxArgs v) {
 
 // ---------------------------------------------------------------- keys
 __global__ void __launch_bounds__(kThreads) k_vx_keys(VxArgs v) {
+  if (!*v.any_lsd) return;  // every cloud took the bucket mode
   __shared__ uint32_t sh[kWarps + 1];
   __shared__ uint32_t hist[kVxMaxPasses][256];
   const uint32_t total = *v.total_tiles;
@@ -403,6 +405,7 @@ __device__ __forceinline__ bool sort_tile(const VxArgs& v, uint32_t t, int pass,
 }
 
 __global__ void __launch_bounds__(kThreads) k_vx_upsweep(VxArgs v, uint32_t pass) {
+  if (!*v.any_lsd) return;  // every cloud took the bucket mode
   __shared__ uint32_t h[256];
   const uint32_t total = *v.total_tiles;
   const uint64_t* src = (pass & 1u) ? v.w1 : v.w0;
@@ -432,6 +435,7 @@ __global__ void __launch_bounds__(kThreads) k_vx_upsweep(VxArgs v, uint32_t pass
 // grid (n_samples, 8): warp w of CTA y scans digit 32*y + w over the cloud's
 // sort tiles: cnt[t][d] := base[d] + sum of cnt[t'][d] for t' < t.
 __global__ void __launch_bounds__(1024) k_vx_colscan(VxArgs v, uint32_t pass) {
+  if (!*v.any_lsd) return;  // every cloud took the bucket mode
   const uint32_t s = blockIdx.x;
   const VxCloud& c = v.cl[s];
   if (!c.active || c.msd || pass >= c.passes) return;
@@ -458,6 +462,7 @@ __global__ void __launch_bounds__(1024) k_vx_colscan(VxArgs v, uint32_t pass) {
 // in 8 rounds of 32 (lane order = word order); per-warp digit counts (match
 // ranks), then per (digit, warp) bases from the tile's scanned offsets.
 __global__ void __launch_bounds__(kThreads) k_vx_downsweep(VxArgs v, uint32_t pass) {
+  if (!*v.any_lsd) return;  // every cloud took the bucket mode
   __shared__ uint32_t wc[kWarps][256];
   const uint32_t total = *v.total_tiles;
   const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -521,6 +526,7 @@ __device__ __forceinline__ const uint64_t* sorted(const VxArgs& v, const VxCloud
 }
 
 __global__ void __launch_bounds__(kThreads) k_vx_segcount(VxArgs v) {
+  if (!*v.any_lsd) return;  // every cloud took the bucket mode
   __shared__ uint32_t sh[kWarps + 1];
   const uint32_t total = *v.total_tiles;
   for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
@@ -545,6 +551,7 @@ __global__ void __launch_bounds__(kThreads) k_vx_segcount(VxArgs v) {
 }
 
 __global__ void __launch_bounds__(kThreads) k_vx_segscan(VxArgs v) {
+  if (!*v.any_lsd) return;  // every cloud took the bucket mode
   __shared__ uint32_t sh[kWarps + 1];
   __shared__ uint32_t carry;
   const uint32_t s = blockIdx.x;
@@ -570,6 +577,7 @@ __global__ void __launch_bounds__(kThreads) k_vx_segscan(VxArgs v) {
 // (one sorted position per thread per round: coalesced word reads and
 // stores, independent random loads -- many in flight).
 __global__ void __launch_bounds__(kThreads) k_vx_gather(VxArgs v) {
+  if (!*v.any_lsd) return;  // every cloud took the bucket mode
   const uint32_t total = *v.total_tiles;
   for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
     uint32_t s, j, nw;
@@ -638,6 +646,7 @@ __global__ void __launch_bounds__(kThreads) k_vx_gather(VxArgs v) {
 // means / first point written to A at the voxel index (A's payload is dead
 // after k_vx_gather; the voxelized cloud lives in A from here on).
 __global__ void __launch_bounds__(kThreads) k_vx_means(VxArgs v) {
+  if (!*v.any_lsd) return;  // every cloud took the bucket mode
   __shared__ uint32_t sh[kWarps + 1];
   const uint32_t total = *v.total_tiles;
   for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
@@ -721,8 +730,10 @@ __device__ __forceinline__ uint64_t point_key(const VxArgs& v, const VxCloud& c,
   return key;
 }
 
-// Per scatter tile (kVxBTile points): bucket histogram of the kept points.
-__global__ void __launch_bounds__(kThreads) k_vx_bhist(VxArgs v) {
+// Per scatter tile (kVxBTile points): bucket histogram of the kept points
+// in shared memory, flushed into the cloud's bucket totals (one global atomic
+// per non-empty bucket of the tile).
+__global__ void __launch_bounds__(kBThreads) k_vx_bhist(VxArgs v) {
   __shared__ uint32_t h[kVxBuckets];
   const uint32_t total = *v.total_btiles;
   for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
@@ -730,51 +741,28 @@ __global__ void __launch_bounds__(kThreads) k_vx_bhist(VxArgs v) {
     const VxCloud& c = v.cl[s];
     if (!c.active) continue;  // uniform
     const uint32_t nb = 1u << c.bb;
-    for (uint32_t k = threadIdx.x; k < nb; k += kThreads) h[k] = 0;
+    for (uint32_t k = threadIdx.x; k < nb; k += kBThreads) h[k] = 0;
     __syncthreads();
     const float* d = reinterpret_cast<const float*>(slot(v, v.A, s) + v.off[v.role_data]);
     const uint32_t i0 = (t - c.btile0) * kVxBTile;
     const uint32_t i1 = min(c.n, i0 + kVxBTile);
-    for (uint32_t i = i0 + threadIdx.x; i < i1; i += kThreads) {
+    for (uint32_t i = i0 + threadIdx.x; i < i1; i += kBThreads) {
       const float x = d[3ull * i], y = d[3ull * i + 1], z = d[3ull * i + 2];
       if (in_box(v, x, y, z)) atomicAdd(&h[point_key(v, c, x, y, z) >> c.lowbits], 1u);
     }
     __syncthreads();
-    uint32_t* out = v.bcnt + (uint64_t)t * kVxBuckets;
-    for (uint32_t k = threadIdx.x; k < nb; k += kThreads) out[k] = h[k];
+    uint32_t* tot = v.boff + (uint64_t)s * (kVxBuckets + 1);
+    for (uint32_t k = threadIdx.x; k < nb; k += kBThreads)
+      if (h[k]) atomicAdd(tot + k, h[k]);
     __syncthreads();
   }
 }
 
-// grid (n_samples, kVxBuckets / 256): thread per bucket (a warp reads 32
-// consecutive buckets of a tile row: coalesced), running exclusive sum down
-// the cloud's scatter tiles (8 rows loaded ahead); totals to boff.
-__global__ void __launch_bounds__(256) k_vx_bcol(VxArgs v) {
-  const uint32_t s = blockIdx.x;
-  const VxCloud& c = v.cl[s];
-  if (!c.active) return;
-  const uint32_t b = blockIdx.y * 256 + threadIdx.x;
-  if (b >= (1u << c.bb)) return;
-  uint32_t* col = v.bcnt + (uint64_t)c.btile0 * kVxBuckets + b;
-  uint32_t carry = 0;
-  for (uint32_t j0 = 0; j0 < c.n_btiles; j0 += 8) {
-    uint32_t x[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) x[q] = j0 + q < c.n_btiles ? col[(uint64_t)(j0 + q) * kVxBuckets] : 0u;
-#pragma unroll
-    for (int q = 0; q < 8; ++q)
-      if (j0 + q < c.n_btiles) {
-        col[(uint64_t)(j0 + q) * kVxBuckets] = carry;
-        carry += x[q];
-      }
-  }
-  v.boff[(uint64_t)s * (kVxBuckets + 1) + b] = carry;
-}
-
-// Per cloud: bucket offsets (exclusive scan), the largest bucket, and the
-// mode: bucket mode when every work item fits shared memory and the item
-// sort word fits 64 bits, else the global LSD sort (whose packed word may in
-// turn not fit: then k_cloud's op_voxel runs the ops).
+// Per cloud: bucket offsets (exclusive scan of the totals), the write
+// cursors (= offsets), the largest bucket, and the mode: bucket mode when the
+// item sort word (key, point index, record position) fits 64 bits, else the
+// global LSD sort (whose packed word may in turn not fit: then k_cloud's
+// op_voxel runs the ops).
 __global__ void __launch_bounds__(1024) k_vx_bbase(VxArgs v) {
   __shared__ uint32_t wsum[33];
   __shared__ uint32_t wmax[32];
@@ -783,6 +771,7 @@ __global__ void __launch_bounds__(1024) k_vx_bbase(VxArgs v) {
   if (!c.active) return;
   const uint32_t nb = 1u << c.bb;
   uint32_t* bo = v.boff + (uint64_t)s * (kVxBuckets + 1);
+  uint32_t* cur = v.bcur + (uint64_t)s * kVxBuckets;
   const uint32_t per = (nb + blockDim.x - 1) / blockDim.x;  // <= 4
   uint32_t x[4] = {0, 0, 0, 0}, sum = 0, mx = 0;
   for (uint32_t q = 0; q < per; ++q) {
@@ -813,102 +802,90 @@ __global__ void __launch_bounds__(1024) k_vx_bbase(VxArgs v) {
   uint32_t run = wsum[w] + inc - sum;
   for (uint32_t q = 0; q < per; ++q) {
     const uint32_t b = threadIdx.x * per + q;
-    if (b < nb) bo[b] = run;
+    if (b < nb) bo[b] = cur[b] = run;
     run += x[q];
   }
   if (threadIdx.x == 0) {
     bo[nb] = wsum[32];  // == kept
     c.max_bucket = wmax[0];
-    const uint32_t pb = c.kept > 1 ? 32u - __clz(c.kept - 1) : 1u;  // item position bits (worst case)
-    const bool fits = v.msd_enabled && (pb < 13 ? 13 : pb) + c.kb <= 64;
+    const uint32_t pb_small = 32u - __clz(kVxItemCap - 1);
+    const uint32_t pb_big = c.kept > 1 ? 32u - __clz(c.kept - 1) : 1u;
+    const uint32_t pb = pb_big > pb_small ? pb_big : pb_small;
+    const bool fits = v.msd_enabled && c.kb + c.ib + pb <= 64;
     c.msd = fits ? 1u : 0u;
     c.n_items = fits ? c.kept / (kVxItemCap / 2) + 1 : 0;
-    if (!fits && (c.kb + c.ib > 64 || c.passes > kVxMaxPasses)) {  // k_cloud's op_voxel handles it
-      c.fallback = 1;
-      c.active = 0;
+    if (!fits) {
+      atomicOr(v.any_lsd, 1u);
+      if (c.kb + c.ib > 64 || c.passes > kVxMaxPasses) {  // k_cloud's op_voxel handles it
+        c.fallback = 1;
+        c.active = 0;
+      }
     }
   }
 }
 
-// Stable scatter of a tile's kept points into their buckets: the tile's
-// (bucket, position) words are sorted in shared memory (stable radix sort),
-// so each bucket's records are written as one contiguous run at
-// bucket offset + tile base, in point order.  Records: the key (w0) and the
-// payload of every moved field (B, same layout as A).
-__global__ void __launch_bounds__(kThreads) k_vx_bscatter(VxArgs v) {
-  extern __shared__ __align__(16) uint8_t dyn[];
-  uint64_t* sw0 = reinterpret_cast<uint64_t*>(dyn);
-  uint64_t* sw1 = sw0 + kVxBTile;
-  uint32_t* h = reinterpret_cast<uint32_t*>(sw1 + kVxBTile);  // [kVxBuckets + 1]
-  uint32_t* scr = h + kVxBuckets + 32;
-  __shared__ uint32_t sh[kWarps + 1];
+// Scatter of a tile's kept points into their buckets: in-tile ranks from
+// shared-memory atomics, one global atomic per non-empty bucket reserves the
+// tile's run.  Order inside a bucket is not the point order; the item sort
+// restores it (the word carries the point index).  Records: word = key << ib
+// | index (w0), the payload of every moved field (B, same layout as A).
+__global__ void __launch_bounds__(kBThreads) k_vx_bscatter(VxArgs v) {
+  __shared__ uint32_t h[kVxBuckets];
+  constexpr uint32_t kPer = kVxBTile / kBThreads;
   const uint32_t total = *v.total_btiles;
   for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
     const uint32_t s = v.btile_cloud[t];
     const VxCloud& c = v.cl[s];
     if (!c.active || !c.msd) continue;  // uniform
     const uint32_t nb = 1u << c.bb;
+    for (uint32_t k = threadIdx.x; k < nb; k += kBThreads) h[k] = 0;
+    __syncthreads();
     const float* d = reinterpret_cast<const float*>(slot(v, v.A, s) + v.off[v.role_data]);
     const uint32_t i0 = (t - c.btile0) * kVxBTile;
-    const uint32_t m = min(c.n, i0 + kVxBTile) - i0;
-    (void)nb;
-    for (uint32_t k = threadIdx.x; k < kVxBuckets; k += kThreads) h[k] = 0;
-    __syncthreads();
-    for (uint32_t j = threadIdx.x; j < m; j += kThreads) {
-      const uint32_t i = i0 + j;
-      const float x = d[3ull * i], y = d[3ull * i + 1], z = d[3ull * i + 2];
-      uint64_t b = kVxBuckets;  // dropped by the crop: sorts last
-      if (in_box(v, x, y, z)) {
-        b = point_key(v, c, x, y, z) >> c.lowbits;
-        atomicAdd(&h[b], 1u);
+    uint64_t key[kPer];
+    uint32_t rank[kPer];
+#pragma unroll
+    for (uint32_t q = 0; q < kPer; ++q) {
+      const uint32_t i = i0 + q * kBThreads + threadIdx.x;
+      rank[q] = ~0u;
+      if (i < c.n) {
+        const float x = d[3ull * i], y = d[3ull * i + 1], z = d[3ull * i + 2];
+        if (in_box(v, x, y, z)) {
+          key[q] = point_key(v, c, x, y, z);
+          rank[q] = atomicAdd(&h[key[q] >> c.lowbits], 1u);
+        }
       }
-      sw0[j] = (b << 13) | j;
     }
     __syncthreads();
-    // tile-local bucket starts (exclusive scan of h, 16 buckets per thread)
-    {
-      constexpr uint32_t per = kVxBuckets / kThreads;
-      uint32_t x[per], sum = 0;
-#pragma unroll
-      for (uint32_t q = 0; q < per; ++q) {
-        x[q] = h[threadIdx.x * per + q];
-        sum += x[q];
-      }
-      uint32_t tot;
-      uint32_t run = block_excl_scan(sum, sh, &tot);
-#pragma unroll
-      for (uint32_t q = 0; q < per; ++q) {
-        h[threadIdx.x * per + q] = run;
-        run += x[q];
-      }
-      if (threadIdx.x == 0) h[kVxBuckets] = tot;
-    }
-    const int r = radix_sort8<4>(sw0, sw1, m, 13, 26, scr);
-    const uint64_t* sorted_w = r ? sw1 : sw0;
+    uint32_t* cur = v.bcur + (uint64_t)s * kVxBuckets;
+    for (uint32_t k = threadIdx.x; k < nb; k += kBThreads)
+      if (h[k]) h[k] = atomicAdd(cur + k, h[k]);  // the tile's run start in the bucket
     __syncthreads();
-    const uint32_t kept = h[kVxBuckets];
-    const uint32_t* bo = v.boff + (uint64_t)s * (kVxBuckets + 1);
-    const uint32_t* tb = v.bcnt + (uint64_t)t * kVxBuckets;
     const uint8_t* A = slot(v, v.A, s);
     uint8_t* B = v.B + (uint64_t)s * v.stride;
     const uint32_t* ha = hdr(v, v.A, s);
     const uint32_t moved = v.mm & ha[1];
-    for (uint32_t j = threadIdx.x; j < kept; j += kThreads) {
-      const uint64_t wj = sorted_w[j];
-      const uint32_t b = (uint32_t)(wj >> 13), li = (uint32_t)(wj & 8191u);
-      const uint32_t pos = bo[b] + tb[b] + (j - h[b]);
-      const uint32_t i = i0 + li;
-      const float x = d[3ull * i], y = d[3ull * i + 1], z = d[3ull * i + 2];
-      v.w0[c.word0 + pos] = point_key(v, c, x, y, z);
+#pragma unroll
+    for (uint32_t q = 0; q < kPer; ++q) {
+      if (rank[q] == ~0u) continue;
+      const uint32_t i = i0 + q * kBThreads + threadIdx.x;
+      const uint32_t pos = h[key[q] >> c.lowbits] + rank[q];
+      v.w0[c.word0 + pos] = (key[q] << c.ib) | i;
       for (int f = 0; f < v.n_bytes_fields; ++f) {
         if (!((moved >> f) & 1u)) continue;
         const uint32_t es = ha[10 + f];
-        if ((es & 3u) == 0) {
+        if (es == 12) {
+          const uint32_t* src = reinterpret_cast<const uint32_t*>(A + v.off[f]) + 3ull * i;
+          uint32_t* dst = reinterpret_cast<uint32_t*>(B + v.off[f]) + 3ull * pos;
+          dst[0] = src[0];
+          dst[1] = src[1];
+          dst[2] = src[2];
+        } else if ((es & 3u) == 0) {
           const uint32_t* src = reinterpret_cast<const uint32_t*>(A + v.off[f]) + (uint64_t)i * (es >> 2);
           uint32_t* dst = reinterpret_cast<uint32_t*>(B + v.off[f]) + (uint64_t)pos * (es >> 2);
-          for (uint32_t q = 0; q < (es >> 2); ++q) dst[q] = src[q];
+          for (uint32_t w = 0; w < (es >> 2); ++w) dst[w] = src[w];
         } else {
-          for (uint32_t q = 0; q < es; ++q) B[v.off[f] + (uint64_t)pos * es + q] = A[v.off[f] + (uint64_t)i * es + q];
+          for (uint32_t w = 0; w < es; ++w) B[v.off[f] + (uint64_t)pos * es + w] = A[v.off[f] + (uint64_t)i * es + w];
         }
       }
     }
@@ -960,7 +937,7 @@ __global__ void __launch_bounds__(kThreads) k_vx_item(VxArgs v) {
     if (threadIdx.x == 0) iv[w] = 0;
     return;
   }
-  const uint64_t kbase = (uint64_t)b0 << c.lowbits;
+  const uint64_t kbase = ((uint64_t)b0 << c.lowbits) << c.ib;  // words = key << ib | point index
   const uint64_t* K = v.w0 + c.word0 + r0;
   // an item above the shared-memory capacity (a dense bucket) sorts in
   // global memory: its key range of w0 and w1 are the ping-pong buffers
@@ -976,7 +953,7 @@ __global__ void __launch_bounds__(kThreads) k_vx_item(VxArgs v) {
   }
   kmax = dev::block_reduce(kmax, dev::OpMax{}, 0ull, red);  // (its barriers order the K reads before a1 writes)
   const uint32_t relbits = kmax ? 64u - __clzll(kmax) : 0u;
-  const int r = relbits ? radix_sort8<4>(a0, a1, m, pb, pb + relbits, scr) : 0;
+  const int r = relbits ? radix_sort8<4>(a0, a1, m, pb, pb + relbits, scr) : 0;  // (key, index) order
   const uint64_t* S = r ? a1 : a0;
   uint32_t* seg = reinterpret_cast<uint32_t*>(r ? a0 : a1);  // the free buffer
   const uint64_t pmask = (1ull << pb) - 1;
@@ -984,12 +961,13 @@ __global__ void __launch_bounds__(kThreads) k_vx_item(VxArgs v) {
   // voxel starts, numbered in order: thread-contiguous ranges, one block scan
   const uint32_t per = (m + kThreads - 1) / kThreads;
   const uint32_t ja = min(m, threadIdx.x * per), jb = min(m, ja + per);
+  const uint32_t ks = pb + c.ib;  // key bits start (above the point index)
   uint32_t cnt = 0;
-  for (uint32_t j = ja; j < jb; ++j) cnt += (j == 0 || (S[j] >> pb) != (S[j - 1] >> pb)) ? 1u : 0u;
+  for (uint32_t j = ja; j < jb; ++j) cnt += (j == 0 || (S[j] >> ks) != (S[j - 1] >> ks)) ? 1u : 0u;
   uint32_t V;
   uint32_t vid = block_excl_scan(cnt, sh, &V);
   for (uint32_t j = ja; j < jb; ++j)
-    if (j == 0 || (S[j] >> pb) != (S[j - 1] >> pb)) seg[vid++] = j;
+    if (j == 0 || (S[j] >> ks) != (S[j - 1] >> ks)) seg[vid++] = j;
   __syncthreads();
   const uint8_t* B = v.B + (uint64_t)s * v.stride;
   uint8_t* T = v.T + (uint64_t)s * v.stride;
@@ -1113,31 +1091,30 @@ __global__ void k_vx_finish(VxArgs v) {
 
 }  // namespace
 
-constexpr size_t kBScatterSmem = 2 * 8 * kVxBTile + 4 * (kVxBuckets + 32) + kSortScratchBytes;
 constexpr size_t kItemSmem = 2 * 8 * kVxItemCap + kSortScratchBytes;
 
-size_t voxel_wave_item_smem() { return kItemSmem > kBScatterSmem ? kItemSmem : kBScatterSmem; }
+size_t voxel_wave_item_smem() { return kItemSmem; }
 
 cudaError_t launch_voxel_wave(const VxArgs& v, uint32_t tiles_bound, uint32_t btiles_bound, int sms,
                               cudaStream_t st) {
   if (!v.n_samples) return cudaSuccess;
   static const bool attrs = [] {
-    cudaFuncSetAttribute(k_vx_bscatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBScatterSmem);
     cudaFuncSetAttribute(k_vx_item, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kItemSmem);
     return true;
   }();
   (void)attrs;
   cudaMemsetAsync(v.cl, 0, sizeof(VxCloud) * v.n_samples, st);
+  cudaMemsetAsync(v.boff, 0, 4ull * (kVxBuckets + 1) * v.n_samples, st);
+  cudaMemsetAsync(v.any_lsd, 0, 4, st);
   k_vx_prep<<<1, 1024, 0, st>>>(v);
   const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(tiles_bound, (uint32_t)sms * 8));
   const uint32_t bgrid = std::max<uint32_t>(1, std::min<uint32_t>(btiles_bound, (uint32_t)sms * 4));
   k_vx_bounds<<<grid, kThreads, 0, st>>>(v);
   k_vx_plan<<<v.n_samples, kThreads, 0, st>>>(v);
   // bucket mode (decided per cloud by k_vx_bbase)
-  k_vx_bhist<<<bgrid, kThreads, 0, st>>>(v);
-  k_vx_bcol<<<dim3(v.n_samples, kVxBuckets / 256), 256, 0, st>>>(v);
+  k_vx_bhist<<<bgrid, kBThreads, 0, st>>>(v);
   k_vx_bbase<<<v.n_samples, 1024, 0, st>>>(v);
-  k_vx_bscatter<<<std::min<uint32_t>(bgrid, (uint32_t)sms), kThreads, kBScatterSmem, st>>>(v);
+  k_vx_bscatter<<<bgrid, kBThreads, 0, st>>>(v);
   k_vx_item<<<dim3(v.max_items, v.n_samples), kThreads, kItemSmem, st>>>(v);
   k_vx_iscan<<<v.n_samples, kThreads, 0, st>>>(v);
   k_vx_compact<<<dim3(v.max_items, v.n_samples), kThreads, 0, st>>>(v);

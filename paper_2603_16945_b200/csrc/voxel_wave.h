@@ -11,8 +11,8 @@ namespace pcp {
 
 constexpr uint32_t kVxMaxPasses = 6;  // 8-bit digits: keys up to 48 bits (wider: k_cloud fallback)
 constexpr uint32_t kVxBuckets = 4096;  // bucket mode: up to 12 top key bits
-constexpr uint32_t kVxBTile = 8192;    // bucket mode: points per scatter tile
-constexpr uint32_t kVxItemCap = 8192;  // bucket mode: records per work item (shared memory)
+constexpr uint32_t kVxBTile = 4096;    // bucket mode: points per scatter tile
+constexpr uint32_t kVxItemCap = 4096;  // bucket mode: records per work item (shared memory)
 
 // Arguments of the stage (by value).  A = decoded clouds (hand-off slots of
 // the decode-only k_cloud launch), voxelized in place by the stage (the rest
@@ -48,8 +48,9 @@ struct VxArgs {
   // bucket mode scratch
   uint32_t* total_btiles;
   uint32_t* btile_cloud;  // [btiles]
-  uint32_t* bcnt;         // [btiles][kVxBuckets]: tile counts -> tile write bases
-  uint32_t* boff;         // [n_samples][kVxBuckets + 1]: bucket offsets
+  uint32_t* bcur;         // [n_samples][kVxBuckets]: bucket write cursors
+  uint32_t* boff;         // [n_samples][kVxBuckets + 1]: bucket totals -> offsets
+  uint32_t* any_lsd;      // a cloud of the wave takes the global LSD sort
   uint32_t* item_v;       // [n_samples][max_items]: voxels per item -> voxel offsets
   uint32_t max_items;
   uint8_t* T;             // voxel results per item before compaction (slots like A)
