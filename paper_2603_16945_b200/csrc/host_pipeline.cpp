@@ -1432,7 +1432,7 @@ struct Pipeline {
       w.vx_tiles.ensure(16 + 3 * 4 * vx_tiles_bound);
       w.vx_cnt.ensure(1024 * vx_tiles_bound);
       w.vx_w0.ensure(8ull * proto.cap_points * w.n);
-      w.vx_w1.ensure(8ull * proto.cap_points * w.n);
+      w.vx_w1.ensure(3 * 8ull * proto.cap_points * w.n);  // LSD pong + bucket-mode dense-item buffers
     }
     if (proto.n_rng) w.mt_pre.ensure(w.n * proto.n_rng * 312 * 8);
     w.h_res.ensure(total - o_sst + 16);
@@ -1518,6 +1518,7 @@ struct Pipeline {
       vx.cnt = w.vx_cnt.as<uint32_t>();
       vx.w0 = w.vx_w0.as<uint64_t>();
       vx.w1 = w.vx_w1.as<uint64_t>();
+      vx.w2 = vx.w1 + (uint64_t)proto.cap_points * w.n;
       vx.total_btiles = w.vx_bt.as<uint32_t>();
       vx.btile_cloud = vx.total_btiles + 4;
       vx.bcur = w.vx_bcnt.as<uint32_t>();

@@ -61,6 +61,14 @@ __device__ __forceinline__ const uint32_t* hdr(const VxArgs& v, const uint8_t* b
   return reinterpret_cast<const uint32_t*>(slot(v, base, s));
 }
 
+// Lowest-set-bit exponent of a finite nonzero float: x = odd * 2^e.
+__device__ __forceinline__ int lowbit_exp(float x) {
+  const uint32_t b = __float_as_uint(x) & 0x7fffffffu;
+  const uint32_t e = b >> 23, m = b & 0x7fffffu;
+  if (e == 0) return -149 + __ffs(m) - 1;
+  return (int)e - 150 + __ffs(m | 0x800000u) - 1;
+}
+
 // App. C key of one coordinate: k = (int32)floorf((p - o) / v)
 __device__ __forceinline__ float qkey(float p, float o, float vs) {
   return floorf(__fdiv_rn(__fsub_rn(p, o), vs));
@@ -808,10 +816,8 @@ __global__ void __launch_bounds__(1024) k_vx_bbase(VxArgs v) {
   if (threadIdx.x == 0) {
     bo[nb] = wsum[32];  // == kept
     c.max_bucket = wmax[0];
-    const uint32_t pb_small = 32u - __clz(kVxItemCap - 1);
-    const uint32_t pb_big = c.kept > 1 ? 32u - __clz(c.kept - 1) : 1u;
-    const uint32_t pb = pb_big > pb_small ? pb_big : pb_small;
-    const bool fits = v.msd_enabled && c.kb + c.ib + pb <= 64;
+    const uint32_t pb = c.kept > 1 ? max(12u, 32u - __clz(c.kept - 1)) : 12u;  // item position bits, worst case
+    const bool fits = v.msd_enabled && c.lowbits + c.bb + pb <= 64 && c.kb + c.ib <= 64;
     c.msd = fits ? 1u : 0u;
     c.n_items = fits ? c.kept / (kVxItemCap / 2) + 1 : 0;
     if (!fits) {
@@ -937,23 +943,26 @@ __global__ void __launch_bounds__(kThreads) k_vx_item(VxArgs v) {
     if (threadIdx.x == 0) iv[w] = 0;
     return;
   }
-  const uint64_t kbase = ((uint64_t)b0 << c.lowbits) << c.ib;  // words = key << ib | point index
+  const uint64_t kbase = (uint64_t)b0 << c.lowbits;  // words = key << ib | point index
   const uint64_t* K = v.w0 + c.word0 + r0;
+  const uint64_t imask = c.ib ? ((1ull << c.ib) - 1) : 0ull;
   // an item above the shared-memory capacity (a dense bucket) sorts in
-  // global memory: its key range of w0 and w1 are the ping-pong buffers
+  // global memory (w2: two words per point of the wave)
   const bool big = m > kVxItemCap;
-  const uint32_t pb = big ? 32u - __clz(m - 1) : 13u;  // position bits
-  uint64_t* a0 = big ? v.w1 + c.word0 + r0 : sw0;
-  uint64_t* a1 = big ? v.w0 + c.word0 + r0 : sw1;
+  const uint32_t pb = big ? 32u - __clz(m - 1) : 12u;  // record position bits
+  uint64_t* a0 = big ? v.w2 + 2 * c.word0 + r0 : sw0;
+  uint64_t* a1 = big ? v.w2 + 2 * c.word0 + c.n + r0 : sw1;
   unsigned long long kmax = 0;
   for (uint32_t j = threadIdx.x; j < m; j += kThreads) {
-    const uint64_t rel = K[j] - kbase;
+    const uint64_t rel = (K[j] >> c.ib) - kbase;
     a0[j] = (rel << pb) | j;
     kmax = max(kmax, (unsigned long long)rel);
   }
-  kmax = dev::block_reduce(kmax, dev::OpMax{}, 0ull, red);  // (its barriers order the K reads before a1 writes)
+  kmax = dev::block_reduce(kmax, dev::OpMax{}, 0ull, red);
   const uint32_t relbits = kmax ? 64u - __clzll(kmax) : 0u;
-  const int r = relbits ? radix_sort8<4>(a0, a1, m, pb, pb + relbits, scr) : 0;  // (key, index) order
+  // by key only: inside a voxel the order is the scatter's, and the sums
+  // below are order-free when exact (else replayed in point order)
+  const int r = relbits ? radix_sort8<4>(a0, a1, m, pb, pb + relbits, scr) : 0;
   const uint64_t* S = r ? a1 : a0;
   uint32_t* seg = reinterpret_cast<uint32_t*>(r ? a0 : a1);  // the free buffer
   const uint64_t pmask = (1ull << pb) - 1;
@@ -961,13 +970,12 @@ __global__ void __launch_bounds__(kThreads) k_vx_item(VxArgs v) {
   // voxel starts, numbered in order: thread-contiguous ranges, one block scan
   const uint32_t per = (m + kThreads - 1) / kThreads;
   const uint32_t ja = min(m, threadIdx.x * per), jb = min(m, ja + per);
-  const uint32_t ks = pb + c.ib;  // key bits start (above the point index)
   uint32_t cnt = 0;
-  for (uint32_t j = ja; j < jb; ++j) cnt += (j == 0 || (S[j] >> ks) != (S[j - 1] >> ks)) ? 1u : 0u;
+  for (uint32_t j = ja; j < jb; ++j) cnt += (j == 0 || (S[j] >> pb) != (S[j - 1] >> pb)) ? 1u : 0u;
   uint32_t V;
   uint32_t vid = block_excl_scan(cnt, sh, &V);
   for (uint32_t j = ja; j < jb; ++j)
-    if (j == 0 || (S[j] >> ks) != (S[j - 1] >> ks)) seg[vid++] = j;
+    if (j == 0 || (S[j] >> pb) != (S[j - 1] >> pb)) seg[vid++] = j;
   __syncthreads();
   const uint8_t* B = v.B + (uint64_t)s * v.stride;
   uint8_t* T = v.T + (uint64_t)s * v.stride;
@@ -975,38 +983,70 @@ __global__ void __launch_bounds__(kThreads) k_vx_item(VxArgs v) {
   const uint32_t moved = v.mm & ha[1];
   for (uint32_t vx = threadIdx.x; vx < V; vx += kThreads) {
     const uint32_t s0 = seg[vx], s1 = vx + 1 < V ? seg[vx + 1] : m;
-    const double cnt = (double)(s1 - s0);
+    const uint32_t n = s1 - s0;
+    const double cnt_d = (double)n;
+    // the voxel's first point (smallest index) for gathered extra fields
+    uint32_t first = (uint32_t)(S[s0] & pmask);
+    uint64_t first_i = K[first] & imask;
+    for (uint32_t k = s0 + 1; k < s1; ++k) {
+      const uint32_t p = (uint32_t)(S[k] & pmask);
+      const uint64_t i = K[p] & imask;
+      if (i < first_i) first_i = i, first = p;
+    }
     for (int f = 0; f < v.n_bytes_fields; ++f) {
       if (!((moved >> f) & 1u)) continue;
       const bool avg = f == v.role_data || f == v.role_normal || f == v.role_color || f == v.role_intensity;
       const uint32_t es = ha[10 + f];
       if (avg) {
-        const float* src = reinterpret_cast<const float*>(B + v.off[f]) + (uint64_t)r0 * (es / 4);
-        float* dst = reinterpret_cast<float*>(T + v.off[f]) + (uint64_t)(r0 + vx) * (es / 4);
-        if (es == 12) {
-          double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+        const uint32_t comps = es / 4;  // 3 or 1
+        const float* src = reinterpret_cast<const float*>(B + v.off[f]) + (uint64_t)r0 * comps;
+        float* dst = reinterpret_cast<float*>(T + v.off[f]) + (uint64_t)(r0 + vx) * comps;
+        for (uint32_t q = 0; q < comps; ++q) {
+          // double sum in sorted order plus an exactness certificate: every
+          // value a multiple of 2^emin and n * max|x| < 2^(53 + emin) =>
+          // every partial sum of every order is exact
+          double acc = 0.0;
+          int emin = 1 << 20, emax = -(1 << 20);
+          bool finite = true;
           for (uint32_t k = s0; k < s1; ++k) {
-            const uint32_t p = (uint32_t)(S[k] & pmask);
-            a0 = __dadd_rn(a0, (double)src[3 * p]);
-            a1 = __dadd_rn(a1, (double)src[3 * p + 1]);
-            a2 = __dadd_rn(a2, (double)src[3 * p + 2]);
+            const float x = src[(S[k] & pmask) * comps + q];
+            acc = __dadd_rn(acc, (double)x);
+            if (x != 0.0f) {
+              if (!isfinite(x)) finite = false;
+              else {
+                emin = min(emin, lowbit_exp(x));
+                emax = max(emax, ilogbf(x));
+              }
+            }
           }
-          dst[0] = __double2float_rn(__ddiv_rn(a0, cnt));
-          dst[1] = __double2float_rn(__ddiv_rn(a1, cnt));
-          dst[2] = __double2float_rn(__ddiv_rn(a2, cnt));
-        } else {
-          double a0 = 0.0;
-          for (uint32_t k = s0; k < s1; ++k) a0 = __dadd_rn(a0, (double)src[S[k] & pmask]);
-          dst[0] = __double2float_rn(__ddiv_rn(a0, cnt));
+          const int nbits = 32 - __clz(n);  // n < 2^nbits
+          const bool exact = finite && (emax == -(1 << 20) || emax + 1 + nbits <= 53 + emin);
+          if (!exact) {  // replay in point order (the App. C sequence)
+            acc = 0.0;
+            uint64_t last = 0;
+            bool any = false;
+            for (uint32_t t2 = 0; t2 < n; ++t2) {  // next larger point index each round
+              uint64_t best = ~0ull;
+              uint32_t bp = 0;
+              for (uint32_t k = s0; k < s1; ++k) {
+                const uint32_t p = (uint32_t)(S[k] & pmask);
+                const uint64_t i = K[p] & imask;
+                if ((!any || i > last) && i < best) best = i, bp = p;
+              }
+              acc = __dadd_rn(acc, (double)src[(uint64_t)bp * comps + q]);
+              last = best;
+              any = true;
+            }
+          }
+          dst[q] = __double2float_rn(__ddiv_rn(acc, cnt_d));
         }
       } else {  // gathered extra field: the voxel's first point
-        const uint32_t p = (uint32_t)(S[s0] & pmask);
-        const uint8_t* src = B + v.off[f] + (uint64_t)(r0 + p) * es;
+        const uint8_t* src = B + v.off[f] + (uint64_t)(r0 + first) * es;
         uint8_t* dst = T + v.off[f] + (uint64_t)(r0 + vx) * es;
         for (uint32_t q = 0; q < es; ++q) dst[q] = src[q];
       }
     }
-    if (v.counts) reinterpret_cast<int32_t*>(T + v.off[kMaxBytesFields])[r0 + vx] = (int32_t)(s1 - s0);
+    if (v.counts) reinterpret_cast<int32_t*>(T + v.off[kMaxBytesFields])[r0 + vx] = (int32_t)n;
   }
   if (threadIdx.x == 0) iv[w] = V;
 }

@@ -45,6 +45,7 @@ struct VxArgs {
   uint32_t* cnt;         // [tiles][256]
   uint64_t* w0;          // [points] sort words (ping)
   uint64_t* w1;          // (pong)
+  uint64_t* w2;          // [2 x points] bucket mode: sort buffers of dense items
   // bucket mode scratch
   uint32_t* total_btiles;
   uint32_t* btile_cloud;  // [btiles]
