@@ -344,7 +344,7 @@ __global__ void __launch_bounds__(kThreads) k_vx_plan(VxArgs v) {
   c.kb = kb;
   c.ib = ib;
   c.passes = (kb + 7) / 8;
-  c.bb = kb < 12 ? kb : 12;
+  c.bb = kb < kVxBucketBits ? kb : kVxBucketBits;
   c.lowbits = kb - c.bb;
 }
 
@@ -742,26 +742,35 @@ __device__ __forceinline__ uint64_t point_key(const VxArgs& v, const VxCloud& c,
 // in shared memory, flushed into the cloud's bucket totals (one global atomic
 // per non-empty bucket of the tile).
 __global__ void __launch_bounds__(kBThreads) k_vx_bhist(VxArgs v) {
-  __shared__ uint32_t h[kVxBuckets];
+  __shared__ uint32_t h[kVxSmemBuckets];
   const uint32_t total = *v.total_btiles;
   for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
     const uint32_t s = v.btile_cloud[t];
     const VxCloud& c = v.cl[s];
     if (!c.active) continue;  // uniform
     const uint32_t nb = 1u << c.bb;
-    for (uint32_t k = threadIdx.x; k < nb; k += kBThreads) h[k] = 0;
-    __syncthreads();
+    const bool sm = nb <= kVxSmemBuckets;  // uniform
+    uint32_t* tot = v.boff + (uint64_t)s * (kVxBuckets + 1);
+    if (sm) {
+      for (uint32_t k = threadIdx.x; k < nb; k += kBThreads) h[k] = 0;
+      __syncthreads();
+    }
     const float* d = reinterpret_cast<const float*>(slot(v, v.A, s) + v.off[v.role_data]);
     const uint32_t i0 = (t - c.btile0) * kVxBTile;
     const uint32_t i1 = min(c.n, i0 + kVxBTile);
     for (uint32_t i = i0 + threadIdx.x; i < i1; i += kBThreads) {
       const float x = d[3ull * i], y = d[3ull * i + 1], z = d[3ull * i + 2];
-      if (in_box(v, x, y, z)) atomicAdd(&h[point_key(v, c, x, y, z) >> c.lowbits], 1u);
+      if (in_box(v, x, y, z)) {
+        const uint32_t b = (uint32_t)(point_key(v, c, x, y, z) >> c.lowbits);
+        if (sm) atomicAdd(&h[b], 1u);
+        else atomicAdd(tot + b, 1u);  // many buckets: spread-address global reductions
+      }
     }
-    __syncthreads();
-    uint32_t* tot = v.boff + (uint64_t)s * (kVxBuckets + 1);
-    for (uint32_t k = threadIdx.x; k < nb; k += kBThreads)
-      if (h[k]) atomicAdd(tot + k, h[k]);
+    if (sm) {
+      __syncthreads();
+      for (uint32_t k = threadIdx.x; k < nb; k += kBThreads)
+        if (h[k]) atomicAdd(tot + k, h[k]);
+    }
     __syncthreads();
   }
 }
@@ -780,13 +789,13 @@ __global__ void __launch_bounds__(1024) k_vx_bbase(VxArgs v) {
   const uint32_t nb = 1u << c.bb;
   uint32_t* bo = v.boff + (uint64_t)s * (kVxBuckets + 1);
   uint32_t* cur = v.bcur + (uint64_t)s * kVxBuckets;
-  const uint32_t per = (nb + blockDim.x - 1) / blockDim.x;  // <= 4
-  uint32_t x[4] = {0, 0, 0, 0}, sum = 0, mx = 0;
+  const uint32_t per = (nb + blockDim.x - 1) / blockDim.x;  // <= 64
+  uint32_t sum = 0, mx = 0;
   for (uint32_t q = 0; q < per; ++q) {
     const uint32_t b = threadIdx.x * per + q;
-    x[q] = b < nb ? bo[b] : 0;
-    sum += x[q];
-    mx = max(mx, x[q]);
+    const uint32_t x = b < nb ? bo[b] : 0;
+    sum += x;
+    mx = max(mx, x);
   }
   const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t inc = warp_incl_scan(sum);
@@ -810,8 +819,11 @@ __global__ void __launch_bounds__(1024) k_vx_bbase(VxArgs v) {
   uint32_t run = wsum[w] + inc - sum;
   for (uint32_t q = 0; q < per; ++q) {
     const uint32_t b = threadIdx.x * per + q;
-    if (b < nb) bo[b] = cur[b] = run;
-    run += x[q];
+    if (b < nb) {
+      const uint32_t x = bo[b];
+      bo[b] = cur[b] = run;
+      run += x;
+    }
   }
   if (threadIdx.x == 0) {
     bo[nb] = wsum[32];  // == kept
@@ -836,7 +848,7 @@ __global__ void __launch_bounds__(1024) k_vx_bbase(VxArgs v) {
 // restores it (the word carries the point index).  Records: word = key << ib
 // | index (w0), the payload of every moved field (B, same layout as A).
 __global__ void __launch_bounds__(kBThreads) k_vx_bscatter(VxArgs v) {
-  __shared__ uint32_t h[kVxBuckets];
+  __shared__ uint32_t h[kVxSmemBuckets];
   constexpr uint32_t kPer = kVxBTile / kBThreads;
   const uint32_t total = *v.total_btiles;
   for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
@@ -844,8 +856,12 @@ __global__ void __launch_bounds__(kBThreads) k_vx_bscatter(VxArgs v) {
     const VxCloud& c = v.cl[s];
     if (!c.active || !c.msd) continue;  // uniform
     const uint32_t nb = 1u << c.bb;
-    for (uint32_t k = threadIdx.x; k < nb; k += kBThreads) h[k] = 0;
-    __syncthreads();
+    const bool sm = nb <= kVxSmemBuckets;  // uniform
+    uint32_t* cur = v.bcur + (uint64_t)s * kVxBuckets;
+    if (sm) {
+      for (uint32_t k = threadIdx.x; k < nb; k += kBThreads) h[k] = 0;
+      __syncthreads();
+    }
     const float* d = reinterpret_cast<const float*>(slot(v, v.A, s) + v.off[v.role_data]);
     const uint32_t i0 = (t - c.btile0) * kVxBTile;
     uint64_t key[kPer];
@@ -858,15 +874,17 @@ __global__ void __launch_bounds__(kBThreads) k_vx_bscatter(VxArgs v) {
         const float x = d[3ull * i], y = d[3ull * i + 1], z = d[3ull * i + 2];
         if (in_box(v, x, y, z)) {
           key[q] = point_key(v, c, x, y, z);
-          rank[q] = atomicAdd(&h[key[q] >> c.lowbits], 1u);
+          const uint32_t b = (uint32_t)(key[q] >> c.lowbits);
+          rank[q] = sm ? atomicAdd(&h[b], 1u) : atomicAdd(cur + b, 1u);  // in-tile rank / final position
         }
       }
     }
-    __syncthreads();
-    uint32_t* cur = v.bcur + (uint64_t)s * kVxBuckets;
-    for (uint32_t k = threadIdx.x; k < nb; k += kBThreads)
-      if (h[k]) h[k] = atomicAdd(cur + k, h[k]);  // the tile's run start in the bucket
-    __syncthreads();
+    if (sm) {
+      __syncthreads();
+      for (uint32_t k = threadIdx.x; k < nb; k += kBThreads)
+        if (h[k]) h[k] = atomicAdd(cur + k, h[k]);  // the tile's run start in the bucket
+      __syncthreads();
+    }
     const uint8_t* A = slot(v, v.A, s);
     uint8_t* B = v.B + (uint64_t)s * v.stride;
     const uint32_t* ha = hdr(v, v.A, s);
@@ -875,7 +893,7 @@ __global__ void __launch_bounds__(kBThreads) k_vx_bscatter(VxArgs v) {
     for (uint32_t q = 0; q < kPer; ++q) {
       if (rank[q] == ~0u) continue;
       const uint32_t i = i0 + q * kBThreads + threadIdx.x;
-      const uint32_t pos = h[key[q] >> c.lowbits] + rank[q];
+      const uint32_t pos = sm ? h[key[q] >> c.lowbits] + rank[q] : rank[q];
       v.w0[c.word0 + pos] = (key[q] << c.ib) | i;
       for (int f = 0; f < v.n_bytes_fields; ++f) {
         if (!((moved >> f) & 1u)) continue;

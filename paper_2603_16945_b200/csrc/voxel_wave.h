@@ -10,7 +10,9 @@
 namespace pcp {
 
 constexpr uint32_t kVxMaxPasses = 6;  // 8-bit digits: keys up to 48 bits (wider: k_cloud fallback)
-constexpr uint32_t kVxBuckets = 4096;  // bucket mode: up to 12 top key bits
+constexpr uint32_t kVxBucketBits = 16;  // bucket mode: up to 16 top key bits
+constexpr uint32_t kVxBuckets = 1u << kVxBucketBits;
+constexpr uint32_t kVxSmemBuckets = 4096;  // histograms / ranks in shared memory up to this many
 constexpr uint32_t kVxBTile = 4096;    // bucket mode: points per scatter tile
 constexpr uint32_t kVxItemCap = 4096;  // bucket mode: records per work item (shared memory)
 
