@@ -995,39 +995,89 @@ __global__ void __launch_bounds__(kThreads) k_vx_item(VxArgs v) {
   for (uint32_t j = ja; j < jb; ++j)
     if (j == 0 || (S[j] >> pb) != (S[j - 1] >> pb)) seg[vid++] = j;
   __syncthreads();
-  const uint8_t* B = v.B + (uint64_t)s * v.stride;
+  // payload into sorted order (T[r0 + k] = B[r0 + S[k]]): every voxel's run
+  // becomes contiguous; results go to B[r0 + voxel] (B's item range is dead
+  // after this gather) and are compacted into A afterwards
+  uint8_t* B = v.B + (uint64_t)s * v.stride;
   uint8_t* T = v.T + (uint64_t)s * v.stride;
   const uint32_t* ha = hdr(v, v.A, s);
   const uint32_t moved = v.mm & ha[1];
-  for (uint32_t vx = threadIdx.x; vx < V; vx += kThreads) {
-    const uint32_t s0 = seg[vx], s1 = vx + 1 < V ? seg[vx + 1] : m;
-    const uint32_t n = s1 - s0;
-    const double cnt_d = (double)n;
-    // the voxel's first point (smallest index) for gathered extra fields
-    uint32_t first = (uint32_t)(S[s0] & pmask);
-    uint64_t first_i = K[first] & imask;
-    for (uint32_t k = s0 + 1; k < s1; ++k) {
-      const uint32_t p = (uint32_t)(S[k] & pmask);
-      const uint64_t i = K[p] & imask;
-      if (i < first_i) first_i = i, first = p;
+  for (int f = 0; f < v.n_bytes_fields; ++f) {
+    if (!((moved >> f) & 1u)) continue;
+    const uint32_t es = ha[10 + f];
+    if ((es & 3u) == 0) {
+      const uint32_t wpp = es >> 2;
+      const uint32_t* src = reinterpret_cast<const uint32_t*>(B + v.off[f]) + (uint64_t)r0 * wpp;
+      uint32_t* dst = reinterpret_cast<uint32_t*>(T + v.off[f]) + (uint64_t)r0 * wpp;
+      for (uint32_t e = threadIdx.x; e < m * wpp; e += kThreads) {
+        const uint32_t k = e / wpp, q = e - k * wpp;
+        dst[e] = src[(S[k] & pmask) * wpp + q];
+      }
+    } else {
+      for (uint32_t e = threadIdx.x; e < m * es; e += kThreads) {
+        const uint32_t k = e / es, q = e - k * es;
+        T[v.off[f] + (uint64_t)r0 * es + e] = B[v.off[f] + ((uint64_t)r0 + (S[k] & pmask)) * es + q];
+      }
     }
+  }
+  __syncthreads();
+  // point index of sorted position k (the order voxel sums fall back to)
+  auto pidx = [&](uint32_t k) -> uint64_t { return K[S[k] & pmask] & imask; };
+  // mean of one component over sorted positions [s0, s1): exact double sum
+  // in any order under the certificate, else replayed in point order
+  auto finish_mean = [&](const float* src, uint32_t comps, uint32_t q, uint32_t s0, uint32_t s1, double acc,
+                         int emin, int emax, bool finite) -> float {
+    const uint32_t n = s1 - s0;
+    const int nbits = 32 - __clz(n);
+    const bool exact = finite && (emax == -(1 << 20) || emax + 1 + nbits <= 53 + emin);
+    if (!exact) {
+      acc = 0.0;
+      uint64_t last = 0;
+      bool any = false;
+      for (uint32_t t2 = 0; t2 < n; ++t2) {  // next larger point index each round
+        uint64_t best = ~0ull;
+        uint32_t bk = s0;
+        for (uint32_t k = s0; k < s1; ++k) {
+          const uint64_t i = pidx(k);
+          if ((!any || i > last) && i < best) best = i, bk = k;
+        }
+        acc = __dadd_rn(acc, (double)src[(uint64_t)bk * comps + q]);
+        last = best;
+        any = true;
+      }
+    }
+    return __double2float_rn(__ddiv_rn(acc, (double)n));
+  };
+  auto write_voxel = [&](uint32_t vx, uint32_t s0, uint32_t s1, bool warp_mode) {
+    const uint32_t lane = threadIdx.x & 31;
+    // the voxel's first point (smallest index) for gathered extra fields
+    uint32_t first = s0;
+    uint64_t first_i = ~0ull;
+    for (uint32_t k = s0 + (warp_mode ? lane : 0); k < s1; k += warp_mode ? 32 : 1) {
+      const uint64_t i = pidx(k);
+      if (i < first_i) first_i = i, first = k;
+    }
+    if (warp_mode)
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const uint64_t oi = __shfl_xor_sync(0xffffffffu, first_i, o);
+        const uint32_t ok = __shfl_xor_sync(0xffffffffu, first, o);
+        if (oi < first_i) first_i = oi, first = ok;
+      }
     for (int f = 0; f < v.n_bytes_fields; ++f) {
       if (!((moved >> f) & 1u)) continue;
       const bool avg = f == v.role_data || f == v.role_normal || f == v.role_color || f == v.role_intensity;
       const uint32_t es = ha[10 + f];
       if (avg) {
         const uint32_t comps = es / 4;  // 3 or 1
-        const float* src = reinterpret_cast<const float*>(B + v.off[f]) + (uint64_t)r0 * comps;
-        float* dst = reinterpret_cast<float*>(T + v.off[f]) + (uint64_t)(r0 + vx) * comps;
+        const float* src = reinterpret_cast<const float*>(T + v.off[f]) + (uint64_t)r0 * comps;
+        float* dst = reinterpret_cast<float*>(B + v.off[f]) + (uint64_t)(r0 + vx) * comps;
         for (uint32_t q = 0; q < comps; ++q) {
-          // double sum in sorted order plus an exactness certificate: every
-          // value a multiple of 2^emin and n * max|x| < 2^(53 + emin) =>
-          // every partial sum of every order is exact
           double acc = 0.0;
           int emin = 1 << 20, emax = -(1 << 20);
           bool finite = true;
-          for (uint32_t k = s0; k < s1; ++k) {
-            const float x = src[(S[k] & pmask) * comps + q];
+          for (uint32_t k = s0 + (warp_mode ? lane : 0); k < s1; k += warp_mode ? 32 : 1) {
+            const float x = src[(uint64_t)k * comps + q];
             acc = __dadd_rn(acc, (double)x);
             if (x != 0.0f) {
               if (!isfinite(x)) finite = false;
@@ -1037,34 +1087,35 @@ __global__ void __launch_bounds__(kThreads) k_vx_item(VxArgs v) {
               }
             }
           }
-          const int nbits = 32 - __clz(n);  // n < 2^nbits
-          const bool exact = finite && (emax == -(1 << 20) || emax + 1 + nbits <= 53 + emin);
-          if (!exact) {  // replay in point order (the App. C sequence)
-            acc = 0.0;
-            uint64_t last = 0;
-            bool any = false;
-            for (uint32_t t2 = 0; t2 < n; ++t2) {  // next larger point index each round
-              uint64_t best = ~0ull;
-              uint32_t bp = 0;
-              for (uint32_t k = s0; k < s1; ++k) {
-                const uint32_t p = (uint32_t)(S[k] & pmask);
-                const uint64_t i = K[p] & imask;
-                if ((!any || i > last) && i < best) best = i, bp = p;
-              }
-              acc = __dadd_rn(acc, (double)src[(uint64_t)bp * comps + q]);
-              last = best;
-              any = true;
+          if (warp_mode) {
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+              acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+              emin = min(emin, __shfl_xor_sync(0xffffffffu, emin, o));
+              emax = max(emax, __shfl_xor_sync(0xffffffffu, emax, o));
             }
+            finite = __all_sync(0xffffffffu, finite);
           }
-          dst[q] = __double2float_rn(__ddiv_rn(acc, cnt_d));
+          if (!warp_mode || lane == 0) dst[q] = finish_mean(src, comps, q, s0, s1, acc, emin, emax, finite);
         }
-      } else {  // gathered extra field: the voxel's first point
-        const uint8_t* src = B + v.off[f] + (uint64_t)(r0 + first) * es;
-        uint8_t* dst = T + v.off[f] + (uint64_t)(r0 + vx) * es;
+      } else if (!warp_mode || lane == 0) {  // gathered extra field: the voxel's first point
+        const uint8_t* src = T + v.off[f] + ((uint64_t)r0 + first) * es;
+        uint8_t* dst = B + v.off[f] + (uint64_t)(r0 + vx) * es;
         for (uint32_t q = 0; q < es; ++q) dst[q] = src[q];
       }
     }
-    if (v.counts) reinterpret_cast<int32_t*>(T + v.off[kMaxBytesFields])[r0 + vx] = (int32_t)n;
+    if (v.counts && (!warp_mode || lane == 0))
+      reinterpret_cast<int32_t*>(B + v.off[kMaxBytesFields])[r0 + vx] = (int32_t)(s1 - s0);
+  };
+  // small voxels: one thread each; large ones (> 64 points): one warp each
+  constexpr uint32_t kWarpVoxel = 64;
+  for (uint32_t vx = threadIdx.x; vx < V; vx += kThreads) {
+    const uint32_t s0 = seg[vx], s1 = vx + 1 < V ? seg[vx + 1] : m;
+    if (s1 - s0 <= kWarpVoxel) write_voxel(vx, s0, s1, false);
+  }
+  for (uint32_t vx = threadIdx.x >> 5; vx < V; vx += kWarps) {
+    const uint32_t s0 = seg[vx], s1 = vx + 1 < V ? seg[vx + 1] : m;
+    if (s1 - s0 > kWarpVoxel) write_voxel(vx, s0, s1, true);
   }
   if (threadIdx.x == 0) iv[w] = V;
 }
@@ -1091,7 +1142,7 @@ __global__ void __launch_bounds__(kThreads) k_vx_iscan(VxArgs v) {
   if (threadIdx.x == 0) c.V = carry;
 }
 
-// grid (max_items, n_samples): voxel results of item w from T[r0 ..] to A at
+// grid (max_items, n_samples): voxel results of item w from B[r0 ..] to A at
 // the item's voxel offset.
 __global__ void __launch_bounds__(kThreads) k_vx_compact(VxArgs v) {
   const uint32_t s = blockIdx.y, w = blockIdx.x;
@@ -1102,7 +1153,7 @@ __global__ void __launch_bounds__(kThreads) k_vx_compact(VxArgs v) {
   const uint32_t* iv = v.item_v + (uint64_t)s * v.max_items;
   const uint32_t vo = iv[w], vn = (w + 1 < c.n_items ? iv[w + 1] : c.V) - vo;
   if (!vn) return;
-  const uint8_t* T = v.T + (uint64_t)s * v.stride;
+  const uint8_t* T = v.B + (uint64_t)s * v.stride;  // (results were left in B)
   uint8_t* A = v.A + (uint64_t)s * v.stride;
   const uint32_t* ha = hdr(v, v.A, s);
   const uint32_t moved = v.mm & ha[1];
