@@ -1090,6 +1090,14 @@ struct Pipeline {
     v.vx_first = first;
     v.vx_last = last;
     v.max_passes = kVxMaxPasses;
+    // bucket bits: ~2 buckets per point at most, <= 20 bits
+    const uint32_t cap_bits = 32u - (uint32_t)__builtin_clz(std::max<uint32_t>(a.cap_points, 2) - 1);
+    v.bucket_bits = std::min<uint32_t>(kVxMaxBucketBits, cap_bits + 1);
+    v.bstride = 1u << v.bucket_bits;
+    uint32_t pw = 0;
+    for (int f = 0; f < a.n_bytes_fields; ++f)
+      if ((mm >> f) & 1u) pw += (a.field_cap[f] + 3) / 4;
+    v.pay_words = pw <= kVxMaxPayWords ? pw : 0;
   }
 
 
@@ -1423,8 +1431,8 @@ struct Pipeline {
       vx_btiles_bound = w.n * ((proto.cap_points + kVxBTile - 1) / kVxBTile);
       vx_max_items = proto.cap_points / (kVxItemCap / 2) + 2;
       w.vx_bt.ensure(16 + 4 * vx_btiles_bound);
-      w.vx_bcnt.ensure(4ull * kVxBuckets * w.n);
-      w.vx_boff.ensure(4ull * (kVxBuckets + 1) * w.n);
+      w.vx_bcnt.ensure(4ull * vx_proto.bstride * w.n);
+      w.vx_boff.ensure(4ull * (vx_proto.bstride + 1) * w.n);
       w.vx_items.ensure(4ull * vx_max_items * w.n);
       w.vx_T.ensure(proto.handoff_stride * w.n);
       w.handoff_b.ensure(proto.handoff_stride * w.n);

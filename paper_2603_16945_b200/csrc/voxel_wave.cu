@@ -45,6 +45,7 @@ constexpr uint32_t kItems = 8;
 constexpr uint32_t kTile = kThreads * kItems;  // points / words per tile
 constexpr uint32_t kWarps = kThreads / 32;
 constexpr uint32_t kBThreads = 512;  // bucket histogram / scatter
+constexpr uint32_t kIThreads = 512;  // bucket-mode items
 
 __device__ __forceinline__ uint32_t ord_f(float x) {  // float order as unsigned order
   const uint32_t b = __float_as_uint(x);
@@ -344,7 +345,7 @@ __global__ void __launch_bounds__(kThreads) k_vx_plan(VxArgs v) {
   c.kb = kb;
   c.ib = ib;
   c.passes = (kb + 7) / 8;
-  c.bb = kb < kVxBucketBits ? kb : kVxBucketBits;
+  c.bb = kb < v.bucket_bits ? kb : v.bucket_bits;
   c.lowbits = kb - c.bb;
 }
 
@@ -750,7 +751,7 @@ __global__ void __launch_bounds__(kBThreads) k_vx_bhist(VxArgs v) {
     if (!c.active) continue;  // uniform
     const uint32_t nb = 1u << c.bb;
     const bool sm = nb <= kVxSmemBuckets;  // uniform
-    uint32_t* tot = v.boff + (uint64_t)s * (kVxBuckets + 1);
+    uint32_t* tot = v.boff + (uint64_t)s * (v.bstride + 1);
     if (sm) {
       for (uint32_t k = threadIdx.x; k < nb; k += kBThreads) h[k] = 0;
       __syncthreads();
@@ -787,8 +788,8 @@ __global__ void __launch_bounds__(1024) k_vx_bbase(VxArgs v) {
   VxCloud& c = v.cl[s];
   if (!c.active) return;
   const uint32_t nb = 1u << c.bb;
-  uint32_t* bo = v.boff + (uint64_t)s * (kVxBuckets + 1);
-  uint32_t* cur = v.bcur + (uint64_t)s * kVxBuckets;
+  uint32_t* bo = v.boff + (uint64_t)s * (v.bstride + 1);
+  uint32_t* cur = v.bcur + (uint64_t)s * v.bstride;
   const uint32_t per = (nb + blockDim.x - 1) / blockDim.x;  // <= 64
   uint32_t sum = 0, mx = 0;
   for (uint32_t q = 0; q < per; ++q) {
@@ -857,7 +858,7 @@ __global__ void __launch_bounds__(kBThreads) k_vx_bscatter(VxArgs v) {
     if (!c.active || !c.msd) continue;  // uniform
     const uint32_t nb = 1u << c.bb;
     const bool sm = nb <= kVxSmemBuckets;  // uniform
-    uint32_t* cur = v.bcur + (uint64_t)s * kVxBuckets;
+    uint32_t* cur = v.bcur + (uint64_t)s * v.bstride;
     if (sm) {
       for (uint32_t k = threadIdx.x; k < nb; k += kBThreads) h[k] = 0;
       __syncthreads();
@@ -933,22 +934,30 @@ __device__ __forceinline__ void item_range(const VxArgs& v, const VxCloud& c, ui
                                            uint32_t& b0, uint32_t& r0, uint32_t& r1) {
   constexpr uint32_t half = kVxItemCap / 2;
   const uint32_t nb = 1u << c.bb;
-  const uint32_t* bo = v.boff + (uint64_t)s * (kVxBuckets + 1);
+  const uint32_t* bo = v.boff + (uint64_t)s * (v.bstride + 1);
   b0 = lower_bound_u32(bo, nb, w * half);
   const uint32_t b1 = lower_bound_u32(bo, nb, (w + 1) * half);
   r0 = b0 < nb ? bo[b0] : c.kept;
   r1 = b1 < nb ? bo[b1] : c.kept;
 }
 
-// grid (max_items, n_samples): sort the item's records by key in shared
-// memory (stable: ties keep point order), find the voxels, and reduce each
-// voxel's run sequentially in double (App. C means) into T at r0 + voxel.
-__global__ void __launch_bounds__(kThreads) k_vx_item(VxArgs v) {
+// grid (max_items, n_samples), kIThreads threads: sort the item's records by
+// key in shared memory (dense items above kVxItemCap: in global memory, w2),
+// stage the payload in sorted order in shared memory (every voxel's run
+// contiguous), and reduce each voxel: count, first point (smallest index) for
+// gathered extra fields, and per float component the double sum -- order-free
+// under an exactness certificate (every value a multiple of 2^emin and
+// n * max|x| < 2^(53 + emin): every partial sum of every order is exact), else
+// replayed in point order (the App. C sequence).  Results to T[r0 + voxel],
+// compacted into A afterwards.
+__global__ void __launch_bounds__(kIThreads) k_vx_item(VxArgs v) {
   extern __shared__ __align__(16) uint8_t dyn[];
   uint64_t* sw0 = reinterpret_cast<uint64_t*>(dyn);
   uint64_t* sw1 = sw0 + kVxItemCap;
   uint32_t* scr = reinterpret_cast<uint32_t*>(sw1 + kVxItemCap);
-  __shared__ uint32_t sh[kWarps + 1];
+  uint32_t* pay = scr + kSortScratchBytes / 4;  // [kVxItemCap][v.pay_words]
+  constexpr uint32_t kIWarps = kIThreads / 32;
+  __shared__ uint32_t sh[kIWarps + 1];
   __shared__ unsigned long long red[32];
   const uint32_t s = blockIdx.y, w = blockIdx.x;
   const VxCloud& c = v.cl[s];
@@ -964,93 +973,109 @@ __global__ void __launch_bounds__(kThreads) k_vx_item(VxArgs v) {
   const uint64_t kbase = (uint64_t)b0 << c.lowbits;  // words = key << ib | point index
   const uint64_t* K = v.w0 + c.word0 + r0;
   const uint64_t imask = c.ib ? ((1ull << c.ib) - 1) : 0ull;
-  // an item above the shared-memory capacity (a dense bucket) sorts in
-  // global memory (w2: two words per point of the wave)
   const bool big = m > kVxItemCap;
   const uint32_t pb = big ? 32u - __clz(m - 1) : 12u;  // record position bits
   uint64_t* a0 = big ? v.w2 + 2 * c.word0 + r0 : sw0;
   uint64_t* a1 = big ? v.w2 + 2 * c.word0 + c.n + r0 : sw1;
   unsigned long long kmax = 0;
-  for (uint32_t j = threadIdx.x; j < m; j += kThreads) {
+  for (uint32_t j = threadIdx.x; j < m; j += kIThreads) {
     const uint64_t rel = (K[j] >> c.ib) - kbase;
     a0[j] = (rel << pb) | j;
     kmax = max(kmax, (unsigned long long)rel);
   }
   kmax = dev::block_reduce(kmax, dev::OpMax{}, 0ull, red);
   const uint32_t relbits = kmax ? 64u - __clzll(kmax) : 0u;
-  // by key only: inside a voxel the order is the scatter's, and the sums
-  // below are order-free when exact (else replayed in point order)
   const int r = relbits ? radix_sort8<4>(a0, a1, m, pb, pb + relbits, scr) : 0;
   const uint64_t* S = r ? a1 : a0;
   uint32_t* seg = reinterpret_cast<uint32_t*>(r ? a0 : a1);  // the free buffer
   const uint64_t pmask = (1ull << pb) - 1;
   __syncthreads();
   // voxel starts, numbered in order: thread-contiguous ranges, one block scan
-  const uint32_t per = (m + kThreads - 1) / kThreads;
-  const uint32_t ja = min(m, threadIdx.x * per), jb = min(m, ja + per);
-  uint32_t cnt = 0;
-  for (uint32_t j = ja; j < jb; ++j) cnt += (j == 0 || (S[j] >> pb) != (S[j - 1] >> pb)) ? 1u : 0u;
   uint32_t V;
-  uint32_t vid = block_excl_scan(cnt, sh, &V);
-  for (uint32_t j = ja; j < jb; ++j)
-    if (j == 0 || (S[j] >> pb) != (S[j - 1] >> pb)) seg[vid++] = j;
-  __syncthreads();
-  // payload into sorted order (T[r0 + k] = B[r0 + S[k]]): every voxel's run
-  // becomes contiguous; results go to B[r0 + voxel] (B's item range is dead
-  // after this gather) and are compacted into A afterwards
+  {
+    const uint32_t per = (m + kIThreads - 1) / kIThreads;
+    const uint32_t ja = min(m, threadIdx.x * per), jb = min(m, ja + per);
+    uint32_t cnt = 0;
+    for (uint32_t j = ja; j < jb; ++j) cnt += (j == 0 || (S[j] >> pb) != (S[j - 1] >> pb)) ? 1u : 0u;
+    const uint32_t lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+    uint32_t inc = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+      if ((int)lane >= o) inc += y;
+    }
+    if (lane == 31) sh[wp] = inc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t acc = 0;
+      for (uint32_t k = 0; k < kIWarps; ++k) {
+        const uint32_t cw = sh[k];
+        sh[k] = acc;
+        acc += cw;
+      }
+      sh[kIWarps] = acc;
+    }
+    __syncthreads();
+    uint32_t vid = sh[wp] + inc - cnt;
+    V = sh[kIWarps];
+    for (uint32_t j = ja; j < jb; ++j)
+      if (j == 0 || (S[j] >> pb) != (S[j - 1] >> pb)) seg[vid++] = j;
+  }
   uint8_t* B = v.B + (uint64_t)s * v.stride;
-  uint8_t* T = v.T + (uint64_t)s * v.stride;
   const uint32_t* ha = hdr(v, v.A, s);
   const uint32_t moved = v.mm & ha[1];
-  for (int f = 0; f < v.n_bytes_fields; ++f) {
-    if (!((moved >> f) & 1u)) continue;
-    const uint32_t es = ha[10 + f];
-    if ((es & 3u) == 0) {
+  // payload words of the moved fields: field f's words at pay offset fo[f]
+  const uint32_t PW = v.pay_words;
+  uint32_t fo[kMaxBytesFields];
+  {
+    uint32_t o = 0;
+    for (int f = 0; f < v.n_bytes_fields; ++f) {
+      fo[f] = o;
+      if ((moved >> f) & 1u) o += (ha[10 + f] + 3) / 4;
+    }
+  }
+  const bool staged = !big && v.pay_words > 0;
+  if (staged) {  // sorted-order payload into shared memory (independent loads)
+    for (int f = 0; f < v.n_bytes_fields; ++f) {
+      if (!((moved >> f) & 1u)) continue;
+      const uint32_t es = ha[10 + f];
+      if (es & 3u) continue;  // odd-sized extra fields are read from B directly
       const uint32_t wpp = es >> 2;
       const uint32_t* src = reinterpret_cast<const uint32_t*>(B + v.off[f]) + (uint64_t)r0 * wpp;
-      uint32_t* dst = reinterpret_cast<uint32_t*>(T + v.off[f]) + (uint64_t)r0 * wpp;
-      for (uint32_t e = threadIdx.x; e < m * wpp; e += kThreads) {
-        const uint32_t k = e / wpp, q = e - k * wpp;
-        dst[e] = src[(S[k] & pmask) * wpp + q];
-      }
-    } else {
-      for (uint32_t e = threadIdx.x; e < m * es; e += kThreads) {
-        const uint32_t k = e / es, q = e - k * es;
-        T[v.off[f] + (uint64_t)r0 * es + e] = B[v.off[f] + ((uint64_t)r0 + (S[k] & pmask)) * es + q];
+      for (uint32_t e0 = threadIdx.x; e0 < m * wpp; e0 += 4 * kIThreads) {
+        uint32_t x[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t e = e0 + u * kIThreads;
+          if (e < m * wpp) {
+            const uint32_t k = e / wpp, q = e - k * wpp;
+            x[u] = src[(S[k] & pmask) * wpp + q];
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t e = e0 + u * kIThreads;
+          if (e < m * wpp) {
+            const uint32_t k = e / wpp, q = e - k * wpp;
+            pay[k * PW + fo[f] + q] = x[u];
+          }
+        }
       }
     }
   }
   __syncthreads();
-  // point index of sorted position k (the order voxel sums fall back to)
-  auto pidx = [&](uint32_t k) -> uint64_t { return K[S[k] & pmask] & imask; };
-  // mean of one component over sorted positions [s0, s1): exact double sum
-  // in any order under the certificate, else replayed in point order
-  auto finish_mean = [&](const float* src, uint32_t comps, uint32_t q, uint32_t s0, uint32_t s1, double acc,
-                         int emin, int emax, bool finite) -> float {
-    const uint32_t n = s1 - s0;
-    const int nbits = 32 - __clz(n);
-    const bool exact = finite && (emax == -(1 << 20) || emax + 1 + nbits <= 53 + emin);
-    if (!exact) {
-      acc = 0.0;
-      uint64_t last = 0;
-      bool any = false;
-      for (uint32_t t2 = 0; t2 < n; ++t2) {  // next larger point index each round
-        uint64_t best = ~0ull;
-        uint32_t bk = s0;
-        for (uint32_t k = s0; k < s1; ++k) {
-          const uint64_t i = pidx(k);
-          if ((!any || i > last) && i < best) best = i, bk = k;
-        }
-        acc = __dadd_rn(acc, (double)src[(uint64_t)bk * comps + q]);
-        last = best;
-        any = true;
-      }
-    }
-    return __double2float_rn(__ddiv_rn(acc, (double)n));
+  // component q of field f at sorted position k
+  auto comp = [&](int f, uint32_t comps, uint32_t k, uint32_t q) -> float {
+    if (staged) return __uint_as_float(pay[k * PW + fo[f] + q]);
+    return reinterpret_cast<const float*>(B + v.off[f])[((uint64_t)r0 + (S[k] & pmask)) * comps + q];
   };
-  auto write_voxel = [&](uint32_t vx, uint32_t s0, uint32_t s1, bool warp_mode) {
+  auto pidx = [&](uint32_t k) -> uint64_t { return K[S[k] & pmask] & imask; };
+  // thread per small voxel, warp per large voxel; results to T[r0 + voxel]
+  uint8_t* T = v.T + (uint64_t)s * v.stride;
+  constexpr uint32_t kWarpVoxel = 64;
+  auto emit = [&](uint32_t vx, uint32_t s0, uint32_t s1, bool warp_mode) {
     const uint32_t lane = threadIdx.x & 31;
-    // the voxel's first point (smallest index) for gathered extra fields
+    const uint32_t n = s1 - s0;
     uint32_t first = s0;
     uint64_t first_i = ~0ull;
     for (uint32_t k = s0 + (warp_mode ? lane : 0); k < s1; k += warp_mode ? 32 : 1) {
@@ -1069,15 +1094,14 @@ __global__ void __launch_bounds__(kThreads) k_vx_item(VxArgs v) {
       const bool avg = f == v.role_data || f == v.role_normal || f == v.role_color || f == v.role_intensity;
       const uint32_t es = ha[10 + f];
       if (avg) {
-        const uint32_t comps = es / 4;  // 3 or 1
-        const float* src = reinterpret_cast<const float*>(T + v.off[f]) + (uint64_t)r0 * comps;
-        float* dst = reinterpret_cast<float*>(B + v.off[f]) + (uint64_t)(r0 + vx) * comps;
+        const uint32_t comps = es / 4;
+        float* dst = reinterpret_cast<float*>(T + v.off[f]) + (uint64_t)(r0 + vx) * comps;
         for (uint32_t q = 0; q < comps; ++q) {
           double acc = 0.0;
           int emin = 1 << 20, emax = -(1 << 20);
           bool finite = true;
           for (uint32_t k = s0 + (warp_mode ? lane : 0); k < s1; k += warp_mode ? 32 : 1) {
-            const float x = src[(uint64_t)k * comps + q];
+            const float x = comp(f, comps, k, q);
             acc = __dadd_rn(acc, (double)x);
             if (x != 0.0f) {
               if (!isfinite(x)) finite = false;
@@ -1096,26 +1120,49 @@ __global__ void __launch_bounds__(kThreads) k_vx_item(VxArgs v) {
             }
             finite = __all_sync(0xffffffffu, finite);
           }
-          if (!warp_mode || lane == 0) dst[q] = finish_mean(src, comps, q, s0, s1, acc, emin, emax, finite);
+          const int nbits = 32 - __clz(n);
+          const bool exact = finite && (emax == -(1 << 20) || emax + 1 + nbits <= 53 + emin);
+          if (!warp_mode || lane == 0) {
+            if (!exact) {  // replay in point order
+              acc = 0.0;
+              uint64_t last = 0;
+              bool any = false;
+              for (uint32_t t2 = 0; t2 < n; ++t2) {
+                uint64_t best = ~0ull;
+                uint32_t bk = s0;
+                for (uint32_t k = s0; k < s1; ++k) {
+                  const uint64_t i = pidx(k);
+                  if ((!any || i > last) && i < best) best = i, bk = k;
+                }
+                acc = __dadd_rn(acc, (double)comp(f, comps, bk, q));
+                last = best;
+                any = true;
+              }
+            }
+            dst[q] = __double2float_rn(__ddiv_rn(acc, (double)n));
+          }
         }
       } else if (!warp_mode || lane == 0) {  // gathered extra field: the voxel's first point
-        const uint8_t* src = T + v.off[f] + ((uint64_t)r0 + first) * es;
-        uint8_t* dst = B + v.off[f] + (uint64_t)(r0 + vx) * es;
-        for (uint32_t q = 0; q < es; ++q) dst[q] = src[q];
+        uint8_t* dst = T + v.off[f] + (uint64_t)(r0 + vx) * es;
+        if (staged && !(es & 3u)) {
+          for (uint32_t q = 0; q < es / 4; ++q)
+            reinterpret_cast<uint32_t*>(dst)[q] = pay[first * PW + fo[f] + q];
+        } else {
+          const uint8_t* src = B + v.off[f] + ((uint64_t)r0 + (S[first] & pmask)) * es;
+          for (uint32_t q = 0; q < es; ++q) dst[q] = src[q];
+        }
       }
     }
     if (v.counts && (!warp_mode || lane == 0))
-      reinterpret_cast<int32_t*>(B + v.off[kMaxBytesFields])[r0 + vx] = (int32_t)(s1 - s0);
+      reinterpret_cast<int32_t*>(T + v.off[kMaxBytesFields])[r0 + vx] = (int32_t)n;
   };
-  // small voxels: one thread each; large ones (> 64 points): one warp each
-  constexpr uint32_t kWarpVoxel = 64;
-  for (uint32_t vx = threadIdx.x; vx < V; vx += kThreads) {
+  for (uint32_t vx = threadIdx.x; vx < V; vx += kIThreads) {
     const uint32_t s0 = seg[vx], s1 = vx + 1 < V ? seg[vx + 1] : m;
-    if (s1 - s0 <= kWarpVoxel) write_voxel(vx, s0, s1, false);
+    if (s1 - s0 <= kWarpVoxel) emit(vx, s0, s1, false);
   }
-  for (uint32_t vx = threadIdx.x >> 5; vx < V; vx += kWarps) {
+  for (uint32_t vx = threadIdx.x >> 5; vx < V; vx += kIWarps) {
     const uint32_t s0 = seg[vx], s1 = vx + 1 < V ? seg[vx + 1] : m;
-    if (s1 - s0 > kWarpVoxel) write_voxel(vx, s0, s1, true);
+    if (s1 - s0 > kWarpVoxel) emit(vx, s0, s1, true);
   }
   if (threadIdx.x == 0) iv[w] = V;
 }
@@ -1142,7 +1189,7 @@ __global__ void __launch_bounds__(kThreads) k_vx_iscan(VxArgs v) {
   if (threadIdx.x == 0) c.V = carry;
 }
 
-// grid (max_items, n_samples): voxel results of item w from B[r0 ..] to A at
+// grid (max_items, n_samples): voxel results of item w from T[r0 ..] to A at
 // the item's voxel offset.
 __global__ void __launch_bounds__(kThreads) k_vx_compact(VxArgs v) {
   const uint32_t s = blockIdx.y, w = blockIdx.x;
@@ -1153,7 +1200,7 @@ __global__ void __launch_bounds__(kThreads) k_vx_compact(VxArgs v) {
   const uint32_t* iv = v.item_v + (uint64_t)s * v.max_items;
   const uint32_t vo = iv[w], vn = (w + 1 < c.n_items ? iv[w + 1] : c.V) - vo;
   if (!vn) return;
-  const uint8_t* T = v.B + (uint64_t)s * v.stride;  // (results were left in B)
+  const uint8_t* T = v.T + (uint64_t)s * v.stride;
   uint8_t* A = v.A + (uint64_t)s * v.stride;
   const uint32_t* ha = hdr(v, v.A, s);
   const uint32_t moved = v.mm & ha[1];
@@ -1200,20 +1247,21 @@ __global__ void k_vx_finish(VxArgs v) {
 
 }  // namespace
 
-constexpr size_t kItemSmem = 2 * 8 * kVxItemCap + kSortScratchBytes;
-
-size_t voxel_wave_item_smem() { return kItemSmem; }
+size_t voxel_wave_item_smem(uint32_t pay_words) {
+  return 2 * 8 * kVxItemCap + kSortScratchBytes + 4ull * kVxItemCap * pay_words;
+}
 
 cudaError_t launch_voxel_wave(const VxArgs& v, uint32_t tiles_bound, uint32_t btiles_bound, int sms,
                               cudaStream_t st) {
   if (!v.n_samples) return cudaSuccess;
   static const bool attrs = [] {
-    cudaFuncSetAttribute(k_vx_item, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kItemSmem);
+    cudaFuncSetAttribute(k_vx_item, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)voxel_wave_item_smem(kVxMaxPayWords));
     return true;
   }();
   (void)attrs;
   cudaMemsetAsync(v.cl, 0, sizeof(VxCloud) * v.n_samples, st);
-  cudaMemsetAsync(v.boff, 0, 4ull * (kVxBuckets + 1) * v.n_samples, st);
+  cudaMemsetAsync(v.boff, 0, 4ull * (v.bstride + 1) * v.n_samples, st);
   cudaMemsetAsync(v.any_lsd, 0, 4, st);
   k_vx_prep<<<1, 1024, 0, st>>>(v);
   const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(tiles_bound, (uint32_t)sms * 8));
@@ -1224,7 +1272,7 @@ cudaError_t launch_voxel_wave(const VxArgs& v, uint32_t tiles_bound, uint32_t bt
   k_vx_bhist<<<bgrid, kBThreads, 0, st>>>(v);
   k_vx_bbase<<<v.n_samples, 1024, 0, st>>>(v);
   k_vx_bscatter<<<bgrid, kBThreads, 0, st>>>(v);
-  k_vx_item<<<dim3(v.max_items, v.n_samples), kThreads, kItemSmem, st>>>(v);
+  k_vx_item<<<dim3(v.max_items, v.n_samples), kIThreads, voxel_wave_item_smem(v.pay_words), st>>>(v);
   k_vx_iscan<<<v.n_samples, kThreads, 0, st>>>(v);
   k_vx_compact<<<dim3(v.max_items, v.n_samples), kThreads, 0, st>>>(v);
   // global LSD mode (the other clouds)

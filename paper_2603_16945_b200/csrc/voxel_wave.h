@@ -10,11 +10,11 @@
 namespace pcp {
 
 constexpr uint32_t kVxMaxPasses = 6;  // 8-bit digits: keys up to 48 bits (wider: k_cloud fallback)
-constexpr uint32_t kVxBucketBits = 16;  // bucket mode: up to 16 top key bits
-constexpr uint32_t kVxBuckets = 1u << kVxBucketBits;
+constexpr uint32_t kVxMaxBucketBits = 20;  // bucket mode: up to 20 top key bits (1 Mi buckets)
 constexpr uint32_t kVxSmemBuckets = 4096;  // histograms / ranks in shared memory up to this many
+constexpr uint32_t kVxMaxPayWords = 8;     // staged payload per record (32 B): else read from B
 constexpr uint32_t kVxBTile = 4096;    // bucket mode: points per scatter tile
-constexpr uint32_t kVxItemCap = 4096;  // bucket mode: records per work item (shared memory)
+constexpr uint32_t kVxItemCap = 2048;  // bucket mode: records per work item (shared memory)
 
 // Arguments of the stage (by value).  A = decoded clouds (hand-off slots of
 // the decode-only k_cloud launch), voxelized in place by the stage (the rest
@@ -51,8 +51,11 @@ struct VxArgs {
   // bucket mode scratch
   uint32_t* total_btiles;
   uint32_t* btile_cloud;  // [btiles]
-  uint32_t* bcur;         // [n_samples][kVxBuckets]: bucket write cursors
-  uint32_t* boff;         // [n_samples][kVxBuckets + 1]: bucket totals -> offsets
+  uint32_t bucket_bits;   // per-cloud bucket bits cap (<= kVxMaxBucketBits)
+  uint32_t bstride;       // 1 << bucket_bits
+  uint32_t pay_words;     // staged payload words per record (0: not staged)
+  uint32_t* bcur;         // [n_samples][bstride]: bucket write cursors
+  uint32_t* boff;         // [n_samples][bstride + 1]: bucket totals -> offsets
   uint32_t* any_lsd;      // a cloud of the wave takes the global LSD sort
   uint32_t* item_v;       // [n_samples][max_items]: voxels per item -> voxel offsets
   uint32_t max_items;
@@ -68,8 +71,8 @@ struct VxArgs {
 // ceil(points / voxel_wave_tile_points())).
 cudaError_t launch_voxel_wave(const VxArgs& v, uint32_t tiles_bound, uint32_t btiles_bound, int sms,
                               cudaStream_t st);
-// Dynamic shared memory of the bucket-mode item kernel (set once per device).
-size_t voxel_wave_item_smem();
+// Dynamic shared memory of the bucket-mode item kernel.
+size_t voxel_wave_item_smem(uint32_t pay_words);
 uint32_t voxel_wave_tile_points();
 
 }  // namespace pcp
