@@ -152,6 +152,9 @@ class Ref:
         L.ref_bench_composed.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_uint32, u64p,
                                          C.c_size_t, C.POINTER(C.c_double), C.POINTER(C.c_uint64),
                                          C.POINTER(C.c_uint64), C.POINTER(C.c_double)]
+        L.ref_simulate_dp.argtypes = [C.c_char_p, C.c_uint32, C.c_uint64, C.c_uint32,
+                                      C.POINTER(C.c_double), C.c_size_t, C.c_double,
+                                      C.POINTER(C.c_double)]
         L.ref_free.argtypes = [C.c_void_p]
 
     def _check(self, st):
@@ -281,6 +284,15 @@ class Ref:
                                               C.byref(cpu)))
         return {"cost_time_s": t.value, "items": items.value, "batches": batches.value,
                 "avg_cpu_percent": cpu.value}
+
+
+    def simulate_dp(self, primary, num_devices, epochs, per_device_batch, params, lr):
+        """simulate_data_parallel (distributed.cpp:88-164): final params, max divergence."""
+        p = (C.c_double * len(params))(*params)
+        div = C.c_double()
+        self._check(self.L.ref_simulate_dp(str(primary).encode(), num_devices, epochs, per_device_batch,
+                                           p, len(params), lr, C.byref(div)))
+        return list(p), div.value
 
 
 # --------------------------------------------------------------------------- Orc

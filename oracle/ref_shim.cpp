@@ -539,3 +539,30 @@ int ref_bench_composed(const char* primary, const char* graph_json, const char* 
 }
 
 }  // extern "C"
+
+extern "C" {
+
+// simulate_data_parallel (distributed.cpp:88-164) over the dataset's samples
+// in index order; final parameters of device 0 into params (in/out).
+int ref_simulate_dp(const char* primary, std::uint32_t num_devices, std::uint64_t epochs,
+                    std::uint32_t per_device_batch, double* params, std::size_t dim, double lr,
+                    double* max_divergence) {
+  return guarded([&] {
+    DatasetReader rd(primary);
+    IndexTable idx = build_index({rd.header()});
+    std::vector<Sample> ds;
+    for (std::size_t i = 0; i < idx.size(); ++i) ds.push_back(rd.read_sample(idx.sample_meta_list[i]));
+    ToyModel m;
+    m.params.assign(params, params + dim);
+    m.learning_rate = lr;
+    SimOptions o;
+    o.num_devices = num_devices;
+    o.num_epochs = epochs;
+    o.per_device_batch = per_device_batch;
+    const SimReport r = simulate_data_parallel(ds, m, o);
+    for (std::size_t j = 0; j < dim; ++j) params[j] = r.device_params[0][j];
+    *max_divergence = r.max_param_divergence;
+  });
+}
+
+}  // extern "C"
