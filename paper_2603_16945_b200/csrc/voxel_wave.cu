@@ -783,52 +783,60 @@ __global__ void __launch_bounds__(kBThreads) k_vx_bhist(VxArgs v) {
 // op_voxel runs the ops).
 __global__ void __launch_bounds__(1024) k_vx_bbase(VxArgs v) {
   __shared__ uint32_t wsum[33];
-  __shared__ uint32_t wmax[32];
+  __shared__ uint32_t carry, mxs;
   const uint32_t s = blockIdx.x;
   VxCloud& c = v.cl[s];
   if (!c.active) return;
   const uint32_t nb = 1u << c.bb;
   uint32_t* bo = v.boff + (uint64_t)s * (v.bstride + 1);
   uint32_t* cur = v.bcur + (uint64_t)s * v.bstride;
-  const uint32_t per = (nb + blockDim.x - 1) / blockDim.x;  // <= 64
-  uint32_t sum = 0, mx = 0;
-  for (uint32_t q = 0; q < per; ++q) {
-    const uint32_t b = threadIdx.x * per + q;
-    const uint32_t x = b < nb ? bo[b] : 0;
-    sum += x;
-    mx = max(mx, x);
-  }
+  if (threadIdx.x == 0) carry = 0, mxs = 0;
+  __syncthreads();
   const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const uint32_t inc = warp_incl_scan(sum);
+  // chunks of 4 x 1024 buckets: 4 contiguous per thread (one 16-B load)
+  for (uint32_t c0 = 0; c0 < nb; c0 += 4096) {
+    const uint32_t b = c0 + 4 * threadIdx.x;
+    uint4 x = make_uint4(0u, 0u, 0u, 0u);
+    if (b + 3 < nb) x = *reinterpret_cast<const uint4*>(bo + b);
+    else if (b < nb) {
+      x.x = bo[b];
+      if (b + 1 < nb) x.y = bo[b + 1];
+      if (b + 2 < nb) x.z = bo[b + 2];
+    }
+    const uint32_t sum = x.x + x.y + x.z + x.w;
+    uint32_t mx = max(max(x.x, x.y), max(x.z, x.w));
+    const uint32_t inc = warp_incl_scan(sum);
 #pragma unroll
-  for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if (lane == 31) wsum[w] = inc;
-  if (lane == 0) wmax[w] = mx;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t acc = 0, m = 0;
-    for (uint32_t k = 0; k < blockDim.x / 32; ++k) {
-      const uint32_t cw = wsum[k];
-      wsum[k] = acc;
-      acc += cw;
-      m = max(m, wmax[k]);
+    for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 31) wsum[w] = inc;
+    if (lane == 0) atomicMax(&mxs, mx);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t acc = carry;
+      for (uint32_t k = 0; k < 32; ++k) {
+        const uint32_t cw = wsum[k];
+        wsum[k] = acc;
+        acc += cw;
+      }
+      wsum[32] = acc;
     }
-    wsum[32] = acc;
-    wmax[0] = m;
-  }
-  __syncthreads();
-  uint32_t run = wsum[w] + inc - sum;
-  for (uint32_t q = 0; q < per; ++q) {
-    const uint32_t b = threadIdx.x * per + q;
-    if (b < nb) {
-      const uint32_t x = bo[b];
-      bo[b] = cur[b] = run;
-      run += x;
+    __syncthreads();
+    uint32_t run = wsum[w] + inc - sum;
+    const uint4 o = make_uint4(run, run + x.x, run + x.x + x.y, run + x.x + x.y + x.z);
+    if (b + 3 < nb) {
+      *reinterpret_cast<uint4*>(bo + b) = o;
+      *reinterpret_cast<uint4*>(cur + b) = o;
+    } else if (b < nb) {
+      const uint32_t oo[4] = {o.x, o.y, o.z, o.w};
+      for (uint32_t q = 0; b + q < nb; ++q) bo[b + q] = cur[b + q] = oo[q];
     }
+    __syncthreads();
+    if (threadIdx.x == 0) carry = wsum[32];
+    __syncthreads();
   }
   if (threadIdx.x == 0) {
-    bo[nb] = wsum[32];  // == kept
-    c.max_bucket = wmax[0];
+    bo[nb] = carry;  // == kept
+    c.max_bucket = mxs;
     const uint32_t pb = c.kept > 1 ? max(12u, 32u - __clz(c.kept - 1)) : 12u;  // item position bits, worst case
     const bool fits = v.msd_enabled && c.lowbits + c.bb + pb <= 64 && c.kb + c.ib <= 64;
     c.msd = fits ? 1u : 0u;
@@ -959,11 +967,13 @@ __global__ void __launch_bounds__(kIThreads) k_vx_item(VxArgs v) {
   constexpr uint32_t kIWarps = kIThreads / 32;
   __shared__ uint32_t sh[kIWarps + 1];
   __shared__ unsigned long long red[32];
+  __shared__ uint32_t rng[3];
   const uint32_t s = blockIdx.y, w = blockIdx.x;
   const VxCloud& c = v.cl[s];
   if (!c.active || !c.msd || w >= c.n_items) return;
-  uint32_t b0, r0, r1;
-  item_range(v, c, s, w, b0, r0, r1);
+  if (threadIdx.x == 0) item_range(v, c, s, w, rng[0], rng[1], rng[2]);  // two binary searches, once
+  __syncthreads();
+  const uint32_t b0 = rng[0], r0 = rng[1], r1 = rng[2];
   const uint32_t m = r1 - r0;
   uint32_t* iv = v.item_v + (uint64_t)s * v.max_items;
   if (m == 0) {
@@ -1192,11 +1202,13 @@ __global__ void __launch_bounds__(kThreads) k_vx_iscan(VxArgs v) {
 // grid (max_items, n_samples): voxel results of item w from T[r0 ..] to A at
 // the item's voxel offset.
 __global__ void __launch_bounds__(kThreads) k_vx_compact(VxArgs v) {
+  __shared__ uint32_t rng[3];
   const uint32_t s = blockIdx.y, w = blockIdx.x;
   const VxCloud& c = v.cl[s];
   if (!c.active || !c.msd || w >= c.n_items) return;
-  uint32_t b0, r0, r1;
-  item_range(v, c, s, w, b0, r0, r1);
+  if (threadIdx.x == 0) item_range(v, c, s, w, rng[0], rng[1], rng[2]);
+  __syncthreads();
+  const uint32_t r0 = rng[1];
   const uint32_t* iv = v.item_v + (uint64_t)s * v.max_items;
   const uint32_t vo = iv[w], vn = (w + 1 < c.n_items ? iv[w + 1] : c.V) - vo;
   if (!vn) return;
