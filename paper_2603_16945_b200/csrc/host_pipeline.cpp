@@ -1432,7 +1432,7 @@ struct Pipeline {
       vx_max_items = proto.cap_points / (kVxItemCap / 2) + 2;
       w.vx_bt.ensure(16 + 4 * vx_btiles_bound);
       w.vx_bcnt.ensure(4ull * vx_proto.bstride * w.n);
-      w.vx_boff.ensure(4ull * (vx_proto.bstride + 1) * w.n);
+      w.vx_boff.ensure(4ull * (vx_proto.bstride + 4) * w.n);  // per-cloud rows 16-B aligned
       w.vx_items.ensure(4ull * vx_max_items * w.n);
       w.vx_T.ensure(proto.handoff_stride * w.n);
       w.handoff_b.ensure(proto.handoff_stride * w.n);

@@ -751,7 +751,7 @@ __global__ void __launch_bounds__(kBThreads) k_vx_bhist(VxArgs v) {
     if (!c.active) continue;  // uniform
     const uint32_t nb = 1u << c.bb;
     const bool sm = nb <= kVxSmemBuckets;  // uniform
-    uint32_t* tot = v.boff + (uint64_t)s * (v.bstride + 1);
+    uint32_t* tot = v.boff + (uint64_t)s * (v.bstride + 4);
     if (sm) {
       for (uint32_t k = threadIdx.x; k < nb; k += kBThreads) h[k] = 0;
       __syncthreads();
@@ -788,7 +788,7 @@ __global__ void __launch_bounds__(1024) k_vx_bbase(VxArgs v) {
   VxCloud& c = v.cl[s];
   if (!c.active) return;
   const uint32_t nb = 1u << c.bb;
-  uint32_t* bo = v.boff + (uint64_t)s * (v.bstride + 1);
+  uint32_t* bo = v.boff + (uint64_t)s * (v.bstride + 4);
   uint32_t* cur = v.bcur + (uint64_t)s * v.bstride;
   if (threadIdx.x == 0) carry = 0, mxs = 0;
   __syncthreads();
@@ -942,7 +942,7 @@ __device__ __forceinline__ void item_range(const VxArgs& v, const VxCloud& c, ui
                                            uint32_t& b0, uint32_t& r0, uint32_t& r1) {
   constexpr uint32_t half = kVxItemCap / 2;
   const uint32_t nb = 1u << c.bb;
-  const uint32_t* bo = v.boff + (uint64_t)s * (v.bstride + 1);
+  const uint32_t* bo = v.boff + (uint64_t)s * (v.bstride + 4);
   b0 = lower_bound_u32(bo, nb, w * half);
   const uint32_t b1 = lower_bound_u32(bo, nb, (w + 1) * half);
   r0 = b0 < nb ? bo[b0] : c.kept;
@@ -1273,7 +1273,7 @@ cudaError_t launch_voxel_wave(const VxArgs& v, uint32_t tiles_bound, uint32_t bt
   }();
   (void)attrs;
   cudaMemsetAsync(v.cl, 0, sizeof(VxCloud) * v.n_samples, st);
-  cudaMemsetAsync(v.boff, 0, 4ull * (v.bstride + 1) * v.n_samples, st);
+  cudaMemsetAsync(v.boff, 0, 4ull * (v.bstride + 4) * v.n_samples, st);
   cudaMemsetAsync(v.any_lsd, 0, 4, st);
   k_vx_prep<<<1, 1024, 0, st>>>(v);
   const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(tiles_bound, (uint32_t)sms * 8));

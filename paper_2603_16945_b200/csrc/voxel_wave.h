@@ -55,7 +55,7 @@ struct VxArgs {
   uint32_t bstride;       // 1 << bucket_bits
   uint32_t pay_words;     // staged payload words per record (0: not staged)
   uint32_t* bcur;         // [n_samples][bstride]: bucket write cursors
-  uint32_t* boff;         // [n_samples][bstride + 1]: bucket totals -> offsets
+  uint32_t* boff;         // [n_samples][bstride + 4]: bucket totals -> offsets (+ total)
   uint32_t* any_lsd;      // a cloud of the wave takes the global LSD sort
   uint32_t* item_v;       // [n_samples][max_items]: voxels per item -> voxel offsets
   uint32_t max_items;
