@@ -1090,9 +1090,10 @@ struct Pipeline {
     v.vx_first = first;
     v.vx_last = last;
     v.max_passes = kVxMaxPasses;
-    // bucket bits: ~4 points per bucket on average, <= 20 bits
+    // bucket bits: ~1-2 points per bucket on average (dense surfaces still
+    // split into shared-memory items), <= 20 bits
     const uint32_t cap_bits = 32u - (uint32_t)__builtin_clz(std::max<uint32_t>(a.cap_points, 2) - 1);
-    v.bucket_bits = std::min<uint32_t>(kVxMaxBucketBits, cap_bits > 2 ? cap_bits - 2 : 1);
+    v.bucket_bits = std::min<uint32_t>(kVxMaxBucketBits, cap_bits);
     v.bstride = 1u << v.bucket_bits;
     uint32_t pw = 0;
     for (int f = 0; f < a.n_bytes_fields; ++f)
