@@ -1752,7 +1752,7 @@ __device__ __forceinline__ int32_t run_chain(const WaveArgs& a, Cloud& c, Smem& 
         case kDownsample: status = op_downsample(a, c, S, op, seed); break;
         case kFps: status = op_fps<MinBlocks>(a, c, S, op); break;
         case kRangeCrop: status = op_range_crop(a, c, S, op); break;
-        case kVoxel: status = op_voxel<MinBlocks == 1 ? 4 : 1>(a, c, S, op); break;
+        case kVoxel: status = op_voxel<MinBlocks == 1 ? 8 : 4>(a, c, S, op); break;
         default: status = kUnknownOp; break;
       }
     }
