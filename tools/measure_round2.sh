@@ -7,7 +7,7 @@ set -u
 TAG=${1:-r2}
 OUT=gpurun_out/$TAG
 mkdir -p $OUT
-B=$(git rev-parse --short HEAD 2>/dev/null || cat .build_id 2>/dev/null || echo unknown)
+B=$(cat .build_id 2>/dev/null || echo unknown)  # written by the caller before gpurun (no .git on the box)
 nproc > $OUT/nproc.txt
 lscpu | grep -E "Model name|^CPU\(s\)" > $OUT/lscpu.txt 2>/dev/null
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $OUT/smi.txt 2>&1

@@ -24,8 +24,12 @@ for r in rows:
         hdr = r
         continue
     if hdr and len(r) == len(hdr):
+        if r[hdr.index("Metric Name")] != "gpu__time_duration.sum":
+            continue  # launch lists may carry DRAM byte counts too
         k = r[hdr.index("Kernel Name")].split("(")[0].replace("void ", "")
-        v = float(r[hdr.index("Metric Value")].replace(",", ""))
+        unit = r[hdr.index("Metric Unit")] if "Metric Unit" in hdr else "ns"
+        v = float(r[hdr.index("Metric Value")].replace(",", "")) * {"ns": 1, "nsecond": 1, "us": 1e3,
+                                                                   "usecond": 1e3, "ms": 1e6, "msecond": 1e6}.get(unit, 1)
         a = agg.setdefault(k, [0, 0.0])
         a[0] += 1
         a[1] += v
