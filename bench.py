@@ -45,16 +45,17 @@ CONFIGS = {
     "shapenet_part": dict(gen="shapenet", kw={"n_points": 2048}, clouds=16384, group=64, batch=32, cpu_sample=4096,
                           points=2048, desc="ShapeNet-part-shaped 2048-pt clouds + per-point seg "
                           "labels: normalize, downsample 1024 (+seg), random_scale, shuffle; B 32"),
-    "modelnet40": dict(gen="modelnet", kw={"n_points": 10000}, clouds=2048, group=32, batch=32, cpu_sample=256,
+    "modelnet40": dict(gen="modelnet", kw={"n_points": 10000}, clouds=2048, group=32, group_q=8, batch=32,
+                       cpu_sample=256,
                        points=10000, desc="ModelNet40-shaped 10k-pt clouds + normals: normalize, "
                        "FPS 1024, rotate, jitter; B 32"),
-    "kitti": dict(gen="kitti", kw={}, clouds=512, group=16, batch=4, points=120000, cpu_sample=64,
+    "kitti": dict(gen="kitti", kw={}, clouds=512, group=16, group_q=1, batch=4, points=120000, cpu_sample=64,
                   desc="KITTI-shaped ~120k-pt XYZI frames: range crop, voxel 0.05 m (+counts), "
                   "rotate, flip_yz; B 4 (CSR batches)"),
     "s3dis": dict(gen="s3dis", kw={"mean_points": 1_000_000}, clouds=256, group=1, batch=4, cpu_sample=32,
                   points=1_000_000, desc="S3DIS-shaped ~1M-pt XYZRGB rooms: grid 0.04 m, "
                   "random_crop, downsample 4096; B 4"),
-    "scannet": dict(gen="scannet", kw={}, clouds=192, group=4, batch=4, points=275000, cpu_sample=16,
+    "scannet": dict(gen="scannet", kw={}, clouds=192, group=4, group_q=1, batch=4, points=275000, cpu_sample=16,
                     desc="ScanNet-shaped 50k-500k-pt XYZRGB scenes: grid 0.02 m, downsample "
                     "40000, FPS 20000; B 4"),
 }
@@ -96,7 +97,7 @@ def dataset(cfg_name, cfg, world, quantized, rank, barrier):
     8 slices) to local disk with the library's writer (byte-identical to the
     reference's write_dataset, tests/test_host.py); every rank then opens it."""
     from paper_2603_16945_b200 import write_dataset
-    d = f"/tmp/pcp_bench_{cfg_name}_{'q' if quantized else 'raw'}_{cfg['clouds']}x{world}"
+    d = f"/tmp/pcp_bench_{cfg_name}_{'q' if quantized else 'raw'}_{cfg['clouds']}x{world}_g{cfg['group']}"
     primary = os.path.join(d, "ds.pcrecord")
     if rank == 0:
         schema, samples = gen_samples(cfg, cfg["clouds"] * world, quantized)
@@ -111,7 +112,7 @@ def reference_dataset(cfg_name, cfg, quantized, n):
     """The reference arm's input: n clouds of the same workload written by the
     REFERENCE writer (oracle/_ref write_dataset, format.cpp:499-610)."""
     from oracle.ffi import Ref
-    d = f"/tmp/pcp_refarm_{cfg_name}_{'q' if quantized else 'raw'}_{n}"
+    d = f"/tmp/pcp_refarm_{cfg_name}_{'q' if quantized else 'raw'}_{n}_g{cfg['group']}"
     schema, samples = gen_samples(cfg, n, quantized)
     return Ref().write_dataset(d, "ds", schema, samples, slice_count=SLICES, group_size=cfg["group"])
 
@@ -296,8 +297,16 @@ def main():
     ap.add_argument("--e2e-no-d2h", action="store_true", help="diagnostics: e2e without the batch reads")
     ap.add_argument("--cpu-sample", type=int, default=0, help="clouds per CPU step")
     ap.add_argument("--batch", type=int, default=0, help="override the config's batch size (diagnostics)")
+    ap.add_argument("--group", type=int, default=0, help="override the writer's group size (samples per page)")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
+    # quantized pages are one LZ4 block each, decoded by one serial token chain:
+    # those variants are written with ~2 MB pages where the config allows
+    # (SURVEY.md §7 hard part 1: "choose G per config for the quantized variant")
+    if args.quantized and "group_q" in cfg:
+        cfg["group"] = cfg["group_q"]
+    if args.group:
+        cfg["group"] = args.group
     if args.batch:
         cfg["batch"] = args.batch
     if args.clouds_per_gpu:
