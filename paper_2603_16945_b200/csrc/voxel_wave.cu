@@ -988,14 +988,65 @@ __global__ void __launch_bounds__(kIThreads) k_vx_item(VxArgs v) {
   uint64_t* a0 = big ? v.w2 + 2 * c.word0 + r0 : sw0;
   uint64_t* a1 = big ? v.w2 + 2 * c.word0 + c.n + r0 : sw1;
   unsigned long long kmax = 0;
-  for (uint32_t j = threadIdx.x; j < m; j += kIThreads) {
-    const uint64_t rel = (K[j] >> c.ib) - kbase;
-    a0[j] = (rel << pb) | j;
-    kmax = max(kmax, (unsigned long long)rel);
-  }
+  for (uint32_t j = threadIdx.x; j < m; j += kIThreads)
+    kmax = max(kmax, (unsigned long long)((K[j] >> c.ib) - kbase));
   kmax = dev::block_reduce(kmax, dev::OpMax{}, 0ull, red);
   const uint32_t relbits = kmax ? 64u - __clzll(kmax) : 0u;
-  const int r = relbits ? radix_sort8<4>(a0, a1, m, pb, pb + relbits, scr) : 0;
+  int r;
+  if (relbits <= 12) {
+    // few distinct keys (dense voxels): counting sort by key in shared
+    // memory -- order inside a key is arbitrary, the sums are order-free
+    // under the certificate and the first point is a min over the run
+    uint32_t* hist = scr;  // <= 4096 counters
+    const uint32_t range = 1u << relbits;
+    for (uint32_t k = threadIdx.x; k < range; k += kIThreads) hist[k] = 0;
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < m; j += kIThreads) atomicAdd(&hist[(K[j] >> c.ib) - kbase], 1u);
+    __syncthreads();
+    {
+      const uint32_t per = (range + kIThreads - 1) / kIThreads;  // <= 8
+      uint32_t x[8], sum = 0;
+      for (uint32_t q = 0; q < per; ++q) {
+        const uint32_t k = threadIdx.x * per + q;
+        x[q] = k < range ? hist[k] : 0u;
+        sum += x[q];
+      }
+      const uint32_t lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+      uint32_t inc = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if ((int)lane >= o) inc += y;
+      }
+      if (lane == 31) sh[wp] = inc;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        uint32_t acc = 0;
+        for (uint32_t k = 0; k < kIWarps; ++k) {
+          const uint32_t cw = sh[k];
+          sh[k] = acc;
+          acc += cw;
+        }
+      }
+      __syncthreads();
+      uint32_t run = sh[wp] + inc - sum;
+      for (uint32_t q = 0; q < per; ++q) {
+        const uint32_t k = threadIdx.x * per + q;
+        if (k < range) hist[k] = run;
+        run += x[q];
+      }
+    }
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < m; j += kIThreads) {
+      const uint64_t rel = (K[j] >> c.ib) - kbase;
+      a1[atomicAdd(&hist[rel], 1u)] = (rel << pb) | j;
+    }
+    r = 1;
+  } else {
+    for (uint32_t j = threadIdx.x; j < m; j += kIThreads) a0[j] = (((K[j] >> c.ib) - kbase) << pb) | j;
+    __syncthreads();
+    r = radix_sort8<4>(a0, a1, m, pb, pb + relbits, scr);
+  }
   const uint64_t* S = r ? a1 : a0;
   uint32_t* seg = reinterpret_cast<uint32_t*>(r ? a0 : a1);  // the free buffer
   const uint64_t pmask = (1ull << pb) - 1;
