@@ -148,6 +148,13 @@ int pcp_apply_map(int kind, const char* params_json, const pcp_cloud_set* in,
 int pcp_write_dataset(const char* out_dir, const char* stem, const char* schema_json,
                       const uint8_t* samples_tlv, size_t tlv_len, uint32_t n_samples,
                       uint32_t slice_count, uint32_t group_size, uint32_t n_threads);
+/* The same files with every page encoded on `device` (XOR-delta columns, the
+ * reference's greedy LZ4 compressor, stored-raw fallback, payload CRC-32:
+ * encode_block_page / encode_scalar_page, format.cpp:198-274, and
+ * lz4::compress, lz4_block.cpp:33-103), byte-identical. */
+int pcp_write_dataset_device(const char* out_dir, const char* stem, const char* schema_json,
+                             const uint8_t* samples_tlv, size_t tlv_len, uint32_t n_samples,
+                             uint32_t slice_count, uint32_t group_size, int device);
 
 /* ---- pipeline (pipeline.hpp:157-186) -----------------------------------
  * Opens <primary>.pcrecord (+ continuation slices), parses the reference

@@ -76,6 +76,8 @@ def lib():
         L.pcp_map_kind_from_name.argtypes = [C.c_char_p, C.POINTER(C.c_int)]
         L.pcp_write_dataset.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p, C.c_size_t,
                                         C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32]
+        L.pcp_write_dataset_device.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p, C.c_size_t,
+                                               C.c_uint32, C.c_uint32, C.c_uint32, C.c_int]
         L.pcp_pipeline_open.argtypes = [C.c_char_p, C.c_char_p, C.POINTER(C.c_uint64), C.c_uint64,
                                         C.c_int, C.c_char_p, C.POINTER(C.c_void_p)]
         L.pcp_pipeline_open_source.argtypes = [C.c_char_p, C.c_size_t, C.c_char_p, C.POINTER(C.c_uint64),
@@ -137,11 +139,16 @@ def encode_samples(samples: list) -> bytes:
 
 
 def write_dataset(out_dir, stem: str, schema: dict, samples: list, slice_count: int = 1,
-                  group_size: int = 256, n_threads: int = 0) -> str:
-    """write_dataset (format.cpp:499-610), byte-identical to the reference."""
+                  group_size: int = 256, n_threads: int = 0, device: int | None = None) -> str:
+    """write_dataset (format.cpp:499-610), byte-identical to the reference;
+    ``device``: encode the pages on that GPU (pcp_write_dataset_device)."""
     tlv = encode_samples(samples)
-    _check(lib().pcp_write_dataset(str(out_dir).encode(), stem.encode(), json.dumps(schema).encode(),
-                                   tlv, len(tlv), len(samples), slice_count, group_size, n_threads))
+    if device is None:
+        _check(lib().pcp_write_dataset(str(out_dir).encode(), stem.encode(), json.dumps(schema).encode(),
+                                       tlv, len(tlv), len(samples), slice_count, group_size, n_threads))
+    else:
+        _check(lib().pcp_write_dataset_device(str(out_dir).encode(), stem.encode(), json.dumps(schema).encode(),
+                                              tlv, len(tlv), len(samples), slice_count, group_size, device))
     return os.path.join(str(out_dir), stem + ".pcrecord")
 
 

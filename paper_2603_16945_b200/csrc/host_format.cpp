@@ -5,6 +5,11 @@
 // (tests/test_format_host.py checks byte identity against the reference).
 #include "host_format.h"
 
+#include <cuda_runtime.h>
+
+#include "kernels.h"
+#include "page_encode.h"
+
 #include <algorithm>
 #include <cstring>
 #include <filesystem>
@@ -368,13 +373,22 @@ std::vector<uint8_t> finish_page(std::vector<uint8_t> post, uint64_t raw_len, ui
   return out;
 }
 
-EncodedGroup encode_group(const std::vector<FieldSpec>& schema,
-                          const std::vector<SampleIn>& samples, uint64_t first, uint32_t count) {
-  EncodedGroup eg;
-  Group& g = eg.g;
+// A group's raw pages and metadata (write_dataset :536-569) before encoding:
+// the block page (blobs of every sample, bytes fields in schema order), its
+// XOR-delta columns (delta_columns_for_group, :483-493) and the scalar page.
+struct RawGroup {
+  Group g;
+  std::vector<uint8_t> block, scalar;
+  std::vector<std::pair<uint64_t, uint64_t>> cols;  // (offset, length), width 4
+};
+
+RawGroup build_group(const std::vector<FieldSpec>& schema, const std::vector<SampleIn>& samples,
+                     uint64_t first, uint32_t count) {
+  RawGroup rg;
+  Group& g = rg.g;
   g.first_sample = first;
   g.sample_count = count;
-  std::vector<uint8_t> block;
+  std::vector<uint8_t>& block = rg.block;
   for (uint32_t r = 0; r < count; ++r) {
     const SampleIn& s = samples[first + r];
     const uint64_t start = block.size();
@@ -387,7 +401,7 @@ EncodedGroup encode_group(const std::vector<FieldSpec>& schema,
     g.blob_ranges.push_back({start, block.size()});
     g.blob_lens.push_back(std::move(lens));
   }
-  std::vector<uint8_t> scalar;  // append_scalar_record (:384-418)
+  std::vector<uint8_t>& scalar = rg.scalar;  // append_scalar_record (:384-418)
   for (uint32_t r = 0; r < count; ++r) {
     const SampleIn& s = samples[first + r];
     put<uint64_t>(scalar, g.blob_ranges[r][0]);
@@ -400,35 +414,209 @@ EncodedGroup encode_group(const std::vector<FieldSpec>& schema,
       scalar.insert(scalar.end(), s.values[f].begin(), s.values[f].end());
     }
   }
-  // XOR-delta columns (delta_columns_for_group, :483-493) encoded in place
-  bool any = false;
-  std::vector<uint8_t> work = block;
   for (uint32_t r = 0; r < count; ++r) {
     uint64_t at = g.blob_ranges[r][0];
     for (auto len : g.blob_lens[r]) {
-      if (len >= 8 && len % 4 == 0) {
-        any = true;
-        for (uint64_t i = len; i >= 8; i -= 4) {
-          uint32_t cur, prv;
-          std::memcpy(&cur, block.data() + at + i - 4, 4);
-          std::memcpy(&prv, block.data() + at + i - 8, 4);
-          cur ^= prv;
-          std::memcpy(work.data() + at + i - 4, &cur, 4);
-        }
-      }
+      if (len >= 8 && len % 4 == 0) rg.cols.push_back({at, len});
       at += len;
     }
   }
-  eg.scalar = finish_page(scalar, scalar.size(), 0);
-  eg.block = finish_page(std::move(work), block.size(), any ? kFlagInnerDelta : 0);
+  return rg;
+}
+
+EncodedGroup encode_group(const std::vector<FieldSpec>& schema,
+                          const std::vector<SampleIn>& samples, uint64_t first, uint32_t count) {
+  RawGroup rg = build_group(schema, samples, first, count);
+  EncodedGroup eg;
+  eg.g = std::move(rg.g);
+  std::vector<uint8_t> work = rg.block;  // XOR-delta columns encoded in place
+  for (const auto& [at, len] : rg.cols)
+    for (uint64_t i = len; i >= 8; i -= 4) {
+      uint32_t cur, prv;
+      std::memcpy(&cur, rg.block.data() + at + i - 4, 4);
+      std::memcpy(&prv, rg.block.data() + at + i - 8, 4);
+      cur ^= prv;
+      std::memcpy(work.data() + at + i - 4, &cur, 4);
+    }
+  eg.scalar = finish_page(rg.scalar, rg.scalar.size(), 0);
+  eg.block = finish_page(std::move(work), rg.block.size(), rg.cols.empty() ? 0 : kFlagInnerDelta);
   return eg;
+}
+
+// The same pages encoded on the device (page_encode.cu), in batches of about
+// 256 MB of raw pages: identical bytes.
+std::vector<EncodedGroup> encode_groups_device(const std::vector<FieldSpec>& schema,
+                                               const std::vector<SampleIn>& samples, uint32_t group_size,
+                                               uint64_t num_groups, uint32_t n_threads, int device) {
+  int n_dev = 0;
+  if (cudaGetDeviceCount(&n_dev) != cudaSuccess || n_dev == 0)
+    fail(kIoFailure, "no CUDA device: the device writer has no CPU fallback");
+  if (device < 0 || device >= n_dev) fail(kOutOfBounds, "device index out of range");
+  if (cudaSetDevice(device) != cudaSuccess) fail(kIoFailure, "cudaSetDevice failed");
+  std::vector<RawGroup> raw(num_groups);
+  {
+    std::vector<std::thread> th;
+    const uint32_t nt = std::max<uint32_t>(1, std::min<uint64_t>(n_threads, num_groups));
+    for (uint32_t t = 0; t < nt; ++t)
+      th.emplace_back([&, t] {
+        for (uint64_t gi = t; gi < num_groups; gi += nt) {
+          const uint64_t first = gi * group_size;
+          raw[gi] = build_group(schema, samples, first,
+                                (uint32_t)std::min<uint64_t>(group_size, samples.size() - first));
+        }
+      });
+    for (auto& t : th) t.join();
+  }
+  std::vector<EncodedGroup> enc(num_groups);
+  for (uint64_t gi = 0; gi < num_groups; ++gi) enc[gi].g = raw[gi].g;
+  auto CKD = [](cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(kIoFailure, std::string("CUDA ") + what + ": " + cudaGetErrorString(e));
+  };
+  std::vector<uint32_t> shift(kShiftEntries);
+  build_shift_table(shift.data());
+  uint32_t* d_shift = nullptr;
+  CKD(cudaMalloc(&d_shift, shift.size() * 4), "malloc");
+  CKD(cudaMemcpy(d_shift, shift.data(), shift.size() * 4, cudaMemcpyHostToDevice), "memcpy");
+  // page list: scalar page then block page per group
+  struct P {
+    uint64_t g;
+    bool block;
+  };
+  std::vector<P> all;
+  for (uint64_t gi = 0; gi < num_groups; ++gi) all.push_back({gi, false}), all.push_back({gi, true});
+  const uint64_t kBatch = 256ull << 20;
+  size_t k = 0;
+  while (k < all.size()) {
+    size_t e = k;
+    uint64_t bytes = 0;
+    while (e < all.size()) {
+      const auto& pg = all[e].block ? raw[all[e].g].block : raw[all[e].g].scalar;
+      if (e > k && bytes + pg.size() > kBatch) break;
+      bytes += (pg.size() + 15) & ~uint64_t(15);
+      ++e;
+    }
+    const uint32_t np = (uint32_t)(e - k);
+    std::vector<EncPage> pages(np);
+    std::vector<EncColumn> cols;
+    std::vector<int> hb(np), he(np);
+    uint64_t raw_at = 0, hash_at = 0, vis_at = 0, seq_at = 0, comp_at = 0;
+    for (uint32_t i = 0; i < np; ++i) {
+      const RawGroup& rg = raw[all[k + i].g];
+      const auto& pg = all[k + i].block ? rg.block : rg.scalar;
+      EncPage& p = pages[i];
+      p.raw_off = raw_at;
+      p.raw_len = pg.size();
+      const uint64_t nh = pg.size() > 12 ? pg.size() - 12 : 0;
+      p.hash_off = hash_at;
+      hb[i] = (int)hash_at;
+      he[i] = (int)(hash_at + nh);
+      p.vis_off = vis_at;
+      p.seq_off = seq_at;
+      p.comp_off = comp_at;
+      raw_at += (pg.size() + 15) & ~uint64_t(15);
+      hash_at += nh;
+      vis_at += nh / 32 + 2;
+      seq_at += pg.size() / 4 + 2;
+      comp_at += pg.size() + pg.size() / 255 + 64;
+      if (all[k + i].block)
+        for (const auto& [off, len] : rg.cols) cols.push_back({off, len, i, 0});
+    }
+    if (hash_at > (uint64_t)INT32_MAX) fail(kOutOfBounds, "page batch too large");
+    const EncScratchSizes z = enc_scratch_sizes(raw_at, hash_at, np);
+    std::vector<uint8_t> h_raw(raw_at + 16);
+    for (uint32_t i = 0; i < np; ++i) {
+      const auto& pg = all[k + i].block ? raw[all[k + i].g].block : raw[all[k + i].g].scalar;
+      if (!pg.empty()) std::memcpy(h_raw.data() + pages[i].raw_off, pg.data(), pg.size());
+    }
+    // one device allocation carved into the buffers
+    auto al = [](uint64_t v) { return (v + 255) & ~uint64_t(255); };
+    uint64_t o = 0;
+    const uint64_t o_raw = o; o += al(raw_at + 16);
+    const uint64_t o_work = o; o += al(raw_at + 16);
+    const uint64_t o_pages = o; o += al(sizeof(EncPage) * np);
+    const uint64_t o_cols = o; o += al(sizeof(EncColumn) * cols.size() + 16);
+    const uint64_t o_keys = o; o += al(z.keys + 16);
+    const uint64_t o_keys2 = o; o += al(z.keys + 16);
+    const uint64_t o_vals = o; o += al(z.vals + 16);
+    const uint64_t o_vals2 = o; o += al(z.vals + 16);
+    const uint64_t o_hb = o; o += al(4ull * np);
+    const uint64_t o_he = o; o += al(4ull * np);
+    const uint64_t o_prev = o; o += al(z.prev + 16);
+    const uint64_t o_vis = o; o += al(4 * vis_at + 16);
+    const uint64_t o_seqs = o; o += al(sizeof(EncSeq) * seq_at + 16);
+    const uint64_t o_nseq = o; o += al(4ull * np);
+    const uint64_t o_comp = o; o += al(comp_at + 16);
+    const uint64_t o_clen = o; o += al(8ull * np);
+    const uint64_t o_crc = o; o += al(4ull * np);
+    const uint64_t o_cub = o; o += al(z.cub);
+    uint8_t* d = nullptr;
+    CKD(cudaMalloc(&d, o), "malloc");
+    EncArgs a{};
+    a.n_pages = np;
+    a.n_cols = (uint32_t)cols.size();
+    a.raw_total = raw_at;
+    a.hash_total = hash_at;
+    a.raw = d + o_raw;
+    a.work = d + o_work;
+    a.pages = reinterpret_cast<const EncPage*>(d + o_pages);
+    a.cols = reinterpret_cast<const EncColumn*>(d + o_cols);
+    a.keys = reinterpret_cast<uint32_t*>(d + o_keys);
+    a.keys_alt = reinterpret_cast<uint32_t*>(d + o_keys2);
+    a.vals = reinterpret_cast<uint32_t*>(d + o_vals);
+    a.vals_alt = reinterpret_cast<uint32_t*>(d + o_vals2);
+    a.hash_begin = reinterpret_cast<const int*>(d + o_hb);
+    a.hash_end = reinterpret_cast<const int*>(d + o_he);
+    a.prev = reinterpret_cast<uint32_t*>(d + o_prev);
+    a.visited = reinterpret_cast<uint32_t*>(d + o_vis);
+    a.visited_bytes = 4 * vis_at;
+    a.seqs = reinterpret_cast<EncSeq*>(d + o_seqs);
+    a.n_seqs = reinterpret_cast<uint32_t*>(d + o_nseq);
+    a.comp = d + o_comp;
+    a.comp_len = reinterpret_cast<uint64_t*>(d + o_clen);
+    a.crc = reinterpret_cast<uint32_t*>(d + o_crc);
+    a.shift_tab = d_shift;
+    a.cub = d + o_cub;
+    a.cub_bytes = z.cub;
+    CKD(cudaMemcpy(d + o_raw, h_raw.data(), raw_at, cudaMemcpyHostToDevice), "memcpy");
+    CKD(cudaMemcpy(d + o_pages, pages.data(), sizeof(EncPage) * np, cudaMemcpyHostToDevice), "memcpy");
+    if (!cols.empty())
+      CKD(cudaMemcpy(d + o_cols, cols.data(), sizeof(EncColumn) * cols.size(), cudaMemcpyHostToDevice), "memcpy");
+    CKD(cudaMemcpy(d + o_hb, hb.data(), 4ull * np, cudaMemcpyHostToDevice), "memcpy");
+    CKD(cudaMemcpy(d + o_he, he.data(), 4ull * np, cudaMemcpyHostToDevice), "memcpy");
+    CKD(launch_encode_pages(a, nullptr), "page encode");
+    CKD(cudaDeviceSynchronize(), "page encode");
+    std::vector<uint64_t> clen(np);
+    std::vector<uint32_t> crc(np);
+    CKD(cudaMemcpy(clen.data(), d + o_clen, 8ull * np, cudaMemcpyDeviceToHost), "memcpy");
+    CKD(cudaMemcpy(crc.data(), d + o_crc, 4ull * np, cudaMemcpyDeviceToHost), "memcpy");
+    for (uint32_t i = 0; i < np; ++i) {
+      const P& pp = all[k + i];
+      const RawGroup& rg = raw[pp.g];
+      const bool lz = clen[i] < pages[i].raw_len;  // finish_page: LZ4 only when it shrinks
+      const uint64_t pay = lz ? clen[i] : pages[i].raw_len;
+      std::vector<uint8_t> out(kPageHeaderBytes + pay);
+      const uint8_t flags = (pp.block && !rg.cols.empty() ? kFlagInnerDelta : 0) | (lz ? kFlagOuterLz4 : kFlagStoredRaw);
+      out[0] = flags;
+      std::memcpy(out.data() + 1, &pages[i].raw_len, 8);
+      std::memcpy(out.data() + 9, &pay, 8);
+      std::memcpy(out.data() + 17, &crc[i], 4);
+      if (pay)
+        CKD(cudaMemcpy(out.data() + kPageHeaderBytes, d + (lz ? o_comp + pages[i].comp_off : o_work + pages[i].raw_off),
+                       pay, cudaMemcpyDeviceToHost), "memcpy");
+      (pp.block ? enc[pp.g].block : enc[pp.g].scalar) = std::move(out);
+    }
+    cudaFree(d);
+    k = e;
+  }
+  cudaFree(d_shift);
+  return enc;
 }
 
 }  // namespace
 
 Header write_dataset(const std::vector<FieldSpec>& schema, const std::vector<SampleIn>& samples,
                      uint32_t slice_count, uint32_t group_size, const std::string& out_dir,
-                     const std::string& stem, uint32_t n_threads) {
+                     const std::string& stem, uint32_t n_threads, int device) {
   validate_schema(schema);
   if (samples.empty()) fail(kEmptyDataset, "no samples to write");
   if (slice_count < 1 || group_size < 1) fail(kOutOfBounds, "slice_count and group_size must be >= 1");
@@ -452,18 +640,23 @@ Header write_dataset(const std::vector<FieldSpec>& schema, const std::vector<Sam
   }
   const uint64_t num_groups = (samples.size() + group_size - 1) / group_size;
   const uint64_t groups_per_slice = (num_groups + slice_count - 1) / slice_count;
-  std::vector<EncodedGroup> enc(num_groups);
-  n_threads = std::max<uint32_t>(1, std::min<uint64_t>(n_threads, num_groups));
-  std::vector<std::thread> th;
-  for (uint32_t t = 0; t < n_threads; ++t)
-    th.emplace_back([&, t] {
-      for (uint64_t gi = t; gi < num_groups; gi += n_threads) {
-        const uint64_t first = gi * group_size;
-        const uint32_t cnt = (uint32_t)std::min<uint64_t>(group_size, samples.size() - first);
-        enc[gi] = encode_group(schema, samples, first, cnt);
-      }
-    });
-  for (auto& t : th) t.join();
+  std::vector<EncodedGroup> enc;
+  if (device >= 0) {
+    enc = encode_groups_device(schema, samples, group_size, num_groups, n_threads, device);
+  } else {
+    enc.resize(num_groups);
+    n_threads = std::max<uint32_t>(1, std::min<uint64_t>(n_threads, num_groups));
+    std::vector<std::thread> th;
+    for (uint32_t t = 0; t < n_threads; ++t)
+      th.emplace_back([&, t] {
+        for (uint64_t gi = t; gi < num_groups; gi += n_threads) {
+          const uint64_t first = gi * group_size;
+          const uint32_t cnt = (uint32_t)std::min<uint64_t>(group_size, samples.size() - first);
+          enc[gi] = encode_group(schema, samples, first, cnt);
+        }
+      });
+    for (auto& t : th) t.join();
+  }
 
   Header h;
   h.schema = schema;

@@ -91,9 +91,10 @@ struct SampleIn {
   // string characters)
   std::vector<std::vector<uint8_t>> values;
 };
+// device >= 0: the pages are encoded on that GPU (page_encode.cu), same bytes.
 Header write_dataset(const std::vector<FieldSpec>& schema, const std::vector<SampleIn>& samples,
                      uint32_t slice_count, uint32_t group_size, const std::string& out_dir,
-                     const std::string& stem, uint32_t n_threads);
+                     const std::string& stem, uint32_t n_threads, int device = -1);
 
 std::vector<FieldSpec> schema_from_json(const std::string& json_text);
 

@@ -2141,9 +2141,30 @@ int pcp_apply_map(int kind, const char* params_json, const pcp_cloud_set* in,
   });
 }
 
+namespace {
+int write_dataset_impl(const char* out_dir, const char* stem, const char* schema_json, const uint8_t* tlv,
+                       size_t tlv_len, uint32_t n_samples, uint32_t slice_count, uint32_t group_size,
+                       uint32_t n_threads, int device);
+}
+
 int pcp_write_dataset(const char* out_dir, const char* stem, const char* schema_json,
                       const uint8_t* tlv, size_t tlv_len, uint32_t n_samples,
                       uint32_t slice_count, uint32_t group_size, uint32_t n_threads) {
+  return write_dataset_impl(out_dir, stem, schema_json, tlv, tlv_len, n_samples, slice_count, group_size,
+                            n_threads, -1);
+}
+
+int pcp_write_dataset_device(const char* out_dir, const char* stem, const char* schema_json,
+                             const uint8_t* tlv, size_t tlv_len, uint32_t n_samples,
+                             uint32_t slice_count, uint32_t group_size, int device) {
+  return write_dataset_impl(out_dir, stem, schema_json, tlv, tlv_len, n_samples, slice_count, group_size,
+                            16, device);
+}
+
+namespace {
+int write_dataset_impl(const char* out_dir, const char* stem, const char* schema_json, const uint8_t* tlv,
+                       size_t tlv_len, uint32_t n_samples, uint32_t slice_count, uint32_t group_size,
+                       uint32_t n_threads, int device) {
   return guarded([&] {
     const auto schema = schema_from_json(schema_json);
     std::vector<SampleIn> samples(n_samples);
@@ -2182,9 +2203,10 @@ int pcp_write_dataset(const char* out_dir, const char* stem, const char* schema_
       for (size_t f = 0; f < schema.size(); ++f)
         if (!seen[f]) fail(kSchemaMismatch, "missing field '" + schema[f].name + "'");
     }
-    write_dataset(schema, samples, slice_count, group_size, out_dir, stem, n_threads ? n_threads : 8);
+    write_dataset(schema, samples, slice_count, group_size, out_dir, stem, n_threads ? n_threads : 8, device);
   });
 }
+}  // namespace
 
 int pcp_pipeline_open(const char* primary, const char* graph_json, const uint64_t* ids,
                       uint64_t n_ids, int device, const char* options, pcp_pipeline** out) {
