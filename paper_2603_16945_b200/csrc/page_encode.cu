@@ -15,8 +15,9 @@
 //   prev    prev[p] = the previous position with the same hash (any, visited
 //           or not) -> the table lookup becomes a walk down prev[] past
 //           positions inside emitted matches (a visited bitmap)
-//   parse   one thread per page: the reference's loop over positions with
-//           prev[] + bitmap instead of the table; records the sequences
+//   parse   one warp per page: the reference's loop over positions with
+//           prev[] + bitmap instead of the table, 32 positions speculated per
+//           step (the first matching one wins); records the sequences
 //   emit    CTA per page: token/length bytes and literals in parallel at
 //           offsets from a block scan over the sequences' output sizes
 //   crc     the existing CTA-cooperative CRC over the chosen payload
@@ -90,13 +91,20 @@ __global__ void k_enc_prev(const uint32_t* keys, const uint32_t* vals, const Enc
   }
 }
 
-// The reference parse (lz4_block.cpp:75-99), one thread per page.  table[h]
+// The reference parse (lz4_block.cpp:75-99), one WARP per page.  table[h]
 // == the last VISITED position with hash h: walk prev[] down from the
 // previous same-hash position past positions inside emitted matches.
+// Lanes speculate on 32 consecutive positions ip..ip+31: if no match starts
+// before position ip+k, positions ip..ip+k-1 are all visited, so lane k's
+// candidate is the walk from prev[ip+k] that stops at any position >= ip.
+// The first lane whose candidate matches is where the serial parse takes
+// its match (ballot); the lanes before it are literals.  Match extension
+// compares 32 bytes per step.
 __global__ void k_enc_parse(const uint8_t* work, const EncPage* pages, uint32_t n_pages, const uint32_t* prev,
                             uint32_t* visited, EncSeq* seqs, uint32_t* n_seqs) {
-  const uint32_t pi = blockIdx.x * blockDim.x + threadIdx.x;
-  if (pi >= n_pages) return;
+  const uint32_t pi = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const uint32_t lane = threadIdx.x & 31;
+  if (pi >= n_pages) return;  // warp-uniform
   const EncPage pg = pages[pi];
   const uint8_t* src = work + pg.raw_off;
   const uint64_t n = pg.raw_len;
@@ -108,22 +116,51 @@ __global__ void k_enc_parse(const uint8_t* work, const EncPage* pages, uint32_t 
   if (n > kMfLimit) {
     const uint64_t match_limit = n - kMfLimit, end_limit = n - kLastLiterals;
     while (ip < match_limit) {
-      uint32_t cand = pv[ip];
-      while (cand != kNone && !((vis[cand >> 5] >> (cand & 31)) & 1u)) cand = pv[cand];
-      vis[ip >> 5] |= 1u << (ip & 31);  // table[h] = ip
-      if (cand != kNone && ip - cand <= kMaxOffset && read32u(src + cand) == read32u(src + ip)) {
-        uint64_t m = ip + kMinMatch, r = cand + kMinMatch;
-        while (m < end_limit && src[m] == src[r]) ++m, ++r;
-        out[ns++] = EncSeq{(uint32_t)anchor, (uint32_t)(ip - anchor), (uint32_t)(m - ip), (uint32_t)(ip - cand)};
-        ip = m;
-        anchor = ip;
-      } else {
-        ++ip;
+      const uint64_t p = ip + lane;
+      bool hit = false;
+      uint32_t cand = kNone;
+      if (p < match_limit) {
+        cand = pv[p];
+        while (cand != kNone && cand < ip && !((vis[cand >> 5] >> (cand & 31)) & 1u)) cand = pv[cand];
+        hit = cand != kNone && p - cand <= kMaxOffset && read32u(src + cand) == read32u(src + p);
       }
+      const uint32_t hits = __ballot_sync(0xffffffffu, hit);
+      const uint32_t valid = __ballot_sync(0xffffffffu, p < match_limit);
+      const uint32_t k = hits ? __ffs(hits) - 1 : 32u;  // first match lane (or none in this window)
+      // positions ip .. ip+k (inclusive of the match start) become visited
+      const uint32_t upto = min(k + (hits ? 1u : 0u), (uint32_t)__popc(valid));
+      if (lane < upto) atomicOr(&vis[p >> 5], 1u << (p & 31));
+      __syncwarp();
+      if (!hits) {
+        ip += upto;
+        continue;
+      }
+      const uint64_t s0 = ip + k;
+      const uint32_t c0 = __shfl_sync(0xffffffffu, cand, k);
+      // extend: m = s0 + 4 .. end_limit while src[m] == src[r], 32 bytes per step
+      uint64_t m = s0 + kMinMatch, r = (uint64_t)c0 + kMinMatch;
+      while (true) {
+        const uint64_t mm = m + lane;
+        const bool eq = mm < end_limit && src[mm] == src[r + lane];
+        const uint32_t neq = ~__ballot_sync(0xffffffffu, eq);
+        if (neq) {
+          m += __ffs(neq) - 1;
+          break;
+        }
+        m += 32;
+        r += 32;
+      }
+      if (lane == 0)
+        out[ns] = EncSeq{(uint32_t)anchor, (uint32_t)(s0 - anchor), (uint32_t)(m - s0), (uint32_t)(s0 - c0)};
+      ++ns;
+      ip = m;
+      anchor = ip;
     }
   }
-  out[ns++] = EncSeq{(uint32_t)anchor, (uint32_t)(n - anchor), 0u, 0u};  // trailing literals
-  n_seqs[pi] = ns;
+  if (lane == 0) {
+    out[ns] = EncSeq{(uint32_t)anchor, (uint32_t)(n - anchor), 0u, 0u};  // trailing literals
+    n_seqs[pi] = ns + 1;
+  }
 }
 
 __device__ __forceinline__ uint64_t ext_bytes(uint64_t len) {  // put_len_ext for len >= 15
@@ -269,8 +306,8 @@ cudaError_t launch_encode_pages(const EncArgs& e, cudaStream_t st) {
       e.hash_begin, e.hash_end, 0, 16, st);
   if (err != cudaSuccess) return err;
   k_enc_prev<<<g2, 256, 0, st>>>(e.keys_alt, e.vals_alt, e.pages, e.n_pages, e.prev);
-  k_enc_parse<<<(e.n_pages + 63) / 64, 64, 0, st>>>(e.work, e.pages, e.n_pages, e.prev, e.visited, e.seqs,
-                                                    e.n_seqs);
+  k_enc_parse<<<(e.n_pages + 3) / 4, 128, 0, st>>>(e.work, e.pages, e.n_pages, e.prev, e.visited, e.seqs,
+                                                  e.n_seqs);
   k_enc_emit<<<e.n_pages, 512, 0, st>>>(e.work, e.pages, e.seqs, e.n_seqs, e.comp, e.comp_len);
   k_enc_crc<<<std::min<uint32_t>(e.n_pages, 1024), 256, 0, st>>>(e.work, e.comp, e.pages, e.n_pages, e.comp_len,
                                                                  e.shift_tab, e.crc);
