@@ -491,7 +491,7 @@ std::vector<EncodedGroup> encode_groups_device(const std::vector<FieldSpec>& sch
     uint64_t bytes = 0;
     while (e < all.size()) {
       const auto& pg = all[e].block ? raw[all[e].g].block : raw[all[e].g].scalar;
-      if (e > k && bytes + pg.size() > kBatch) break;
+      if (e > k && (bytes + pg.size() > kBatch || e - k >= 4096)) break;  // 256 KB hash table per page
       bytes += (pg.size() + 15) & ~uint64_t(15);
       ++e;
     }
@@ -542,7 +542,7 @@ std::vector<EncodedGroup> encode_groups_device(const std::vector<FieldSpec>& sch
     const uint64_t o_hb = o; o += al(4ull * np);
     const uint64_t o_he = o; o += al(4ull * np);
     const uint64_t o_prev = o; o += al(z.prev + 16);
-    const uint64_t o_vis = o; o += al(4 * vis_at + 16);
+    const uint64_t o_vis = o; o += al(z.visited + 16);
     const uint64_t o_seqs = o; o += al(sizeof(EncSeq) * seq_at + 16);
     const uint64_t o_nseq = o; o += al(4ull * np);
     const uint64_t o_comp = o; o += al(comp_at + 16);
@@ -568,7 +568,7 @@ std::vector<EncodedGroup> encode_groups_device(const std::vector<FieldSpec>& sch
     a.hash_end = reinterpret_cast<const int*>(d + o_he);
     a.prev = reinterpret_cast<uint32_t*>(d + o_prev);
     a.visited = reinterpret_cast<uint32_t*>(d + o_vis);
-    a.visited_bytes = 4 * vis_at;
+    a.visited_bytes = z.visited;
     a.seqs = reinterpret_cast<EncSeq*>(d + o_seqs);
     a.n_seqs = reinterpret_cast<uint32_t*>(d + o_nseq);
     a.comp = d + o_comp;

@@ -15,9 +15,10 @@
 //   prev    prev[p] = the previous position with the same hash (any, visited
 //           or not) -> the table lookup becomes a walk down prev[] past
 //           positions inside emitted matches (a visited bitmap)
-//   parse   one warp per page: the reference's loop over positions with
-//           prev[] + bitmap instead of the table, 32 positions speculated per
-//           step (the first matching one wins); records the sequences
+//   parse   one warp per page: the reference's loop with its hash table,
+//           32 positions speculated per step (candidates inside the step's
+//           literal run come from prev[]; the first matching lane wins);
+//           records the sequences
 //   emit    CTA per page: token/length bytes and literals in parallel at
 //           offsets from a block scan over the sequences' output sizes
 //   crc     the existing CTA-cooperative CRC over the chosen payload
@@ -91,17 +92,17 @@ __global__ void k_enc_prev(const uint32_t* keys, const uint32_t* vals, const Enc
   }
 }
 
-// The reference parse (lz4_block.cpp:75-99), one WARP per page.  table[h]
-// == the last VISITED position with hash h: walk prev[] down from the
-// previous same-hash position past positions inside emitted matches.
-// Lanes speculate on 32 consecutive positions ip..ip+31: if no match starts
-// before position ip+k, positions ip..ip+k-1 are all visited, so lane k's
-// candidate is the walk from prev[ip+k] that stops at any position >= ip.
-// The first lane whose candidate matches is where the serial parse takes
-// its match (ballot); the lanes before it are literals.  Match extension
-// compares 32 bytes per step.
+// The reference parse (lz4_block.cpp:75-99), one WARP per page, with the
+// reference's hash table (last VISITED position per 16-bit hash, stored +1
+// so 0 = empty) in global memory.  Lanes speculate on 32 consecutive
+// positions ip..ip+31: if no match starts before ip+k, positions ip..ip+k-1
+// are visited too, so lane k's candidate is its previous same-hash position
+// when that lies in [ip, ip+k) (prev[]), else the table entry.  The first
+// lane whose candidate matches is where the serial parse takes its match
+// (ballot); positions ip..ip+k are inserted (atomicMax: later positions win).
+// Match extension compares 32 bytes per step.
 __global__ void k_enc_parse(const uint8_t* work, const EncPage* pages, uint32_t n_pages, const uint32_t* prev,
-                            uint32_t* visited, EncSeq* seqs, uint32_t* n_seqs) {
+                            const uint32_t* hashes, uint32_t* table, EncSeq* seqs, uint32_t* n_seqs) {
   const uint32_t pi = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const uint32_t lane = threadIdx.x & 31;
   if (pi >= n_pages) return;  // warp-uniform
@@ -109,7 +110,8 @@ __global__ void k_enc_parse(const uint8_t* work, const EncPage* pages, uint32_t 
   const uint8_t* src = work + pg.raw_off;
   const uint64_t n = pg.raw_len;
   const uint32_t* pv = prev + pg.hash_off;
-  uint32_t* vis = visited + pg.vis_off;
+  const uint32_t* hs = hashes + pg.hash_off;
+  uint32_t* tab = table + (uint64_t)pi * 65536;
   EncSeq* out = seqs + pg.seq_off;
   uint32_t ns = 0;
   uint64_t ip = 0, anchor = 0;
@@ -118,18 +120,23 @@ __global__ void k_enc_parse(const uint8_t* work, const EncPage* pages, uint32_t 
     while (ip < match_limit) {
       const uint64_t p = ip + lane;
       bool hit = false;
-      uint32_t cand = kNone;
+      uint32_t cand = kNone, h = 0;
       if (p < match_limit) {
-        cand = pv[p];
-        while (cand != kNone && cand < ip && !((vis[cand >> 5] >> (cand & 31)) & 1u)) cand = pv[cand];
+        h = hs[p];
+        const uint32_t pp = pv[p];
+        if (pp != kNone && pp >= ip) {
+          cand = pp;  // visited in this speculative literal run
+        } else {
+          const uint32_t t = tab[h];
+          cand = t ? t - 1 : kNone;
+        }
         hit = cand != kNone && p - cand <= kMaxOffset && read32u(src + cand) == read32u(src + p);
       }
       const uint32_t hits = __ballot_sync(0xffffffffu, hit);
       const uint32_t valid = __ballot_sync(0xffffffffu, p < match_limit);
-      const uint32_t k = hits ? __ffs(hits) - 1 : 32u;  // first match lane (or none in this window)
-      // positions ip .. ip+k (inclusive of the match start) become visited
+      const uint32_t k = hits ? __ffs(hits) - 1 : 32u;
       const uint32_t upto = min(k + (hits ? 1u : 0u), (uint32_t)__popc(valid));
-      if (lane < upto) atomicOr(&vis[p >> 5], 1u << (p & 31));
+      if (lane < upto) atomicMax(&tab[h], (uint32_t)p + 1u);  // table[h] = p for the visited positions
       __syncwarp();
       if (!hits) {
         ip += upto;
@@ -137,7 +144,6 @@ __global__ void k_enc_parse(const uint8_t* work, const EncPage* pages, uint32_t 
       }
       const uint64_t s0 = ip + k;
       const uint32_t c0 = __shfl_sync(0xffffffffu, cand, k);
-      // extend: m = s0 + 4 .. end_limit while src[m] == src[r], 32 bytes per step
       uint64_t m = s0 + kMinMatch, r = (uint64_t)c0 + kMinMatch;
       while (true) {
         const uint64_t mm = m + lane;
@@ -276,7 +282,7 @@ EncScratchSizes enc_scratch_sizes(uint64_t raw_total, uint64_t hash_total, uint3
   z.keys = 4 * hash_total;
   z.vals = 4 * hash_total;
   z.prev = 4 * hash_total;
-  z.visited = 4 * (hash_total / 32 + 2ull * n_pages + 1);
+  z.visited = 4ull * 65536 * n_pages;  // per-page hash tables
   z.seqs = sizeof(EncSeq) * (raw_total / kMinMatch + 2ull * n_pages);
   z.comp = raw_total + raw_total / 255 + 64ull * n_pages;
   size_t cub_bytes = 0;
@@ -306,8 +312,8 @@ cudaError_t launch_encode_pages(const EncArgs& e, cudaStream_t st) {
       e.hash_begin, e.hash_end, 0, 16, st);
   if (err != cudaSuccess) return err;
   k_enc_prev<<<g2, 256, 0, st>>>(e.keys_alt, e.vals_alt, e.pages, e.n_pages, e.prev);
-  k_enc_parse<<<(e.n_pages + 3) / 4, 128, 0, st>>>(e.work, e.pages, e.n_pages, e.prev, e.visited, e.seqs,
-                                                  e.n_seqs);
+  k_enc_parse<<<(e.n_pages + 3) / 4, 128, 0, st>>>(e.work, e.pages, e.n_pages, e.prev, e.keys, e.visited,
+                                                  e.seqs, e.n_seqs);
   k_enc_emit<<<e.n_pages, 512, 0, st>>>(e.work, e.pages, e.seqs, e.n_seqs, e.comp, e.comp_len);
   k_enc_crc<<<std::min<uint32_t>(e.n_pages, 1024), 256, 0, st>>>(e.work, e.comp, e.pages, e.n_pages, e.comp_len,
                                                                  e.shift_tab, e.crc);

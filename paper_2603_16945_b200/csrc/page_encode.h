@@ -33,7 +33,7 @@ struct EncArgs {
   const int* hash_begin;   // [n_pages] segment bounds for the sort
   const int* hash_end;
   uint32_t* prev;          // [hash_total]
-  uint32_t* visited;       // bitmap words
+  uint32_t* visited;       // [n_pages][65536] parse hash tables (position + 1)
   uint64_t visited_bytes;
   EncSeq* seqs;
   uint32_t* n_seqs;        // [n_pages]
