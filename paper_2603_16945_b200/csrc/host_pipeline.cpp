@@ -1434,7 +1434,7 @@ struct Pipeline {
       w.vx_bt.ensure(16 + 4 * vx_btiles_bound);
       w.vx_bcnt.ensure(4ull * vx_proto.bstride * w.n);
       w.vx_boff.ensure(4ull * (vx_proto.bstride + 4) * w.n);  // per-cloud rows 16-B aligned
-      w.vx_items.ensure(4ull * vx_max_items * w.n);
+      w.vx_items.ensure(8ull * vx_max_items * w.n);
       w.vx_T.ensure(proto.handoff_stride * w.n);
       w.handoff_b.ensure(proto.handoff_stride * w.n);
       w.vx_cl.ensure(sizeof(VxCloud) * w.n);
@@ -1534,6 +1534,7 @@ struct Pipeline {
       vx.any_lsd = vx.total_btiles + 1;
       vx.boff = w.vx_boff.as<uint32_t>();
       vx.item_v = w.vx_items.as<uint32_t>();
+      vx.item_b = vx.item_v + vx_max_items * w.n;
       vx.max_items = (uint32_t)vx_max_items;
       vx.T = w.vx_T.as<uint8_t>();
       vx.msd_enabled = vx_msd ? 1 : 0;

@@ -849,6 +849,18 @@ __global__ void __launch_bounds__(1024) k_vx_bbase(VxArgs v) {
       }
     }
   }
+  __syncthreads();
+  // first bucket of every work item: item w starts at the first bucket whose
+  // offset is >= w * half (nb when none is), i.e. bucket b starts the items
+  // with bo[b-1] < w * half <= bo[b]
+  if (!c.msd) return;
+  constexpr uint32_t half = kVxItemCap / 2;
+  uint32_t* ib = v.item_b + (uint64_t)s * v.max_items;
+  for (uint32_t b = threadIdx.x; b <= nb; b += blockDim.x) {
+    const uint32_t o = bo[b];
+    const uint32_t wl = b ? bo[b - 1] / half + 1 : 0u;
+    for (uint32_t w = wl; w <= o / half && w < c.n_items; ++w) ib[w] = b;
+  }
 }
 
 // Scatter of a tile's kept points into their buckets: in-tile ranks from
@@ -927,37 +939,66 @@ __global__ void __launch_bounds__(kBThreads) k_vx_bscatter(VxArgs v) {
 }
 
 // Work item w of a cloud: the buckets whose offset falls in
-// [w * half, (w + 1) * half), at most kVxItemCap records.
-__device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t* a, uint32_t n, uint32_t x) {
-  uint32_t lo = 0, hi = n;
-  while (lo < hi) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if (a[mid] < x) lo = mid + 1;
-    else hi = mid;
-  }
-  return lo;
-}
-
+// [w * half, (w + 1) * half), at most kVxItemCap records (first buckets
+// precomputed by k_vx_bbase).
 __device__ __forceinline__ void item_range(const VxArgs& v, const VxCloud& c, uint32_t s, uint32_t w,
                                            uint32_t& b0, uint32_t& r0, uint32_t& r1) {
-  constexpr uint32_t half = kVxItemCap / 2;
   const uint32_t nb = 1u << c.bb;
   const uint32_t* bo = v.boff + (uint64_t)s * (v.bstride + 4);
-  b0 = lower_bound_u32(bo, nb, w * half);
-  const uint32_t b1 = lower_bound_u32(bo, nb, (w + 1) * half);
+  const uint32_t* ib = v.item_b + (uint64_t)s * v.max_items;
+  b0 = ib[w];
+  const uint32_t b1 = w + 1 < c.n_items ? ib[w + 1] : nb;
   r0 = b0 < nb ? bo[b0] : c.kept;
   r1 = b1 < nb ? bo[b1] : c.kept;
 }
 
-// grid (max_items, n_samples), kIThreads threads: sort the item's records by
-// key in shared memory (dense items above kVxItemCap: in global memory, w2),
-// stage the payload in sorted order in shared memory (every voxel's run
-// contiguous), and reduce each voxel: count, first point (smallest index) for
-// gathered extra fields, and per float component the double sum -- order-free
-// under an exactness certificate (every value a multiple of 2^emin and
-// n * max|x| < 2^(53 + emin): every partial sum of every order is exact), else
-// replayed in point order (the App. C sequence).  Results to T[r0 + voxel],
-// compacted into A afterwards.
+// Certificate bookkeeping of one float: lowest set bit exponent (min) and
+// biased exponent (max, an upper bound of ilogb for denormals).
+struct Cert {
+  int emin = 1 << 20;
+  uint32_t ebits = 0;
+  bool any = false, finite = true;
+  __device__ __forceinline__ void add(float x) {
+    const uint32_t b = __float_as_uint(x) & 0x7fffffffu;
+    if (!b) return;
+    const uint32_t e = b >> 23;
+    if (e == 255u) {
+      finite = false;
+      return;
+    }
+    any = true;
+    ebits = max(ebits, e);
+    emin = min(emin, lowbit_exp(x));
+  }
+  __device__ __forceinline__ void warp_merge() {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      emin = min(emin, __shfl_xor_sync(0xffffffffu, emin, o));
+      ebits = max(ebits, __shfl_xor_sync(0xffffffffu, ebits, o));
+    }
+    any = __any_sync(0xffffffffu, any);
+    finite = __all_sync(0xffffffffu, finite);
+  }
+  // every partial sum of n such values, in any order, is exact in double
+  __device__ __forceinline__ bool exact(uint32_t n) const {
+    const int nbits = 32 - __clz(n);
+    return finite && (!any || (int)ebits - 127 + 1 + nbits <= 53 + emin);
+  }
+};
+
+// grid (max_items, n_samples), kIThreads threads.  An item's records (keys
+// cached in registers) are sorted by key in shared memory -- a counting sort
+// with warp-aggregated atomics when the item spans <= 4096 keys (dense
+// voxels: order inside a key is arbitrary), else radix passes; items above
+// kVxItemCap records sort in global memory (w2).  The payload of the moved
+// fields and the point indices are staged in sorted order in shared memory
+// (for the counting sort in the same pass, from coalesced record-order
+// reads), so every voxel's run is contiguous.  Each voxel is then reduced --
+// count, first point (smallest index) for gathered extra fields, and per
+// float component the double sum, order-free under an exactness certificate
+// (every value a multiple of 2^emin and n * max|x| < 2^(53 + emin): every
+// partial sum of every order is exact), else replayed in point order (the
+// App. C sequence).  Results to T[r0 + voxel], compacted into A afterwards.
 __global__ void __launch_bounds__(kIThreads) k_vx_item(VxArgs v) {
   extern __shared__ __align__(16) uint8_t dyn[];
   uint64_t* sw0 = reinterpret_cast<uint64_t*>(dyn);
@@ -965,21 +1006,21 @@ __global__ void __launch_bounds__(kIThreads) k_vx_item(VxArgs v) {
   uint32_t* scr = reinterpret_cast<uint32_t*>(sw1 + kVxItemCap);
   uint32_t* pay = scr + kSortScratchBytes / 4;  // [kVxItemCap][v.pay_words]
   constexpr uint32_t kIWarps = kIThreads / 32;
+  constexpr uint32_t kPer = kVxItemCap / kIThreads;  // records per thread (small items)
   __shared__ uint32_t sh[kIWarps + 1];
   __shared__ unsigned long long red[32];
-  __shared__ uint32_t rng[3];
   const uint32_t s = blockIdx.y, w = blockIdx.x;
   const VxCloud& c = v.cl[s];
   if (!c.active || !c.msd || w >= c.n_items) return;
-  if (threadIdx.x == 0) item_range(v, c, s, w, rng[0], rng[1], rng[2]);  // two binary searches, once
-  __syncthreads();
-  const uint32_t b0 = rng[0], r0 = rng[1], r1 = rng[2];
+  uint32_t b0, r0, r1;
+  item_range(v, c, s, w, b0, r0, r1);
   const uint32_t m = r1 - r0;
   uint32_t* iv = v.item_v + (uint64_t)s * v.max_items;
   if (m == 0) {
     if (threadIdx.x == 0) iv[w] = 0;
     return;
   }
+  const uint32_t lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
   const uint64_t kbase = (uint64_t)b0 << c.lowbits;  // words = key << ib | point index
   const uint64_t* K = v.w0 + c.word0 + r0;
   const uint64_t imask = c.ib ? ((1ull << c.ib) - 1) : 0ull;
@@ -987,21 +1028,70 @@ __global__ void __launch_bounds__(kIThreads) k_vx_item(VxArgs v) {
   const uint32_t pb = big ? 32u - __clz(m - 1) : 12u;  // record position bits
   uint64_t* a0 = big ? v.w2 + 2 * c.word0 + r0 : sw0;
   uint64_t* a1 = big ? v.w2 + 2 * c.word0 + c.n + r0 : sw1;
+  uint8_t* B = v.B + (uint64_t)s * v.stride;
+  const uint32_t* ha = hdr(v, v.A, s);
+  const uint32_t moved = v.mm & ha[1];
+  // payload words of the moved 4-byte-multiple fields: field f's words at fo[f]
+  const uint32_t PW = v.pay_words;
+  uint32_t fo[kMaxBytesFields];
+  {
+    uint32_t o = 0;
+    for (int f = 0; f < v.n_bytes_fields; ++f) {
+      fo[f] = o;
+      if ((moved >> f) & 1u) o += (ha[10 + f] + 3) / 4;
+    }
+  }
+  const bool staged = !big && PW > 0;
+  auto stage = [&](uint32_t j, uint32_t k) {  // record j's payload to sorted slot k
+    for (int f = 0; f < v.n_bytes_fields; ++f) {
+      if (!((moved >> f) & 1u)) continue;
+      const uint32_t es = ha[10 + f];
+      if (es & 3u) continue;  // odd-sized extra fields are read from B directly
+      const uint32_t wpp = es >> 2;
+      const uint32_t* src = reinterpret_cast<const uint32_t*>(B + v.off[f]) + (uint64_t)(r0 + j) * wpp;
+      uint32_t* dst = pay + k * PW + fo[f];
+      if (wpp == 3) {
+        const uint32_t x0 = src[0], x1 = src[1], x2 = src[2];
+        dst[0] = x0, dst[1] = x1, dst[2] = x2;
+      } else {
+        for (uint32_t q = 0; q < wpp; ++q) dst[q] = src[q];
+      }
+    }
+  };
+  uint64_t kw[kPer];
   unsigned long long kmax = 0;
-  for (uint32_t j = threadIdx.x; j < m; j += kIThreads)
-    kmax = max(kmax, (unsigned long long)((K[j] >> c.ib) - kbase));
+  if (!big) {
+#pragma unroll
+    for (uint32_t q = 0; q < kPer; ++q) {
+      const uint32_t j = threadIdx.x + q * kIThreads;
+      kw[q] = j < m ? K[j] : 0ull;
+      if (j < m) kmax = max(kmax, (unsigned long long)((kw[q] >> c.ib) - kbase));
+    }
+  } else {
+    for (uint32_t j = threadIdx.x; j < m; j += kIThreads)
+      kmax = max(kmax, (unsigned long long)((K[j] >> c.ib) - kbase));
+  }
   kmax = dev::block_reduce(kmax, dev::OpMax{}, 0ull, red);
   const uint32_t relbits = kmax ? 64u - __clzll(kmax) : 0u;
-  int r;
-  if (relbits <= 12) {
-    // few distinct keys (dense voxels): counting sort by key in shared
-    // memory -- order inside a key is arbitrary, the sums are order-free
-    // under the certificate and the first point is a min over the run
+  const uint64_t* S;
+  uint32_t* seg;   // voxel starts (<= m entries): first half of the free buffer
+  uint32_t* sidx = nullptr;  // point index per sorted slot: its second half
+  if (!big && relbits <= 12) {
+    // counting sort; ranks from warp-aggregated atomics (dense voxels put
+    // most of a warp's records on one key)
     uint32_t* hist = scr;  // <= 4096 counters
     const uint32_t range = 1u << relbits;
     for (uint32_t k = threadIdx.x; k < range; k += kIThreads) hist[k] = 0;
     __syncthreads();
-    for (uint32_t j = threadIdx.x; j < m; j += kIThreads) atomicAdd(&hist[(K[j] >> c.ib) - kbase], 1u);
+    const uint32_t lt = (1u << lane) - 1u;
+    uint32_t rel[kPer], peers[kPer];
+#pragma unroll
+    for (uint32_t q = 0; q < kPer; ++q) {
+      const uint32_t j = threadIdx.x + q * kIThreads;
+      rel[q] = j < m ? (uint32_t)((kw[q] >> c.ib) - kbase) : 0xffffffffu;
+      peers[q] = __match_any_sync(0xffffffffu, rel[q]);
+      if (j < m && (peers[q] & lt) == 0) atomicAdd(&hist[rel[q]], (uint32_t)__popc(peers[q]));
+    }
     __syncthreads();
     {
       const uint32_t per = (range + kIThreads - 1) / kIThreads;  // <= 8
@@ -1011,13 +1101,7 @@ __global__ void __launch_bounds__(kIThreads) k_vx_item(VxArgs v) {
         x[q] = k < range ? hist[k] : 0u;
         sum += x[q];
       }
-      const uint32_t lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
-      uint32_t inc = sum;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-        if ((int)lane >= o) inc += y;
-      }
+      const uint32_t inc = warp_incl_scan(sum);
       if (lane == 31) sh[wp] = inc;
       __syncthreads();
       if (threadIdx.x == 0) {
@@ -1037,18 +1121,48 @@ __global__ void __launch_bounds__(kIThreads) k_vx_item(VxArgs v) {
       }
     }
     __syncthreads();
-    for (uint32_t j = threadIdx.x; j < m; j += kIThreads) {
-      const uint64_t rel = (K[j] >> c.ib) - kbase;
-      a1[atomicAdd(&hist[rel], 1u)] = (rel << pb) | j;
+    seg = reinterpret_cast<uint32_t*>(sw0);
+    sidx = seg + kVxItemCap;
+#pragma unroll
+    for (uint32_t q = 0; q < kPer; ++q) {
+      const uint32_t j = threadIdx.x + q * kIThreads;
+      const uint32_t leader = __ffs(peers[q]) - 1;
+      uint32_t base = 0;
+      if (j < m && lane == leader) base = atomicAdd(&hist[rel[q]], (uint32_t)__popc(peers[q]));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (j < m) {
+        const uint32_t k = base + __popc(peers[q] & lt);
+        sw1[k] = ((uint64_t)rel[q] << pb) | j;
+        sidx[k] = (uint32_t)(kw[q] & imask);
+        if (staged) stage(j, k);
+      }
     }
-    r = 1;
+    S = sw1;
   } else {
-    for (uint32_t j = threadIdx.x; j < m; j += kIThreads) a0[j] = (((K[j] >> c.ib) - kbase) << pb) | j;
+    if (!big) {
+#pragma unroll
+      for (uint32_t q = 0; q < kPer; ++q) {
+        const uint32_t j = threadIdx.x + q * kIThreads;
+        if (j < m) a0[j] = (((kw[q] >> c.ib) - kbase) << pb) | j;
+      }
+    } else {
+      for (uint32_t j = threadIdx.x; j < m; j += kIThreads) a0[j] = (((K[j] >> c.ib) - kbase) << pb) | j;
+    }
     __syncthreads();
-    r = radix_sort8<4>(a0, a1, m, pb, pb + relbits, scr);
+    const int r = radix_sort8<4>(a0, a1, m, pb, pb + relbits, scr);
+    S = r ? a1 : a0;
+    seg = reinterpret_cast<uint32_t*>(r ? a0 : a1);
+    if (!big) {
+      __syncthreads();
+      sidx = seg + kVxItemCap;
+      const uint64_t pm = (1ull << pb) - 1;
+      for (uint32_t k = threadIdx.x; k < m; k += kIThreads) {
+        const uint32_t j = (uint32_t)(S[k] & pm);
+        sidx[k] = (uint32_t)(K[j] & imask);
+        if (staged) stage(j, k);
+      }
+    }
   }
-  const uint64_t* S = r ? a1 : a0;
-  uint32_t* seg = reinterpret_cast<uint32_t*>(r ? a0 : a1);  // the free buffer
   const uint64_t pmask = (1ull << pb) - 1;
   __syncthreads();
   // voxel starts, numbered in order: thread-contiguous ranges, one block scan
@@ -1058,13 +1172,7 @@ __global__ void __launch_bounds__(kIThreads) k_vx_item(VxArgs v) {
     const uint32_t ja = min(m, threadIdx.x * per), jb = min(m, ja + per);
     uint32_t cnt = 0;
     for (uint32_t j = ja; j < jb; ++j) cnt += (j == 0 || (S[j] >> pb) != (S[j - 1] >> pb)) ? 1u : 0u;
-    const uint32_t lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
-    uint32_t inc = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-      if ((int)lane >= o) inc += y;
-    }
+    const uint32_t inc = warp_incl_scan(cnt);
     if (lane == 31) sh[wp] = inc;
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -1082,64 +1190,22 @@ __global__ void __launch_bounds__(kIThreads) k_vx_item(VxArgs v) {
     for (uint32_t j = ja; j < jb; ++j)
       if (j == 0 || (S[j] >> pb) != (S[j - 1] >> pb)) seg[vid++] = j;
   }
-  uint8_t* B = v.B + (uint64_t)s * v.stride;
-  const uint32_t* ha = hdr(v, v.A, s);
-  const uint32_t moved = v.mm & ha[1];
-  // payload words of the moved fields: field f's words at pay offset fo[f]
-  const uint32_t PW = v.pay_words;
-  uint32_t fo[kMaxBytesFields];
-  {
-    uint32_t o = 0;
-    for (int f = 0; f < v.n_bytes_fields; ++f) {
-      fo[f] = o;
-      if ((moved >> f) & 1u) o += (ha[10 + f] + 3) / 4;
-    }
-  }
-  const bool staged = !big && v.pay_words > 0;
-  if (staged) {  // sorted-order payload into shared memory (independent loads)
-    for (int f = 0; f < v.n_bytes_fields; ++f) {
-      if (!((moved >> f) & 1u)) continue;
-      const uint32_t es = ha[10 + f];
-      if (es & 3u) continue;  // odd-sized extra fields are read from B directly
-      const uint32_t wpp = es >> 2;
-      const uint32_t* src = reinterpret_cast<const uint32_t*>(B + v.off[f]) + (uint64_t)r0 * wpp;
-      for (uint32_t e0 = threadIdx.x; e0 < m * wpp; e0 += 4 * kIThreads) {
-        uint32_t x[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const uint32_t e = e0 + u * kIThreads;
-          if (e < m * wpp) {
-            const uint32_t k = e / wpp, q = e - k * wpp;
-            x[u] = src[(S[k] & pmask) * wpp + q];
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const uint32_t e = e0 + u * kIThreads;
-          if (e < m * wpp) {
-            const uint32_t k = e / wpp, q = e - k * wpp;
-            pay[k * PW + fo[f] + q] = x[u];
-          }
-        }
-      }
-    }
-  }
   __syncthreads();
   // component q of field f at sorted position k
   auto comp = [&](int f, uint32_t comps, uint32_t k, uint32_t q) -> float {
     if (staged) return __uint_as_float(pay[k * PW + fo[f] + q]);
     return reinterpret_cast<const float*>(B + v.off[f])[((uint64_t)r0 + (S[k] & pmask)) * comps + q];
   };
-  auto pidx = [&](uint32_t k) -> uint64_t { return K[S[k] & pmask] & imask; };
+  auto pidx = [&](uint32_t k) -> uint64_t { return sidx ? (uint64_t)sidx[k] : K[S[k] & pmask] & imask; };
   // thread per small voxel, warp per large voxel; results to T[r0 + voxel]
   uint8_t* T = v.T + (uint64_t)s * v.stride;
   constexpr uint32_t kWarpVoxel = 64;
   auto emit = [&](uint32_t vx, uint32_t s0, uint32_t s1, bool warp_mode) {
-    const uint32_t lane = threadIdx.x & 31;
     const uint32_t n = s1 - s0;
+    const uint32_t k0 = s0 + (warp_mode ? lane : 0), dk = warp_mode ? 32 : 1;
     uint32_t first = s0;
     uint64_t first_i = ~0ull;
-    for (uint32_t k = s0 + (warp_mode ? lane : 0); k < s1; k += warp_mode ? 32 : 1) {
+    for (uint32_t k = k0; k < s1; k += dk) {
       const uint64_t i = pidx(k);
       if (i < first_i) first_i = i, first = k;
     }
@@ -1150,6 +1216,7 @@ __global__ void __launch_bounds__(kIThreads) k_vx_item(VxArgs v) {
         const uint32_t ok = __shfl_xor_sync(0xffffffffu, first, o);
         if (oi < first_i) first_i = oi, first = ok;
       }
+    const bool writer = !warp_mode || lane == 0;
     for (int f = 0; f < v.n_bytes_fields; ++f) {
       if (!((moved >> f) & 1u)) continue;
       const bool avg = f == v.role_data || f == v.role_normal || f == v.role_color || f == v.role_intensity;
@@ -1157,35 +1224,31 @@ __global__ void __launch_bounds__(kIThreads) k_vx_item(VxArgs v) {
       if (avg) {
         const uint32_t comps = es / 4;
         float* dst = reinterpret_cast<float*>(T + v.off[f]) + (uint64_t)(r0 + vx) * comps;
-        for (uint32_t q = 0; q < comps; ++q) {
-          double acc = 0.0;
-          int emin = 1 << 20, emax = -(1 << 20);
-          bool finite = true;
-          for (uint32_t k = s0 + (warp_mode ? lane : 0); k < s1; k += warp_mode ? 32 : 1) {
-            const float x = comp(f, comps, k, q);
-            acc = __dadd_rn(acc, (double)x);
-            if (x != 0.0f) {
-              if (!isfinite(x)) finite = false;
-              else {
-                emin = min(emin, lowbit_exp(x));
-                emax = max(emax, ilogbf(x));
+        for (uint32_t q0 = 0; q0 < comps; q0 += 4) {  // up to 4 components per pass
+          const uint32_t nq = min(4u, comps - q0);
+          double acc[4] = {0.0, 0.0, 0.0, 0.0};
+          Cert ct[4];
+          for (uint32_t k = k0; k < s1; k += dk) {
+#pragma unroll
+            for (uint32_t u = 0; u < 4; ++u) {
+              if (u < nq) {
+                const float x = comp(f, comps, k, q0 + u);
+                acc[u] = __dadd_rn(acc[u], (double)x);
+                ct[u].add(x);
               }
             }
           }
-          if (warp_mode) {
 #pragma unroll
-            for (int o = 16; o; o >>= 1) {
-              acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
-              emin = min(emin, __shfl_xor_sync(0xffffffffu, emin, o));
-              emax = max(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+          for (uint32_t u = 0; u < 4; ++u) {
+            if (u >= nq) continue;
+            if (warp_mode) {
+#pragma unroll
+              for (int o = 16; o; o >>= 1) acc[u] = __dadd_rn(acc[u], __shfl_xor_sync(0xffffffffu, acc[u], o));
+              ct[u].warp_merge();
             }
-            finite = __all_sync(0xffffffffu, finite);
-          }
-          const int nbits = 32 - __clz(n);
-          const bool exact = finite && (emax == -(1 << 20) || emax + 1 + nbits <= 53 + emin);
-          if (!warp_mode || lane == 0) {
-            if (!exact) {  // replay in point order
-              acc = 0.0;
+            if (!writer) continue;
+            if (!ct[u].exact(n)) {  // replay in point order
+              acc[u] = 0.0;
               uint64_t last = 0;
               bool any = false;
               for (uint32_t t2 = 0; t2 < n; ++t2) {
@@ -1195,15 +1258,15 @@ __global__ void __launch_bounds__(kIThreads) k_vx_item(VxArgs v) {
                   const uint64_t i = pidx(k);
                   if ((!any || i > last) && i < best) best = i, bk = k;
                 }
-                acc = __dadd_rn(acc, (double)comp(f, comps, bk, q));
+                acc[u] = __dadd_rn(acc[u], (double)comp(f, comps, bk, q0 + u));
                 last = best;
                 any = true;
               }
             }
-            dst[q] = __double2float_rn(__ddiv_rn(acc, (double)n));
+            dst[q0 + u] = __double2float_rn(__ddiv_rn(acc[u], (double)n));
           }
         }
-      } else if (!warp_mode || lane == 0) {  // gathered extra field: the voxel's first point
+      } else if (writer) {  // gathered extra field: the voxel's first point
         uint8_t* dst = T + v.off[f] + (uint64_t)(r0 + vx) * es;
         if (staged && !(es & 3u)) {
           for (uint32_t q = 0; q < es / 4; ++q)
@@ -1214,14 +1277,13 @@ __global__ void __launch_bounds__(kIThreads) k_vx_item(VxArgs v) {
         }
       }
     }
-    if (v.counts && (!warp_mode || lane == 0))
-      reinterpret_cast<int32_t*>(T + v.off[kMaxBytesFields])[r0 + vx] = (int32_t)n;
+    if (v.counts && writer) reinterpret_cast<int32_t*>(T + v.off[kMaxBytesFields])[r0 + vx] = (int32_t)n;
   };
   for (uint32_t vx = threadIdx.x; vx < V; vx += kIThreads) {
     const uint32_t s0 = seg[vx], s1 = vx + 1 < V ? seg[vx + 1] : m;
     if (s1 - s0 <= kWarpVoxel) emit(vx, s0, s1, false);
   }
-  for (uint32_t vx = threadIdx.x >> 5; vx < V; vx += kIWarps) {
+  for (uint32_t vx = wp; vx < V; vx += kIWarps) {
     const uint32_t s0 = seg[vx], s1 = vx + 1 < V ? seg[vx + 1] : m;
     if (s1 - s0 > kWarpVoxel) emit(vx, s0, s1, true);
   }
@@ -1253,13 +1315,11 @@ __global__ void __launch_bounds__(kThreads) k_vx_iscan(VxArgs v) {
 // grid (max_items, n_samples): voxel results of item w from T[r0 ..] to A at
 // the item's voxel offset.
 __global__ void __launch_bounds__(kThreads) k_vx_compact(VxArgs v) {
-  __shared__ uint32_t rng[3];
   const uint32_t s = blockIdx.y, w = blockIdx.x;
   const VxCloud& c = v.cl[s];
   if (!c.active || !c.msd || w >= c.n_items) return;
-  if (threadIdx.x == 0) item_range(v, c, s, w, rng[0], rng[1], rng[2]);
-  __syncthreads();
-  const uint32_t r0 = rng[1];
+  uint32_t b0, r0, r1;
+  item_range(v, c, s, w, b0, r0, r1);
   const uint32_t* iv = v.item_v + (uint64_t)s * v.max_items;
   const uint32_t vo = iv[w], vn = (w + 1 < c.n_items ? iv[w + 1] : c.V) - vo;
   if (!vn) return;

@@ -58,6 +58,7 @@ struct VxArgs {
   uint32_t* boff;         // [n_samples][bstride + 4]: bucket totals -> offsets (+ total)
   uint32_t* any_lsd;      // a cloud of the wave takes the global LSD sort
   uint32_t* item_v;       // [n_samples][max_items]: voxels per item -> voxel offsets
+  uint32_t* item_b;       // [n_samples][max_items]: first bucket of each item
   uint32_t max_items;
   uint8_t* T;             // voxel results per item before compaction (slots like A)
   int32_t msd_enabled;    // 0: every cloud takes the LSD path
