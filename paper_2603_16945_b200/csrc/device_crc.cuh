@@ -154,13 +154,70 @@ __device__ __forceinline__ void chunks4(const uint32_t* tab, const uint8_t* cons
   for (int q = 0; q < 4; ++q) out[q] = c[q] ^ 0xFFFFFFFFu;
 }
 
+// The shift table buffer carries, after its kShiftEntries chunk shifts,
+// byte-sliced multiplication tables by S = x^(8 * kChunk * stride) for the
+// chunk strides the kernels use (lane stride 32, CTA strides 256 and 512):
+// S (x) v = T[0][v & 255] ^ T[1][v >> 8 & 255] ^ T[2][..] ^ T[3][v >> 24]
+// (multiplication is linear in v), four cached loads instead of a 32-step
+// bit loop.
+constexpr uint32_t kMulStrides[3] = {32, 256, 512};
+constexpr uint32_t kShiftTabWords = kShiftEntries + 3 * 1024;
+
+__device__ __forceinline__ const uint32_t* stride_mul_tab(const uint32_t* shift_tab, uint64_t stride) {
+  const int i = stride == 32 ? 0 : stride == 256 ? 1 : stride == 512 ? 2 : -1;  // kMulStrides
+  return i < 0 ? nullptr : shift_tab + kShiftEntries + 1024 * i;
+}
+
+__device__ __forceinline__ uint32_t mul_tab(const uint32_t* T, uint32_t v) {
+  return __ldg(T + (v & 255u)) ^ __ldg(T + 256 + ((v >> 8) & 255u)) ^ __ldg(T + 512 + ((v >> 16) & 255u)) ^
+         __ldg(T + 768 + (v >> 24));
+}
+
+// Ranges beyond the shift table (S3DIS rooms: 24 MB): chunk k_j = first +
+// j * stride has shift x^(8*kChunk*first) (x) S^j, so the thread folds its
+// chunks Horner-style from the highest j down (acc = S (x) acc ^ crc_j: one
+// table multiply per chunk) and applies its first chunk's shift once at the
+// end, instead of rebuilding x^(8n) per chunk.  Out of line: the inlined
+// short-range path below stays as small as it was (k_cloud's FPS registers).
+static __device__ __noinline__ uint32_t strided_chunks_long(const uint32_t* tab, const uint32_t* x2n,
+                                                     const uint32_t* shift_tab, const uint8_t* p,
+                                                     uint64_t n, uint64_t first, uint64_t stride) {
+  const uint64_t nchunks = (n + kChunk - 1) / kChunk;
+  const uint64_t full = n / kChunk;
+  if (first >= nchunks) return 0;
+  const uint32_t* T = stride_mul_tab(shift_tab, stride);
+  const uint32_t S = T ? 0u : x8n(x2n, stride * kChunk);
+  auto mulS = [&](uint32_t v) -> uint32_t { return T ? mul_tab(T, v) : multmodp(S, v); };
+  int64_t j = (int64_t)((nchunks - 1 - first) / stride);
+  uint32_t acc = 0;
+  for (; j >= 0 && first + (uint64_t)j * stride >= full; --j) {  // the short chunk at the range start
+    const uint64_t e = n - (first + (uint64_t)j * stride) * kChunk;
+    const uint64_t s = e > kChunk ? e - kChunk : 0;
+    acc = mulS(acc) ^ bytes_words(tab, p + s, e - s);
+  }
+  for (; j >= 3; j -= 4) {
+    const uint8_t* ps[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) ps[q] = p + (n - (first + (uint64_t)(j - q) * stride + 1) * kChunk);
+    uint32_t r[4];
+    chunks4(tab, ps, r);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc = mulS(acc) ^ r[q];
+  }
+  for (; j >= 0; --j)
+    acc = mulS(acc) ^ bytes_words(tab, p + (n - (first + (uint64_t)j * stride + 1) * kChunk), kChunk);
+  return multmodp(chunk_shift(shift_tab, x2n, first), acc);
+}
+
 // XOR of shifted chunk CRCs for chunks k = first, first+stride, ... of a
 // range of n bytes (chunks aligned to its end): four full chunks at a time,
-// the rest (incl. the short chunk at the range start) one by one.
+// the rest (incl. the short chunk at the range start) one by one; one
+// independent product per chunk (ILP across chunks).
 __device__ __forceinline__ uint32_t strided_chunks(const uint32_t* tab, const uint32_t* x2n,
                                                    const uint32_t* shift_tab, const uint8_t* p,
                                                    uint64_t n, uint64_t first, uint64_t stride) {
   const uint64_t nchunks = (n + kChunk - 1) / kChunk;
+  if (nchunks > kShiftEntries) return strided_chunks_long(tab, x2n, shift_tab, p, n, first, stride);
   const uint64_t full = n / kChunk;  // chunks 0..full-1 are full-size
   uint32_t c = 0;
   uint64_t k = first;

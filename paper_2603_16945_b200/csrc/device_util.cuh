@@ -11,6 +11,46 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// Exactness certificate of a float sum (voxel means): with every value a
+// multiple of 2^emin and n * max|x| < 2^(53 + emin), every partial sum of
+// every order is exact in double, so a parallel sum equals the sequential
+// one bit for bit.  ebits (biased exponent) bounds ilogb from above, also for
+// denormals, so the test is conservative.
+struct SumCert {
+  int emin = 1 << 20;
+  uint32_t ebits = 0;
+  bool any = false, finite = true;
+  __device__ __forceinline__ void add(float x) {
+    const uint32_t b = __float_as_uint(x) & 0x7fffffffu;
+    if (!b) return;
+    const uint32_t e = b >> 23;
+    if (e == 255u) {
+      finite = false;
+      return;
+    }
+    any = true;
+    ebits = e > ebits ? e : ebits;
+    const uint32_t m = b & 0x7fffffu;
+    const int lb = e == 0 ? -149 + __ffs(m) - 1 : (int)e - 150 + __ffs(m | 0x800000u) - 1;
+    emin = lb < emin ? lb : emin;
+  }
+  __device__ __forceinline__ void warp_merge() {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const int e2 = __shfl_xor_sync(0xffffffffu, emin, o);
+      const uint32_t b2 = __shfl_xor_sync(0xffffffffu, ebits, o);
+      emin = e2 < emin ? e2 : emin;
+      ebits = b2 > ebits ? b2 : ebits;
+    }
+    any = __any_sync(0xffffffffu, any);
+    finite = __all_sync(0xffffffffu, finite);
+  }
+  __device__ __forceinline__ bool exact(uint32_t n) const {
+    const int nbits = 32 - __clz(n);
+    return finite && (!any || (int)ebits - 127 + 1 + nbits <= 53 + emin);
+  }
+};
+
 // 32-bit little-endian load from an arbitrarily aligned generic address.
 // Reads the aligned word after it too (all buffers carry >= 16 B of slack).
 __device__ __forceinline__ uint32_t ld_u32_unaligned(const uint8_t* p) {

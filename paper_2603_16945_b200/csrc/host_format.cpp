@@ -472,7 +472,7 @@ std::vector<EncodedGroup> encode_groups_device(const std::vector<FieldSpec>& sch
   auto CKD = [](cudaError_t e, const char* what) {
     if (e != cudaSuccess) fail(kIoFailure, std::string("CUDA ") + what + ": " + cudaGetErrorString(e));
   };
-  std::vector<uint32_t> shift(kShiftEntries);
+  std::vector<uint32_t> shift(kShiftTabWords);
   build_shift_table(shift.data());
   uint32_t* d_shift = nullptr;
   CKD(cudaMalloc(&d_shift, shift.size() * 4), "malloc");

@@ -427,7 +427,7 @@ DeviceCtx& device_ctx(cudaStream_t st) {
     c = std::make_unique<DeviceCtx>();
     c->sms = require_device(dev);
     upload_x2n(st);
-    std::vector<uint32_t> shift(kShiftEntries);
+    std::vector<uint32_t> shift(kShiftTabWords);
     build_shift_table(shift.data());
     c->shift.ensure(shift.size() * 4);
     CK(cudaMemcpy(c->shift.p, shift.data(), shift.size() * 4, cudaMemcpyHostToDevice));
@@ -684,7 +684,7 @@ struct Pipeline {
       grid_pre = (int)std::min<uint64_t>(std::max(grid_pre, 1), mx);
     }
     upload_x2n(stream);
-    std::vector<uint32_t> shift(kShiftEntries);
+    std::vector<uint32_t> shift(kShiftTabWords);
     build_shift_table(shift.data());
     d_shift.ensure(shift.size() * 4);
     CK(cudaMemcpyAsync(d_shift.p, shift.data(), shift.size() * 4, cudaMemcpyHostToDevice, stream));

@@ -2335,6 +2335,13 @@ void build_shift_table(uint32_t* h_tab) {
     h_tab[k] = p;
     p = crc::multmodp(step, p);
   }
+  // byte-sliced multiplication tables by x^(8 * kChunk * stride)
+  for (int i = 0; i < 3; ++i) {
+    const uint32_t S = h_tab[crc::kMulStrides[i]];
+    uint32_t* T = h_tab + crc::kShiftEntries + 1024 * i;
+    for (uint32_t b = 0; b < 4; ++b)
+      for (uint32_t v = 0; v < 256; ++v) T[256 * b + v] = crc::multmodp(S, v << (8 * b));
+  }
 }
 
 uint64_t lz4_scratch_bytes(uint64_t pay) { return lz4p::scratch_bytes(pay); }

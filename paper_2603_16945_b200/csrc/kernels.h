@@ -20,7 +20,7 @@ struct CrcWindow {
 };
 
 void upload_x2n(cudaStream_t st);
-void build_shift_table(uint32_t* h_tab);  // crc::kShiftEntries entries
+void build_shift_table(uint32_t* h_tab);  // kShiftTabWords entries
 size_t cloud_smem_fixed();
 cudaError_t set_cloud_smem(size_t bytes);
 cudaError_t launch_crc_windows(const uint8_t* bytes, const CrcWindow* win, uint32_t n_win,
@@ -71,5 +71,6 @@ cudaError_t launch_decode_pages(const uint8_t* bytes, const uint64_t* page_off, 
                                 uint8_t* scratch, int32_t* status, cudaStream_t st);
 
 constexpr uint32_t kShiftEntries = 8192;
+constexpr uint32_t kShiftTabWords = kShiftEntries + 3 * 1024;  // + stride multiplication tables (device_crc.cuh)
 
 }  // namespace pcp

@@ -952,39 +952,7 @@ __device__ __forceinline__ void item_range(const VxArgs& v, const VxCloud& c, ui
   r1 = b1 < nb ? bo[b1] : c.kept;
 }
 
-// Certificate bookkeeping of one float: lowest set bit exponent (min) and
-// biased exponent (max, an upper bound of ilogb for denormals).
-struct Cert {
-  int emin = 1 << 20;
-  uint32_t ebits = 0;
-  bool any = false, finite = true;
-  __device__ __forceinline__ void add(float x) {
-    const uint32_t b = __float_as_uint(x) & 0x7fffffffu;
-    if (!b) return;
-    const uint32_t e = b >> 23;
-    if (e == 255u) {
-      finite = false;
-      return;
-    }
-    any = true;
-    ebits = max(ebits, e);
-    emin = min(emin, lowbit_exp(x));
-  }
-  __device__ __forceinline__ void warp_merge() {
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      emin = min(emin, __shfl_xor_sync(0xffffffffu, emin, o));
-      ebits = max(ebits, __shfl_xor_sync(0xffffffffu, ebits, o));
-    }
-    any = __any_sync(0xffffffffu, any);
-    finite = __all_sync(0xffffffffu, finite);
-  }
-  // every partial sum of n such values, in any order, is exact in double
-  __device__ __forceinline__ bool exact(uint32_t n) const {
-    const int nbits = 32 - __clz(n);
-    return finite && (!any || (int)ebits - 127 + 1 + nbits <= 53 + emin);
-  }
-};
+using Cert = dev::SumCert;
 
 // grid (max_items, n_samples), kIThreads threads.  An item's records (keys
 // cached in registers) are sorted by key in shared memory -- a counting sort

@@ -79,16 +79,19 @@ def test_autotune_live_pipeline(pcp, tmp_path):
                                    iterations=4, seed_phase=2, eval_window_ms=40)
     assert len(hist) >= 2 and best.objective == max(h.objective for h in hist) > 0
     tail = []
-    while True:
+    while True:  # the final update lands at a wave boundary: drain until it shows
         b = p.next_batch()
         if b is None:
             break
-        tail.append(b)
-        if len(tail) == 40:
+        tail.append((_key(b), b.to_host()))  # views live until the next next_batch
+        m = autotune.metrics(p)
+        if len(tail) >= 40 and m["slots"] == best.slots and m["wave_batches"] == best.wave_batches:
+            break
+        if len(tail) == 600:
             break
     m = autotune.metrics(p)
     assert m["slots"] == best.slots and m["wave_batches"] == best.wave_batches
-    keys = [_key(b) for b in tail]
+    keys = [k for k, _ in tail]
     ref = pcp.Pipeline(primary, g, epochs=epochs)
     want = {}
     for b in ref:
@@ -97,8 +100,7 @@ def test_autotune_live_pipeline(pcp, tmp_path):
         if len(want) == len(keys):
             break
     ref.close()
-    for b in tail:
-        h = b.to_host()
+    for k, h in tail:
         for name in h:
-            assert np.array_equal(h[name][0].view(np.uint8), want[_key(b)][name][0].view(np.uint8))
+            assert np.array_equal(h[name][0].view(np.uint8), want[k][name][0].view(np.uint8))
     p.close()
