@@ -649,9 +649,8 @@ __device__ int32_t op_normalize(const WaveArgs& a, Cloud& c, Smem& S) {
 __device__ void first_draws(Smem& S, Seed seed, int k, uint64_t* out) {
   __shared__ uint64_t o[8];
   if (threadIdx.x == 0) {
-    if (seed.pre) {  // words 0..kM+k of the pre-seeded state (k_seed_states)
-      for (int i = 0; i < k; ++i)
-        o[i] = rng::temper(rng::twist_word(seed.pre[i], seed.pre[i + 1], seed.pre[i + rng::kM]));
+    if (seed.pre) {  // the op's first outputs, tempered by k_seed_states
+      for (int i = 0; i < k; ++i) o[i] = seed.pre[i];
     } else {
       rng::first_outputs(seed.v, k, o, S.mt);
     }
@@ -2404,6 +2403,22 @@ cudaError_t launch_clustered(K kern, const WaveArgs& a, int grid, int threads, s
 // each: the 311-step serial recurrence (std::mt19937_64::seed) leaves
 // k_cloud's critical path, where thread 0 ran it while the CTA waited (~8 K
 // cycles per downsample and ~4 K per first_draws op).  Op order: rng_slot.
+// Ops that take only their first few engine outputs (first_draws) get those
+// outputs, tempered, instead of the 312-word state: the recurrence stops at
+// word kM + k and 8 k bytes are written instead of 2.5 KB.  Full states
+// (jitter, colour augment, downsample) are written 32 B per store, so every
+// lane fills whole sectors.
+__device__ __forceinline__ int first_draw_count(int kind) {
+  switch (kind) {
+    case kTranslate: return 3;
+    case kRandomCrop: return 6;
+    case kRotate:
+    case kRandomScale:
+    case kFlipYz: return 1;
+    default: return 0;  // full state
+  }
+}
+
 __global__ void __launch_bounds__(64) k_seed_states(WaveArgs a) {
   const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (uint64_t)a.n_samples * a.n_rng) return;
@@ -2413,10 +2428,28 @@ __global__ void __launch_bounds__(64) k_seed_states(WaveArgs a) {
   const SampleWork sw = a.samples[s];
   uint64_t x = rng::mix_seed(a.base_seed, sw.epoch, sw.index, a.ops[k].seed_op_id);
   uint64_t* out = a.mt_pre + t * rng::kN;
-  out[0] = x;
+  const int nd = first_draw_count(a.ops[k].kind);
+  if (nd > 0) {
+    uint64_t lo[9], hi[8];  // words 0..nd and kM..kM+nd-1
+    lo[0] = x;
+    for (uint32_t i = 1; i < (uint32_t)rng::kM + nd; ++i) {
+      x = rng::seed_step(x, i);
+      if (i <= (uint32_t)nd) lo[i] = x;
+      if (i >= (uint32_t)rng::kM) hi[i - rng::kM] = x;
+    }
+    for (int i = 0; i < nd; ++i) out[i] = rng::temper(rng::twist_word(lo[i], lo[i + 1], hi[i]));
+    return;
+  }
+  uint64_t w4[4];
+  w4[0] = x;
   for (uint32_t i = 1; i < (uint32_t)rng::kN; ++i) {
     x = rng::seed_step(x, i);
-    out[i] = x;
+    w4[i & 3] = x;
+    if ((i & 3) == 3) {
+      uint4* o = reinterpret_cast<uint4*>(out + i - 3);
+      o[0] = make_uint4((uint32_t)w4[0], (uint32_t)(w4[0] >> 32), (uint32_t)w4[1], (uint32_t)(w4[1] >> 32));
+      o[1] = make_uint4((uint32_t)w4[2], (uint32_t)(w4[2] >> 32), (uint32_t)w4[3], (uint32_t)(w4[3] >> 32));
+    }
   }
 }
 
