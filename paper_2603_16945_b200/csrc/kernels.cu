@@ -1425,28 +1425,40 @@ __device__ int radix_sort(uint64_t* k0, uint32_t* v0, uint64_t* k1, uint32_t* v1
   return cur;
 }
 
-// Smallest coordinate per axis with the sequential `if (v < o) o = v`
+// Per-axis extremes of a cloud in one pass: the plain min / max over the
+// non-NaN coordinates and whether any coordinate is NaN.  With `origin`, also
+// the smallest coordinate per axis with the sequential `if (v < o) o = v`
 // semantics starting from point 0 (App. C voxel origin): NaN at point 0
 // poisons the axis; later NaNs never win; equal values keep the first.
 template <int U>
-__device__ void seq_min3(const float* d, uint32_t n, Smem& S, float* lo) {
-  float l3[3] = {INFINITY, INFINITY, INFINITY};
+__device__ void axis_extremes(const float* d, uint32_t n, Smem& S, float* mn, float* mx, bool& any_nan,
+                              float* origin) {
+  float l3[3] = {INFINITY, INFINITY, INFINITY}, h3[3] = {-INFINITY, -INFINITY, -INFINITY};
+  uint32_t nan = 0;
   for (uint32_t i0 = threadIdx.x; i0 < n; i0 += U * blockDim.x) {  // all axes, U points in flight
     float v[U][3];
 #pragma unroll
     for (int u = 0; u < U; ++u)
 #pragma unroll
-      for (int k = 0; k < 3; ++k) v[u][k] = i0 + u * blockDim.x < n ? d[3 * (i0 + u * blockDim.x) + k] : INFINITY;
+      for (int k = 0; k < 3; ++k) v[u][k] = i0 + u * blockDim.x < n ? d[3 * (i0 + u * blockDim.x) + k] : d[k];
 #pragma unroll
     for (int u = 0; u < U; ++u)
 #pragma unroll
-      for (int k = 0; k < 3; ++k) l3[k] = fminf(l3[k], v[u][k]);
+      for (int k = 0; k < 3; ++k) {
+        l3[k] = fminf(l3[k], v[u][k]);
+        h3[k] = fmaxf(h3[k], v[u][k]);
+        nan |= isnan(v[u][k]) ? 1u : 0u;
+      }
   }
+  any_nan = dev::block_reduce(nan, dev::OpOr{}, 0u, S.red) != 0;
   for (int k = 0; k < 3; ++k) {
-    lo[k] = dev::block_reduce(l3[k], [](float x, float y) { return fminf(x, y); }, INFINITY, S.red);
+    mn[k] = dev::block_reduce(l3[k], [](float x, float y) { return fminf(x, y); }, INFINITY, S.red);
+    mx[k] = dev::block_reduce(h3[k], [](float x, float y) { return fmaxf(x, y); }, -INFINITY, S.red);
+    if (!origin) continue;
+    origin[k] = mn[k];
     const float p0 = d[k];
-    if (isnan(p0)) lo[k] = p0;
-    else if (lo[k] == 0.0f) {  // first zero in point order keeps its sign
+    if (isnan(p0)) origin[k] = p0;
+    else if (origin[k] == 0.0f) {  // first zero in point order keeps its sign
       if (threadIdx.x == 0) {
         float z = 0.0f;
         for (uint32_t i = 0; i < n; ++i)
@@ -1454,7 +1466,7 @@ __device__ void seq_min3(const float* d, uint32_t n, Smem& S, float* lo) {
         S.f32s[k] = z;
       }
       __syncthreads();
-      lo[k] = S.f32s[k];
+      origin[k] = S.f32s[k];
       __syncthreads();
     }
   }
@@ -1481,41 +1493,34 @@ __device__ int32_t op_voxel(const WaveArgs& a, Cloud& c, Smem& S, const OpDesc& 
       vt = t1;
     }
   };
-  float o[3];
+  // origin + extent in one pass over the coordinates.  The App. C key
+  // floorf((p - o) / v) is monotone in p (fsub_rn, fdiv_rn by v > 0 and
+  // floorf all are), and NaN only arises from a NaN or infinite coordinate
+  // (the extremes themselves) or origin, so every key is in [0, 2^21) iff no
+  // coordinate is NaN and the keys of the per-axis min and max are, and the
+  // largest key per axis is the max coordinate's: no per-point division here.
+  float o[3], cmin[3], cmax[3];
+  bool any_nan = false;
   if (op.has_origin) {
     o[0] = op.origin[0]; o[1] = op.origin[1]; o[2] = op.origin[2];
+    axis_extremes<U>(d, n, S, cmin, cmax, any_nan, nullptr);
   } else {
-    seq_min3<U>(d, n, S, o);
+    axis_extremes<U>(d, n, S, cmin, cmax, any_nan, o);
   }
   uint32_t* idx = reinterpret_cast<uint32_t*>(c.ix[0]);
   uint32_t* idx2 = reinterpret_cast<uint32_t*>(c.ix[1]);
-  // pass 1: range check and per-axis extent (no stores)
-  uint32_t bad = 0, mx[3] = {0, 0, 0};
-  for (uint32_t i0 = threadIdx.x; i0 < n; i0 += U * blockDim.x) {  // U points in flight
-    float v[U][3];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const uint32_t i = i0 + u * blockDim.x;
-#pragma unroll
-      for (int ax = 0; ax < 3; ++ax) v[u][ax] = i < n ? d[3 * i + ax] : o[ax];
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-#pragma unroll
-      for (int ax = 0; ax < 3; ++ax) {
-        const float q = floorf(__fdiv_rn(__fsub_rn(v[u][ax], o[ax]), op.voxel));
-        if (!(q >= 0.0f && q < 2097152.0f)) bad = 1;
-        else mx[ax] = max(mx[ax], (uint32_t)q);
-      }
+  bool bad = any_nan;
+  uint32_t mx[3] = {0, 0, 0};
+  for (int ax = 0; ax < 3; ++ax) {
+    const float ql = floorf(__fdiv_rn(__fsub_rn(cmin[ax], o[ax]), op.voxel));
+    const float qh = floorf(__fdiv_rn(__fsub_rn(cmax[ax], o[ax]), op.voxel));
+    if (!(ql >= 0.0f && ql < 2097152.0f) || !(qh >= 0.0f && qh < 2097152.0f)) bad = true;
+    else mx[ax] = (uint32_t)qh;
   }
-  bad = dev::block_reduce(bad, dev::OpOr{}, 0u, S.red);
   if (bad) return kOutOfBounds;
   vmark(0);  // origin + extent pass
   uint32_t bx[3];
-  for (int ax = 0; ax < 3; ++ax) {
-    const uint32_t m = dev::block_reduce(mx[ax], dev::OpMax{}, 0u, S.red);
-    bx[ax] = m ? 32u - __clz(m) : 0u;
-  }
+  for (int ax = 0; ax < 3; ++ax) bx[ax] = mx[ax] ? 32u - __clz(mx[ax]) : 0u;
   // compact sort key, monotone in the App. C key (kz major, then ky, kx)
   const uint32_t kb = bx[0] + bx[1] + bx[2];
   const uint32_t ib = n > 1 ? 32u - __clz(n - 1) : 0u;  // point-index bits

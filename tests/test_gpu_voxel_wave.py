@@ -99,6 +99,8 @@ STATUS_CASES = {
     "below_origin": ("low_x", CROP_VOX, 2),
     "nan": ("nan", [("grid_subsample", {"voxel_size": 0.5}), "flip_yz"], 1),
     "nan_at_point0": ("nan0", [("grid_subsample", {"voxel_size": 0.5}), "flip_yz"], 1),
+    "inf": ("inf", [("grid_subsample", {"voxel_size": 0.5}), "flip_yz"], 1),
+    "beyond_key_range": ("far", [("grid_subsample", {"voxel_size": 0.5}), "flip_yz"], 1),
 }
 
 
@@ -121,6 +123,10 @@ def test_vx_statuses_match_cta_path(pcp, tmp_path, case):
                 p[1234, 1] = np.nan
             elif mut == "nan0":
                 p[0, 2] = np.nan
+            elif mut == "inf":
+                p[2500, 2] = np.inf
+            elif mut == "far":  # key 2^21 on y: one past the App. C key range
+                p[1500, 1] = p[:, 1].min() + 0.5 * 2097152.0 + 10.0
             else:
                 p[77, 0] = 0.2
         samples.append({"data": p.reshape(-1).view(np.uint8),
@@ -140,6 +146,11 @@ def test_vx_statuses_match_cta_path(pcp, tmp_path, case):
         p.close()
     assert msgs[0][0] == msgs[1][0], msgs
     assert f"op {op}:" in msgs[0][0], msgs[0][0]
+    # App. C: an empty cloud after the crop is EmptyCloud; every key outside
+    # [0, 2^21) (NaN, inf, below the origin, too far) is OutOfBounds
+    # (oracle/pcpipe_oracle.c op_voxel)
+    want = "EmptyCloud" if mut == "shift" else "OutOfBounds"
+    assert want in msgs[0][0], msgs[0][0]
     for a, b in zip(msgs[0][1], msgs[1][1]):
         for k in b:
             assert np.array_equal(a[k][0].view(np.uint8), b[k][0].view(np.uint8))

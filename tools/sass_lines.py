@@ -17,6 +17,8 @@ rows = list(csv.reader(open(dump)))
 hdr = rows[1]
 data = [r for r in rows[2:] if len(r) == len(hdr)]
 S = hdr.index("Warp Stall Sampling (All Samples)")
+if os.environ.get("METRIC"):  # e.g. METRIC="Instructions Executed"
+    S = hdr.index(os.environ["METRIC"])
 base = int(data[0][0], 16)
 samples = {int(r[0], 16) - base: int(r[S] or 0) for r in data}
 stall_cols = [i for i, h in enumerate(hdr) if h.startswith("stall_") and "Not Issued" not in h]
