@@ -499,6 +499,8 @@ def main():
                 "per_gpu_clouds_per_sec": value / world, "roofline": roof,
                 "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
                 "gpu_launches": st1["launches"] - st0["launches"],
+                "k_cloud_launch": {k: st1.get(k) for k in ("cloud_grid", "cloud_min_blocks", "smem_bytes",
+                                                             "smem_mode", "fps_cluster")},
                 "batches_per_step": nb / args.steps}
         if "op_cycles" in st1:  # PCP_OP_TIMING=1 diagnostics: share of k_cloud CTA time
             oc = st1["op_cycles"]

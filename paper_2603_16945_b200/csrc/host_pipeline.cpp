@@ -1948,6 +1948,9 @@ struct Pipeline {
            {"threads", threads},
            {"slots", (uint64_t)slots.size()},
            {"smem_bytes", smem},
+           {"cloud_grid", grid},
+           {"cloud_min_blocks", proto.min_blocks},
+           {"fps_cluster", proto.fps_cluster},
            {"smem_mode", proto.smem_mode},
            {"cap_points", proto.cap_points},
            {"resident", resident},
