@@ -93,17 +93,23 @@ def env():
 
 
 def dataset(cfg_name, cfg, world, quantized, rank, barrier):
-    """Rank 0 writes the synthetic dataset (clouds_per_gpu x world clouds,
-    8 slices) to local disk with the library's writer (byte-identical to the
-    reference's write_dataset, tests/test_host.py); every rank then opens it."""
+    """The synthetic dataset on local disk, written with the library's writer
+    (byte-identical to the reference's write_dataset, tests/test_host.py).
+    N = 1: clouds_per_gpu clouds in 8 slices.  N > 1: rank r's shard of the
+    global set -- clouds [r*C, (r+1)*C), generated with their global seeds --
+    written by rank r as its own dataset, all ranks in parallel (one process
+    would hold and write N x 6 GB of S3DIS rooms serially), so each rank
+    reads only its own shard and no data crosses ranks."""
     from paper_2603_16945_b200 import write_dataset
-    d = f"/tmp/pcp_bench_{cfg_name}_{'q' if quantized else 'raw'}_{cfg['clouds']}x{world}_g{cfg['group']}"
+    C = cfg["clouds"]
+    d = f"/tmp/pcp_bench_{cfg_name}_{'q' if quantized else 'raw'}_{C}x{world}_g{cfg['group']}"
+    if world > 1:
+        d += f"_r{rank}"
     primary = os.path.join(d, "ds.pcrecord")
-    if rank == 0:
-        schema, samples = gen_samples(cfg, cfg["clouds"] * world, quantized)
-        write_dataset(d, "ds", schema, samples, slice_count=SLICES, group_size=cfg["group"],
-                      n_threads=min(32, os.cpu_count() or 1))
-        del samples
+    schema, samples = gen_samples(cfg, C, quantized, first=rank * C)
+    write_dataset(d, "ds", schema, samples, slice_count=SLICES, group_size=cfg["group"],
+                  n_threads=max(1, min(32, (os.cpu_count() or 1) // world)))
+    del samples
     barrier()
     return primary
 
@@ -316,7 +322,9 @@ def main():
     config = {"workload": args.config, "desc": cfg["desc"], "variant": coords,
               "clouds_per_gpu_per_step": cfg["clouds"], "points_per_cloud": cfg["points"],
               "batch": cfg["batch"], "group_size": cfg["group"], "slices": SLICES,
-              "parallelism": f"record-sharded by slice, {world} independent pipelines",
+              "parallelism": (f"record-sharded: rank r owns clouds [r*C, (r+1)*C) of the global set as "
+                              f"its own dataset, {world} independent pipelines" if world > 1 else
+                              "1 pipeline over all 8 slices"),
               "l2": "inputs per step > 126 MB L2 (no flush needed)"}
     metric = "point clouds/sec (PcRecord -> training batch)"
     cpu_sample = args.cpu_sample or cfg["cpu_sample"]
@@ -353,9 +361,17 @@ def main():
 
     import torch
     import torch.distributed as dist
+    if os.environ.get("PCP_BENCH_SHARED_GPU"):
+        # plumbing test only (tests/test_gpu_bench_multirank.py): every rank on
+        # cuda:0 with gloo collectives -- ranks share one GPU, so its numbers
+        # are not a measurement
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if os.environ.get("PCP_BENCH_SHARED_GPU"):
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         barrier = dist.barrier
     else:
         barrier = lambda: None
@@ -363,7 +379,7 @@ def main():
     from paper_2603_16945_b200 import shard
     primary = dataset(args.config, cfg, world, args.quantized, rank, barrier)
     idx = shard.read_index(primary)
-    ids = shard.slice_shard(idx, world, rank)
+    ids = None  # the rank's dataset is its shard
     g = graph_for(args.config, cfg)
 
     def timed(resident, steps, d2h):
