@@ -465,6 +465,7 @@ struct Wave {
   DevBuf handoff_b;  // vx stage output (voxelized clouds B)
   DevBuf vx_cl, vx_tiles, vx_cnt, vx_w0, vx_w1;  // vx stage scratch
   DevBuf vx_bt, vx_bcnt, vx_boff, vx_items, vx_T;  // vx bucket mode
+  DevBuf pj_ptr, pj_changed, pj_flags;  // LZ4 phase 4 by pointer jumping: source per raw byte, round / block flags
   cudaEvent_t v0 = nullptr, v1 = nullptr;        // vx stage
   DevBuf mt_pre;   // pre-seeded MT19937-64 states [n][n_rng][312] (k_seed_states)
   uint32_t n_todo = 0;
@@ -571,6 +572,11 @@ struct Pipeline {
   bool vx_allowed = false, vx_on = false;  // default off until it beats the one-CTA path
   uint64_t vx_min_points = 32768;
   bool vx_msd = true;  // option "vx_buckets": bucket mode of the vx stage
+  // LZ4 phase 4 by page-wide pointer jumping: -1 auto (unless the block
+  // pages average >= 32 samples), 0 never, 1 always (option
+  // "lz4_pointer_jumping", env PCP_LZ4_PJ)
+  int lz4_pj = std::getenv("PCP_LZ4_PJ") ? std::atoi(std::getenv("PCP_LZ4_PJ")) : -1;
+  uint64_t lz4_pj_waves = 0;  // waves whose LZ4 phase 4 ran as pointer jumping
   VxArgs vx_proto{};
   double vx_kernel_ms = 0;
   uint64_t vx_alg_bytes = 0;
@@ -652,6 +658,7 @@ struct Pipeline {
       vx_allowed = o.value("vx", vx_allowed);
       vx_min_points = o.value("vx_min_points", vx_min_points);
       vx_msd = o.value("vx_buckets", vx_msd);
+      if (o.contains("lz4_pointer_jumping")) lz4_pj = o["lz4_pointer_jumping"].get<bool>() ? 1 : 0;
     }
     if (src_header) {  // pages come from the caller: header bytes only, no files
       h = parse_header_bytes(src_header->data(), src_header->size());
@@ -1445,7 +1452,31 @@ struct Pipeline {
     }
     if (proto.n_rng) w.mt_pre.ensure(w.n * proto.n_rng * 312 * 8);
     w.h_res.ensure(total - o_sst + 16);
+    // phase 4 of the LZ4 pages: page-wide pointer jumping, or a warp per page
+    // for pages of many small clouds (C2's 64 x 32 KB: float literals the warp
+    // skips and short label chains), where it measured faster
+    uint32_t n_lz4 = 0, max_raw = 0;
+    uint64_t lz4_block_samples = 0, n_lz4_block = 0;
+    for (uint32_t pg_i : todo)
+      if (pages[pg_i].flags & kFlagOuterLz4) {
+        ++n_lz4;
+        max_raw = std::max<uint32_t>(max_raw, (uint32_t)std::min<uint64_t>(pages[pg_i].raw_len, 0xFFFFFFFFull));
+        if (pg_i >= ng) {
+          ++n_lz4_block;
+          lz4_block_samples += h.groups[groups[pg_i - ng]].sample_count;
+        }
+      }
+    const bool many_small = n_lz4_block > 0 && lz4_block_samples >= 32 * n_lz4_block;
+    const bool pj = n_lz4 > 0 && (lz4_pj > 0 || (lz4_pj < 0 && !many_small));
+    uint32_t pj_rounds = 0;
+    if (pj) {
+      pj_rounds = (max_raw > 1 ? 32u - __builtin_clz(max_raw - 1) : 0u) + 1u;  // ceil(log2) + 1
+      w.pj_ptr.ensure(4ull * (raw_at + 64));
+      w.pj_changed.ensure(4ull * pj_rounds * todo.size() + 64);
+      w.pj_flags.ensure(raw_at / 256 + todo.size() + 64);  // per 256-B block (+1 per page)
+    }
     if (dry) return;
+    if (pj) ++lz4_pj_waves;
     uint8_t* ht = w.h_tables.as<uint8_t>();
     std::memcpy(ht + o_pages, pages.data(), pages.size() * sizeof(PageRef));
     std::memcpy(ht + o_groups, gw.data(), gw.size() * sizeof(GroupWork));
@@ -1565,7 +1596,9 @@ struct Pipeline {
     CK(cudaEventRecord(w.d0, w.stream));
     CK(launch_page_decode(bytes, a.raw, a.pages, reinterpret_cast<const uint32_t*>(dt + o_todo),
                           reinterpret_cast<const uint64_t*>(dt + o_tsc), w.lz4_scratch.as<uint8_t>(),
-                          (uint32_t)todo.size(), a.page_status, w.stream, tm));
+                          (uint32_t)todo.size(), a.page_status, w.stream, tm,
+                          pj ? w.pj_ptr.as<uint32_t>() : nullptr, pj ? w.pj_changed.as<uint32_t>() : nullptr,
+                          pj_rounds, pj ? w.pj_flags.as<uint8_t>() : nullptr));
     CK(cudaEventRecord(w.d1, w.stream));
     w.n_todo = (uint32_t)todo.size();
     w.decode_alg_bytes = 0;
@@ -1928,6 +1961,7 @@ struct Pipeline {
            {"crc_kernel_alg_bytes", crc_alg_bytes},
            {"csr_kernel_ms", csr_kernel_ms},
            {"vx", vx_on},
+           {"lz4_pj_waves", lz4_pj_waves},
            {"kernels", json{{"k_vx_*(voxel stage)", json{{"ms", vx_kernel_ms}, {"alg_bytes", vx_alg_bytes}}}}},
            {"csr_kernel_alg_bytes", csr_alg_bytes},
            {"serial", serial},

@@ -256,6 +256,136 @@ __global__ void __launch_bounds__(kMatchThreads) k_page_matches(uint8_t* raw, co
   }
 }
 
+// Phase 4 by page-wide pointer jumping: a warp per page
+// resolves megabytes of match chains in stream order while most of the GPU
+// idles (KITTI / S3DIS quantised pages: one cloud per page).  Here every
+// output byte of a pending page gets a pointer to its source -- P[b] = b for
+// literal bytes, b - off inside a match (the byte-wise overlapping copy) --
+// and rounds of P[b] = P[P[b]] run over all pages at once.  Pointers only
+// move to earlier ancestors, so in-place updates are safe and every chain
+// ends at a literal byte within ceil(log2(depth)) + 1 rounds; then one gather
+// out[b] = out[P[b]].  Work is tracked per 256-byte block: blocks without
+// match bytes are never visited, and a block none of whose pointers moved in
+// a round points only at literal bytes (roots never move), so it is retired.
+// Phase 3 already checked every match: this is pure data movement.
+// grid (n_todo, kPjSplit); warps take blocks.  Per page, the block flags
+// live at F + raw_dst / 256 (bit 0: active, bit 1: holds match bytes).
+constexpr uint32_t kPjSplit = 64;
+constexpr uint32_t kPjBlock = 256;
+
+__device__ __forceinline__ bool pj_page(uint8_t* raw, const PageRef* pages, const uint32_t* todo,
+                                        const uint64_t* scratch_off, uint8_t* scratch, uint32_t* ptr,
+                                        uint8_t* flags, uint32_t w, uint32_t*& P, uint8_t*& dst,
+                                        uint8_t*& F, uint32_t& len, lz4p::Scratch& sc) {
+  const PageRef pg = pages[todo[w]];
+  if (!(pg.flags & kFlagOuterLz4)) return false;
+  sc = lz4p::carve_scratch(scratch + scratch_off[w], pg.pay_len);
+  if (sc.hdr[1] != 1u) return false;
+  P = ptr + pg.raw_dst;  // raw_dst is 16-B aligned; blocks are page-relative
+  dst = raw + pg.raw_dst;
+  F = flags + pg.raw_dst / kPjBlock + w;  // disjoint per page: nblk <= (raw_len / 256) + 1
+  len = (uint32_t)pg.raw_len;
+  return true;
+}
+
+__global__ void __launch_bounds__(256) k_pj_init(uint8_t* raw, const PageRef* pages, const uint32_t* todo,
+                                                 const uint64_t* scratch_off, uint8_t* scratch,
+                                                 uint32_t* ptr, uint8_t* flags) {
+  uint32_t* P;
+  uint8_t *dst, *F;
+  uint32_t len;
+  lz4p::Scratch sc;
+  if (!pj_page(raw, pages, todo, scratch_off, scratch, ptr, flags, blockIdx.x, P, dst, F, len, sc)) return;
+  const uint32_t step = kPjSplit * blockDim.x;
+  for (uint32_t b = blockIdx.y * blockDim.x + threadIdx.x; b < len; b += step) P[b] = b;
+  const uint32_t nblk = (len + kPjBlock - 1) / kPjBlock;
+  for (uint32_t k = blockIdx.y * blockDim.x + threadIdx.x; k < nblk; k += step) F[k] = 0;
+}
+
+__global__ void __launch_bounds__(256) k_pj_matches(uint8_t* raw, const PageRef* pages, const uint32_t* todo,
+                                                    const uint64_t* scratch_off, uint8_t* scratch,
+                                                    uint32_t* ptr, uint8_t* flags) {
+  uint32_t* P;
+  uint8_t *dst, *F;
+  uint32_t len;
+  lz4p::Scratch sc;
+  if (!pj_page(raw, pages, todo, scratch_off, scratch, ptr, flags, blockIdx.x, P, dst, F, len, sc)) return;
+  const uint32_t M = sc.hdr[0];
+  const uint32_t step = kPjSplit * blockDim.x;
+  for (uint32_t m = blockIdx.y * blockDim.x + threadIdx.x; m < M; m += step) {
+    const uint32_t mo = sc.m_mo[m], ml = sc.m_ml[m], off = sc.m_off[m];
+    for (uint32_t i = 0; i < ml; ++i) P[mo + i] = mo + i - off;
+    if (ml)
+      for (uint32_t k = mo / kPjBlock; k <= (mo + ml - 1) / kPjBlock; ++k) F[k] = 3;
+  }
+}
+
+// round r; changed[r * n_todo + w] = some pointer of page w moved this round
+__global__ void __launch_bounds__(256) k_pj_round(uint8_t* raw, const PageRef* pages, const uint32_t* todo,
+                                                  const uint64_t* scratch_off, uint8_t* scratch,
+                                                  uint32_t* ptr, uint8_t* flags, uint32_t* changed,
+                                                  uint32_t n_todo, uint32_t r) {
+  const uint32_t w = blockIdx.x;
+  if (r > 0 && changed[(r - 1) * n_todo + w] == 0) return;  // page converged
+  uint32_t* P;
+  uint8_t *dst, *F;
+  uint32_t len;
+  lz4p::Scratch sc;
+  if (!pj_page(raw, pages, todo, scratch_off, scratch, ptr, flags, w, P, dst, F, len, sc)) return;
+  const uint32_t lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const uint32_t nblk = (len + kPjBlock - 1) / kPjBlock;
+  bool any = false;
+  for (uint32_t k = blockIdx.y * nw + (threadIdx.x >> 5); k < nblk; k += kPjSplit * nw) {
+    if (!(F[k] & 1u)) continue;  // warp-uniform
+    const uint32_t b0 = k * kPjBlock;
+    uint32_t p[kPjBlock / 32];
+#pragma unroll
+    for (int u = 0; u < (int)(kPjBlock / 32); ++u) {
+      const uint32_t b = b0 + u * 32 + lane;
+      p[u] = b < len ? P[b] : b;
+    }
+    bool ch = false;
+#pragma unroll
+    for (int u = 0; u < (int)(kPjBlock / 32); ++u) {
+      const uint32_t b = b0 + u * 32 + lane;
+      if (p[u] != b) {
+        const uint32_t q = P[p[u]];
+        if (q != p[u]) {
+          P[b] = q;
+          ch = true;
+        }
+      }
+    }
+    ch = __any_sync(0xffffffffu, ch);
+    if (!ch && lane == 0) F[k] = 2;  // every pointer of the block is at a root: retired
+    any |= ch;
+  }
+  if (__syncthreads_or(any) && threadIdx.x == 0) changed[r * n_todo + w] = 1;
+}
+
+__global__ void __launch_bounds__(256) k_pj_gather(uint8_t* raw, const PageRef* pages, const uint32_t* todo,
+                                                   const uint64_t* scratch_off, uint8_t* scratch,
+                                                   uint32_t* ptr, uint8_t* flags) {
+  uint32_t* P;
+  uint8_t *dst, *F;
+  uint32_t len;
+  lz4p::Scratch sc;
+  if (!pj_page(raw, pages, todo, scratch_off, scratch, ptr, flags, blockIdx.x, P, dst, F, len, sc)) return;
+  const uint32_t lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const uint32_t nblk = (len + kPjBlock - 1) / kPjBlock;
+  for (uint32_t k = blockIdx.y * nw + (threadIdx.x >> 5); k < nblk; k += kPjSplit * nw) {
+    if (!(F[k] & 2u)) continue;  // literal-only block: final already
+#pragma unroll
+    for (int u = 0; u < (int)(kPjBlock / 32); ++u) {
+      const uint32_t b = k * kPjBlock + u * 32 + lane;
+      if (b < len) {
+        const uint32_t p = P[b];
+        if (p != b) dst[b] = dst[p];  // p is a literal byte: final, never written here
+      }
+    }
+  }
+}
+
 // =========================================================================
 // Scalar-record parse: one thread walks one group's decoded scalar page
 // (parse_scalar_record, format.cpp:426-474).  Values of non-bytes fields are
@@ -2366,7 +2496,8 @@ cudaError_t launch_crc_windows(const uint8_t* bytes, const CrcWindow* win, uint3
 cudaError_t launch_page_decode(const uint8_t* bytes, uint8_t* raw, const PageRef* pages,
                                const uint32_t* todo, const uint64_t* scratch_off,
                                uint8_t* scratch, uint32_t n_todo, int32_t* status,
-                               cudaStream_t st, long long* timing) {
+                               cudaStream_t st, long long* timing, uint32_t* pj_ptr,
+                               uint32_t* pj_changed, uint32_t pj_rounds, uint8_t* pj_flags) {
   if (!n_todo) return cudaSuccess;
   static bool carve = [] {  // static shared memory only: ask for the max carveout
     cudaFuncSetAttribute(k_page_decode, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -2380,6 +2511,17 @@ cudaError_t launch_page_decode(const uint8_t* bytes, uint8_t* raw, const PageRef
     const int v = e ? std::atoi(e) : (int)kMatchThreads;
     return (uint32_t)std::max(32, std::min((int)kMatchThreads, v / 32 * 32));
   }();
+  if (pj_ptr) {  // phase 4 by page-wide pointer jumping
+    const dim3 g(n_todo, kPjSplit);
+    k_pj_init<<<g, 256, 0, st>>>(raw, pages, todo, scratch_off, scratch, pj_ptr, pj_flags);
+    k_pj_matches<<<g, 256, 0, st>>>(raw, pages, todo, scratch_off, scratch, pj_ptr, pj_flags);
+    cudaMemsetAsync(pj_changed, 0, 4ull * pj_rounds * n_todo, st);
+    for (uint32_t r = 0; r < pj_rounds; ++r)
+      k_pj_round<<<g, 256, 0, st>>>(raw, pages, todo, scratch_off, scratch, pj_ptr, pj_flags, pj_changed,
+                                   n_todo, r);
+    k_pj_gather<<<g, 256, 0, st>>>(raw, pages, todo, scratch_off, scratch, pj_ptr, pj_flags);
+    return cudaGetLastError();
+  }
   k_page_matches<<<n_todo, match_threads, 0, st>>>(raw, pages, todo, scratch_off, scratch, n_todo, timing);
   return cudaGetLastError();
 }

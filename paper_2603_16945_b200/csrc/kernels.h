@@ -29,7 +29,9 @@ cudaError_t launch_crc_windows(const uint8_t* bytes, const CrcWindow* win, uint3
 cudaError_t launch_page_decode(const uint8_t* bytes, uint8_t* raw, const PageRef* pages,
                                const uint32_t* todo, const uint64_t* scratch_off,
                                uint8_t* scratch, uint32_t n_todo, int32_t* status,
-                               cudaStream_t st, long long* timing = nullptr);
+                               cudaStream_t st, long long* timing = nullptr,
+                               uint32_t* pj_ptr = nullptr, uint32_t* pj_changed = nullptr,
+                               uint32_t pj_rounds = 0, uint8_t* pj_flags = nullptr);  // pj_ptr: phase 4 by pointer jumping
 uint64_t lz4_scratch_bytes(uint64_t pay);  // per LZ4 page
 // scalar parse → cloud interpreter → page verdicts → sample status
 // grid_pre: the prefix launch of a split chain (a.split_at > 0), one CTA per cloud

@@ -21,13 +21,14 @@ def _run(pcp, primary, graph, **kw):
     return pcp.run_pipeline(primary, graph, **kw)
 
 
-@pytest.mark.parametrize("quantized", [False, True])
-def test_shapenet_chain_parity(pcp, ref, orc, tmp_path, quantized):
-    """C2 chain: normalize → downsample 1024 (+seg) → random_scale → shuffle."""
+@pytest.mark.parametrize("quantized,pj", [(False, None), (True, False), (True, True)])
+def test_shapenet_chain_parity(pcp, ref, orc, tmp_path, quantized, pj):
+    """C2 chain: normalize → downsample 1024 (+seg) → random_scale → shuffle;
+    LZ4 pages with either phase-4 path."""
     from paper_2603_16945_b200 import synth
     primary = _ds(pcp, tmp_path, "shapenet", 70, group=16, slices=2, quantized=quantized)
     g = synth.graph(synth.CHAINS["shapenet_part"], batch_size=8)
-    got = _run(pcp, primary, g)
+    got = _run(pcp, primary, g, **({} if pj is None else {"lz4_pointer_jumping": pj}))
     want = expected_run(ref, orc, primary, g)
     assert_batches_equal(got, want)
 
@@ -301,11 +302,13 @@ def _adversarial_blob(rng, n):
     return np.concatenate(out)[:n]
 
 
+@pytest.mark.parametrize("pj", [False, True])
 @pytest.mark.parametrize("seed", [1, 2, 3, 4, 5, 6])
-def test_lz4_adversarial_pages_through_pipeline(pcp, ref, tmp_path, seed):
-    """Pipeline decode (k_page_decode + k_page_matches: skim with skipped
-    windows, pointer-jumping match groups, slow path) of adversarial LZ4 pages
-    is byte-exact against the reference reader."""
+def test_lz4_adversarial_pages_through_pipeline(pcp, ref, tmp_path, seed, pj):
+    """Pipeline decode of adversarial LZ4 pages (k_page_decode: skim with
+    skipped windows, slow path; phase 4 by k_page_matches' pointer-jumping
+    match groups, or page-wide pointer jumping) is byte-exact against the
+    reference reader."""
     rng = np.random.default_rng(seed)
     schema = {"fields": {"blob": {"type": "bytes"}, "id": {"type": "int32"}}}
     samples = [{"blob": _adversarial_blob(rng, int(rng.integers(20000, 300000))),
@@ -315,7 +318,7 @@ def test_lz4_adversarial_pages_through_pipeline(pcp, ref, tmp_path, seed):
     for b in pcp.Pipeline(primary, {"base_seed": 1, "drop_remainder": False, "ops": [
             {"id": 0, "kind": "source", "num_workers": 1, "queue_capacity": 8},
             {"id": 1, "kind": "batch", "batch_size": 4, "num_workers": 1, "queue_capacity": 8},
-            {"id": 2, "kind": "sink", "num_workers": 1, "queue_capacity": 8}]}):
+            {"id": 2, "kind": "sink", "num_workers": 1, "queue_capacity": 8}]}, lz4_pointer_jumping=pj):
         host = b.to_host()
         arr, offs = host["blob"]
         for k in range(b.n_samples):
@@ -349,3 +352,20 @@ def test_corrupt_payload_host_batches_serves_intact_batches(pcp, tmp_path, resid
         p.next_host_batch()
     assert ei.value.errc == "WorkerPanic" and "ChecksumMismatch" in str(ei.value)
     p.close()
+
+
+def test_lz4_phase4_path_choice(pcp, ref, orc, tmp_path):
+    """Auto choice of the LZ4 phase-4 path: pages of >= 32
+    clouds on average keep the warp-per-page resolver, pages of few large
+    clouds take page-wide pointer jumping; both give the oracle's batches."""
+    from paper_2603_16945_b200 import synth
+    g = synth.graph(synth.CHAINS["shapenet_part"][:2], batch_size=8)
+    for group, want_pj in ((32, False), (4, True)):
+        primary = _ds(pcp, tmp_path / f"g{group}", "shapenet", 128, group=group, slices=2, quantized=True)
+        p = pcp.Pipeline(primary, g)
+        got = [{"epoch": b.epoch, "batch_index": b.batch_index, "samples": b.samples()} for b in p]
+        st = p.stats()
+        p.close()
+        assert st["block_pages_lz4"] > 0
+        assert (st["lz4_pj_waves"] > 0) == want_pj, st
+        assert_batches_equal(got, expected_run(ref, orc, primary, g))
