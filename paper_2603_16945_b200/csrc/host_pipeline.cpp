@@ -1792,13 +1792,14 @@ struct Pipeline {
       if (lz4_timing && wn.n_todo) {
         std::vector<long long> tm(wn.n_todo * 16);
         CK(cudaMemcpy(tm.data(), wn.lz4_timing.p, tm.size() * 8, cudaMemcpyDeviceToHost));
-        for (uint32_t i = 0; i < wn.n_todo; ++i)
-          if (tm[i * 16 + 4])
-            for (int ph = 0; ph < 4; ++ph) {  // phase 4 runs in k_page_matches: its own clocks
-              const long long* q = &tm[i * 16];
-              const double c = ph < 3 ? (double)(q[ph + 1] - q[ph]) : (double)(q[12] - q[11]);
-              lz4_phase_cycles[ph] = std::max(lz4_phase_cycles[ph], c);
-            }
+        for (uint32_t i = 0; i < wn.n_todo; ++i) {
+          const long long* q = &tm[i * 16];
+          if (!q[3]) continue;  // not an LZ4 page (or the warp fallback)
+          // [0] skim (phases 1-2), [1] phase 3, [2] phase 4 (warp path: k_page_matches' clocks)
+          const double c[3] = {(double)(q[2] - q[0]), (double)(q[3] - q[2]),
+                               q[12] ? (double)(q[12] - q[11]) : 0.0};
+          for (int ph = 0; ph < 3; ++ph) lz4_phase_cycles[ph] = std::max(lz4_phase_cycles[ph], c[ph]);
+        }
       }
       if (src_done) src_done(src_user, wn.epoch, wn.pos0, wn.n);  // its pages are on the device
       cur = nxt;

@@ -24,5 +24,5 @@ st = p.stats()
 p.close()
 c = st["lz4_max_phase_cycles"]
 print(gen, "pages", n // group, "raw MB/page", round(sum(s["data"].nbytes for s in samples[:group]) / 1e6, 2),
-      "skim(ph1-2) ms %.2f  ph2-3 ms %.2f  ph3 ms %.2f  ph4 ms %.2f" % tuple(x / 1.965e6 for x in c),
+      "max per page: skim (phases 1-2) %.2f ms, phase 3 %.2f ms, warp phase 4 %.2f ms" % tuple(x / 1.965e6 for x in c[:3]),
       "decode_ms", round(st["decode_kernel_ms"], 2), "pj_waves", st["lz4_pj_waves"])
