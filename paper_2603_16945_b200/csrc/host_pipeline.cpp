@@ -577,6 +577,9 @@ struct Pipeline {
   // "lz4_pointer_jumping", env PCP_LZ4_PJ)
   int lz4_pj = std::getenv("PCP_LZ4_PJ") ? std::atoi(std::getenv("PCP_LZ4_PJ")) : -1;
   uint64_t lz4_pj_waves = 0;  // waves whose LZ4 phase 4 ran as pointer jumping
+  bool stagger_start = !(std::getenv("PCP_STAGGER") && std::atoi(std::getenv("PCP_STAGGER")) == 0);
+  uint64_t waves_launched_total = 0;
+  cudaEvent_t first_k1 = nullptr;  // the first wave's end-of-chain event (slot-owned)
   VxArgs vx_proto{};
   double vx_kernel_ms = 0;
   uint64_t vx_alg_bytes = 0;
@@ -1603,8 +1606,16 @@ struct Pipeline {
     w.n_todo = (uint32_t)todo.size();
     w.decode_alg_bytes = 0;
     for (uint32_t pi : todo) w.decode_alg_bytes += pages[pi].pay_len + pages[pi].raw_len;
+    // the pipeline's second wave starts its op chain after the first wave's:
+    // launched together, the two waves split every SM between their clouds
+    // and the pipeline could stay in a slow interleaved regime for a whole run
+    // (S3DIS: ~57 instead of ~35 ms per wave in about a third of fresh 10-epoch
+    // runs; tools/s3dis_var3.py); with the first wave leading, later waves
+    // fill SMs as its clouds finish (6 of 6 runs 6.4-6.8 K rooms/s)
+    if (stagger_start && waves_launched_total == 1 && first_k1) CK(cudaStreamWaitEvent(w.stream, first_k1, 0));
     CK(launch_wave(a, grid, grid_pre, threads, smem, w.stream, w.k0, w.k1, vx_on ? &vx : nullptr,
                    (uint32_t)vx_tiles_bound, (uint32_t)vx_btiles_bound, sms, w.v0, w.v1, w.handoff.as<uint8_t>()));
+    if (waves_launched_total++ == 0) first_k1 = w.k1;
     launches += (wins.empty() ? 0 : 1) + (todo.empty() ? 0 : 2) + (ng ? 1 : 0) + (proto.n_rng ? 1 : 0) + 1 + 1 + 1 +
                 (vx_on ? 2 + 14 + 3 * kVxMaxPasses : 0) + (proto.split_at ? 1 : 0);
     if (vx_on) {
