@@ -164,7 +164,8 @@ int pcp_write_dataset_device(const char* out_dir, const char* stem, const char* 
  * walk is the seed index, like Item.index (pipeline.cpp:447-448).
  * Options: JSON {"epochs": n, "resident": true|false, "wave_batches": k,
  * "slots": s, "host_batches": true|false, "stream": true|false,
- * "reader_threads": t, "serial": true|false, "vx": true|false}.
+ * "reader_threads": t, "serial": true|false, "vx": true|false,
+ * "lz4_pointer_jumping": true|false}.
  *   resident      pages of the walk's slices in HBM (read once at open);
  *                 false: in pinned host memory, H2D per wave
  *   stream        no copy at open: reader threads read each wave's pages from
@@ -174,6 +175,9 @@ int pcp_write_dataset_device(const char* out_dir, const char* stem, const char* 
  *                 like the reference's host Batch: one D2H per field per wave
  *   serial        one wave in flight (non-overlapped per-kernel timing)
  *   vx            multi-CTA voxel stage for large clouds
+ *   lz4_pointer_jumping  LZ4 match resolution over all pages of a wave at
+ *                 once (default: unless the block pages average >= 32
+ *                 samples) or one warp per page
  * Only the slices the walk touches are read (shard-local loading). */
 typedef struct pcp_pipeline pcp_pipeline;
 

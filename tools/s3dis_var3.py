@@ -20,6 +20,17 @@ g = bench.graph_for("s3dis", cfg)
 def timed(steps, slots):
     p = P.Pipeline(primary, g, epochs=steps, slots=slots)
     torch.cuda.synchronize()
+    if os.environ.get("SPIN_MS"):  # keep the GPU busy right before the timed region (clock ramp test)
+        x = torch.randn(8192, 8192, device="cuda")
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record()
+        while True:
+            x = x @ x
+            x = x / x.norm()
+            s1.record()
+            s1.synchronize()
+            if s0.elapsed_time(s1) > float(os.environ["SPIN_MS"]):
+                break
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     while p.next_batch_raw() is not None:
