@@ -1469,8 +1469,10 @@ struct Pipeline {
           lz4_block_samples += h.groups[groups[pg_i - ng]].sample_count;
         }
       }
+    // (waves whose only LZ4 pages are the small scalar pages keep the warp:
+    // a pages x 64 grid of near-empty CTAs per round would only crowd the SMs)
     const bool many_small = n_lz4_block > 0 && lz4_block_samples >= 32 * n_lz4_block;
-    const bool pj = n_lz4 > 0 && (lz4_pj > 0 || (lz4_pj < 0 && !many_small));
+    const bool pj = n_lz4 > 0 && (lz4_pj > 0 || (lz4_pj < 0 && n_lz4_block > 0 && !many_small));
     uint32_t pj_rounds = 0;
     if (pj) {
       pj_rounds = (max_raw > 1 ? 32u - __builtin_clz(max_raw - 1) : 0u) + 1u;  // ceil(log2) + 1
@@ -1601,7 +1603,8 @@ struct Pipeline {
                           reinterpret_cast<const uint64_t*>(dt + o_tsc), w.lz4_scratch.as<uint8_t>(),
                           (uint32_t)todo.size(), a.page_status, w.stream, tm,
                           pj ? w.pj_ptr.as<uint32_t>() : nullptr, pj ? w.pj_changed.as<uint32_t>() : nullptr,
-                          pj_rounds, pj ? w.pj_flags.as<uint8_t>() : nullptr));
+                          pj_rounds, pj ? w.pj_flags.as<uint8_t>() : nullptr,
+                          std::max<uint32_t>(1, std::min<uint32_t>(64, (max_raw + 65535) / 65536))));
     CK(cudaEventRecord(w.d1, w.stream));
     w.n_todo = (uint32_t)todo.size();
     w.decode_alg_bytes = 0;

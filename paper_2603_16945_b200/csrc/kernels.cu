@@ -296,7 +296,7 @@ __global__ void __launch_bounds__(256) k_pj_init(uint8_t* raw, const PageRef* pa
   uint32_t len;
   lz4p::Scratch sc;
   if (!pj_page(raw, pages, todo, scratch_off, scratch, ptr, flags, blockIdx.x, P, dst, F, len, sc)) return;
-  const uint32_t step = kPjSplit * blockDim.x;
+  const uint32_t step = gridDim.y * blockDim.x;
   for (uint32_t b = blockIdx.y * blockDim.x + threadIdx.x; b < len; b += step) P[b] = b;
   const uint32_t nblk = (len + kPjBlock - 1) / kPjBlock;
   for (uint32_t k = blockIdx.y * blockDim.x + threadIdx.x; k < nblk; k += step) F[k] = 0;
@@ -311,7 +311,7 @@ __global__ void __launch_bounds__(256) k_pj_matches(uint8_t* raw, const PageRef*
   lz4p::Scratch sc;
   if (!pj_page(raw, pages, todo, scratch_off, scratch, ptr, flags, blockIdx.x, P, dst, F, len, sc)) return;
   const uint32_t M = sc.hdr[0];
-  const uint32_t step = kPjSplit * blockDim.x;
+  const uint32_t step = gridDim.y * blockDim.x;
   for (uint32_t m = blockIdx.y * blockDim.x + threadIdx.x; m < M; m += step) {
     const uint32_t mo = sc.m_mo[m], ml = sc.m_ml[m], off = sc.m_off[m];
     for (uint32_t i = 0; i < ml; ++i) P[mo + i] = mo + i - off;
@@ -335,7 +335,7 @@ __global__ void __launch_bounds__(256) k_pj_round(uint8_t* raw, const PageRef* p
   const uint32_t lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const uint32_t nblk = (len + kPjBlock - 1) / kPjBlock;
   bool any = false;
-  for (uint32_t k = blockIdx.y * nw + (threadIdx.x >> 5); k < nblk; k += kPjSplit * nw) {
+  for (uint32_t k = blockIdx.y * nw + (threadIdx.x >> 5); k < nblk; k += gridDim.y * nw) {
     if (!(F[k] & 1u)) continue;  // warp-uniform
     const uint32_t b0 = k * kPjBlock;
     uint32_t p[kPjBlock / 32];
@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(256) k_pj_gather(uint8_t* raw, const PageRef* 
   if (!pj_page(raw, pages, todo, scratch_off, scratch, ptr, flags, blockIdx.x, P, dst, F, len, sc)) return;
   const uint32_t lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const uint32_t nblk = (len + kPjBlock - 1) / kPjBlock;
-  for (uint32_t k = blockIdx.y * nw + (threadIdx.x >> 5); k < nblk; k += kPjSplit * nw) {
+  for (uint32_t k = blockIdx.y * nw + (threadIdx.x >> 5); k < nblk; k += gridDim.y * nw) {
     if (!(F[k] & 2u)) continue;  // literal-only block: final already
 #pragma unroll
     for (int u = 0; u < (int)(kPjBlock / 32); ++u) {
@@ -2497,7 +2497,8 @@ cudaError_t launch_page_decode(const uint8_t* bytes, uint8_t* raw, const PageRef
                                const uint32_t* todo, const uint64_t* scratch_off,
                                uint8_t* scratch, uint32_t n_todo, int32_t* status,
                                cudaStream_t st, long long* timing, uint32_t* pj_ptr,
-                               uint32_t* pj_changed, uint32_t pj_rounds, uint8_t* pj_flags) {
+                               uint32_t* pj_changed, uint32_t pj_rounds, uint8_t* pj_flags,
+                               uint32_t pj_split) {
   if (!n_todo) return cudaSuccess;
   static bool carve = [] {  // static shared memory only: ask for the max carveout
     cudaFuncSetAttribute(k_page_decode, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -2512,7 +2513,7 @@ cudaError_t launch_page_decode(const uint8_t* bytes, uint8_t* raw, const PageRef
     return (uint32_t)std::max(32, std::min((int)kMatchThreads, v / 32 * 32));
   }();
   if (pj_ptr) {  // phase 4 by page-wide pointer jumping
-    const dim3 g(n_todo, kPjSplit);
+    const dim3 g(n_todo, pj_split);  // CTAs per page: ~64 KB of the largest page each, <= kPjSplit
     k_pj_init<<<g, 256, 0, st>>>(raw, pages, todo, scratch_off, scratch, pj_ptr, pj_flags);
     k_pj_matches<<<g, 256, 0, st>>>(raw, pages, todo, scratch_off, scratch, pj_ptr, pj_flags);
     cudaMemsetAsync(pj_changed, 0, 4ull * pj_rounds * n_todo, st);

@@ -31,7 +31,8 @@ cudaError_t launch_page_decode(const uint8_t* bytes, uint8_t* raw, const PageRef
                                uint8_t* scratch, uint32_t n_todo, int32_t* status,
                                cudaStream_t st, long long* timing = nullptr,
                                uint32_t* pj_ptr = nullptr, uint32_t* pj_changed = nullptr,
-                               uint32_t pj_rounds = 0, uint8_t* pj_flags = nullptr);  // pj_ptr: phase 4 by pointer jumping
+                               uint32_t pj_rounds = 0, uint8_t* pj_flags = nullptr,
+                               uint32_t pj_split = 64);  // pj_ptr: phase 4 by pointer jumping
 uint64_t lz4_scratch_bytes(uint64_t pay);  // per LZ4 page
 // scalar parse → cloud interpreter → page verdicts → sample status
 // grid_pre: the prefix launch of a split chain (a.split_at > 0), one CTA per cloud
