@@ -49,13 +49,13 @@ CONFIGS = {
                        cpu_sample=256,
                        points=10000, desc="ModelNet40-shaped 10k-pt clouds + normals: normalize, "
                        "FPS 1024, rotate, jitter; B 32"),
-    "kitti": dict(gen="kitti", kw={}, clouds=512, group=16, group_q=1, batch=4, points=120000, cpu_sample=64,
+    "kitti": dict(gen="kitti", kw={}, clouds=512, group=16, group_q=1, batch=4, points=120000, cpu_sample=128,
                   desc="KITTI-shaped ~120k-pt XYZI frames: range crop, voxel 0.05 m (+counts), "
                   "rotate, flip_yz; B 4 (CSR batches)"),
-    "s3dis": dict(gen="s3dis", kw={"mean_points": 1_000_000}, clouds=256, group=1, batch=4, cpu_sample=32,
+    "s3dis": dict(gen="s3dis", kw={"mean_points": 1_000_000}, clouds=256, group=1, batch=4, cpu_sample=128,
                   points=1_000_000, desc="S3DIS-shaped ~1M-pt XYZRGB rooms: grid 0.04 m, "
                   "random_crop, downsample 4096; B 4"),
-    "scannet": dict(gen="scannet", kw={}, clouds=192, group=4, group_q=1, batch=4, points=275000, cpu_sample=16,
+    "scannet": dict(gen="scannet", kw={}, clouds=192, group=4, group_q=1, batch=4, points=275000, cpu_sample=64,
                     desc="ScanNet-shaped 50k-500k-pt XYZRGB scenes: grid 0.02 m, downsample "
                     "40000, FPS 20000; B 4"),
 }
@@ -210,6 +210,12 @@ def graph_for(cfg_name, cfg, workers=1):
 
 
 APPC_OPS = {"fps", "voxel", "grid_subsample", "range_crop"}
+
+
+# cpu_sample: clouds per reference step.  run_benchmark excludes the first
+# batch from its clock, so a step needs several clouds per host thread (a
+# sample of one cloud per worker finishes all clouds together and leaves the
+# clock almost nothing: 16 ScanNet scenes on 16 threads read 488 K clouds/s).
 
 
 def cpu_reference(primary, graph, sample_ids, steps, warmup):
