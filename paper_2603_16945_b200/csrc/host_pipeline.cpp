@@ -1604,7 +1604,7 @@ struct Pipeline {
                           (uint32_t)todo.size(), a.page_status, w.stream, tm,
                           pj ? w.pj_ptr.as<uint32_t>() : nullptr, pj ? w.pj_changed.as<uint32_t>() : nullptr,
                           pj_rounds, pj ? w.pj_flags.as<uint8_t>() : nullptr,
-                          std::max<uint32_t>(1, std::min<uint32_t>(64, (max_raw + 65535) / 65536))));
+                          (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(64, ((uint64_t)max_raw + 65535) / 65536))));
     CK(cudaEventRecord(w.d1, w.stream));
     w.n_todo = (uint32_t)todo.size();
     w.decode_alg_bytes = 0;
