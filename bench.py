@@ -522,7 +522,8 @@ def main():
                 "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
                 "gpu_launches": st1["launches"] - st0["launches"],
                 "k_cloud_launch": {k: st1.get(k) for k in ("cloud_grid", "cloud_min_blocks", "smem_bytes",
-                                                             "smem_mode", "fps_cluster")},
+                                                             "smem_mode", "fps_cluster", "slots",
+                                                             "slab_bytes_per_slot")},
                 "batches_per_step": nb / args.steps}
         if "op_cycles" in st1:  # PCP_OP_TIMING=1 diagnostics: share of k_cloud CTA time
             oc = st1["op_cycles"]

@@ -706,10 +706,11 @@ struct Pipeline {
     // default: 4 slots (3 waves in flight: the LZ4 match phase of one wave
     // overlaps the decode / k_cloud of the others); 5 when every cloud's
     // buffers sit in shared memory (C2 +2%, measured: tools/sweep_slots.sh),
-    // fewer when the per-CTA global slabs of large-cloud chains would exceed ~48 GB
+    // fewer when the per-CTA global slabs of large-cloud chains would exceed
+    // 100 GiB (S3DIS: 4 slots of 26 GB; 3-4 slots measured +3% over 2)
     if (!slots_set && !proto.gscratch_per_cta) n_slots = 5;
     if (!slots_set && proto.gscratch_per_cta)
-      while (n_slots > 2 && (uint64_t)n_slots * proto.gscratch_per_cta * std::max(grid, grid_pre) > (48ull << 30))
+      while (n_slots > 2 && (uint64_t)n_slots * proto.gscratch_per_cta * std::max(grid, grid_pre) > (100ull << 30))
         --n_slots;
     slots.reserve(8);  // reconfiguration resizes in place (Wave owns device buffers)
     slots.resize(n_slots);
@@ -1998,6 +1999,8 @@ struct Pipeline {
            {"slots", (uint64_t)slots.size()},
            {"smem_bytes", smem},
            {"cloud_grid", grid},
+           {"slots", (uint64_t)slots.size()},
+           {"slab_bytes_per_slot", proto.gscratch_per_cta * (uint64_t)std::max(grid, grid_pre)},
            {"cloud_min_blocks", proto.min_blocks},
            {"fps_cluster", proto.fps_cluster},
            {"smem_mode", proto.smem_mode},
