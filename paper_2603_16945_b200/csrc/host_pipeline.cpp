@@ -713,8 +713,21 @@ struct Pipeline {
       while (n_slots > 2 && (uint64_t)n_slots * proto.gscratch_per_cta * std::max(grid, grid_pre) > (100ull << 30))
         --n_slots;
     slots.reserve(8);  // reconfiguration resizes in place (Wave owns device buffers)
-    slots.resize(n_slots);
-    for (auto& w : slots) create_slot(w);
+    // each slot is pre-sized for its largest wave as it is created; beyond two,
+    // a slot is added only while the device keeps room for one more plus a
+    // margin (quantized S3DIS: slabs + raw pages + LZ4 pointer arrays ~60 GB
+    // per slot)
+    size_t per_slot = 0;
+    for (uint32_t k = 0; k < n_slots; ++k) {
+      size_t f0 = 0, f1 = 0, tot = 0;
+      CK(cudaMemGetInfo(&f0, &tot));
+      if (k >= 2 && per_slot && f0 < per_slot + std::max<size_t>(8ull << 30, tot / 16)) break;
+      slots.emplace_back();
+      create_slot(slots.back());
+      CK(cudaMemGetInfo(&f1, &tot));
+      per_slot = std::max<size_t>(per_slot, f0 > f1 ? f0 - f1 : 0);
+    }
+    n_slots = (uint32_t)slots.size();
     t_start = std::chrono::steady_clock::now();
     if (stream_files && !plan.empty()) reader = std::thread([this] { reader_main(); });
     if (const char* e = std::getenv("PCP_TIMELINE")) timeline_on = std::atoi(e) != 0;
